@@ -54,7 +54,7 @@ def build_cuda(force: bool = False) -> str:
     if force or _stale(out, srcs):
         _run([NVCC, ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
               "--expt-relaxed-constexpr", "-Xptxas", "-v,-warn-spills", f"-I{INCLUDE}", f"-I{CSRC}",
-              *srcs, "-o", out, "-lcuda"])
+              *srcs, "-o", out])
     return out
 
 

@@ -1,0 +1,104 @@
+/*
+ * coe_cuda.h -- C-ABI of the sm_100a kernels and the GPU serving runtime.
+ *
+ * Plain pointers and sizes only (device pointers unless stated otherwise);
+ * every call is stream-ordered on the caller's cudaStream_t, returns 0 or a
+ * COE_CUDA_ERR_* code, and leaves the message in coe_cuda_last_error().
+ *
+ * Reference interfaces each entry point replaces (the reference models these
+ * steps with closed-form costs; SURVEY.md §2 "Kernels and collectives"):
+ *   coe_group_sort   <- scheduler.arrange_position + engine._Queue.insert
+ *                       (scheduler.py:100-108, engine.py:251-254)
+ *   coe_run_compact  <- engine._Queue.head_run + scheduler.batch_cap/split_batch
+ *                       (engine.py:270-283, scheduler.py:111-137)
+ *   coe_grouped_mlp  <- CostModel.exec_latency as used by Simulation._start_batch
+ *                       (costmodel.py:55-64, engine.py:693-716)
+ *   coe_swap_in      <- CostModel.load_latency_from as used by Simulation._start_load
+ *                       (costmodel.py:69-73, engine.py:643-677)
+ *   coe_runtime_*    <- Simulation.run's physical side (engine.py:762-781)
+ */
+#ifndef COE_CUDA_H
+#define COE_CUDA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *cudaStream_t;
+
+enum { COE_CUDA_OK = 0, COE_CUDA_ERR_CONFIG = 2, COE_CUDA_ERR_CHECK = 4, COE_CUDA_ERR_CUDA = 6 };
+
+const char *coe_cuda_last_error(void);
+
+/* ---------------- K1 / K2: GPU grouping ---------------------------------- */
+
+/* Stable LSD radix sort of n admissions by key = executor << rank_bits | run_rank.
+ * executor/run_rank: [n] int32 (admission order); out_perm: [n] sorted indices.
+ * scratch: coe_group_sort_scratch_bytes(n) bytes.  This is the segmented
+ * (per-executor) stable sort by run-rank that reproduces the reference's
+ * arranged queue order. */
+int64_t coe_group_sort_scratch_bytes(int64_t n);
+int coe_group_sort(const int32_t *executor, const int32_t *run_rank, int64_t n, int rank_bits, int num_passes,
+                   int32_t *out_perm, int32_t *out_keys, void *scratch, cudaStream_t stream);
+
+/* Compaction: gathers the sorted admissions into per-member arrays, finds
+ * each planned batch's offset inside its executor's segment, and checks that
+ * every batch is a single run (one key) -- the head-run/split contract.
+ *   batch_exec/batch_size: [num_batches] in per-executor op order
+ *   out_batch_off: [num_batches]; out_member_req/stage: [n]
+ *   out_run_count: [1] number of distinct runs; out_violations: [1] batches
+ *   spanning more than one run (must be 0). */
+int coe_run_compact(const int32_t *perm, const int32_t *sorted_keys, const int32_t *adm_request,
+                    const int32_t *adm_stage, int64_t n, int rank_bits, const int32_t *batch_exec,
+                    const int32_t *batch_size, int num_batches, int num_executors, int32_t *out_batch_off,
+                    int32_t *out_member_req,
+                    int32_t *out_member_stage, int32_t *out_run_count, int32_t *out_violations, void *scratch,
+                    cudaStream_t stream);
+int64_t coe_run_compact_scratch_bytes(int64_t n, int num_batches, int num_executors);
+
+/* ---------------- K3: grouped expert MLP (tcgen05) ------------------------ */
+
+typedef struct coe_mlp_config {
+  int32_t d, h, T;              /* model dim, hidden dim, rows per request       */
+  void *act0, *act1;            /* ping-pong activations [act_rows, d] bf16      */
+  int64_t act_rows;             /* requests * T                                  */
+  void *h_scratch;              /* [h_rows, h] bf16                              */
+  int64_t h_rows;
+  void *slab;                   /* expert slots: [num_slots][W1 h*d | W2 d*h]    */
+  int32_t num_slots;
+  int64_t slot_stride_bytes;
+} coe_mlp_config;
+
+/* One planned batch inside a wave.  tile_start is the wave-relative prefix of
+ * tiles (ceil(rows/128) * N/256) for the pass the array is used with. */
+typedef struct coe_mlp_group {
+  int32_t rows;        /* members * T                                        */
+  int32_t slot;        /* expert slot holding W1/W2                          */
+  int32_t batch;       /* index into batch_off                               */
+  int32_t h_row;       /* first row of this group in h_scratch               */
+  int32_t tile_start;
+  int32_t pad[3];
+} coe_mlp_group;
+
+typedef struct coe_mlp coe_mlp;
+int coe_mlp_create(const coe_mlp_config *cfg, coe_mlp **out);
+void coe_mlp_destroy(coe_mlp *m);
+int coe_mlp_max_groups(void);
+/* which: bit0 = up projection (gelu(X W1^T) -> H), bit1 = down (H W2^T -> Y). */
+int coe_grouped_mlp(coe_mlp *m, const coe_mlp_group *groups_up, const coe_mlp_group *groups_down, int num_groups,
+                    int tiles_up, int tiles_down, const int32_t *batch_off, const int32_t *member_req,
+                    const int32_t *member_stage, int which, cudaStream_t stream);
+
+/* ---------------- seeded synthetic data ---------------------------------- */
+
+/* Fill n bf16 values with the counter-based uniform generator shared with the
+ * oracle (oracle/synth.py): value(i) = scale * (u(seed, i) - 0.5) * 2. */
+int coe_fill_uniform_bf16(void *dst, int64_t n, uint64_t seed, float scale, cudaStream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* COE_CUDA_H */
