@@ -1,0 +1,136 @@
+"""Generate golden traces / metrics by running the UNMODIFIED reference.
+
+Run in the build container (needs ``/root/reference``):
+
+    python tests/golden/make_golden.py
+
+For every case it imports ``coesim`` from ``/root/reference/pkg/src``, runs
+``engine.Simulation`` on the committed documents and freezes
+``metrics_json`` and ``trace_jsonl`` (engine.py:832-838).  N-stage cases
+(configs 2 and 5) use a one-method subclass overriding ``_on_arrival``
+(engine.py:720-727) so the tail of a route template is taken iff
+``detect_u < branch_prob`` -- SURVEY §0.5.  Large runs store the SHA-256 of
+the trace instead of the full text.  Output: ``tests/golden/<case>.json.gz``.
+"""
+
+from __future__ import annotations
+
+import gzip
+import hashlib
+import json
+import os
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, "/root/reference/pkg/src")
+
+from coesim import engine, workload  # noqa: E402
+from coesim.costmodel import load_device_preset  # noqa: E402
+from coesim.types import DeviceProfile, ModelRegistry  # noqa: E402
+
+CONFIGS = os.path.join(ROOT, "paper_2503_02354_b200", "data", "configs")
+FULL_TRACE_LIMIT = 12000
+
+
+def read(path):
+    opener = gzip.open if path.endswith(".gz") else open
+    with opener(path, "rt") as fh:
+        return json.load(fh)
+
+
+class NStage(engine.Simulation):
+    """Reference engine with N-stage chain templates (only _on_arrival differs)."""
+
+    routes_doc: dict = {}
+
+    def _on_arrival(self, t, req):
+        route = self.routes_doc.get(req.component_type)
+        if route is None:
+            return super()._on_arrival(t, req)
+        experts = list(route["experts"])
+        req.chain = experts if (len(experts) > 1 and req.detect_u < route["branch_prob"]) else experts[:1]
+        self._record(t, None, "arrival", None, req.request_id)
+        self._admit(t, req, follow_up=False)
+
+
+def run_case(registry_doc, device_doc, stream_doc, routes_doc, run):
+    registry = ModelRegistry.from_doc(registry_doc)
+    device = DeviceProfile.from_doc(device_doc)
+    stream = workload.stream_from_doc(stream_doc)
+    cfg = engine.RunConfig(registry=registry, device=device, stream=stream, trace=True, **run)
+    sim_cls = NStage if routes_doc else engine.Simulation
+    if routes_doc:
+        NStage.routes_doc = routes_doc
+    metrics, trace = sim_cls(cfg).run()
+    return engine.metrics_json(metrics), engine.trace_jsonl(trace)
+
+
+def config_case(name, requests, **run_overrides):
+    base = os.path.join(CONFIGS, name)
+    cfg = read(os.path.join(base, "config.json"))
+    routes_path = os.path.join(base, "routes.json")
+    routes = read(routes_path) if os.path.exists(routes_path) else None
+    run = dict(cfg["run"])
+    run.update(run_overrides)
+    if run.get("alloc_override") is None:
+        run.pop("alloc_override", None)
+    inputs = {"config": name, "requests": requests, "run": run}
+    docs = (read(os.path.join(base, "registry.json")), read(os.path.join(base, "device.json")),
+            read(os.path.join(base, f"stream_{requests}.json.gz")), routes)
+    return inputs, docs
+
+
+def inline_case(device_name, components, requests, interarrival, gen_seed, **run):
+    reg = workload.generate_registry(num_components=components, seed=gen_seed)
+    stream = workload.generate_stream(reg, requests, interarrival_s=interarrival, seed=gen_seed)
+    docs = (reg.to_doc(), load_device_preset(device_name).to_doc(), workload.stream_to_doc(stream), None)
+    inputs = {"registry": docs[0], "device": docs[1], "stream": docs[2], "run": dict(run)}
+    return inputs, docs
+
+
+def cases():
+    out = {}
+    out["c1_1k"] = config_case("c1", 1000)
+    out["c2_1k"] = config_case("c2", 1000)
+    out["c3_1k"] = config_case("c3", 1000)
+    out["c3_1k_samba_lru"] = config_case("c3", 1000, policy="samba_lru")
+    out["c3_1k_samba_fifo"] = config_case("c3", 1000, policy="samba_fifo")
+    out["c4_1k_g2"] = config_case("c4", 1000, gpu_executors=2)
+    out["c4_1k_g4"] = config_case("c4", 1000, gpu_executors=4)
+    out["c4_1k_g8"] = config_case("c4", 1000, gpu_executors=8)
+    out["c5_1k_g8"] = config_case("c5", 1000, gpu_executors=8)
+    out["c2_10k"] = config_case("c2", 10000)
+    out["c3_10k"] = config_case("c3", 10000)
+    for policy in ("coserve", "coserve_em_ra", "coserve_em", "coserve_none", "samba_lru", "samba_fifo",
+                   "samba_parallel"):
+        out[f"numa_a80_{policy}"] = inline_case("numa-3080ti", 80, 300, 0.004, 3, policy=policy, seed=3,
+                                                gpu_executors=3, cpu_executors=1, search_enabled=False)
+    out["numa_a80_coserve_search"] = inline_case("numa-3080ti", 80, 300, 0.004, 4, policy="coserve", seed=4,
+                                                 gpu_executors=2, cpu_executors=1, search_enabled=True,
+                                                 search_sample_requests=150)
+    out["uma_a40_coserve"] = inline_case("uma-m2", 40, 200, 0.004, 7, policy="coserve", seed=7,
+                                         gpu_executors=2, cpu_executors=1, search_enabled=False)
+    out["uma_a40_samba_fifo"] = inline_case("uma-m2", 40, 200, 0.004, 7, policy="samba_fifo", seed=7,
+                                            gpu_executors=2, cpu_executors=1, search_enabled=False)
+    return out
+
+
+def main(only=None):
+    for name, (inputs, docs) in cases().items():
+        if only and name not in only:
+            continue
+        metrics_text, trace_text = run_case(*docs, inputs["run"])
+        doc = {"name": name, "inputs": inputs, "metrics_json": metrics_text,
+               "trace_sha256": hashlib.sha256(trace_text.encode()).hexdigest(),
+               "trace_lines": trace_text.count("\n")}
+        if doc["trace_lines"] <= FULL_TRACE_LIMIT:
+            doc["trace_jsonl"] = trace_text
+        path = os.path.join(HERE, f"{name}.json.gz")
+        with gzip.open(path, "wt", compresslevel=9) as fh:
+            json.dump(doc, fh, sort_keys=True)
+        print(f"{name}: {doc['trace_lines']} trace lines, {os.path.getsize(path) / 1024:.0f} KiB")
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:] or None)
