@@ -62,7 +62,8 @@ int64_t coe_run_compact_scratch_bytes(int64_t n, int num_batches, int num_execut
 
 typedef struct coe_mlp_config {
   int32_t d, h, T;              /* model dim, hidden dim, rows per request       */
-  void *act0, *act1;            /* ping-pong activations [act_rows, d] bf16      */
+  void *x;                      /* request inputs (stage 0) [act_rows, d] bf16   */
+  void *act0, *act1;            /* stage s>0 reads act[(s-1)&1], writes act[s&1] */
   int64_t act_rows;             /* requests * T                                  */
   void *h_scratch;              /* [h_rows, h] bf16                              */
   int64_t h_rows;
@@ -90,6 +91,78 @@ int coe_mlp_max_groups(void);
 int coe_grouped_mlp(coe_mlp *m, const coe_mlp_group *groups_up, const coe_mlp_group *groups_down, int num_groups,
                     int tiles_up, int tiles_down, const int32_t *batch_off, const int32_t *member_req,
                     const int32_t *member_stage, int which, cudaStream_t stream);
+
+/* ---------------- GPU serving runtime (one executor per GPU) --------------- */
+
+/* The physical half of the serving path: executes the planner's op log for
+ * one executor -- GPU grouping (K1/K2) of the step's admissions, waves of
+ * grouped expert MLPs (K3) on the compute stream, swap-ins (K4) from the
+ * pinned host expert store into fixed HBM slots on a copy-engine stream,
+ * issued as soon as the victim slot's last wave has finished (dependency-
+ * aware prefetch).  Decisions are never changed by physical timing. */
+typedef struct coe_runtime_config {
+  int32_t d, h, T;
+  int32_t num_experts;
+  int32_t num_slots;        /* HBM expert slots = expert budget / expert bytes       */
+  int32_t max_requests;     /* capacity of the X / P0 / P1 activation buffers        */
+  int64_t max_wave_rows;    /* rows of the H scratch (caps a wave)                   */
+  int64_t max_admissions;
+  int64_t max_batches;
+  uint64_t weight_seed;     /* synthetic expert weights, see coe_expert_seed         */
+  int32_t profile;          /* record per-copy / per-wave events for overlap stats   */
+} coe_runtime_config;
+
+typedef struct coe_step_input {
+  int32_t executor;                         /* ops / admissions of other executors ignored */
+  int64_t num_admissions;
+  const void *admissions;                   /* coe_admission[] (coe_planner.h)            */
+  int64_t num_ops;
+  const void *ops;                          /* coe_op[] (coe_planner.h)                   */
+  int64_t num_op_args;
+  const int32_t *op_args;
+  int32_t num_initial;                      /* initial residency of this executor          */
+  const int32_t *initial;
+} coe_step_input;
+
+typedef struct coe_step_stats {
+  int64_t admissions, batches, waves, launches;
+  int64_t loads, load_bytes, restores, restore_bytes;
+  int64_t max_wave_rows;
+  int32_t max_wave_groups;
+  int32_t rank_bits;
+} coe_step_stats;
+
+typedef struct coe_step_timing {
+  float total_ms;           /* step start -> both streams drained                    */
+  float copy_busy_ms;       /* union of swap-in copy intervals                        */
+  float compute_busy_ms;    /* union of wave intervals (grouping included)           */
+  float overlap_ms;         /* intersection of the two                               */
+  float mlp_ms;             /* sum of K3 wave durations                              */
+  float group_ms;           /* K1 + K2                                                */
+} coe_step_timing;
+
+typedef struct coe_runtime coe_runtime;
+int coe_runtime_create(const coe_runtime_config *cfg, coe_runtime **out);
+void coe_runtime_destroy(coe_runtime *rt);
+/* generate every expert's W1/W2 on the GPU and stage them in the pinned host store */
+int coe_runtime_init_experts(coe_runtime *rt);
+/* seeded request inputs straight into the device X buffer (device-resident runs) */
+int coe_runtime_fill_inputs(coe_runtime *rt, uint64_t seed, int32_t num_requests);
+/* host (pinned) -> X for the first num_requests requests, on the compute stream */
+int coe_runtime_upload_inputs(coe_runtime *rt, const void *host, int32_t num_requests);
+int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_step_stats *stats);
+/* gather each request's final activation (stage last_stage[r]) and copy to host */
+int coe_runtime_download_outputs(coe_runtime *rt, const int32_t *last_stage_host, int32_t num_requests, void *host);
+int coe_runtime_synchronize(coe_runtime *rt);
+/* after synchronize: K2 run count / violations, and the grouped members */
+int coe_runtime_check(coe_runtime *rt, int32_t *runs, int32_t *violations);
+int coe_runtime_members(coe_runtime *rt, int32_t *member_req, int32_t *member_stage, int32_t *batch_off);
+int coe_runtime_timing(coe_runtime *rt, coe_step_timing *out);
+/* device pointers (tests / benches): 0 X, 1 P0, 2 P1, 3 H scratch, 4 slot slab */
+void *coe_runtime_buffer(coe_runtime *rt, int which);
+int coe_runtime_slot_of(coe_runtime *rt, int32_t expert);
+cudaStream_t coe_runtime_stream(coe_runtime *rt, int which);
+uint64_t coe_expert_seed(uint64_t weight_seed, int32_t expert, int32_t matrix);
 
 /* ---------------- seeded synthetic data ---------------------------------- */
 

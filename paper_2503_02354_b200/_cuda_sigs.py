@@ -9,7 +9,7 @@ from ctypes import POINTER, c_char_p, c_float, c_int, c_int32, c_int64, c_uint64
 class MlpConfig(ctypes.Structure):
     _fields_ = [
         ("d", c_int32), ("h", c_int32), ("T", c_int32),
-        ("act0", c_void_p), ("act1", c_void_p), ("act_rows", c_int64),
+        ("x", c_void_p), ("act0", c_void_p), ("act1", c_void_p), ("act_rows", c_int64),
         ("h_scratch", c_void_p), ("h_rows", c_int64),
         ("slab", c_void_p), ("num_slots", c_int32), ("slot_stride_bytes", c_int64),
     ]

@@ -8,9 +8,9 @@
 //   mode 0 (up):   H[g]   = gelu(X[g] . W1[slot_g]^T)   X rows gathered per request
 //   mode 1 (down): Y[g]   = H[g] . W2[slot_g]^T          Y rows scattered per request
 //
-// X/Y live in two ping-pong activation buffers [requests*T, d]; a request at
-// chain stage s reads buffer s&1 and its next stage's input is written to
-// buffer (s+1)&1.  Which requests form a group comes from the GPU grouping
+// Activations are [requests*T, d] row blocks: stage 0 reads the request
+// inputs X, stage s > 0 reads ping-pong buffer P[(s-1)&1]; the output of stage
+// s is written to P[s&1] (so X stays pristine across steps).  Which requests form a group comes from the GPU grouping
 // (coe_group_sort / coe_run_compact): member_req/member_stage are the sorted
 // admissions and batch_off the start of each planned batch inside them.
 //
@@ -67,6 +67,9 @@ struct GemmArgs {
   __nv_bfloat16 *out_act1;
 };
 
+// A-operand source of a member at chain stage s: 0 = X, 1 = P0, 2 = P1.
+__device__ __forceinline__ int a_source(int stage) { return stage == 0 ? 0 : 1 + ((stage - 1) & 1); }
+
 __device__ __forceinline__ float gelu_tanh(float x) {
   float u = 0.7978845608028654f * (x + 0.044715f * x * x * x);
   float t;
@@ -103,7 +106,8 @@ __device__ __forceinline__ TileCoord decode_tile(int t, const int32_t *tile_star
 
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tm_a0, const __grid_constant__ CUtensorMap tm_a1,
-                        const __grid_constant__ CUtensorMap tm_b, GemmArgs args) {
+                        const __grid_constant__ CUtensorMap tm_a2, const __grid_constant__ CUtensorMap tm_b,
+                        GemmArgs args) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *stage_base = smem;
@@ -121,6 +125,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp == 0 && lane == 0) {
     sm100::prefetch_tmap(&tm_a0);
     sm100::prefetch_tmap(&tm_a1);
+    sm100::prefetch_tmap(&tm_a2);
     sm100::prefetch_tmap(&tm_b);
     for (int s = 0; s < STAGES; ++s) {
       sm100::mbar_init(&full_bar[s], 1);
@@ -161,7 +166,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             int j = r / args.T;
             int req = args.member_req[boff + j];
             box_row[b] = req * args.T + (r - j * args.T);
-            box_par[b] = args.member_stage[boff + j] & 1;
+            box_par[b] = a_source(args.member_stage[boff + j]);
           }
           a_bytes = (uint32_t)(nboxes * args.a_box_rows * BK * 2);
         } else {
@@ -176,7 +181,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           uint8_t *sb = sa + A_BYTES;
           sm100::mbar_arrive_expect_tx(&full_bar[stage], a_bytes + B_BYTES);
           for (int b = 0; b < nboxes; ++b)
-            sm100::tma_load_2d(sa + b * args.a_box_rows * 128, box_par[b] ? &tm_a1 : &tm_a0, &full_bar[stage],
+            sm100::tma_load_2d(sa + b * args.a_box_rows * 128,
+                               box_par[b] == 0 ? &tm_a0 : (box_par[b] == 1 ? &tm_a1 : &tm_a2), &full_bar[stage],
                                kb * BK, box_row[b]);
           sm100::tma_load_3d(sb, &tm_b, &full_bar[stage], kb * BK, c.n_blk * BN, grp.slot);
           if (++stage == STAGES) {
@@ -241,7 +247,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const int j = row / args.T;
           const int req = args.member_req[boff + j];
           const int st = args.member_stage[boff + j];
-          __nv_bfloat16 *dst = ((st + 1) & 1) ? args.out_act1 : args.out_act0;
+          __nv_bfloat16 *dst = (st & 1) ? args.out_act1 : args.out_act0;
           out_row = dst + ((size_t)req * args.T + (row - j * args.T)) * args.N;
         }
         out_row += c.n_blk * BN;
@@ -337,7 +343,7 @@ bool make_map_3d(CUtensorMap *map, void *base, uint64_t slots, uint64_t rows, ui
 
 struct coe_mlp {
   coe_mlp_config cfg;
-  CUtensorMap act0, act1, hmap, hmap_dummy, w1, w2;
+  CUtensorMap xmap, act0, act1, hmap, w1, w2;
   int num_sms;
   int a_box_rows;
 };
@@ -357,6 +363,7 @@ int coe_mlp_create(const coe_mlp_config *cfg, coe_mlp **out) {
   m->cfg = *cfg;
   m->a_box_rows = cfg->T < BM ? cfg->T : BM;
   bool ok = true;
+  ok &= make_map_2d(&m->xmap, cfg->x, (uint64_t)cfg->act_rows, cfg->d, m->a_box_rows);
   ok &= make_map_2d(&m->act0, cfg->act0, (uint64_t)cfg->act_rows, cfg->d, m->a_box_rows);
   ok &= make_map_2d(&m->act1, cfg->act1, (uint64_t)cfg->act_rows, cfg->d, m->a_box_rows);
   ok &= make_map_2d(&m->hmap, cfg->h_scratch, (uint64_t)cfg->h_rows, cfg->h, BM);
@@ -416,9 +423,9 @@ int coe_grouped_mlp(coe_mlp *m, const coe_mlp_group *groups_up, const coe_mlp_gr
     if (a.total_tiles <= 0) continue;
     int grid = a.total_tiles < m->num_sms ? a.total_tiles : m->num_sms;
     if (pass == 0)
-      grouped_gemm_kernel<<<grid, NUM_THREADS, SMEM_BYTES, stream>>>(m->act0, m->act1, m->w1, a);
+      grouped_gemm_kernel<<<grid, NUM_THREADS, SMEM_BYTES, stream>>>(m->xmap, m->act0, m->act1, m->w1, a);
     else
-      grouped_gemm_kernel<<<grid, NUM_THREADS, SMEM_BYTES, stream>>>(m->hmap, m->hmap, m->w2, a);
+      grouped_gemm_kernel<<<grid, NUM_THREADS, SMEM_BYTES, stream>>>(m->hmap, m->hmap, m->hmap, m->w2, a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
       coe_set_error(std::string("grouped_gemm_kernel launch: ") + cudaGetErrorString(e));

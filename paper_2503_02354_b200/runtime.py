@@ -1,0 +1,252 @@
+"""Host-side driver of the B200 serving runtime (``libcoe_cuda.so``).
+
+``B200Runtime`` owns one executor's GPU state: the fixed-budget HBM expert
+cache (slots), the pinned host expert store, activation buffers and the
+compute / copy streams.  ``step(plan)`` hands the native planner's op log
+(``engine.Plan``) to ``coe_runtime_step`` zero-copy; everything after that is
+stream-ordered GPU work (K1 group sort, K2 compaction, K3 grouped MLP waves,
+K4 swap-ins).  There is no CPU fallback: constructing a runtime without the
+CUDA library or a GPU raises.
+
+Reference seams: the *device* seam of ``CostModel``
+(costmodel.py:39-92) gains physical ``execute`` / ``swap_in`` behaviour here,
+while the numeric returns of the cost model keep driving decisions.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from ._cuda_sigs import check as _check
+
+DEFAULT_WEIGHT_SEED = 0xC0E5E4E
+DEFAULT_INPUT_SEED = 0x1A7E5
+
+
+class StepInput(ctypes.Structure):
+    _fields_ = [
+        ("executor", ctypes.c_int32),
+        ("num_admissions", ctypes.c_int64), ("admissions", ctypes.c_void_p),
+        ("num_ops", ctypes.c_int64), ("ops", ctypes.c_void_p),
+        ("num_op_args", ctypes.c_int64), ("op_args", ctypes.c_void_p),
+        ("num_initial", ctypes.c_int32), ("initial", ctypes.c_void_p),
+    ]
+
+
+class StepStats(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int64) for n in ("admissions", "batches", "waves", "launches", "loads", "load_bytes",
+                                               "restores", "restore_bytes", "max_wave_rows")] + \
+               [("max_wave_groups", ctypes.c_int32), ("rank_bits", ctypes.c_int32)]
+
+    def as_dict(self) -> dict:
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+class StepTiming(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_float) for n in ("total_ms", "copy_busy_ms", "compute_busy_ms", "overlap_ms", "mlp_ms",
+                                               "group_ms")]
+
+    def as_dict(self) -> dict:
+        return {name: float(getattr(self, name)) for name, _ in self._fields_}
+
+
+class RuntimeConfig(ctypes.Structure):
+    _fields_ = [("d", ctypes.c_int32), ("h", ctypes.c_int32), ("T", ctypes.c_int32),
+                ("num_experts", ctypes.c_int32), ("num_slots", ctypes.c_int32), ("max_requests", ctypes.c_int32),
+                ("max_wave_rows", ctypes.c_int64), ("max_admissions", ctypes.c_int64),
+                ("max_batches", ctypes.c_int64), ("weight_seed", ctypes.c_uint64), ("profile", ctypes.c_int32)]
+
+
+_declared = False
+
+
+def _lib():
+    global _declared
+    lib = _native.cuda_lib()
+    if not _declared:
+        P, V, I32, I64 = ctypes.POINTER, ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+        lib.coe_runtime_create.argtypes = [P(RuntimeConfig), P(V)]
+        lib.coe_runtime_destroy.argtypes = [V]
+        lib.coe_runtime_destroy.restype = None
+        lib.coe_runtime_init_experts.argtypes = [V]
+        lib.coe_runtime_fill_inputs.argtypes = [V, ctypes.c_uint64, I32]
+        lib.coe_runtime_upload_inputs.argtypes = [V, V, I32]
+        lib.coe_runtime_step.argtypes = [V, P(StepInput), P(StepStats)]
+        lib.coe_runtime_download_outputs.argtypes = [V, V, I32, V]
+        lib.coe_runtime_synchronize.argtypes = [V]
+        lib.coe_runtime_check.argtypes = [V, P(I32), P(I32)]
+        lib.coe_runtime_members.argtypes = [V, V, V, V]
+        lib.coe_runtime_timing.argtypes = [V, P(StepTiming)]
+        lib.coe_runtime_buffer.argtypes = [V, ctypes.c_int]
+        lib.coe_runtime_buffer.restype = V
+        lib.coe_runtime_slot_of.argtypes = [V, I32]
+        lib.coe_runtime_stream.argtypes = [V, ctypes.c_int]
+        lib.coe_runtime_stream.restype = V
+        lib.coe_expert_seed.argtypes = [ctypes.c_uint64, I32, I32]
+        lib.coe_expert_seed.restype = ctypes.c_uint64
+        for name in ("coe_runtime_create", "coe_runtime_init_experts", "coe_runtime_fill_inputs",
+                     "coe_runtime_upload_inputs", "coe_runtime_step", "coe_runtime_download_outputs",
+                     "coe_runtime_synchronize", "coe_runtime_check", "coe_runtime_members", "coe_runtime_timing",
+                     "coe_runtime_slot_of"):
+            getattr(lib, name).restype = ctypes.c_int
+        _declared = True
+    return lib
+
+
+def expert_seed(weight_seed: int, expert: int, matrix: int) -> int:
+    return int(_lib().coe_expert_seed(weight_seed, expert, matrix))
+
+
+@dataclass
+class RuntimeShape:
+    d: int
+    h: int
+    T: int
+
+    @property
+    def expert_bytes(self) -> int:
+        return 2 * self.d * self.h * 2
+
+
+def shape_of(workload) -> RuntimeShape:
+    shapes = set(workload.shapes.values())
+    if len(shapes) != 1:
+        raise NotImplementedError(
+            f"{workload.name}: the single-shape runtime serves one (d, h, T) per executor, got {sorted(shapes)}")
+    d, h, T = shapes.pop()
+    return RuntimeShape(d, h, T)
+
+
+class B200Runtime:
+    """One executor's GPU serving state (see module docstring)."""
+
+    def __init__(self, shape: RuntimeShape, num_experts: int, num_slots: int, max_requests: int,
+                 max_admissions: int, max_wave_rows: int | None = None, weight_seed: int = DEFAULT_WEIGHT_SEED,
+                 profile: bool = False, init_experts: bool = True):
+        import torch
+
+        if not torch.cuda.is_available():
+            raise RuntimeError("B200Runtime needs a CUDA device (no CPU fallback)")
+        torch.cuda.init()
+        self.lib = _lib()
+        self.shape = shape
+        self.num_experts = num_experts
+        self.num_slots = num_slots
+        self.max_requests = max_requests
+        self.weight_seed = weight_seed
+        rows = max_wave_rows or max(128, min(32768, max_admissions * shape.T))
+        cfg = RuntimeConfig(shape.d, shape.h, shape.T, num_experts, num_slots, max_requests, rows, max_admissions,
+                            max_admissions, weight_seed, 1 if profile else 0)
+        self.profile = profile
+        self.handle = ctypes.c_void_p()
+        _check(self.lib, self.lib.coe_runtime_create(ctypes.byref(cfg), ctypes.byref(self.handle)), "runtime create")
+        if init_experts:
+            _check(self.lib, self.lib.coe_runtime_init_experts(self.handle), "init experts")
+
+    @classmethod
+    def for_plan(cls, plan, shape: RuntimeShape, executor: int = 0, **kw) -> "B200Runtime":
+        """Size a runtime for a resolved plan: slots = expert budget / expert bytes."""
+        resolved = plan.resolved
+        proc, budget, _inf, _k = resolved.executors[executor]
+        if proc != "gpu":
+            raise ValueError("B200Runtime serves gpu executors only")
+        # slot count follows the planner's byte budget (ModelPool, expert_pool.py:27-59); the
+        # physical slot size is the shape's (equal to param_bytes for the committed configs)
+        largest = max(spec.param_bytes for spec in resolved.config.registry.experts.values())
+        slots = min(int(budget // largest), len(resolved.expert_ids))
+        adm = sum(len(c) for c in resolved.chains)
+        return cls(shape, len(resolved.expert_ids), max(1, slots), len(resolved.request_ids), adm, **kw)
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            self.lib.coe_runtime_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- data --------------------------------------------------------------
+    def fill_inputs(self, num_requests: int, seed: int = DEFAULT_INPUT_SEED) -> None:
+        _check(self.lib, self.lib.coe_runtime_fill_inputs(self.handle, seed, num_requests), "fill inputs")
+
+    def upload_inputs(self, host_ptr: int, num_requests: int) -> None:
+        _check(self.lib, self.lib.coe_runtime_upload_inputs(self.handle, host_ptr, num_requests), "upload")
+
+    def download_outputs(self, last_stage: np.ndarray, host_ptr: int) -> None:
+        last = np.ascontiguousarray(last_stage, dtype=np.int32)
+        _check(self.lib, self.lib.coe_runtime_download_outputs(self.handle, last.ctypes.data, len(last), host_ptr),
+               "download")
+
+    def buffer(self, which: int) -> int:
+        return int(self.lib.coe_runtime_buffer(self.handle, which) or 0)
+
+    def stream_handle(self, which: int = 0) -> int:
+        return int(self.lib.coe_runtime_stream(self.handle, which) or 0)
+
+    # -- execution ---------------------------------------------------------
+    def step(self, plan, executor: int = 0) -> dict:
+        lib = plan.lib
+        h = plan.handle
+        init = np.ascontiguousarray(plan.initial_residency()[executor], dtype=np.int32)
+        self._init_keep = init
+        inp = StepInput(
+            executor,
+            lib.coe_plan_num_admissions(h), ctypes.cast(lib.coe_plan_admissions(h), ctypes.c_void_p),
+            lib.coe_plan_num_ops(h), ctypes.cast(lib.coe_plan_ops(h), ctypes.c_void_p),
+            lib.coe_plan_num_op_args(h), ctypes.cast(lib.coe_plan_op_args(h), ctypes.c_void_p),
+            len(init), init.ctypes.data if len(init) else None,
+        )
+        stats = StepStats()
+        _check(self.lib, self.lib.coe_runtime_step(self.handle, ctypes.byref(inp), ctypes.byref(stats)), "step")
+        return stats.as_dict()
+
+    def synchronize(self) -> None:
+        _check(self.lib, self.lib.coe_runtime_synchronize(self.handle), "synchronize")
+
+    def check(self) -> tuple:
+        runs, viol = ctypes.c_int32(), ctypes.c_int32()
+        _check(self.lib, self.lib.coe_runtime_check(self.handle, ctypes.byref(runs), ctypes.byref(viol)), "check")
+        return runs.value, viol.value
+
+    def members(self, num_admissions: int, num_batches: int):
+        req = np.zeros(max(1, num_admissions), np.int32)
+        stage = np.zeros(max(1, num_admissions), np.int32)
+        boff = np.zeros(max(1, num_batches), np.int32)
+        _check(self.lib, self.lib.coe_runtime_members(self.handle, req.ctypes.data, stage.ctypes.data,
+                                                      boff.ctypes.data), "members")
+        return req[:num_admissions], stage[:num_admissions], boff[:num_batches]
+
+    def timing(self) -> dict:
+        t = StepTiming()
+        _check(self.lib, self.lib.coe_runtime_timing(self.handle, ctypes.byref(t)), "timing")
+        return t.as_dict()
+
+
+def batches_from_plan(plan, executor: int = 0) -> list:
+    """(expert, [(request, stage), ...]) per planned batch of ``executor``, in op order."""
+    ops = plan.ops()
+    args = plan.op_args()
+    out = []
+    for op in ops:
+        if op["executor"] != executor or op["kind"] != _native.OP_BATCH:
+            continue
+        o, n = int(op["offset"]), int(op["count"])
+        pairs = args[o:o + 2 * n].reshape(n, 2)
+        out.append((int(op["expert"]), [(int(r), int(s)) for r, s in pairs]))
+    return out
+
+
+def last_stages(plan) -> np.ndarray:
+    return np.array([len(c) - 1 for c in plan.resolved.chains], dtype=np.int32)
+
+
+def env_flag(name: str, default: str = "0") -> bool:
+    return os.environ.get(name, default) not in ("0", "", "false", "False")
