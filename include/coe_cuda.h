@@ -160,6 +160,8 @@ int coe_runtime_members(coe_runtime *rt, int32_t *member_req, int32_t *member_st
 int coe_runtime_timing(coe_runtime *rt, coe_step_timing *out);
 /* device pointers (tests / benches): 0 X, 1 P0, 2 P1, 3 H scratch, 4 slot slab */
 void *coe_runtime_buffer(coe_runtime *rt, int which);
+/* synchronous device -> host copy of the first `bytes` of buffer `which` */
+int coe_runtime_read_buffer(coe_runtime *rt, int which, void *host, int64_t bytes);
 int coe_runtime_slot_of(coe_runtime *rt, int32_t expert);
 cudaStream_t coe_runtime_stream(coe_runtime *rt, int which);
 uint64_t coe_expert_seed(uint64_t weight_seed, int32_t expert, int32_t matrix);

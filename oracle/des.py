@@ -481,6 +481,7 @@ class _Run:
             x["busy"] = True
             x["busy_s"] += lat
             self.loads.append((x["id"], eid, victims, tier))
+            self.ops.append(("load", x["id"], eid, list(victims)))
             self._rec(t, x["id"], "load", eid, None)
             self._push(t + lat, "load_done", x["id"])
             return
@@ -501,6 +502,7 @@ class _Run:
         x["busy"] = True
         x["busy_s"] += dur
         self.batches.append((x["id"], eid, [(e[0], e[7]) for e in batch]))
+        self.ops.append(("batch", x["id"], eid, [(e[0], e[7]) for e in batch]))
         self._rec(t, x["id"], "batch_start", eid, None)
         self._push(t + dur, "batch_done", (x["id"], len(batch), eid))
 
@@ -552,7 +554,7 @@ class _Run:
     def run(self):
         self._initial()
         self.heap, self.seq, self.trace = [], 0, []
-        self.batches, self.loads = [], []
+        self.batches, self.loads, self.ops = [], [], []
         self.completed = self.fu_made = self.fu_done = self.evictions = self.stale = 0
         self.last = 0.0
         for rid in self.requests:
@@ -592,7 +594,7 @@ class _Run:
             "per_executor": per, "alloc": {p: self.alloc[p] for p in sorted(self.alloc)},
         }
         return {"metrics": metrics, "trace": self.trace, "batches": self.batches, "loads": self.loads,
-                "initial": self.initial}
+                "ops": self.ops, "initial": self.initial}
 
 
 DEFAULTS = {

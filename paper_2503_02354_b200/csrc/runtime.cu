@@ -310,6 +310,16 @@ void *coe_runtime_buffer(coe_runtime *rt, int which) {
 
 cudaStream_t coe_runtime_stream(coe_runtime *rt, int which) { return which == 0 ? rt->compute : rt->copy; }
 
+int coe_runtime_read_buffer(coe_runtime *rt, int which, void *host, int64_t bytes) {
+  void *src = coe_runtime_buffer(rt, which);
+  if (!src || which == 5) {
+    coe_set_error("read_buffer: not a device buffer");
+    return COE_CUDA_ERR_CONFIG;
+  }
+  if (!ok(cudaStreamSynchronize(rt->compute), "read_buffer sync")) return fail_cuda();
+  return ok(cudaMemcpy(host, src, (size_t)bytes, cudaMemcpyDeviceToHost), "read_buffer") ? COE_CUDA_OK : fail_cuda();
+}
+
 int coe_runtime_slot_of(coe_runtime *rt, int32_t expert) {
   if (expert < 0 || expert >= (int32_t)rt->expert_slot.size()) return -1;
   return rt->expert_slot[expert];

@@ -85,6 +85,8 @@ def _lib():
         lib.coe_runtime_buffer.argtypes = [V, ctypes.c_int]
         lib.coe_runtime_buffer.restype = V
         lib.coe_runtime_slot_of.argtypes = [V, I32]
+        lib.coe_runtime_read_buffer.argtypes = [V, ctypes.c_int, V, I64]
+        lib.coe_runtime_read_buffer.restype = ctypes.c_int
         lib.coe_runtime_stream.argtypes = [V, ctypes.c_int]
         lib.coe_runtime_stream.restype = V
         lib.coe_expert_seed.argtypes = [ctypes.c_uint64, I32, I32]
@@ -187,6 +189,9 @@ class B200Runtime:
 
     def buffer(self, which: int) -> int:
         return int(self.lib.coe_runtime_buffer(self.handle, which) or 0)
+
+    def read_buffer(self, which: int, host_ptr: int, nbytes: int) -> None:
+        _check(self.lib, self.lib.coe_runtime_read_buffer(self.handle, which, host_ptr, nbytes), "read buffer")
 
     def stream_handle(self, which: int = 0) -> int:
         return int(self.lib.coe_runtime_stream(self.handle, which) or 0)
