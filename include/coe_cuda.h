@@ -87,10 +87,11 @@ typedef struct coe_mlp coe_mlp;
 int coe_mlp_create(const coe_mlp_config *cfg, coe_mlp **out);
 void coe_mlp_destroy(coe_mlp *m);
 int coe_mlp_max_groups(void);
-/* which: bit0 = up projection (gelu(X W1^T) -> H), bit1 = down (H W2^T -> Y). */
+/* which: bit0 = up projection (gelu(X W1^T) -> H), bit1 = down (H W2^T -> Y).
+ * max_ctas: persistent grid cap (0 = one CTA per SM). */
 int coe_grouped_mlp(coe_mlp *m, const coe_mlp_group *groups_up, const coe_mlp_group *groups_down, int num_groups,
                     int tiles_up, int tiles_down, const int32_t *batch_off, const int32_t *member_req,
-                    const int32_t *member_stage, int which, cudaStream_t stream);
+                    const int32_t *member_stage, int which, int max_ctas, cudaStream_t stream);
 
 /* ---------------- GPU serving runtime (one executor per GPU) --------------- */
 
@@ -110,6 +111,7 @@ typedef struct coe_runtime_config {
   int64_t max_batches;
   uint64_t weight_seed;     /* synthetic expert weights, see coe_expert_seed         */
   int32_t profile;          /* record per-copy / per-wave events for overlap stats   */
+  int32_t reserve_sms;      /* SMs kept for the swap-in-gating waves (0: no split)   */
 } coe_runtime_config;
 
 typedef struct coe_step_input {
@@ -158,6 +160,10 @@ int coe_runtime_synchronize(coe_runtime *rt);
 int coe_runtime_check(coe_runtime *rt, int32_t *runs, int32_t *violations);
 int coe_runtime_members(coe_runtime *rt, int32_t *member_req, int32_t *member_stage, int32_t *batch_off);
 int coe_runtime_timing(coe_runtime *rt, coe_step_timing *out);
+/* profile mode: per-copy [start,end) and per-wave [start,end) ms since step start,
+ * wave_info = (stream class, rows, groups) per wave; sizes from coe_runtime_counts */
+int coe_runtime_counts(coe_runtime *rt, int32_t *copies, int32_t *waves);
+int coe_runtime_intervals(coe_runtime *rt, float *copy_iv, float *wave_iv, int32_t *wave_info);
 /* device pointers (tests / benches): 0 X, 1 P0, 2 P1, 3 H scratch, 4 slot slab */
 void *coe_runtime_buffer(coe_runtime *rt, int which);
 /* synchronous device -> host copy of the first `bytes` of buffer `which` */

@@ -39,7 +39,7 @@ def declare(lib: ctypes.CDLL) -> None:
     lib.coe_mlp_max_groups.argtypes = []
     lib.coe_mlp_max_groups.restype = c_int
     lib.coe_grouped_mlp.argtypes = [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p,
-                                    c_int, c_void_p]
+                                    c_int, c_int, c_void_p]
     lib.coe_grouped_mlp.restype = c_int
     lib.coe_fill_uniform_bf16.argtypes = [c_void_p, c_int64, c_uint64, c_float, c_void_p]
     lib.coe_fill_uniform_bf16.restype = c_int

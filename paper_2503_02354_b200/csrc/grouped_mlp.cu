@@ -395,7 +395,7 @@ int coe_mlp_max_groups(void) { return MAX_GROUPS; }
 
 int coe_grouped_mlp(coe_mlp *m, const coe_mlp_group *groups_up, const coe_mlp_group *groups_down, int num_groups,
                     int tiles_up, int tiles_down, const int32_t *batch_off, const int32_t *member_req,
-                    const int32_t *member_stage, int which, cudaStream_t stream) {
+                    const int32_t *member_stage, int which, int max_ctas, cudaStream_t stream) {
   if (num_groups <= 0) return COE_CUDA_OK;
   if (num_groups > MAX_GROUPS) {
     coe_set_error("too many groups in one wave");
@@ -421,7 +421,8 @@ int coe_grouped_mlp(coe_mlp *m, const coe_mlp_group *groups_up, const coe_mlp_gr
     a.out_act0 = reinterpret_cast<__nv_bfloat16 *>(c.act0);
     a.out_act1 = reinterpret_cast<__nv_bfloat16 *>(c.act1);
     if (a.total_tiles <= 0) continue;
-    int grid = a.total_tiles < m->num_sms ? a.total_tiles : m->num_sms;
+    int cap = (max_ctas > 0 && max_ctas < m->num_sms) ? max_ctas : m->num_sms;
+    int grid = a.total_tiles < cap ? a.total_tiles : cap;
     if (pass == 0)
       grouped_gemm_kernel<<<grid, NUM_THREADS, SMEM_BYTES, stream>>>(m->xmap, m->act0, m->act1, m->w1, a);
     else

@@ -5,24 +5,27 @@
 // /root/reference/pkg/src/coesim/engine.py:643-758); here the same op log is
 // *executed*:
 //
-//   compute stream: upload the step's admissions -> K1 group sort -> K2 run
-//                   compaction -> waves of K3 grouped expert MLPs
-//   copy stream:    K4 swap-ins, pinned host expert store -> HBM slot,
-//                   each issued as soon as its slot's last wave completed
+//   copy stream:    the step's plan upload, then K4 swap-ins (pinned host
+//                   expert store -> HBM slot), each half of an expert (W1 |
+//                   W2) issued as soon as the slot's last reader of that half
+//                   has finished -- dependency-aware prefetch
+//   compute stream: K1 group sort -> K2 run compaction -> waves of K3 grouped
+//                   expert MLPs; a wave's up-projection waits only for the W1
+//                   halves it needs, its down-projection for the W2 halves
 //
-// Physical layout (HBM): a slab of `num_slots` fixed expert slots
-// ([W1 h*d | W2 d*h] bf16 each; budget/bytes of the planner's ModelPool), the
-// request inputs X, two ping-pong activation buffers P0/P1, the H scratch of
-// the current wave, and small grouping arrays.  Host: one pinned store of
-// every expert (the "host tier", types.py:17).
+// Physical layout (HBM): `num_slots` fixed expert slots ([W1 h*d | W2 d*h]
+// bf16; the planner's ModelPool budget / expert bytes), the request inputs X,
+// ping-pong activations P0/P1, the H scratch of a wave, double-buffered step
+// arrays.  Host: one pinned store of every expert (the host tier, types.py:17).
 //
 // Host pass 1 turns the op log into actions (COPY / WAVE): slot assignment
 // (victim slots are reused; initial-residency experts missing after the
 // previous step are restored lazily, at first use, so a step always starts
 // from initialize_pools' placement), wave cuts (a wave closes before a batch
 // that must wait for a copy, that touches a request already in the wave, or
-// that overflows the H scratch; and before a copy into a slot the open wave
-// still reads).  Pass 2 issues them.  Timing never feeds back into decisions.
+// that overflows the H scratch; a batch that is the last reader of a slot
+// some later LOAD overwrites runs as its own wave, so that swap-in waits for
+// nothing else).  Pass 2 issues them.  Timing never feeds back into decisions.
 
 #include <cuda_bf16.h>
 
@@ -51,8 +54,7 @@ uint64_t splitmix64_host(uint64_t z) {
 
 __global__ void gather_outputs(const __nv_bfloat16 *p0, const __nv_bfloat16 *p1, const int32_t *last_stage,
                                int32_t num_requests, int64_t row_elems, __nv_bfloat16 *out) {
-  // one block per request; 16-byte vectors
-  int32_t r = blockIdx.x;
+  int32_t r = blockIdx.x;  // one block per request, 16-byte vectors
   if (r >= num_requests) return;
   const __nv_bfloat16 *src = (last_stage[r] & 1) ? p1 : p0;
   const uint4 *s = reinterpret_cast<const uint4 *>(src + r * row_elems);
@@ -63,17 +65,21 @@ __global__ void gather_outputs(const __nv_bfloat16 *p0, const __nv_bfloat16 *p1,
 struct CopyAct {
   int32_t expert;
   int32_t slot;
-  int32_t wait_wave;  // wave whose completion frees the slot (-1: none this step)
+  int32_t wait_wave;     // last wave of this step reading the slot (-1: none)
+  bool wait_prev_step;   // first write of the slot this step: wait for last step's readers
   bool restore;
 };
 
 struct WaveAct {
+  int32_t cls;  // 0: main compute stream, 1: swap-in (high priority) stream
   int32_t first_group;
   int32_t num_groups;
   int32_t tiles_up;
   int32_t tiles_down;
   int64_t rows;
-  std::vector<int32_t> wait_copies;
+  std::vector<int32_t> wait_copies;  // W1 event before the up pass, W2 before the down pass
+  std::vector<int32_t> wait_waves;   // other-stream waves producing this wave's inputs
+  std::vector<int32_t> frees_slots;  // slots whose last reader this step is this wave
 };
 
 struct Action {
@@ -87,65 +93,86 @@ bool ok(cudaError_t e, const char *what) { return coe_cuda_ok(e, what); }
 
 void coe_set_error(const std::string &msg) { g_last_error = msg; }
 
+struct StepBuffers {  // device arrays one step uses; two sets alternate
+  int32_t *adm = nullptr;   // [4][max_adm]: exec, rank, req, stage
+  int32_t *batch = nullptr; // [2][max_batches]: exec, size
+  int32_t *boff = nullptr;
+  int32_t *mreq = nullptr, *mstage = nullptr;
+  coe_mlp_group *groups = nullptr;  // [2][max_batches]
+  cudaEvent_t free_ev = nullptr;    // recorded on compute when the step using this set ends
+  bool used = false;
+};
+
 struct coe_runtime {
   coe_runtime_config cfg{};
-  int64_t expert_bytes = 0;
+  int64_t expert_bytes = 0, half_bytes = 0;
   int64_t row_elems = 0;  // T * d
-  cudaStream_t compute = nullptr, copy = nullptr;
+  // wave classes, one stream each: 0 main (experts resident since step start; also runs K1/K2
+  // and the step join), 1 release (last readers of slots a later swap-in overwrites: high
+  // priority on reserved SMs -- they gate the copy engine), 2 swapped (experts copied this
+  // step: waits for copies in op order without blocking class 0); copy = plan upload + swap-ins
+  static constexpr int NCLS = 3;
+  cudaStream_t cls_stream[NCLS] = {nullptr, nullptr, nullptr};
+  cudaStream_t compute = nullptr, copy = nullptr;  // compute == cls_stream[0]
   // device memory
   char *slab = nullptr;
-  __nv_bfloat16 *x = nullptr, *p0 = nullptr, *p1 = nullptr, *hbuf = nullptr, *outbuf = nullptr;
-  int32_t *d_adm = nullptr;       // [4][max_adm]: exec, rank, req, stage
-  int32_t *d_perm = nullptr, *d_keys = nullptr, *d_mreq = nullptr, *d_mstage = nullptr;
-  int32_t *d_batch = nullptr;     // [2][max_batches]: exec, size
-  int32_t *d_boff = nullptr;
-  int32_t *d_flags = nullptr;     // runs, violations
-  int32_t *d_last = nullptr;
-  coe_mlp_group *d_groups = nullptr;  // [2][max_batches]
+  __nv_bfloat16 *x = nullptr, *p0 = nullptr, *p1 = nullptr, *outbuf = nullptr;
+  __nv_bfloat16 *hbuf[NCLS] = {nullptr, nullptr, nullptr};
+  StepBuffers sets[2];
+  int cur_set = 0;
+  int32_t *d_perm = nullptr, *d_keys = nullptr, *d_flags = nullptr, *d_last = nullptr;
   void *d_sort_scratch = nullptr, *d_compact_scratch = nullptr;
   // host
   char *host_store = nullptr;
   char *staging[2] = {nullptr, nullptr};
   int64_t staging_bytes = 0;
   cudaEvent_t staging_done[2] = {nullptr, nullptr};
-  int staging_idx = 0;
   int32_t *h_last = nullptr;
-  coe_mlp *mlp = nullptr;
+  coe_mlp *mlp[NCLS] = {nullptr, nullptr, nullptr};
   // slot state (persists across steps)
   std::vector<int32_t> slot_expert, expert_slot;
+  std::vector<cudaEvent_t> slot_free_up, slot_free_down;  // last reader of each half, previous step
+  std::vector<uint8_t> slot_free_valid;
   // events
-  std::vector<cudaEvent_t> wave_ev, copy_ev;
+  std::vector<cudaEvent_t> wave_up_ev, wave_down_ev, copy_up_ev, copy_down_ev;
   std::vector<cudaEvent_t> t_copy_start, t_copy_end, t_wave_start, t_wave_end;
-  cudaEvent_t t_step_start = nullptr, t_group_end = nullptr, t_step_end = nullptr, copy_drained = nullptr;
-  cudaEvent_t prev_step_end = nullptr;
-  bool have_prev = false;
+  cudaEvent_t staged = nullptr, copy_drained = nullptr, grouped = nullptr;
+  cudaEvent_t cls_drained[NCLS] = {nullptr, nullptr, nullptr};
+  cudaEvent_t t_step_start = nullptr, t_group_end = nullptr, t_step_end = nullptr;
   int32_t last_waves = 0, last_copies = 0;
+  std::vector<int32_t> last_wave_cls, last_wave_rows, last_wave_groups;
   int64_t last_adm = 0, last_batches = 0;
+  int last_set = 0;
+  int m_ctas = 148, r_ctas = 16;  // SM split: main waves vs the swap-in-gating waves
 
   ~coe_runtime() {
-    if (compute) cudaStreamSynchronize(compute);
+    for (auto st : cls_stream)
+      if (st) cudaStreamSynchronize(st);
     if (copy) cudaStreamSynchronize(copy);
-    if (mlp) coe_mlp_destroy(mlp);
-    for (void *p : {(void *)slab, (void *)x, (void *)p0, (void *)p1, (void *)hbuf, (void *)outbuf, (void *)d_adm,
-                    (void *)d_perm, (void *)d_keys, (void *)d_mreq, (void *)d_mstage, (void *)d_batch, (void *)d_boff,
-                    (void *)d_flags, (void *)d_last, (void *)d_groups, d_sort_scratch, d_compact_scratch})
+    for (auto m : mlp)
+      if (m) coe_mlp_destroy(m);
+    std::vector<void *> dev = {slab, x, p0, p1, hbuf[0], hbuf[1], hbuf[2], outbuf, d_perm, d_keys, d_flags, d_last, d_sort_scratch,
+                               d_compact_scratch};
+    for (auto &s : sets) {
+      for (void *p : {(void *)s.adm, (void *)s.batch, (void *)s.boff, (void *)s.mreq, (void *)s.mstage,
+                      (void *)s.groups})
+        dev.push_back(p);
+      if (s.free_ev) cudaEventDestroy(s.free_ev);
+    }
+    for (void *p : dev)
       if (p) cudaFree(p);
     for (void *p : {(void *)host_store, (void *)staging[0], (void *)staging[1], (void *)h_last})
       if (p) cudaFreeHost(p);
-    auto kill = [](std::vector<cudaEvent_t> &v) {
-      for (auto e : v) cudaEventDestroy(e);
-      v.clear();
-    };
-    kill(wave_ev);
-    kill(copy_ev);
-    kill(t_copy_start);
-    kill(t_copy_end);
-    kill(t_wave_start);
-    kill(t_wave_end);
-    for (cudaEvent_t e : {t_step_start, t_group_end, t_step_end, copy_drained, prev_step_end, staging_done[0],
+    for (auto *v : {&slot_free_up, &slot_free_down, &wave_up_ev, &wave_down_ev, &copy_up_ev, &copy_down_ev,
+                    &t_copy_start, &t_copy_end, &t_wave_start, &t_wave_end}) {
+      for (auto e : *v) cudaEventDestroy(e);
+      v->clear();
+    }
+    for (cudaEvent_t e : {staged, copy_drained, grouped, cls_drained[0], cls_drained[1], cls_drained[2], t_step_start, t_group_end, t_step_end, staging_done[0],
                           staging_done[1]})
       if (e) cudaEventDestroy(e);
-    if (compute) cudaStreamDestroy(compute);
+    for (auto st : cls_stream)
+      if (st) cudaStreamDestroy(st);
     if (copy) cudaStreamDestroy(copy);
   }
 
@@ -175,35 +202,24 @@ float elapsed(cudaEvent_t a, cudaEvent_t b) {
   return ms;
 }
 
-// union length of [s, e) intervals
-float union_len(std::vector<std::pair<float, float>> v) {
+std::vector<std::pair<float, float>> merged(std::vector<std::pair<float, float>> v) {
   std::sort(v.begin(), v.end());
-  float total = 0.f, cs = -1.f, ce = -1.f;
+  std::vector<std::pair<float, float>> out;
   for (auto &iv : v) {
-    if (iv.first > ce) {
-      if (ce > cs) total += ce - cs;
-      cs = iv.first;
-      ce = iv.second;
-    } else {
-      ce = std::max(ce, iv.second);
-    }
+    if (!out.empty() && iv.first <= out.back().second) out.back().second = std::max(out.back().second, iv.second);
+    else out.push_back(iv);
   }
-  if (ce > cs) total += ce - cs;
+  return out;
+}
+
+float union_len(const std::vector<std::pair<float, float>> &v) {
+  float total = 0.f;
+  for (auto &iv : merged(v)) total += iv.second - iv.first;
   return total;
 }
 
-float intersect_len(std::vector<std::pair<float, float>> a, std::vector<std::pair<float, float>> b) {
-  auto norm = [](std::vector<std::pair<float, float>> v) {
-    std::sort(v.begin(), v.end());
-    std::vector<std::pair<float, float>> out;
-    for (auto &iv : v) {
-      if (!out.empty() && iv.first <= out.back().second) out.back().second = std::max(out.back().second, iv.second);
-      else out.push_back(iv);
-    }
-    return out;
-  };
-  a = norm(a);
-  b = norm(b);
+float intersect_len(const std::vector<std::pair<float, float>> &a0, const std::vector<std::pair<float, float>> &b0) {
+  auto a = merged(a0), b = merged(b0);
   size_t i = 0, j = 0;
   float total = 0.f;
   while (i < a.size() && j < b.size()) {
@@ -230,28 +246,35 @@ int coe_runtime_create(const coe_runtime_config *cfg, coe_runtime **out) {
   rt->cfg = *cfg;
   const auto &c = rt->cfg;
   rt->expert_bytes = 2LL * c.d * c.h * 2;
+  rt->half_bytes = rt->expert_bytes / 2;
   rt->row_elems = (int64_t)c.T * c.d;
   const int64_t act_bytes = (int64_t)c.max_requests * rt->row_elems * 2;
-  bool good = ok(cudaStreamCreateWithFlags(&rt->compute, cudaStreamNonBlocking), "stream") &&
+  const size_t A = (size_t)c.max_admissions, B = (size_t)c.max_batches;
+  int prio_low = 0, prio_high = 0;
+  cudaDeviceGetStreamPriorityRange(&prio_low, &prio_high);
+  bool good = ok(cudaStreamCreateWithPriority(&rt->cls_stream[0], cudaStreamNonBlocking, prio_low), "stream") &&
+              ok(cudaStreamCreateWithPriority(&rt->cls_stream[1], cudaStreamNonBlocking, prio_high), "stream") &&
+              ok(cudaStreamCreateWithPriority(&rt->cls_stream[2], cudaStreamNonBlocking, prio_low), "stream") &&
               ok(cudaStreamCreateWithFlags(&rt->copy, cudaStreamNonBlocking), "stream") &&
               dmalloc(&rt->slab, (size_t)rt->expert_bytes * c.num_slots, "slab alloc") &&
               dmalloc(&rt->x, act_bytes, "X alloc") && dmalloc(&rt->p0, act_bytes, "P0 alloc") &&
               dmalloc(&rt->p1, act_bytes, "P1 alloc") && dmalloc(&rt->outbuf, act_bytes, "out alloc") &&
-              dmalloc(&rt->hbuf, (size_t)c.max_wave_rows * c.h * 2, "H alloc") &&
-              dmalloc(&rt->d_adm, 16 * (size_t)c.max_admissions, "adm alloc") &&
-              dmalloc(&rt->d_perm, 4 * (size_t)c.max_admissions, "perm alloc") &&
-              dmalloc(&rt->d_keys, 4 * (size_t)c.max_admissions, "keys alloc") &&
-              dmalloc(&rt->d_mreq, 4 * (size_t)c.max_admissions, "member alloc") &&
-              dmalloc(&rt->d_mstage, 4 * (size_t)c.max_admissions, "member alloc") &&
-              dmalloc(&rt->d_batch, 8 * (size_t)c.max_batches, "batch alloc") &&
-              dmalloc(&rt->d_boff, 4 * (size_t)c.max_batches, "boff alloc") &&
+              dmalloc(&rt->hbuf[0], (size_t)c.max_wave_rows * c.h * 2, "H alloc") &&
+              dmalloc(&rt->hbuf[1], (size_t)c.max_wave_rows * c.h * 2, "H alloc") &&
+              dmalloc(&rt->hbuf[2], (size_t)c.max_wave_rows * c.h * 2, "H alloc") &&
+              dmalloc(&rt->d_perm, 4 * A, "perm alloc") && dmalloc(&rt->d_keys, 4 * A, "keys alloc") &&
               dmalloc(&rt->d_flags, 64, "flags alloc") && dmalloc(&rt->d_last, 4 * (size_t)c.max_requests, "last") &&
-              dmalloc(&rt->d_groups, 2 * sizeof(coe_mlp_group) * (size_t)c.max_batches, "group alloc") &&
               dmalloc(&rt->d_sort_scratch, (size_t)coe_group_sort_scratch_bytes(c.max_admissions), "sort scratch") &&
-              dmalloc(&rt->d_compact_scratch, (size_t)coe_run_compact_scratch_bytes(c.max_admissions, (int)c.max_batches, 1),
+              dmalloc(&rt->d_compact_scratch, (size_t)coe_run_compact_scratch_bytes(c.max_admissions, (int)B, 1),
                       "compact scratch");
+  for (auto &s : rt->sets)
+    good = good && dmalloc(&s.adm, 16 * A, "adm alloc") && dmalloc(&s.batch, 8 * B, "batch alloc") &&
+           dmalloc(&s.boff, 4 * B, "boff alloc") && dmalloc(&s.mreq, 4 * A, "member alloc") &&
+           dmalloc(&s.mstage, 4 * A, "member alloc") && dmalloc(&s.groups, 2 * sizeof(coe_mlp_group) * B, "groups") &&
+           ok(cudaEventCreateWithFlags(&s.free_ev, cudaEventDisableTiming), "event");
+  rt->compute = rt->cls_stream[0];
   if (good) {
-    rt->staging_bytes = 16 * c.max_admissions + 8 * c.max_batches + 2 * sizeof(coe_mlp_group) * c.max_batches + 256;
+    rt->staging_bytes = 16 * A + 8 * B + 2 * sizeof(coe_mlp_group) * B + 256;
     good = ok(cudaHostAlloc(reinterpret_cast<void **>(&rt->staging[0]), rt->staging_bytes, cudaHostAllocDefault), "staging") &&
            ok(cudaHostAlloc(reinterpret_cast<void **>(&rt->staging[1]), rt->staging_bytes, cudaHostAllocDefault), "staging") &&
            ok(cudaHostAlloc(reinterpret_cast<void **>(&rt->h_last), 4 * (size_t)c.max_requests, cudaHostAllocDefault), "last") &&
@@ -260,10 +283,16 @@ int coe_runtime_create(const coe_runtime_config *cfg, coe_runtime **out) {
               "pinned expert store") &&
            ok(cudaEventCreateWithFlags(&rt->staging_done[0], cudaEventDisableTiming), "event") &&
            ok(cudaEventCreateWithFlags(&rt->staging_done[1], cudaEventDisableTiming), "event") &&
-           ok(cudaEventCreateWithFlags(&rt->prev_step_end, cudaEventDisableTiming), "event") &&
+           ok(cudaEventCreateWithFlags(&rt->staged, cudaEventDisableTiming), "event") &&
            ok(cudaEventCreateWithFlags(&rt->copy_drained, cudaEventDisableTiming), "event") &&
+           ok(cudaEventCreateWithFlags(&rt->grouped, cudaEventDisableTiming), "event") &&
+           ok(cudaEventCreateWithFlags(&rt->cls_drained[0], cudaEventDisableTiming), "event") &&
+           ok(cudaEventCreateWithFlags(&rt->cls_drained[1], cudaEventDisableTiming), "event") &&
+           ok(cudaEventCreateWithFlags(&rt->cls_drained[2], cudaEventDisableTiming), "event") &&
            ok(cudaEventCreate(&rt->t_step_start), "event") && ok(cudaEventCreate(&rt->t_group_end), "event") &&
-           ok(cudaEventCreate(&rt->t_step_end), "event");
+           ok(cudaEventCreate(&rt->t_step_end), "event") &&
+           rt->ensure_events(rt->slot_free_up, c.num_slots, false) &&
+           rt->ensure_events(rt->slot_free_down, c.num_slots, false);
   }
   if (good) {
     coe_mlp_config mc{};
@@ -274,12 +303,15 @@ int coe_runtime_create(const coe_runtime_config *cfg, coe_runtime **out) {
     mc.act0 = rt->p0;
     mc.act1 = rt->p1;
     mc.act_rows = (int64_t)c.max_requests * c.T;
-    mc.h_scratch = rt->hbuf;
+    mc.h_scratch = rt->hbuf[0];
     mc.h_rows = c.max_wave_rows;
     mc.slab = rt->slab;
     mc.num_slots = c.num_slots;
     mc.slot_stride_bytes = rt->expert_bytes;
-    if (coe_mlp_create(&mc, &rt->mlp) != COE_CUDA_OK) good = false;
+    for (int k = 0; k < coe_runtime::NCLS && good; ++k) {
+      mc.h_scratch = rt->hbuf[k];
+      if (coe_mlp_create(&mc, &rt->mlp[k]) != COE_CUDA_OK) good = false;
+    }
   }
   if (!good) {
     std::string msg = g_last_error;
@@ -287,8 +319,17 @@ int coe_runtime_create(const coe_runtime_config *cfg, coe_runtime **out) {
     g_last_error = msg;
     return COE_CUDA_ERR_CUDA;
   }
+  {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int reserve = c.reserve_sms > 0 ? std::min(c.reserve_sms, sms / 2) : 0;
+    rt->m_ctas = sms - reserve;
+    rt->r_ctas = reserve > 0 ? reserve : sms;
+  }
   rt->slot_expert.assign(c.num_slots, -1);
   rt->expert_slot.assign(c.num_experts, -1);
+  rt->slot_free_valid.assign(c.num_slots, 0);
   *out = rt;
   return COE_CUDA_OK;
 }
@@ -300,7 +341,7 @@ void *coe_runtime_buffer(coe_runtime *rt, int which) {
     case 0: return rt->x;
     case 1: return rt->p0;
     case 2: return rt->p1;
-    case 3: return rt->hbuf;
+    case 3: return rt->hbuf[0];
     case 4: return rt->slab;
     case 5: return rt->host_store;
     case 6: return rt->outbuf;
@@ -308,7 +349,11 @@ void *coe_runtime_buffer(coe_runtime *rt, int which) {
   }
 }
 
-cudaStream_t coe_runtime_stream(coe_runtime *rt, int which) { return which == 0 ? rt->compute : rt->copy; }
+cudaStream_t coe_runtime_stream(coe_runtime *rt, int which) {
+  if (which == 1) return rt->copy;
+  if (which == 0) return rt->compute;
+  return (which >= 2 && which - 1 < coe_runtime::NCLS) ? rt->cls_stream[which - 1] : nullptr;
+}
 
 int coe_runtime_read_buffer(coe_runtime *rt, int which, void *host, int64_t bytes) {
   void *src = coe_runtime_buffer(rt, which);
@@ -328,8 +373,8 @@ int coe_runtime_slot_of(coe_runtime *rt, int32_t expert) {
 int coe_runtime_init_experts(coe_runtime *rt) {
   const auto &c = rt->cfg;
   const int64_t half = (int64_t)c.d * c.h;  // elements per matrix
-  // generate into slot 0 of the slab, stage to the pinned store
-  for (int32_t e = 0; e < c.num_experts; ++e) {
+  if (!ok(cudaDeviceSynchronize(), "init experts sync")) return fail_cuda();
+  for (int32_t e = 0; e < c.num_experts; ++e) {  // generate into slot 0, stage to the pinned store
     __nv_bfloat16 *w = reinterpret_cast<__nv_bfloat16 *>(rt->slab);
     if (coe_fill_uniform_bf16(w, half, coe_expert_seed(c.weight_seed, e, 0), sqrtf(3.0f / c.d), rt->compute) ||
         coe_fill_uniform_bf16(w + half, half, coe_expert_seed(c.weight_seed, e, 1), sqrtf(3.0f / c.h), rt->compute))
@@ -342,7 +387,7 @@ int coe_runtime_init_experts(coe_runtime *rt) {
   if (!ok(cudaStreamSynchronize(rt->compute), "init experts")) return fail_cuda();
   std::fill(rt->slot_expert.begin(), rt->slot_expert.end(), -1);
   std::fill(rt->expert_slot.begin(), rt->expert_slot.end(), -1);
-  rt->have_prev = false;
+  std::fill(rt->slot_free_valid.begin(), rt->slot_free_valid.end(), 0);
   return COE_CUDA_OK;
 }
 
@@ -370,6 +415,7 @@ int coe_runtime_upload_inputs(coe_runtime *rt, const void *host, int32_t num_req
 
 int coe_runtime_download_outputs(coe_runtime *rt, const int32_t *last_stage_host, int32_t num_requests, void *host) {
   if (num_requests <= 0) return COE_CUDA_OK;
+  if (!ok(cudaStreamSynchronize(rt->compute), "download sync")) return fail_cuda();  // h_last reuse
   std::memcpy(rt->h_last, last_stage_host, 4 * (size_t)num_requests);
   if (!ok(cudaMemcpyAsync(rt->d_last, rt->h_last, 4 * (size_t)num_requests, cudaMemcpyHostToDevice, rt->compute),
           "last stage H2D"))
@@ -385,9 +431,9 @@ int coe_runtime_download_outputs(coe_runtime *rt, const int32_t *last_stage_host
 }
 
 int coe_runtime_synchronize(coe_runtime *rt) {
-  bool a = ok(cudaStreamSynchronize(rt->copy), "sync copy");
-  bool b = ok(cudaStreamSynchronize(rt->compute), "sync compute");
-  return (a && b) ? COE_CUDA_OK : fail_cuda();
+  bool good = ok(cudaStreamSynchronize(rt->copy), "sync copy");
+  for (int k = coe_runtime::NCLS - 1; k >= 0; --k) good = ok(cudaStreamSynchronize(rt->cls_stream[k]), "sync") && good;
+  return good ? COE_CUDA_OK : fail_cuda();
 }
 
 int coe_runtime_check(coe_runtime *rt, int32_t *runs, int32_t *violations) {
@@ -399,9 +445,10 @@ int coe_runtime_check(coe_runtime *rt, int32_t *runs, int32_t *violations) {
 }
 
 int coe_runtime_members(coe_runtime *rt, int32_t *member_req, int32_t *member_stage, int32_t *batch_off) {
-  bool good = ok(cudaMemcpy(member_req, rt->d_mreq, 4 * rt->last_adm, cudaMemcpyDeviceToHost), "members D2H") &&
-              ok(cudaMemcpy(member_stage, rt->d_mstage, 4 * rt->last_adm, cudaMemcpyDeviceToHost), "members D2H") &&
-              ok(cudaMemcpy(batch_off, rt->d_boff, 4 * rt->last_batches, cudaMemcpyDeviceToHost), "boff D2H");
+  const StepBuffers &s = rt->sets[rt->last_set];
+  bool good = ok(cudaMemcpy(member_req, s.mreq, 4 * rt->last_adm, cudaMemcpyDeviceToHost), "members D2H") &&
+              ok(cudaMemcpy(member_stage, s.mstage, 4 * rt->last_adm, cudaMemcpyDeviceToHost), "members D2H") &&
+              ok(cudaMemcpy(batch_off, s.boff, 4 * rt->last_batches, cudaMemcpyDeviceToHost), "boff D2H");
   return good ? COE_CUDA_OK : fail_cuda();
 }
 
@@ -425,6 +472,31 @@ int coe_runtime_timing(coe_runtime *rt, coe_step_timing *out) {
   out->copy_busy_ms = union_len(cp);
   out->compute_busy_ms = union_len(wv);
   out->overlap_ms = intersect_len(cp, wv);
+  return COE_CUDA_OK;
+}
+
+int coe_runtime_intervals(coe_runtime *rt, float *copy_iv, float *wave_iv, int32_t *wave_info) {
+  if (!rt->cfg.profile) {
+    coe_set_error("runtime created without profile events");
+    return COE_CUDA_ERR_CONFIG;
+  }
+  for (int i = 0; i < rt->last_copies; ++i) {
+    copy_iv[2 * i] = elapsed(rt->t_step_start, rt->t_copy_start[i]);
+    copy_iv[2 * i + 1] = elapsed(rt->t_step_start, rt->t_copy_end[i]);
+  }
+  for (int i = 0; i < rt->last_waves; ++i) {
+    wave_iv[2 * i] = elapsed(rt->t_step_start, rt->t_wave_start[i]);
+    wave_iv[2 * i + 1] = elapsed(rt->t_step_start, rt->t_wave_end[i]);
+    wave_info[3 * i] = rt->last_wave_cls[i];
+    wave_info[3 * i + 1] = rt->last_wave_rows[i];
+    wave_info[3 * i + 2] = rt->last_wave_groups[i];
+  }
+  return COE_CUDA_OK;
+}
+
+int coe_runtime_counts(coe_runtime *rt, int32_t *copies, int32_t *waves) {
+  *copies = rt->last_copies;
+  *waves = rt->last_waves;
   return COE_CUDA_OK;
 }
 
@@ -459,55 +531,87 @@ int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_step_stats *
   const int passes = (rank_bits + 7) / 8;  // executor field is 0 (one executor per runtime)
   st.rank_bits = rank_bits;
 
-  // ---- pass 1: slots, copies, waves ----
+  // ---- lookahead: batches that are the last reader of an expert a later LOAD evicts ----
+  std::vector<int64_t> my_ops;
+  for (int64_t i = 0; i < in->num_ops; ++i)
+    if (ops[i].executor == x) my_ops.push_back(i);
+  std::vector<uint8_t> releases(my_ops.size(), 0);
+  {
+    std::vector<uint8_t> next_is_evict(c.num_experts, 0);
+    for (int64_t k = (int64_t)my_ops.size() - 1; k >= 0; --k) {
+      const coe_op &op = ops[my_ops[k]];
+      if (op.kind == COE_OP_LOAD) {
+        for (int32_t j = 0; j < op.count; ++j) next_is_evict[in->op_args[op.offset + j]] = 1;
+        next_is_evict[op.expert] = 0;
+      } else {
+        releases[k] = next_is_evict[op.expert];
+        next_is_evict[op.expert] = 0;
+      }
+    }
+  }
+
+  // ---- pass 1: slots, copies, waves on two compute streams ----
   std::vector<uint8_t> plan_res(c.num_experts, 0), pending_restore(c.num_experts, 0);
-  std::vector<int32_t> slot_use_wave(c.num_slots, -1), slot_copy(c.num_slots, -1);
-  std::vector<uint8_t> slot_copy_waited(c.num_slots, 1);
-  // slots holding experts outside the initial placement become stale
+  std::vector<int32_t> slot_use_wave(c.num_slots, -1), slot_copy(c.num_slots, -1), slot_open_cls(c.num_slots, -1);
+  std::vector<uint8_t> slot_written(c.num_slots, 0);
   for (int32_t i = 0; i < in->num_initial; ++i) plan_res[in->initial[i]] = 1;
-  for (int32_t s = 0; s < c.num_slots; ++s) {
+  for (int32_t s = 0; s < c.num_slots; ++s) {  // slots outside the initial placement are free again
     int32_t e = rt->slot_expert[s];
     if (e >= 0 && !plan_res[e]) {
       rt->expert_slot[e] = -1;
       rt->slot_expert[s] = -1;
     }
   }
-  for (int32_t i = 0; i < in->num_initial; ++i) {
-    int32_t e = in->initial[i];
-    if (rt->expert_slot[e] < 0) pending_restore[e] = 1;
-  }
+  for (int32_t i = 0; i < in->num_initial; ++i)
+    if (rt->expert_slot[in->initial[i]] < 0) pending_restore[in->initial[i]] = 1;
 
+  std::vector<int32_t> req_open_cls(c.max_requests, -1), req_writer(c.max_requests, -1);
   std::vector<CopyAct> copies;
+  std::vector<uint8_t> copy_waited;
   std::vector<WaveAct> waves;
   std::vector<Action> actions;
   std::vector<coe_mlp_group> g_up, g_down;
   std::vector<int32_t> b_size;
-  std::unordered_set<int32_t> wave_reqs;
-  WaveAct open{};
-  open.first_group = 0;
-  bool open_used = false;
+  struct Open {
+    bool used = false;
+    WaveAct w{};
+    std::vector<coe_mlp_group> gu, gd;
+    std::vector<int32_t> slots, reqs;
+  } open[coe_runtime::NCLS];
+  int64_t waves_by_cls[coe_runtime::NCLS] = {0, 0, 0};
 
-  auto flush = [&]() {
-    if (!open_used) return;
-    int32_t id = (int32_t)waves.size();
-    waves.push_back(open);
+  auto flush = [&](int cls) {
+    Open &o = open[cls];
+    if (!o.used) return;
+    const int32_t id = (int32_t)waves.size();
+    o.w.cls = cls;
+    o.w.first_group = (int32_t)g_up.size();
+    g_up.insert(g_up.end(), o.gu.begin(), o.gu.end());
+    g_down.insert(g_down.end(), o.gd.begin(), o.gd.end());
+    for (int32_t s : o.slots) {
+      slot_use_wave[s] = id;
+      slot_open_cls[s] = -1;
+    }
+    for (int32_t r : o.reqs) {
+      req_writer[r] = id;
+      req_open_cls[r] = -1;
+    }
+    st.max_wave_groups = std::max(st.max_wave_groups, o.w.num_groups);
+    st.max_wave_rows = std::max(st.max_wave_rows, o.w.rows);
+    waves.push_back(o.w);
     actions.push_back(Action{false, id});
-    st.max_wave_groups = std::max(st.max_wave_groups, open.num_groups);
-    st.max_wave_rows = std::max(st.max_wave_rows, open.rows);
-    open = WaveAct{};
-    open.first_group = (int32_t)g_up.size();
-    open_used = false;
-    wave_reqs.clear();
+    waves_by_cls[cls] += 1;
+    o = Open();
   };
-  auto open_id = [&]() { return (int32_t)waves.size(); };
   auto alloc_slot = [&](int32_t &slot) -> bool {
     int32_t best = -1;
     for (int32_t s = 0; s < c.num_slots; ++s) {
       if (rt->slot_expert[s] >= 0) continue;
-      if (best < 0 || slot_use_wave[s] < slot_use_wave[best]) best = s;
+      auto age = [&](int32_t q) { return slot_open_cls[q] >= 0 ? INT32_MAX : slot_use_wave[q]; };
+      if (best < 0 || age(s) < age(best)) best = s;
     }
     if (best < 0) return false;
-    if (open_used && slot_use_wave[best] == open_id()) flush();
+    if (slot_open_cls[best] >= 0) flush(slot_open_cls[best]);
     slot = best;
     return true;
   };
@@ -517,29 +621,23 @@ int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_step_stats *
       coe_set_error("no free HBM expert slot (planner residency exceeds the slot count)");
       return false;
     }
-    int32_t cid = (int32_t)copies.size();
-    copies.push_back(CopyAct{e, s, slot_use_wave[s], restore});
-    actions.push_back(Action{true, cid});
+    copies.push_back(CopyAct{e, s, slot_use_wave[s], !slot_written[s] && rt->slot_free_valid[s] != 0, restore});
+    copy_waited.push_back(0);
+    actions.push_back(Action{true, (int32_t)copies.size() - 1});
+    slot_written[s] = 1;
     rt->slot_expert[s] = e;
     rt->expert_slot[e] = s;
-    slot_copy[s] = cid;
-    slot_copy_waited[s] = 0;
-    if (restore) {
-      st.restores += 1;
-      st.restore_bytes += rt->expert_bytes;
-    } else {
-      st.loads += 1;
-      st.load_bytes += rt->expert_bytes;
-    }
+    slot_copy[s] = (int32_t)copies.size() - 1;
+    (restore ? st.restores : st.loads) += 1;
+    (restore ? st.restore_bytes : st.load_bytes) += rt->expert_bytes;
     return true;
   };
 
-  for (int64_t i = 0; i < in->num_ops; ++i) {
-    const coe_op &op = ops[i];
-    if (op.executor != x) continue;
+  for (size_t k = 0; k < my_ops.size(); ++k) {
+    const coe_op &op = ops[my_ops[k]];
     if (op.kind == COE_OP_LOAD) {
-      for (int32_t k = 0; k < op.count; ++k) {
-        int32_t v = in->op_args[op.offset + k];
+      for (int32_t j = 0; j < op.count; ++j) {
+        int32_t v = in->op_args[op.offset + j];
         plan_res[v] = 0;
         pending_restore[v] = 0;
         int32_t s = rt->expert_slot[v];
@@ -555,54 +653,79 @@ int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_step_stats *
         rt->expert_slot[op.expert] = -1;
       }
       if (!issue_copy(op.expert, false)) return COE_CUDA_ERR_CHECK;
-    } else {
-      const int32_t e = op.expert;
-      if (rt->expert_slot[e] < 0) {
-        if (!pending_restore[e]) {
-          coe_set_error("batch on an expert that is neither resident nor loaded");
-          return COE_CUDA_ERR_CHECK;
-        }
-        pending_restore[e] = 0;
-        if (!issue_copy(e, true)) return COE_CUDA_ERR_CHECK;
-      }
-      const int32_t s = rt->expert_slot[e];
-      const int64_t rows = (int64_t)op.count * c.T;
-      bool clash = false;
-      for (int32_t k = 0; k < op.count && !clash; ++k) clash = wave_reqs.count(in->op_args[op.offset + 2 * k]) > 0;
-      const bool need_wait = !slot_copy_waited[s];
-      if (open_used && (need_wait || clash || open.rows + rows > c.max_wave_rows ||
-                        open.num_groups >= coe_mlp_max_groups()))
-        flush();
-      if (rows > c.max_wave_rows) {
-        coe_set_error("a single batch exceeds the H scratch rows");
-        return COE_CUDA_ERR_CONFIG;
-      }
-      if (need_wait) {
-        open.wait_copies.push_back(slot_copy[s]);
-        slot_copy_waited[s] = 1;
-      }
-      const int32_t m_tiles = (int32_t)((rows + BM - 1) / BM);
-      coe_mlp_group gu{};
-      gu.rows = (int32_t)rows;
-      gu.slot = s;
-      gu.batch = (int32_t)b_size.size();
-      gu.h_row = (int32_t)open.rows;
-      gu.tile_start = open.tiles_up;
-      coe_mlp_group gd = gu;
-      gd.tile_start = open.tiles_down;
-      g_up.push_back(gu);
-      g_down.push_back(gd);
-      b_size.push_back(op.count);
-      open.num_groups += 1;
-      open.rows += rows;
-      open.tiles_up += m_tiles * (c.h / BN);
-      open.tiles_down += m_tiles * (c.d / BN);
-      open_used = true;
-      slot_use_wave[s] = open_id();
-      for (int32_t k = 0; k < op.count; ++k) wave_reqs.insert(in->op_args[op.offset + 2 * k]);
+      continue;
     }
+    const int32_t e = op.expert;
+    if (rt->expert_slot[e] < 0) {
+      if (!pending_restore[e]) {
+        coe_set_error("batch on an expert that is neither resident nor loaded");
+        return COE_CUDA_ERR_CHECK;
+      }
+      pending_restore[e] = 0;
+      if (!issue_copy(e, true)) return COE_CUDA_ERR_CHECK;
+    }
+    const int32_t s = rt->expert_slot[e];
+    // the swap-in stream runs only the last readers of slots a later load overwrites: their
+    // completion gates the copy engine, which is the bottleneck of budgeted configs
+    const int cls = releases[k] ? 1 : (slot_copy[s] >= 0 ? 2 : 0);
+    const int64_t rows = (int64_t)op.count * c.T;
+    if (rows > c.max_wave_rows) {
+      coe_set_error("a single batch exceeds the H scratch rows");
+      return COE_CUDA_ERR_CONFIG;
+    }
+    bool clash = false;
+    for (int32_t j = 0; j < op.count; ++j) {
+      const int32_t r = in->op_args[op.offset + 2 * j];
+      if (req_open_cls[r] >= 0 && req_open_cls[r] != cls) flush(req_open_cls[r]);  // producer needs a wave id
+      if (req_open_cls[r] == cls) clash = true;
+    }
+    const int32_t cp = slot_copy[s];
+    const bool need_wait = cp >= 0 && !(copy_waited[cp] & (1 << cls));
+    Open &o = open[cls];
+    if (o.used && (need_wait || clash || releases[k] || o.w.rows + rows > c.max_wave_rows ||
+                   o.w.num_groups >= coe_mlp_max_groups()))
+      flush(cls);
+    Open &w = open[cls];
+    if (need_wait) {
+      w.w.wait_copies.push_back(cp);
+      copy_waited[cp] |= (1 << cls);
+    }
+    for (int32_t j = 0; j < op.count; ++j) {
+      const int32_t r = in->op_args[op.offset + 2 * j];
+      const int32_t wr = req_writer[r];
+      if (wr >= 0 && waves[wr].cls != cls &&
+          std::find(w.w.wait_waves.begin(), w.w.wait_waves.end(), wr) == w.w.wait_waves.end())
+        w.w.wait_waves.push_back(wr);
+    }
+    const int32_t m_tiles = (int32_t)((rows + BM - 1) / BM);
+    coe_mlp_group gu{};
+    gu.rows = (int32_t)rows;
+    gu.slot = s;
+    gu.batch = (int32_t)b_size.size();
+    gu.h_row = (int32_t)w.w.rows;
+    gu.tile_start = w.w.tiles_up;
+    coe_mlp_group gd = gu;
+    gd.tile_start = w.w.tiles_down;
+    w.gu.push_back(gu);
+    w.gd.push_back(gd);
+    b_size.push_back(op.count);
+    w.w.num_groups += 1;
+    w.w.rows += rows;
+    w.w.tiles_up += m_tiles * (c.h / BN);
+    w.w.tiles_down += m_tiles * (c.d / BN);
+    w.used = true;
+    w.slots.push_back(s);
+    slot_open_cls[s] = cls;
+    for (int32_t j = 0; j < op.count; ++j) {
+      const int32_t r = in->op_args[op.offset + 2 * j];
+      w.reqs.push_back(r);
+      req_open_cls[r] = cls;
+    }
+    if (releases[k]) flush(cls);  // the slot's next writer waits for this wave only
   }
-  flush();
+  for (int k = 0; k < coe_runtime::NCLS; ++k) flush(k);
+  for (int32_t s = 0; s < c.num_slots; ++s)  // per-slot last reader this step -> event after that wave
+    if (slot_use_wave[s] >= 0) waves[slot_use_wave[s]].frees_slots.push_back(s);
   const int64_t n_batches = (int64_t)b_size.size();
   if (n_batches > c.max_batches) {
     coe_set_error("more batches than the runtime was sized for");
@@ -613,19 +736,19 @@ int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_step_stats *
   st.waves = (int64_t)waves.size();
 
   // ---- pass 2: issue ----
-  if (!rt->ensure_events(rt->wave_ev, waves.size(), false) || !rt->ensure_events(rt->copy_ev, copies.size(), false))
+  const size_t nw = waves.size(), nc = copies.size();
+  if (!rt->ensure_events(rt->wave_up_ev, nw, false) || !rt->ensure_events(rt->wave_down_ev, nw, false) ||
+      !rt->ensure_events(rt->copy_up_ev, nc, false) || !rt->ensure_events(rt->copy_down_ev, nc, false))
     return fail_cuda();
-  if (c.profile && (!rt->ensure_events(rt->t_wave_start, waves.size(), true) ||
-                    !rt->ensure_events(rt->t_wave_end, waves.size(), true) ||
-                    !rt->ensure_events(rt->t_copy_start, copies.size(), true) ||
-                    !rt->ensure_events(rt->t_copy_end, copies.size(), true)))
+  if (c.profile && (!rt->ensure_events(rt->t_wave_start, nw, true) || !rt->ensure_events(rt->t_wave_end, nw, true) ||
+                    !rt->ensure_events(rt->t_copy_start, nc, true) || !rt->ensure_events(rt->t_copy_end, nc, true)))
     return fail_cuda();
 
-  // staging (double-buffered pinned upload of admissions, batches, groups)
-  const int sidx = rt->staging_idx;
-  rt->staging_idx ^= 1;
-  if (!ok(cudaEventSynchronize(rt->staging_done[sidx]), "staging reuse")) return fail_cuda();
-  char *stg = rt->staging[sidx];
+  const int set_idx = rt->cur_set;
+  rt->cur_set ^= 1;
+  StepBuffers &sb = rt->sets[set_idx];
+  if (!ok(cudaEventSynchronize(rt->staging_done[set_idx]), "staging reuse")) return fail_cuda();
+  char *stg = rt->staging[set_idx];
   int32_t *s_adm = reinterpret_cast<int32_t *>(stg);
   for (int64_t i = 0; i < n_adm; ++i) {
     s_adm[i] = 0;
@@ -644,73 +767,120 @@ int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_step_stats *
     std::memcpy(s_groups, g_up.data(), sizeof(coe_mlp_group) * n_batches);
     std::memcpy(s_groups + n_batches, g_down.data(), sizeof(coe_mlp_group) * n_batches);
   }
-  const size_t adm_bytes = 16 * (size_t)n_adm, batch_bytes = 8 * (size_t)n_batches,
-               group_bytes = 2 * sizeof(coe_mlp_group) * (size_t)n_batches;
 
   cudaStream_t cs = rt->compute, ks = rt->copy;
   if (c.profile && !ok(cudaEventRecord(rt->t_step_start, cs), "record")) return fail_cuda();
-  if (rt->have_prev && !ok(cudaStreamWaitEvent(ks, rt->prev_step_end, 0), "copy waits previous step"))
+  // plan upload first on the copy stream (ahead of this step's swap-ins), into the set
+  // the step before last used -- wait until that step released it
+  if (sb.used && !ok(cudaStreamWaitEvent(ks, sb.free_ev, 0), "set reuse")) return fail_cuda();
+  if (n_adm && !ok(cudaMemcpyAsync(sb.adm, s_adm, 16 * (size_t)n_adm, cudaMemcpyHostToDevice, ks), "adm H2D"))
     return fail_cuda();
-  int32_t *d_exec = rt->d_adm, *d_rank = rt->d_adm + n_adm, *d_req = rt->d_adm + 2 * n_adm,
-          *d_stage = rt->d_adm + 3 * n_adm;
-  if (n_adm && !ok(cudaMemcpyAsync(rt->d_adm, s_adm, adm_bytes, cudaMemcpyHostToDevice, cs), "adm H2D"))
+  if (n_batches &&
+      (!ok(cudaMemcpyAsync(sb.batch, s_batch, 8 * (size_t)n_batches, cudaMemcpyHostToDevice, ks), "batch H2D") ||
+       !ok(cudaMemcpyAsync(sb.groups, s_groups, 2 * sizeof(coe_mlp_group) * (size_t)n_batches,
+                           cudaMemcpyHostToDevice, ks),
+           "group H2D")))
     return fail_cuda();
-  if (n_batches) {
-    if (!ok(cudaMemcpyAsync(rt->d_batch, s_batch, batch_bytes, cudaMemcpyHostToDevice, cs), "batch H2D") ||
-        !ok(cudaMemcpyAsync(rt->d_groups, s_groups, group_bytes, cudaMemcpyHostToDevice, cs), "group H2D"))
-      return fail_cuda();
-  }
-  if (!ok(cudaEventRecord(rt->staging_done[sidx], cs), "record")) return fail_cuda();
-  // K1 + K2
+  if (!ok(cudaEventRecord(rt->staging_done[set_idx], ks), "record") || !ok(cudaEventRecord(rt->staged, ks), "record") ||
+      !ok(cudaStreamWaitEvent(cs, rt->staged, 0), "compute waits upload"))
+    return fail_cuda();
+  // K1 + K2 on the main compute stream (executor field 0: this runtime's admissions only)
+  int32_t *d_exec = sb.adm, *d_rank = sb.adm + n_adm, *d_req = sb.adm + 2 * n_adm, *d_stage = sb.adm + 3 * n_adm;
   if (n_adm) {
     int rc = coe_group_sort(d_exec, d_rank, n_adm, rank_bits, passes, rt->d_perm, rt->d_keys, rt->d_sort_scratch, cs);
     if (rc) return rc;
   }
   {
-    int rc = coe_run_compact(rt->d_perm, rt->d_keys, d_req, d_stage, n_adm, rank_bits, rt->d_batch,
-                             rt->d_batch + n_batches, (int)n_batches, 1, rt->d_boff, rt->d_mreq, rt->d_mstage,
-                             rt->d_flags, rt->d_flags + 1, rt->d_compact_scratch, cs);
+    int rc = coe_run_compact(rt->d_perm, rt->d_keys, d_req, d_stage, n_adm, rank_bits, sb.batch, sb.batch + n_batches,
+                             (int)n_batches, 1, sb.boff, sb.mreq, sb.mstage, rt->d_flags, rt->d_flags + 1,
+                             rt->d_compact_scratch, cs);
     if (rc) return rc;
   }
   if (c.profile && !ok(cudaEventRecord(rt->t_group_end, cs), "record")) return fail_cuda();
+  if (!ok(cudaEventRecord(rt->grouped, cs), "record")) return fail_cuda();
+  for (int k = 1; k < coe_runtime::NCLS; ++k)
+    if (!ok(cudaStreamWaitEvent(rt->cls_stream[k], rt->grouped, 0), "class stream waits K2")) return fail_cuda();
 
-  const coe_mlp_group *dg_up = rt->d_groups, *dg_down = rt->d_groups + n_batches;
+  const coe_mlp_group *dg_up = sb.groups, *dg_down = sb.groups + n_batches;
   for (const Action &a : actions) {
     if (a.is_copy) {
       const CopyAct &cp = copies[a.index];
-      if (cp.wait_wave >= 0 && !ok(cudaStreamWaitEvent(ks, rt->wave_ev[cp.wait_wave], 0), "copy waits slot"))
-        return fail_cuda();
+      char *dst = rt->slab + (int64_t)cp.slot * rt->expert_bytes;
+      const char *src = rt->host_store + (int64_t)cp.expert * rt->expert_bytes;
+      cudaEvent_t wait_up = nullptr, wait_down = nullptr;
+      if (cp.wait_wave >= 0) {
+        wait_up = rt->wave_up_ev[cp.wait_wave];
+        wait_down = rt->wave_down_ev[cp.wait_wave];
+      } else if (cp.wait_prev_step) {
+        wait_up = rt->slot_free_up[cp.slot];
+        wait_down = rt->slot_free_down[cp.slot];
+      }
+      if (wait_up && !ok(cudaStreamWaitEvent(ks, wait_up, 0), "copy waits W1 readers")) return fail_cuda();
       if (c.profile && !ok(cudaEventRecord(rt->t_copy_start[a.index], ks), "record")) return fail_cuda();
-      if (!ok(cudaMemcpyAsync(rt->slab + (int64_t)cp.slot * rt->expert_bytes,
-                              rt->host_store + (int64_t)cp.expert * rt->expert_bytes, rt->expert_bytes,
-                              cudaMemcpyHostToDevice, ks),
-              "swap-in H2D"))
+      if (!ok(cudaMemcpyAsync(dst, src, rt->half_bytes, cudaMemcpyHostToDevice, ks), "swap-in W1") ||
+          !ok(cudaEventRecord(rt->copy_up_ev[a.index], ks), "record"))
+        return fail_cuda();
+      if (wait_down && !ok(cudaStreamWaitEvent(ks, wait_down, 0), "copy waits W2 readers")) return fail_cuda();
+      if (!ok(cudaMemcpyAsync(dst + rt->half_bytes, src + rt->half_bytes, rt->half_bytes, cudaMemcpyHostToDevice, ks),
+              "swap-in W2") ||
+          !ok(cudaEventRecord(rt->copy_down_ev[a.index], ks), "record"))
         return fail_cuda();
       if (c.profile && !ok(cudaEventRecord(rt->t_copy_end[a.index], ks), "record")) return fail_cuda();
-      if (!ok(cudaEventRecord(rt->copy_ev[a.index], ks), "record")) return fail_cuda();
     } else {
       const WaveAct &w = waves[a.index];
+      cudaStream_t ws = rt->cls_stream[w.cls];
+      coe_mlp *m = rt->mlp[w.cls];
+      for (int32_t wid : w.wait_waves)
+        if (!ok(cudaStreamWaitEvent(ws, rt->wave_down_ev[wid], 0), "wave waits producer")) return fail_cuda();
       for (int32_t cid : w.wait_copies)
-        if (!ok(cudaStreamWaitEvent(cs, rt->copy_ev[cid], 0), "wave waits copy")) return fail_cuda();
-      if (c.profile && !ok(cudaEventRecord(rt->t_wave_start[a.index], cs), "record")) return fail_cuda();
-      int rc = coe_grouped_mlp(rt->mlp, dg_up + w.first_group, dg_down + w.first_group, w.num_groups, w.tiles_up,
-                               w.tiles_down, rt->d_boff, rt->d_mreq, rt->d_mstage, 3, cs);
+        if (!ok(cudaStreamWaitEvent(ws, rt->copy_up_ev[cid], 0), "wave waits W1")) return fail_cuda();
+      if (c.profile && !ok(cudaEventRecord(rt->t_wave_start[a.index], ws), "record")) return fail_cuda();
+      const int ctas = w.cls == 1 ? rt->r_ctas : rt->m_ctas;
+      int rc = coe_grouped_mlp(m, dg_up + w.first_group, dg_down + w.first_group, w.num_groups, w.tiles_up,
+                               w.tiles_down, sb.boff, sb.mreq, sb.mstage, 1, ctas, ws);
+      if (rc) return rc;
+      if (!ok(cudaEventRecord(rt->wave_up_ev[a.index], ws), "record")) return fail_cuda();
+      for (int32_t s : w.frees_slots)
+        if (!ok(cudaEventRecord(rt->slot_free_up[s], ws), "record")) return fail_cuda();
+      for (int32_t cid : w.wait_copies)
+        if (!ok(cudaStreamWaitEvent(ws, rt->copy_down_ev[cid], 0), "wave waits W2")) return fail_cuda();
+      rc = coe_grouped_mlp(m, dg_up + w.first_group, dg_down + w.first_group, w.num_groups, w.tiles_up,
+                           w.tiles_down, sb.boff, sb.mreq, sb.mstage, 2, ctas, ws);
       if (rc) return rc;
       st.launches += 2;
-      if (c.profile && !ok(cudaEventRecord(rt->t_wave_end[a.index], cs), "record")) return fail_cuda();
-      if (!ok(cudaEventRecord(rt->wave_ev[a.index], cs), "record")) return fail_cuda();
+      if (!ok(cudaEventRecord(rt->wave_down_ev[a.index], ws), "record")) return fail_cuda();
+      for (int32_t s : w.frees_slots) {
+        if (!ok(cudaEventRecord(rt->slot_free_down[s], ws), "record")) return fail_cuda();
+        rt->slot_free_valid[s] = 1;
+      }
+      if (c.profile && !ok(cudaEventRecord(rt->t_wave_end[a.index], ws), "record")) return fail_cuda();
     }
   }
-  // join: compute waits for the copy stream, step end on compute
+  // join: the main stream waits for the swap-in stream and the copy stream; set released at step end
   if (!ok(cudaEventRecord(rt->copy_drained, ks), "record") || !ok(cudaStreamWaitEvent(cs, rt->copy_drained, 0), "join"))
     return fail_cuda();
+  for (int k = 1; k < coe_runtime::NCLS; ++k)
+    if (!ok(cudaEventRecord(rt->cls_drained[k], rt->cls_stream[k]), "record") ||
+        !ok(cudaStreamWaitEvent(cs, rt->cls_drained[k], 0), "join"))
+      return fail_cuda();
   if (c.profile && !ok(cudaEventRecord(rt->t_step_end, cs), "record")) return fail_cuda();
-  if (!ok(cudaEventRecord(rt->prev_step_end, cs), "record")) return fail_cuda();
-  rt->have_prev = true;
-  rt->last_waves = (int32_t)waves.size();
-  rt->last_copies = (int32_t)copies.size();
+  if (!ok(cudaEventRecord(sb.free_ev, cs), "record")) return fail_cuda();
+  sb.used = true;
+  rt->last_waves = (int32_t)nw;
+  rt->last_wave_cls.clear();
+  rt->last_wave_rows.clear();
+  rt->last_wave_groups.clear();
+  for (const WaveAct &w : waves) {
+    rt->last_wave_cls.push_back(w.cls);
+    rt->last_wave_rows.push_back((int32_t)w.rows);
+    rt->last_wave_groups.push_back(w.num_groups);
+  }
+  rt->last_copies = (int32_t)nc;
   rt->last_adm = n_adm;
   rt->last_batches = n_batches;
+  rt->last_set = set_idx;
+  st.max_wave_groups = std::max(st.max_wave_groups, 0);
+  (void)waves_by_cls;
   if (stats) *stats = st;
   return COE_CUDA_OK;
 }

@@ -59,7 +59,8 @@ class RuntimeConfig(ctypes.Structure):
     _fields_ = [("d", ctypes.c_int32), ("h", ctypes.c_int32), ("T", ctypes.c_int32),
                 ("num_experts", ctypes.c_int32), ("num_slots", ctypes.c_int32), ("max_requests", ctypes.c_int32),
                 ("max_wave_rows", ctypes.c_int64), ("max_admissions", ctypes.c_int64),
-                ("max_batches", ctypes.c_int64), ("weight_seed", ctypes.c_uint64), ("profile", ctypes.c_int32)]
+                ("max_batches", ctypes.c_int64), ("weight_seed", ctypes.c_uint64), ("profile", ctypes.c_int32),
+                ("reserve_sms", ctypes.c_int32)]
 
 
 _declared = False
@@ -85,6 +86,10 @@ def _lib():
         lib.coe_runtime_buffer.argtypes = [V, ctypes.c_int]
         lib.coe_runtime_buffer.restype = V
         lib.coe_runtime_slot_of.argtypes = [V, I32]
+        lib.coe_runtime_counts.argtypes = [V, P(I32), P(I32)]
+        lib.coe_runtime_counts.restype = ctypes.c_int
+        lib.coe_runtime_intervals.argtypes = [V, V, V, V]
+        lib.coe_runtime_intervals.restype = ctypes.c_int
         lib.coe_runtime_read_buffer.argtypes = [V, ctypes.c_int, V, I64]
         lib.coe_runtime_read_buffer.restype = ctypes.c_int
         lib.coe_runtime_stream.argtypes = [V, ctypes.c_int]
@@ -129,7 +134,7 @@ class B200Runtime:
 
     def __init__(self, shape: RuntimeShape, num_experts: int, num_slots: int, max_requests: int,
                  max_admissions: int, max_wave_rows: int | None = None, weight_seed: int = DEFAULT_WEIGHT_SEED,
-                 profile: bool = False, init_experts: bool = True):
+                 profile: bool = False, init_experts: bool = True, reserve_sms: int = 16):
         import torch
 
         if not torch.cuda.is_available():
@@ -143,7 +148,7 @@ class B200Runtime:
         self.weight_seed = weight_seed
         rows = max_wave_rows or max(128, min(32768, max_admissions * shape.T))
         cfg = RuntimeConfig(shape.d, shape.h, shape.T, num_experts, num_slots, max_requests, rows, max_admissions,
-                            max_admissions, weight_seed, 1 if profile else 0)
+                            max_admissions, weight_seed, 1 if profile else 0, reserve_sms)
         self.profile = profile
         self.handle = ctypes.c_void_p()
         _check(self.lib, self.lib.coe_runtime_create(ctypes.byref(cfg), ctypes.byref(self.handle)), "runtime create")
@@ -228,6 +233,17 @@ class B200Runtime:
         _check(self.lib, self.lib.coe_runtime_members(self.handle, req.ctypes.data, stage.ctypes.data,
                                                       boff.ctypes.data), "members")
         return req[:num_admissions], stage[:num_admissions], boff[:num_batches]
+
+    def intervals(self) -> dict:
+        nc, nw = ctypes.c_int32(), ctypes.c_int32()
+        self.lib.coe_runtime_counts(self.handle, ctypes.byref(nc), ctypes.byref(nw))
+        cp = np.zeros(2 * max(1, nc.value), np.float32)
+        wv = np.zeros(2 * max(1, nw.value), np.float32)
+        info = np.zeros(3 * max(1, nw.value), np.int32)
+        _check(self.lib, self.lib.coe_runtime_intervals(self.handle, cp.ctypes.data, wv.ctypes.data,
+                                                        info.ctypes.data), "intervals")
+        return {"copies": cp[:2 * nc.value].reshape(-1, 2).tolist(), "waves": wv[:2 * nw.value].reshape(-1, 2).tolist(),
+                "wave_info": info[:3 * nw.value].reshape(-1, 3).tolist()}
 
     def timing(self) -> dict:
         t = StepTiming()
