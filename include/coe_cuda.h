@@ -112,6 +112,8 @@ typedef struct coe_runtime_config {
   uint64_t weight_seed;     /* synthetic expert weights, see coe_expert_seed         */
   int32_t profile;          /* record per-copy / per-wave events for overlap stats   */
   int32_t reserve_sms;      /* SMs kept for the swap-in-gating waves (0: no split)   */
+  int32_t swapped_stream;   /* experiments: waves on experts swapped in this step on
+                               their own stream (default 0: main stream)             */
 } coe_runtime_config;
 
 typedef struct coe_step_input {
@@ -163,6 +165,10 @@ int coe_runtime_timing(coe_runtime *rt, coe_step_timing *out);
 /* profile mode: per-copy [start,end) and per-wave [start,end) ms since step start,
  * wave_info = (stream class, rows, groups) per wave; sizes from coe_runtime_counts */
 int coe_runtime_counts(coe_runtime *rt, int32_t *copies, int32_t *waves);
+/* K3 in isolation on the runtime's buffers: one wave of `groups` batches x
+ * `requests_per_group` requests; average up / down projection launch times */
+int coe_runtime_bench_mlp(coe_runtime *rt, int32_t groups, int32_t requests_per_group, int32_t iters,
+                          float *up_ms, float *down_ms);
 int coe_runtime_intervals(coe_runtime *rt, float *copy_iv, float *wave_iv, int32_t *wave_info);
 /* device pointers (tests / benches): 0 X, 1 P0, 2 P1, 3 H scratch, 4 slot slab */
 void *coe_runtime_buffer(coe_runtime *rt, int which);

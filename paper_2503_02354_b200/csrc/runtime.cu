@@ -475,6 +475,65 @@ int coe_runtime_timing(coe_runtime *rt, coe_step_timing *out) {
   return COE_CUDA_OK;
 }
 
+int coe_runtime_bench_mlp(coe_runtime *rt, int32_t groups, int32_t requests_per_group, int32_t iters,
+                          float *up_ms, float *down_ms) {
+  const auto &c = rt->cfg;
+  const int64_t rows = (int64_t)requests_per_group * c.T;
+  const int32_t nreq = groups * requests_per_group;
+  if (groups < 1 || requests_per_group < 1 || nreq > c.max_requests || rows * groups > c.max_wave_rows ||
+      groups > coe_mlp_max_groups()) {
+    coe_set_error("bench_mlp: wave does not fit the runtime's buffers");
+    return COE_CUDA_ERR_CONFIG;
+  }
+  std::vector<coe_mlp_group> gu(groups), gd(groups);
+  std::vector<int32_t> boff(groups), mreq(nreq), mst(nreq, 0);
+  int tu = 0, td = 0;
+  for (int32_t g = 0; g < groups; ++g) {
+    const int32_t mt = (int32_t)((rows + BM - 1) / BM);
+    gu[g] = coe_mlp_group{(int32_t)rows, g % c.num_slots, g, (int32_t)(g * rows), tu, {0, 0, 0}};
+    gd[g] = gu[g];
+    gd[g].tile_start = td;
+    tu += mt * (c.h / BN);
+    td += mt * (c.d / BN);
+    boff[g] = g * requests_per_group;
+  }
+  for (int32_t r = 0; r < nreq; ++r) mreq[r] = r;
+  coe_mlp_group *d_g = nullptr;
+  int32_t *d_i = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr;
+  bool good = dmalloc(&d_g, 2 * sizeof(coe_mlp_group) * groups, "bench alloc") &&
+              dmalloc(&d_i, 4 * (size_t)(groups + 2 * nreq), "bench alloc") &&
+              ok(cudaMemcpy(d_g, gu.data(), sizeof(coe_mlp_group) * groups, cudaMemcpyHostToDevice), "bench H2D") &&
+              ok(cudaMemcpy(d_g + groups, gd.data(), sizeof(coe_mlp_group) * groups, cudaMemcpyHostToDevice), "H2D") &&
+              ok(cudaMemcpy(d_i, boff.data(), 4 * groups, cudaMemcpyHostToDevice), "H2D") &&
+              ok(cudaMemcpy(d_i + groups, mreq.data(), 4 * (size_t)nreq, cudaMemcpyHostToDevice), "H2D") &&
+              ok(cudaMemcpy(d_i + groups + nreq, mst.data(), 4 * (size_t)nreq, cudaMemcpyHostToDevice), "H2D") &&
+              ok(cudaEventCreate(&e0), "event") && ok(cudaEventCreate(&e1), "event") && ok(cudaEventCreate(&e2), "event");
+  cudaStream_t cs = rt->compute;
+  float tot_up = 0.f, tot_down = 0.f;
+  for (int it = -2; good && it < iters; ++it) {  // two untimed warm-up launches
+    good = ok(cudaEventRecord(e0, cs), "record") &&
+           coe_grouped_mlp(rt->mlp[0], d_g, d_g + groups, groups, tu, td, d_i, d_i + groups, d_i + groups + nreq, 1, 0,
+                           cs) == COE_CUDA_OK &&
+           ok(cudaEventRecord(e1, cs), "record") &&
+           coe_grouped_mlp(rt->mlp[0], d_g, d_g + groups, groups, tu, td, d_i, d_i + groups, d_i + groups + nreq, 2, 0,
+                           cs) == COE_CUDA_OK &&
+           ok(cudaEventRecord(e2, cs), "record") && ok(cudaEventSynchronize(e2), "sync");
+    if (good && it >= 0) {
+      tot_up += elapsed(e0, e1);
+      tot_down += elapsed(e1, e2);
+    }
+  }
+  if (d_g) cudaFree(d_g);
+  if (d_i) cudaFree(d_i);
+  for (cudaEvent_t e : {e0, e1, e2})
+    if (e) cudaEventDestroy(e);
+  if (!good) return COE_CUDA_ERR_CUDA;
+  *up_ms = tot_up / iters;
+  *down_ms = tot_down / iters;
+  return COE_CUDA_OK;
+}
+
 int coe_runtime_intervals(coe_runtime *rt, float *copy_iv, float *wave_iv, int32_t *wave_info) {
   if (!rt->cfg.profile) {
     coe_set_error("runtime created without profile events");
@@ -667,7 +726,10 @@ int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_step_stats *
     const int32_t s = rt->expert_slot[e];
     // the swap-in stream runs only the last readers of slots a later load overwrites: their
     // completion gates the copy engine, which is the bottleneck of budgeted configs
-    const int cls = releases[k] ? 1 : (slot_copy[s] >= 0 ? 2 : 0);
+    // class 2 (a separate stream for experts swapped in this step) measured slower than
+    // sharing the main stream (c3: 1117 vs 1068 ms/step): the two low-priority streams
+    // starve each other's cross-stream producers.  Kept selectable for experiments.
+    const int cls = releases[k] ? 1 : ((slot_copy[s] >= 0 && c.swapped_stream) ? 2 : 0);
     const int64_t rows = (int64_t)op.count * c.T;
     if (rows > c.max_wave_rows) {
       coe_set_error("a single batch exceeds the H scratch rows");

@@ -60,7 +60,7 @@ class RuntimeConfig(ctypes.Structure):
                 ("num_experts", ctypes.c_int32), ("num_slots", ctypes.c_int32), ("max_requests", ctypes.c_int32),
                 ("max_wave_rows", ctypes.c_int64), ("max_admissions", ctypes.c_int64),
                 ("max_batches", ctypes.c_int64), ("weight_seed", ctypes.c_uint64), ("profile", ctypes.c_int32),
-                ("reserve_sms", ctypes.c_int32)]
+                ("reserve_sms", ctypes.c_int32), ("swapped_stream", ctypes.c_int32)]
 
 
 _declared = False
@@ -86,6 +86,8 @@ def _lib():
         lib.coe_runtime_buffer.argtypes = [V, ctypes.c_int]
         lib.coe_runtime_buffer.restype = V
         lib.coe_runtime_slot_of.argtypes = [V, I32]
+        lib.coe_runtime_bench_mlp.argtypes = [V, I32, I32, I32, P(ctypes.c_float), P(ctypes.c_float)]
+        lib.coe_runtime_bench_mlp.restype = ctypes.c_int
         lib.coe_runtime_counts.argtypes = [V, P(I32), P(I32)]
         lib.coe_runtime_counts.restype = ctypes.c_int
         lib.coe_runtime_intervals.argtypes = [V, V, V, V]
@@ -148,7 +150,7 @@ class B200Runtime:
         self.weight_seed = weight_seed
         rows = max_wave_rows or max(128, min(32768, max_admissions * shape.T))
         cfg = RuntimeConfig(shape.d, shape.h, shape.T, num_experts, num_slots, max_requests, rows, max_admissions,
-                            max_admissions, weight_seed, 1 if profile else 0, reserve_sms)
+                            max_admissions, weight_seed, 1 if profile else 0, reserve_sms, 0)
         self.profile = profile
         self.handle = ctypes.c_void_p()
         _check(self.lib, self.lib.coe_runtime_create(ctypes.byref(cfg), ctypes.byref(self.handle)), "runtime create")
@@ -244,6 +246,12 @@ class B200Runtime:
                                                         info.ctypes.data), "intervals")
         return {"copies": cp[:2 * nc.value].reshape(-1, 2).tolist(), "waves": wv[:2 * nw.value].reshape(-1, 2).tolist(),
                 "wave_info": info[:3 * nw.value].reshape(-1, 3).tolist()}
+
+    def bench_mlp(self, groups: int, requests_per_group: int, iters: int = 10) -> tuple:
+        up, down = ctypes.c_float(), ctypes.c_float()
+        _check(self.lib, self.lib.coe_runtime_bench_mlp(self.handle, groups, requests_per_group, iters,
+                                                        ctypes.byref(up), ctypes.byref(down)), "bench_mlp")
+        return up.value, down.value
 
     def timing(self) -> dict:
         t = StepTiming()

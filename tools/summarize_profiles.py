@@ -1,0 +1,86 @@
+"""Summarise ncu outputs from gpurun_out/ into profiles/ (tracked).
+
+    python tools/summarize_profiles.py <round-tag>
+Reads gpurun_out/launches.csv (gpu__time_duration.sum launch list) and
+gpurun_out/k3_full.ncu-rep (--set full capture of grouped_gemm_kernel).
+"""
+import collections, csv, io, json, os, subprocess, sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+OUT = os.path.join(ROOT, "gpurun_out")
+PROF = os.path.join(ROOT, "profiles")
+tag = sys.argv[1] if len(sys.argv) > 1 else "r1"
+os.makedirs(PROF, exist_ok=True)
+SCALE = {"ns": 1e-6, "nsecond": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0, "s": 1e3, "second": 1e3}
+
+
+def launches():
+    path = os.path.join(OUT, "launches.csv")
+    if not os.path.exists(path):
+        return None
+    rows = list(csv.reader(open(path)))
+    hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+    hdr, data = rows[hi], rows[hi + 1:]
+    ki, mi, vi, ui = (hdr.index(n) for n in ("Kernel Name", "Metric Name", "Metric Value", "Metric Unit"))
+    tot, cnt = collections.defaultdict(float), collections.Counter()
+    for r in data:
+        if len(r) <= max(ki, mi, vi, ui) or r[mi] != "gpu__time_duration.sum":
+            continue
+        name = r[ki].replace("<unnamed>::", "").split("(")[0]
+        tot[name] += float(r[vi].replace(",", "")) * SCALE[r[ui]]
+        cnt[name] += 1
+    total = sum(tot.values())
+    lines = [f"# ncu launch list ({sum(cnt.values())} launches, serialised + cold-cache: compare SHARES)",
+             f"{'kernel':58s} {'launches':>8s} {'total_ms':>10s} {'share':>7s}"]
+    for k, v in sorted(tot.items(), key=lambda x: -x[1]):
+        lines.append(f"{k[:58]:58s} {cnt[k]:8d} {v:10.2f} {100 * v / total:6.2f}%")
+    lines.append(f"{'TOTAL':58s} {sum(cnt.values()):8d} {total:10.2f}")
+    return "\n".join(lines) + "\n", {k: {"launches": cnt[k], "ms": tot[k], "share": tot[k] / total} for k in tot}
+
+
+def full():
+    path = os.path.join(OUT, "k3_full.ncu-rep")
+    if not os.path.exists(path):
+        return None
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units, data = rows[0], rows[1], rows[2:]
+    keys = {
+        "duration_ms": "gpu__time_duration.sum",
+        "dram_read": "dram__bytes_read.sum",
+        "dram_write": "dram__bytes_write.sum",
+        "tensor_utchmma_pct": "sm__ops_path_tensor_op_utchmma_src_bf16_dst_fp32_sparsity_off.avg.pct_of_peak_sustained_elapsed",
+        "tensor_pipe_realtime_pct": "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+        "dram_throughput_pct": "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+        "sm_clock_ghz": "sm__cycles_elapsed.avg.per_second",
+        "registers": "launch__registers_per_thread",
+        "grid": "launch__grid_size",
+    }
+    unit_scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ms": 1, "msecond": 1, "us": 1e-3,
+                  "usecond": 1e-3, "ns": 1e-6, "nsecond": 1e-6}
+    out = []
+    for r in data:
+        rec = {}
+        for k, m in keys.items():
+            if m in hdr:
+                i = hdr.index(m)
+                rec[k] = float(r[i].replace(",", "")) * unit_scale.get(units[i], 1)
+        out.append(rec)
+    return out
+
+
+res = launches()
+if res:
+    text, table = res
+    open(os.path.join(PROF, f"{tag}_launches_summary.txt"), "w").write(text)
+    print(text)
+kf = full()
+if kf:
+    k3 = {"launches": kf, "note": "ncu --set full --clock-control none, tools/k3_profile.py 16 8: one wave of 16 "
+                                  "batches x 8 requests x T=256 (32768 rows), d=4096 h=12288; launch 0 = up "
+                                  "projection (gelu), launch 1 = down projection",
+          "flops_per_launch": 2.0 * 32768 * 4096 * 12288}
+    k3["dram_bytes_per_wave"] = sum(l["dram_read"] + l["dram_write"] for l in kf)
+    k3["algorithmic_bytes_per_wave"] = 2 * (16 * 4096 * 12288 * 2) + 2 * (32768 * 4096 * 2) + 2 * (32768 * 12288 * 2)
+    json.dump(k3, open(os.path.join(PROF, f"k3_ncu_summary.json"), "w"), indent=1)
+    print(json.dumps(k3, indent=1))
