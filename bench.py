@@ -197,7 +197,14 @@ def main() -> None:
     cfg = configs.run_config(w, trace=False)
     plan0 = engine.plan(cfg)
     n_req = len(plan0.resolved.request_ids)
-    rt = runtime.B200Runtime.for_plan(plan0, shape, executor=rank, profile=True)
+    store_path = None
+    if world > 1:  # one shared pinned expert store per node instead of one per rank
+        store_path = f"/dev/shm/coe_store_{args.config}_{os.environ.get('MASTER_PORT', '0')}"
+    rt = runtime.B200Runtime.for_plan(plan0, shape, executor=rank, profile=True, store_path=store_path,
+                                      init_experts=(local == 0))
+    if dist is not None:
+        dist.barrier()  # local rank 0 has filled the shared store
+        rt.attach_comm(rank, world)
     rt.fill_inputs(n_req)
     stream = torch.cuda.ExternalStream(rt.stream_handle(0))
 
@@ -283,6 +290,9 @@ def main() -> None:
                          f"+ {res['loads']} swap-in memcpys"}
 
     if rank != 0:
+        if dist is not None:
+            dist.barrier()
+            dist.destroy_process_group()
         return
     peaks, peak_src = load_peaks()
     flops = algorithmic_flops(plan_last, shape)
@@ -343,6 +353,9 @@ def main() -> None:
     }
     print(json.dumps(line), flush=True)
     if dist is not None:
+        dist.barrier()
+        if store_path and os.path.exists(store_path):
+            os.unlink(store_path)
         dist.destroy_process_group()
 
 

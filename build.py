@@ -21,7 +21,17 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = "-gencode=arch=compute_100a,code=sm_100a"
 
 PLANNER_SOURCES = ["planner.cpp"]
-CUDA_SOURCES = ["group_sort.cu", "grouped_mlp.cu", "runtime.cu"]
+CUDA_SOURCES = ["group_sort.cu", "grouped_mlp.cu", "runtime.cu", "comm.cu"]
+
+
+def _nccl_include() -> str:
+    try:
+        import nvidia.nccl
+
+        return os.path.join(list(nvidia.nccl.__path__)[0], "include")
+    except Exception:  # pragma: no cover
+        return "/usr/include"
+
 
 
 def _run(cmd: list) -> None:
@@ -44,7 +54,7 @@ def build_planner(force: bool = False) -> str:
     if force or _stale(out, srcs):
         # -ffp-contract=off: the virtual clock must round exactly like CPython floats
         _run(["g++", "-O2", "-std=c++17", "-fPIC", "-shared", "-ffp-contract=off", "-fno-fast-math",
-              "-Wall", f"-I{INCLUDE}", *srcs, "-o", out])
+              "-Wall", f"-I{INCLUDE}", f"-I{CSRC}", *srcs, "-o", out])
     return out
 
 
@@ -54,7 +64,8 @@ def build_cuda(force: bool = False) -> str:
     if force or _stale(out, srcs):
         _run([NVCC, ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
               "--expt-relaxed-constexpr", "-Xptxas", "-v,-warn-spills", f"-I{INCLUDE}", f"-I{CSRC}",
-              *srcs, "-o", out])
+              f"-I{_nccl_include()}",
+              *srcs, "-o", out, "-ldl"])
     return out
 
 

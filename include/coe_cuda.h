@@ -114,6 +114,8 @@ typedef struct coe_runtime_config {
   int32_t reserve_sms;      /* SMs kept for the swap-in-gating waves (0: no split)   */
   int32_t swapped_stream;   /* experiments: waves on experts swapped in this step on
                                their own stream (default 0: main stream)             */
+  const char *store_path;   /* NULL: private pinned store; else a shared file mapping
+                               (one copy per node for N ranks; host-registered)     */
 } coe_runtime_config;
 
 typedef struct coe_step_input {
@@ -177,6 +179,19 @@ int coe_runtime_read_buffer(coe_runtime *rt, int which, void *host, int64_t byte
 int coe_runtime_slot_of(coe_runtime *rt, int32_t expert);
 cudaStream_t coe_runtime_stream(coe_runtime *rt, int which);
 uint64_t coe_expert_seed(uint64_t weight_seed, int32_t expert, int32_t matrix);
+
+/* ---------------- follow-up hops (NCCL over NVLink) ----------------------- */
+
+/* A communicator for hop traffic (NCCL 2.28, dlopen'ed from nccl_path; NULL =
+ * "libnccl.so.2").  Rank 0 creates the 128-byte unique id, the host
+ * distributes it (torch.distributed), every rank calls coe_comm_create. */
+typedef struct coe_comm coe_comm;
+int coe_comm_unique_id(const char *nccl_path, void *out128);
+int coe_comm_create(const char *nccl_path, int rank, int world, const void *id128, coe_comm **out);
+void coe_comm_destroy(coe_comm *c);
+/* Attach to a runtime (rank == the executor it serves); steps then exchange
+ * hopped activations on a dedicated hop stream. */
+int coe_runtime_attach_comm(coe_runtime *rt, coe_comm *comm);
 
 /* ---------------- seeded synthetic data ---------------------------------- */
 

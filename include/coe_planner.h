@@ -167,6 +167,13 @@ const int32_t *coe_plan_op_args(const coe_plan *plan);   /* victims: expert ids;
 int64_t coe_plan_num_admissions(const coe_plan *plan);
 const coe_admission *coe_plan_admissions(const coe_plan *plan);
 
+/* Cross-executor follow-up hops in global (admission) order: the output of
+ * `stage` of `request` moves src -> dst (engine.py:751-753 admits the
+ * follow-up on another executor).  Returns the hop count; fills at most
+ * `capacity` entries.  Requires record_ops. */
+int64_t coe_plan_hops(const coe_plan *plan, int64_t capacity, int64_t *index, int32_t *src, int32_t *dst,
+                      int32_t *request, int32_t *stage);
+
 #ifdef __cplusplus
 }
 #endif

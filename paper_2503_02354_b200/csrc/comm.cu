@@ -1,0 +1,108 @@
+// comm.cu -- NCCL point-to-point for follow-up hops (loaded with dlopen).
+//
+// The runtime moves a hopped request's T x d activation from the GPU that ran
+// its previous stage to the GPU its next stage was assigned to
+// (engine.py:751-753 admits the follow-up there).  NCCL 2.28 (the library
+// torch ships, site-packages/nvidia/nccl) is dlopen'ed so the kernel library
+// has no link-time NCCL dependency; one communicator per runtime, all hop
+// traffic on the runtime's hop stream, one ncclSend / ncclRecv per hop in the
+// global hop order (hops.h).
+#include <dlfcn.h>
+
+#include <cstring>
+#include <string>
+
+#include "coe_cuda.h"
+#include "comm.h"
+#include "common.cuh"
+
+namespace {
+
+struct NcclApi {
+  void *handle = nullptr;
+  ncclResult_t (*get_unique_id)(ncclUniqueId *) = nullptr;
+  ncclResult_t (*comm_init_rank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  const char *(*error_string)(ncclResult_t) = nullptr;
+};
+
+NcclApi g_nccl;
+
+bool load_nccl(const char *path) {
+  if (g_nccl.handle) return true;
+  void *h = dlopen(path && *path ? path : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) {
+    coe_set_error(std::string("dlopen NCCL failed: ") + dlerror());
+    return false;
+  }
+  g_nccl.handle = h;
+  g_nccl.get_unique_id = reinterpret_cast<decltype(g_nccl.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+  g_nccl.comm_init_rank = reinterpret_cast<decltype(g_nccl.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+  g_nccl.comm_destroy = reinterpret_cast<decltype(g_nccl.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+  g_nccl.send = reinterpret_cast<decltype(g_nccl.send)>(dlsym(h, "ncclSend"));
+  g_nccl.recv = reinterpret_cast<decltype(g_nccl.recv)>(dlsym(h, "ncclRecv"));
+  g_nccl.error_string = reinterpret_cast<decltype(g_nccl.error_string)>(dlsym(h, "ncclGetErrorString"));
+  if (!g_nccl.get_unique_id || !g_nccl.comm_init_rank || !g_nccl.send || !g_nccl.recv) {
+    coe_set_error("NCCL library lacks point-to-point symbols");
+    return false;
+  }
+  return true;
+}
+
+bool nccl_ok(ncclResult_t r, const char *what) {
+  if (r == ncclSuccess) return true;
+  coe_set_error(std::string(what) + ": " + (g_nccl.error_string ? g_nccl.error_string(r) : "nccl error"));
+  return false;
+}
+
+}  // namespace
+
+struct coe_comm {
+  ncclComm_t comm = nullptr;
+  int rank = 0, world = 1;
+};
+
+bool coe_comm_send_bf16(coe_comm *c, const void *buf, size_t count, int peer, cudaStream_t stream) {
+  return nccl_ok(g_nccl.send(buf, count, ncclBfloat16, peer, c->comm, stream), "ncclSend");
+}
+
+bool coe_comm_recv_bf16(coe_comm *c, void *buf, size_t count, int peer, cudaStream_t stream) {
+  return nccl_ok(g_nccl.recv(buf, count, ncclBfloat16, peer, c->comm, stream), "ncclRecv");
+}
+
+int coe_comm_rank(const coe_comm *c) { return c->rank; }
+
+extern "C" {
+
+int coe_comm_unique_id(const char *nccl_path, void *out128) {
+  if (!load_nccl(nccl_path)) return COE_CUDA_ERR_CONFIG;
+  ncclUniqueId id;
+  if (!nccl_ok(g_nccl.get_unique_id(&id), "ncclGetUniqueId")) return COE_CUDA_ERR_CUDA;
+  std::memcpy(out128, &id, sizeof(id));
+  return COE_CUDA_OK;
+}
+
+int coe_comm_create(const char *nccl_path, int rank, int world, const void *id128, coe_comm **out) {
+  if (!load_nccl(nccl_path)) return COE_CUDA_ERR_CONFIG;
+  ncclUniqueId id;
+  std::memcpy(&id, id128, sizeof(id));
+  auto *c = new coe_comm();
+  c->rank = rank;
+  c->world = world;
+  if (!nccl_ok(g_nccl.comm_init_rank(&c->comm, world, id, rank), "ncclCommInitRank")) {
+    delete c;
+    return COE_CUDA_ERR_CUDA;
+  }
+  *out = c;
+  return COE_CUDA_OK;
+}
+
+void coe_comm_destroy(coe_comm *c) {
+  if (!c) return;
+  if (c->comm && g_nccl.comm_destroy) g_nccl.comm_destroy(c->comm);
+  delete c;
+}
+
+}  // extern "C"

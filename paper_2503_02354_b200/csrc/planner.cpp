@@ -23,6 +23,7 @@
 // and one admission record per (request, stage) for the GPU grouping kernel.
 
 #include "coe_planner.h"
+#include "hops.h"
 
 #include <algorithm>
 #include <chrono>
@@ -838,6 +839,20 @@ const coe_op *coe_plan_ops(const coe_plan *p) { return p->ops.data(); }
 int64_t coe_plan_num_op_args(const coe_plan *p) { return (int64_t)p->op_args.size(); }
 const int32_t *coe_plan_op_args(const coe_plan *p) { return p->op_args.data(); }
 int64_t coe_plan_num_admissions(const coe_plan *p) { return (int64_t)p->adms.size(); }
+
+int64_t coe_plan_hops(const coe_plan *p, int64_t capacity, int64_t *index, int32_t *src, int32_t *dst,
+                      int32_t *request, int32_t *stage) {
+  std::vector<coe::Hop> hops = coe::hop_schedule(p->adms.data(), (int64_t)p->adms.size(), p->R);
+  int64_t n = (int64_t)hops.size();
+  for (int64_t i = 0; i < n && i < capacity; ++i) {
+    index[i] = hops[i].index;
+    src[i] = hops[i].src;
+    dst[i] = hops[i].dst;
+    request[i] = hops[i].request;
+    stage[i] = hops[i].stage;
+  }
+  return n;
+}
 const coe_admission *coe_plan_admissions(const coe_plan *p) { return p->adms.data(); }
 
 }  // extern "C"

@@ -28,16 +28,23 @@
 // nothing else).  Pass 2 issues them.  Timing never feeds back into decisions.
 
 #include <cuda_bf16.h>
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <cstring>
+#include <climits>
 #include <string>
+#include <unordered_map>
 #include <unordered_set>
 #include <vector>
 
 #include "coe_cuda.h"
 #include "coe_planner.h"
+#include "comm.h"
 #include "common.cuh"
+#include "hops.h"
 
 namespace {
 
@@ -79,6 +86,8 @@ struct WaveAct {
   int64_t rows;
   std::vector<int32_t> wait_copies;  // W1 event before the up pass, W2 before the down pass
   std::vector<int32_t> wait_waves;   // other-stream waves producing this wave's inputs
+  std::vector<int32_t> wait_recvs;   // hops (local index) this wave consumes
+  int64_t min_send = INT64_MAX;      // smallest global index of a hop this wave produces
   std::vector<int32_t> frees_slots;  // slots whose last reader this step is this wave
 };
 
@@ -124,6 +133,8 @@ struct coe_runtime {
   void *d_sort_scratch = nullptr, *d_compact_scratch = nullptr;
   // host
   char *host_store = nullptr;
+  bool store_mapped = false;  // shared (mmap + cudaHostRegister) instead of cudaHostAlloc
+  size_t store_bytes = 0;
   char *staging[2] = {nullptr, nullptr};
   int64_t staging_bytes = 0;
   cudaEvent_t staging_done[2] = {nullptr, nullptr};
@@ -143,12 +154,18 @@ struct coe_runtime {
   std::vector<int32_t> last_wave_cls, last_wave_rows, last_wave_groups;
   int64_t last_adm = 0, last_batches = 0;
   int last_set = 0;
+  coe_comm *comm = nullptr;            // hop transport (N > 1)
+  cudaStream_t hop = nullptr;
+  std::vector<cudaEvent_t> recv_ev;
+  cudaEvent_t hop_drained = nullptr, step_end = nullptr;
+  bool have_step_end = false;
   int m_ctas = 148, r_ctas = 16;  // SM split: main waves vs the swap-in-gating waves
 
   ~coe_runtime() {
     for (auto st : cls_stream)
       if (st) cudaStreamSynchronize(st);
     if (copy) cudaStreamSynchronize(copy);
+    if (hop) cudaStreamSynchronize(hop);
     for (auto m : mlp)
       if (m) coe_mlp_destroy(m);
     std::vector<void *> dev = {slab, x, p0, p1, hbuf[0], hbuf[1], hbuf[2], outbuf, d_perm, d_keys, d_flags, d_last, d_sort_scratch,
@@ -161,19 +178,26 @@ struct coe_runtime {
     }
     for (void *p : dev)
       if (p) cudaFree(p);
-    for (void *p : {(void *)host_store, (void *)staging[0], (void *)staging[1], (void *)h_last})
+    for (void *p : {(void *)staging[0], (void *)staging[1], (void *)h_last})
       if (p) cudaFreeHost(p);
-    for (auto *v : {&slot_free_up, &slot_free_down, &wave_up_ev, &wave_down_ev, &copy_up_ev, &copy_down_ev,
+    if (host_store && store_mapped) {
+      cudaHostUnregister(host_store);
+      munmap(host_store, store_bytes);
+    } else if (host_store) {
+      cudaFreeHost(host_store);
+    }
+    for (auto *v : {&recv_ev, &slot_free_up, &slot_free_down, &wave_up_ev, &wave_down_ev, &copy_up_ev, &copy_down_ev,
                     &t_copy_start, &t_copy_end, &t_wave_start, &t_wave_end}) {
       for (auto e : *v) cudaEventDestroy(e);
       v->clear();
     }
-    for (cudaEvent_t e : {staged, copy_drained, grouped, cls_drained[0], cls_drained[1], cls_drained[2], t_step_start, t_group_end, t_step_end, staging_done[0],
+    for (cudaEvent_t e : {hop_drained, step_end, staged, copy_drained, grouped, cls_drained[0], cls_drained[1], cls_drained[2], t_step_start, t_group_end, t_step_end, staging_done[0],
                           staging_done[1]})
       if (e) cudaEventDestroy(e);
     for (auto st : cls_stream)
       if (st) cudaStreamDestroy(st);
     if (copy) cudaStreamDestroy(copy);
+    if (hop) cudaStreamDestroy(hop);
   }
 
   bool ensure_events(std::vector<cudaEvent_t> &v, size_t n, bool timing) {
@@ -233,6 +257,31 @@ float intersect_len(const std::vector<std::pair<float, float>> &a0, const std::v
 
 }  // namespace
 
+// The host tier: one pinned copy of every expert.  With store_path set (multi-GPU on one
+// node) the copy lives in a shared file mapping registered with every process's CUDA
+// context, so N ranks share one 60 GB store instead of pinning N copies.
+static bool rt_alloc_store(coe_runtime *rt, const char *path) {
+  rt->store_bytes = (size_t)rt->expert_bytes * rt->cfg.num_experts;
+  if (!path || !*path)
+    return ok(cudaHostAlloc(reinterpret_cast<void **>(&rt->host_store), rt->store_bytes, cudaHostAllocDefault),
+              "pinned expert store");
+  int fd = open(path, O_RDWR | O_CREAT, 0600);
+  if (fd < 0 || ftruncate(fd, (off_t)rt->store_bytes) != 0) {
+    if (fd >= 0) close(fd);
+    coe_set_error(std::string("cannot create shared expert store ") + path);
+    return false;
+  }
+  void *p = mmap(nullptr, rt->store_bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+  close(fd);
+  if (p == MAP_FAILED) {
+    coe_set_error("mmap of the shared expert store failed");
+    return false;
+  }
+  rt->host_store = static_cast<char *>(p);
+  rt->store_mapped = true;
+  return ok(cudaHostRegister(p, rt->store_bytes, cudaHostRegisterPortable), "cudaHostRegister expert store");
+}
+
 extern "C" {
 
 const char *coe_cuda_last_error(void) { return g_last_error.c_str(); }
@@ -256,6 +305,7 @@ int coe_runtime_create(const coe_runtime_config *cfg, coe_runtime **out) {
               ok(cudaStreamCreateWithPriority(&rt->cls_stream[1], cudaStreamNonBlocking, prio_high), "stream") &&
               ok(cudaStreamCreateWithPriority(&rt->cls_stream[2], cudaStreamNonBlocking, prio_low), "stream") &&
               ok(cudaStreamCreateWithFlags(&rt->copy, cudaStreamNonBlocking), "stream") &&
+              ok(cudaStreamCreateWithFlags(&rt->hop, cudaStreamNonBlocking), "stream") &&
               dmalloc(&rt->slab, (size_t)rt->expert_bytes * c.num_slots, "slab alloc") &&
               dmalloc(&rt->x, act_bytes, "X alloc") && dmalloc(&rt->p0, act_bytes, "P0 alloc") &&
               dmalloc(&rt->p1, act_bytes, "P1 alloc") && dmalloc(&rt->outbuf, act_bytes, "out alloc") &&
@@ -278,14 +328,14 @@ int coe_runtime_create(const coe_runtime_config *cfg, coe_runtime **out) {
     good = ok(cudaHostAlloc(reinterpret_cast<void **>(&rt->staging[0]), rt->staging_bytes, cudaHostAllocDefault), "staging") &&
            ok(cudaHostAlloc(reinterpret_cast<void **>(&rt->staging[1]), rt->staging_bytes, cudaHostAllocDefault), "staging") &&
            ok(cudaHostAlloc(reinterpret_cast<void **>(&rt->h_last), 4 * (size_t)c.max_requests, cudaHostAllocDefault), "last") &&
-           ok(cudaHostAlloc(reinterpret_cast<void **>(&rt->host_store), (size_t)rt->expert_bytes * c.num_experts,
-                            cudaHostAllocDefault),
-              "pinned expert store") &&
+           rt_alloc_store(rt, c.store_path) &&
            ok(cudaEventCreateWithFlags(&rt->staging_done[0], cudaEventDisableTiming), "event") &&
            ok(cudaEventCreateWithFlags(&rt->staging_done[1], cudaEventDisableTiming), "event") &&
            ok(cudaEventCreateWithFlags(&rt->staged, cudaEventDisableTiming), "event") &&
            ok(cudaEventCreateWithFlags(&rt->copy_drained, cudaEventDisableTiming), "event") &&
            ok(cudaEventCreateWithFlags(&rt->grouped, cudaEventDisableTiming), "event") &&
+           ok(cudaEventCreateWithFlags(&rt->hop_drained, cudaEventDisableTiming), "event") &&
+           ok(cudaEventCreateWithFlags(&rt->step_end, cudaEventDisableTiming), "event") &&
            ok(cudaEventCreateWithFlags(&rt->cls_drained[0], cudaEventDisableTiming), "event") &&
            ok(cudaEventCreateWithFlags(&rt->cls_drained[1], cudaEventDisableTiming), "event") &&
            ok(cudaEventCreateWithFlags(&rt->cls_drained[2], cudaEventDisableTiming), "event") &&
@@ -431,7 +481,7 @@ int coe_runtime_download_outputs(coe_runtime *rt, const int32_t *last_stage_host
 }
 
 int coe_runtime_synchronize(coe_runtime *rt) {
-  bool good = ok(cudaStreamSynchronize(rt->copy), "sync copy");
+  bool good = ok(cudaStreamSynchronize(rt->copy), "sync copy") && ok(cudaStreamSynchronize(rt->hop), "sync hop");
   for (int k = coe_runtime::NCLS - 1; k >= 0; --k) good = ok(cudaStreamSynchronize(rt->cls_stream[k]), "sync") && good;
   return good ? COE_CUDA_OK : fail_cuda();
 }
@@ -472,6 +522,11 @@ int coe_runtime_timing(coe_runtime *rt, coe_step_timing *out) {
   out->copy_busy_ms = union_len(cp);
   out->compute_busy_ms = union_len(wv);
   out->overlap_ms = intersect_len(cp, wv);
+  return COE_CUDA_OK;
+}
+
+int coe_runtime_attach_comm(coe_runtime *rt, coe_comm *comm) {
+  rt->comm = comm;
   return COE_CUDA_OK;
 }
 
@@ -609,6 +664,24 @@ int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_step_stats *
     }
   }
 
+  // ---- hops touching this executor (global admission order, hops.h) ----
+  const std::vector<coe::Hop> all_hops = coe::hop_schedule(adm, in->num_admissions, c.max_requests);
+  std::vector<int32_t> my_hops;                      // indices into all_hops, in global order
+  std::unordered_map<int64_t, int32_t> hop_in, hop_out;  // (request, consumer/producer stage) -> my_hops slot
+  auto hkey = [](int32_t r, int32_t st) { return ((int64_t)r << 8) | st; };
+  for (size_t i = 0; i < all_hops.size(); ++i) {
+    const coe::Hop &h = all_hops[i];
+    if (h.src != x && h.dst != x) continue;
+    if (h.dst == x) hop_in[hkey(h.request, h.stage + 1)] = (int32_t)my_hops.size();
+    if (h.src == x) hop_out[hkey(h.request, h.stage)] = (int32_t)my_hops.size();
+    my_hops.push_back((int32_t)i);
+  }
+  if (!my_hops.empty() && !rt->comm) {
+    coe_set_error("plan moves activations between executors: attach a communicator (coe_runtime_attach_comm)");
+    return COE_CUDA_ERR_CONFIG;
+  }
+  std::vector<int32_t> hop_producer_wave(my_hops.size(), -1);
+
   // ---- pass 1: slots, copies, waves on two compute streams ----
   std::vector<uint8_t> plan_res(c.num_experts, 0), pending_restore(c.num_experts, 0);
   std::vector<int32_t> slot_use_wave(c.num_slots, -1), slot_copy(c.num_slots, -1), slot_open_cls(c.num_slots, -1);
@@ -635,7 +708,7 @@ int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_step_stats *
     bool used = false;
     WaveAct w{};
     std::vector<coe_mlp_group> gu, gd;
-    std::vector<int32_t> slots, reqs;
+    std::vector<int32_t> slots, reqs, sends;
   } open[coe_runtime::NCLS];
   int64_t waves_by_cls[coe_runtime::NCLS] = {0, 0, 0};
 
@@ -655,6 +728,7 @@ int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_step_stats *
       req_writer[r] = id;
       req_open_cls[r] = -1;
     }
+    for (int32_t hslot : o.sends) hop_producer_wave[hslot] = id;
     st.max_wave_groups = std::max(st.max_wave_groups, o.w.num_groups);
     st.max_wave_rows = std::max(st.max_wave_rows, o.w.rows);
     waves.push_back(o.w);
@@ -735,6 +809,20 @@ int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_step_stats *
       coe_set_error("a single batch exceeds the H scratch rows");
       return COE_CUDA_ERR_CONFIG;
     }
+    // incoming hops: every open wave producing an earlier hop must be issued first, so the
+    // hop stream (global order) never waits on a wave that waits on it
+    int64_t need_recv = -1;
+    std::vector<int32_t> recvs;
+    for (int32_t j = 0; j < op.count; ++j) {
+      auto it = hop_in.find(hkey(in->op_args[op.offset + 2 * j], in->op_args[op.offset + 2 * j + 1]));
+      if (it != hop_in.end()) {
+        recvs.push_back(it->second);
+        need_recv = std::max<int64_t>(need_recv, all_hops[my_hops[it->second]].index);
+      }
+    }
+    if (need_recv >= 0)
+      for (int k2 = 0; k2 < coe_runtime::NCLS; ++k2)
+        if (open[k2].used && open[k2].w.min_send < need_recv) flush(k2);
     bool clash = false;
     for (int32_t j = 0; j < op.count; ++j) {
       const int32_t r = in->op_args[op.offset + 2 * j];
@@ -751,6 +839,14 @@ int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_step_stats *
     if (need_wait) {
       w.w.wait_copies.push_back(cp);
       copy_waited[cp] |= (1 << cls);
+    }
+    for (int32_t hslot : recvs) w.w.wait_recvs.push_back(hslot);
+    for (int32_t j = 0; j < op.count; ++j) {
+      auto it = hop_out.find(hkey(in->op_args[op.offset + 2 * j], in->op_args[op.offset + 2 * j + 1]));
+      if (it != hop_out.end()) {
+        w.sends.push_back(it->second);
+        w.w.min_send = std::min<int64_t>(w.w.min_send, all_hops[my_hops[it->second]].index);
+      }
     }
     for (int32_t j = 0; j < op.count; ++j) {
       const int32_t r = in->op_args[op.offset + 2 * j];
@@ -800,7 +896,8 @@ int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_step_stats *
   // ---- pass 2: issue ----
   const size_t nw = waves.size(), nc = copies.size();
   if (!rt->ensure_events(rt->wave_up_ev, nw, false) || !rt->ensure_events(rt->wave_down_ev, nw, false) ||
-      !rt->ensure_events(rt->copy_up_ev, nc, false) || !rt->ensure_events(rt->copy_down_ev, nc, false))
+      !rt->ensure_events(rt->copy_up_ev, nc, false) || !rt->ensure_events(rt->copy_down_ev, nc, false) ||
+      !rt->ensure_events(rt->recv_ev, my_hops.size(), false))
     return fail_cuda();
   if (c.profile && (!rt->ensure_events(rt->t_wave_start, nw, true) || !rt->ensure_events(rt->t_wave_end, nw, true) ||
                     !rt->ensure_events(rt->t_copy_start, nc, true) || !rt->ensure_events(rt->t_copy_end, nc, true)))
@@ -863,6 +960,36 @@ int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_step_stats *
   for (int k = 1; k < coe_runtime::NCLS; ++k)
     if (!ok(cudaStreamWaitEvent(rt->cls_stream[k], rt->grouped, 0), "class stream waits K2")) return fail_cuda();
 
+  // hop stream: starts after the previous step (its receives overwrite P rows) and issues
+  // this executor's sends / receives strictly in global hop order
+  if (!my_hops.empty() && rt->have_step_end && !ok(cudaStreamWaitEvent(rt->hop, rt->step_end, 0), "hop waits step"))
+    return fail_cuda();
+  size_t hop_cursor = 0;
+  int32_t waves_issued = 0;
+  const size_t row_elems = (size_t)rt->row_elems;
+  auto issue_hops_until = [&](int64_t limit) -> bool {
+    while (hop_cursor < my_hops.size() && all_hops[my_hops[hop_cursor]].index <= limit) {
+      const coe::Hop &h = all_hops[my_hops[hop_cursor]];
+      __nv_bfloat16 *row = ((h.stage & 1) ? rt->p1 : rt->p0) + (size_t)h.request * row_elems;
+      if (h.src == x) {
+        const int32_t pw = hop_producer_wave[hop_cursor];
+        if (pw < 0 || pw >= waves_issued) {
+          coe_set_error("internal: hop send issued before its producer wave");
+          return false;
+        }
+        if (!ok(cudaStreamWaitEvent(rt->hop, rt->wave_down_ev[pw], 0), "send waits producer") ||
+            !coe_comm_send_bf16(rt->comm, row, row_elems, h.dst, rt->hop))
+          return false;
+      } else {
+        if (!coe_comm_recv_bf16(rt->comm, row, row_elems, h.src, rt->hop) ||
+            !ok(cudaEventRecord(rt->recv_ev[hop_cursor], rt->hop), "record"))
+          return false;
+      }
+      ++hop_cursor;
+    }
+    return true;
+  };
+
   const coe_mlp_group *dg_up = sb.groups, *dg_down = sb.groups + n_batches;
   for (const Action &a : actions) {
     if (a.is_copy) {
@@ -892,6 +1019,13 @@ int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_step_stats *
       const WaveAct &w = waves[a.index];
       cudaStream_t ws = rt->cls_stream[w.cls];
       coe_mlp *m = rt->mlp[w.cls];
+      if (!w.wait_recvs.empty()) {
+        int64_t limit = -1;
+        for (int32_t hslot : w.wait_recvs) limit = std::max<int64_t>(limit, all_hops[my_hops[hslot]].index);
+        if (!issue_hops_until(limit)) return COE_CUDA_ERR_CUDA;
+        for (int32_t hslot : w.wait_recvs)
+          if (!ok(cudaStreamWaitEvent(ws, rt->recv_ev[hslot], 0), "wave waits hop")) return fail_cuda();
+      }
       for (int32_t wid : w.wait_waves)
         if (!ok(cudaStreamWaitEvent(ws, rt->wave_down_ev[wid], 0), "wave waits producer")) return fail_cuda();
       for (int32_t cid : w.wait_copies)
@@ -916,8 +1050,13 @@ int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_step_stats *
         rt->slot_free_valid[s] = 1;
       }
       if (c.profile && !ok(cudaEventRecord(rt->t_wave_end[a.index], ws), "record")) return fail_cuda();
+      waves_issued = a.index + 1;
     }
   }
+  if (!issue_hops_until(INT64_MAX)) return COE_CUDA_ERR_CUDA;
+  if (!my_hops.empty() && (!ok(cudaEventRecord(rt->hop_drained, rt->hop), "record") ||
+                           !ok(cudaStreamWaitEvent(cs, rt->hop_drained, 0), "join hop")))
+    return fail_cuda();
   // join: the main stream waits for the swap-in stream and the copy stream; set released at step end
   if (!ok(cudaEventRecord(rt->copy_drained, ks), "record") || !ok(cudaStreamWaitEvent(cs, rt->copy_drained, 0), "join"))
     return fail_cuda();
@@ -926,7 +1065,9 @@ int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_step_stats *
         !ok(cudaStreamWaitEvent(cs, rt->cls_drained[k], 0), "join"))
       return fail_cuda();
   if (c.profile && !ok(cudaEventRecord(rt->t_step_end, cs), "record")) return fail_cuda();
-  if (!ok(cudaEventRecord(sb.free_ev, cs), "record")) return fail_cuda();
+  if (!ok(cudaEventRecord(sb.free_ev, cs), "record") || !ok(cudaEventRecord(rt->step_end, cs), "record"))
+    return fail_cuda();
+  rt->have_step_end = true;
   sb.used = true;
   rt->last_waves = (int32_t)nw;
   rt->last_wave_cls.clear();

@@ -60,7 +60,7 @@ class RuntimeConfig(ctypes.Structure):
                 ("num_experts", ctypes.c_int32), ("num_slots", ctypes.c_int32), ("max_requests", ctypes.c_int32),
                 ("max_wave_rows", ctypes.c_int64), ("max_admissions", ctypes.c_int64),
                 ("max_batches", ctypes.c_int64), ("weight_seed", ctypes.c_uint64), ("profile", ctypes.c_int32),
-                ("reserve_sms", ctypes.c_int32), ("swapped_stream", ctypes.c_int32)]
+                ("reserve_sms", ctypes.c_int32), ("swapped_stream", ctypes.c_int32), ("store_path", ctypes.c_char_p)]
 
 
 _declared = False
@@ -88,6 +88,14 @@ def _lib():
         lib.coe_runtime_slot_of.argtypes = [V, I32]
         lib.coe_runtime_bench_mlp.argtypes = [V, I32, I32, I32, P(ctypes.c_float), P(ctypes.c_float)]
         lib.coe_runtime_bench_mlp.restype = ctypes.c_int
+        lib.coe_comm_unique_id.argtypes = [ctypes.c_char_p, V]
+        lib.coe_comm_unique_id.restype = ctypes.c_int
+        lib.coe_comm_create.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.c_int, V, P(V)]
+        lib.coe_comm_create.restype = ctypes.c_int
+        lib.coe_comm_destroy.argtypes = [V]
+        lib.coe_comm_destroy.restype = None
+        lib.coe_runtime_attach_comm.argtypes = [V, V]
+        lib.coe_runtime_attach_comm.restype = ctypes.c_int
         lib.coe_runtime_counts.argtypes = [V, P(I32), P(I32)]
         lib.coe_runtime_counts.restype = ctypes.c_int
         lib.coe_runtime_intervals.argtypes = [V, V, V, V]
@@ -136,7 +144,8 @@ class B200Runtime:
 
     def __init__(self, shape: RuntimeShape, num_experts: int, num_slots: int, max_requests: int,
                  max_admissions: int, max_wave_rows: int | None = None, weight_seed: int = DEFAULT_WEIGHT_SEED,
-                 profile: bool = False, init_experts: bool = True, reserve_sms: int = 16):
+                 profile: bool = False, init_experts: bool = True, reserve_sms: int = 16,
+                 store_path: str | None = None):
         import torch
 
         if not torch.cuda.is_available():
@@ -150,7 +159,8 @@ class B200Runtime:
         self.weight_seed = weight_seed
         rows = max_wave_rows or max(128, min(32768, max_admissions * shape.T))
         cfg = RuntimeConfig(shape.d, shape.h, shape.T, num_experts, num_slots, max_requests, rows, max_admissions,
-                            max_admissions, weight_seed, 1 if profile else 0, reserve_sms, 0)
+                            max_admissions, weight_seed, 1 if profile else 0, reserve_sms, 0,
+                            store_path.encode() if store_path else None)
         self.profile = profile
         self.handle = ctypes.c_void_p()
         _check(self.lib, self.lib.coe_runtime_create(ctypes.byref(cfg), ctypes.byref(self.handle)), "runtime create")
@@ -175,6 +185,26 @@ class B200Runtime:
         if getattr(self, "handle", None):
             self.lib.coe_runtime_destroy(self.handle)
             self.handle = None
+        if getattr(self, "comm", None):
+            self.lib.coe_comm_destroy(self.comm)
+            self.comm = None
+
+    def attach_comm(self, rank: int, world: int) -> None:
+        """Create the NCCL hop communicator (one executor per rank) and attach it.
+
+        The 128-byte unique id travels over the default torch.distributed group."""
+        import torch.distributed as dist
+
+        path = nccl_library().encode()
+        uid = (ctypes.c_char * 128)()
+        if rank == 0:
+            _check(self.lib, self.lib.coe_comm_unique_id(path, uid), "nccl unique id")
+        box = [bytes(uid)]
+        dist.broadcast_object_list(box, src=0)
+        uid = (ctypes.c_char * 128).from_buffer_copy(box[0])
+        self.comm = ctypes.c_void_p()
+        _check(self.lib, self.lib.coe_comm_create(path, rank, world, uid, ctypes.byref(self.comm)), "nccl comm")
+        _check(self.lib, self.lib.coe_runtime_attach_comm(self.handle, self.comm), "attach comm")
 
     def __del__(self):
         try:
@@ -257,6 +287,31 @@ class B200Runtime:
         t = StepTiming()
         _check(self.lib, self.lib.coe_runtime_timing(self.handle, ctypes.byref(t)), "timing")
         return t.as_dict()
+
+
+def nccl_library() -> str:
+    """Path of the NCCL torch loads (pip nvidia-nccl), dlopen'ed by libcoe_cuda."""
+    try:
+        import nvidia.nccl
+
+        path = os.path.join(list(nvidia.nccl.__path__)[0], "lib", "libnccl.so.2")
+        if os.path.exists(path):
+            return path
+    except Exception:
+        pass
+    return "libnccl.so.2"
+
+
+def hops_from_plan(plan) -> list:
+    """Cross-executor hops (index, src, dst, request, stage) in global order (coe_plan_hops)."""
+    lib, h = plan.lib, plan.handle
+    lib.coe_plan_hops.argtypes = [ctypes.c_void_p, ctypes.c_int64] + [ctypes.c_void_p] * 5
+    lib.coe_plan_hops.restype = ctypes.c_int64
+    n = lib.coe_plan_hops(h, 0, None, None, None, None, None)
+    idx = np.zeros(max(1, n), np.int64)
+    cols = [np.zeros(max(1, n), np.int32) for _ in range(4)]
+    lib.coe_plan_hops(h, n, idx.ctypes.data, *(c.ctypes.data for c in cols))
+    return [(int(idx[i]), int(cols[0][i]), int(cols[1][i]), int(cols[2][i]), int(cols[3][i])) for i in range(n)]
 
 
 def batches_from_plan(plan, executor: int = 0) -> list:
