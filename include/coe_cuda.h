@@ -116,6 +116,9 @@ typedef struct coe_runtime_config {
                                their own stream (default 0: main stream)             */
   const char *store_path;   /* NULL: private pinned store; else a shared file mapping
                                (one copy per node for N ranks; host-registered)     */
+  int64_t wave_rows_cap;    /* main-stream wave size cap (0: max_wave_rows)          */
+  int64_t urgent_rows_cap;  /* cap when a wave carries reads an imminent swap-in
+                               waits for (0: wave_rows_cap)                          */
 } coe_runtime_config;
 
 typedef struct coe_step_input {
@@ -192,6 +195,8 @@ void coe_comm_destroy(coe_comm *c);
 /* Attach to a runtime (rank == the executor it serves); steps then exchange
  * hopped activations on a dedicated hop stream. */
 int coe_runtime_attach_comm(coe_runtime *rt, coe_comm *comm);
+/* scheduling knobs (see coe_runtime_config); reserve_sms < 0 keeps the current split */
+int coe_runtime_set_knobs(coe_runtime *rt, int64_t wave_rows_cap, int64_t urgent_rows_cap, int32_t reserve_sms);
 
 /* ---------------- seeded synthetic data ---------------------------------- */
 

@@ -55,23 +55,35 @@ def estimate_exec(d: int, h: int, T: int) -> dict:
 
 
 def load_exec_table() -> dict:
+    """Measured per-shape constants (tools/hwprofile.py on a B200), keyed by shape."""
     if os.path.exists(EXEC_TABLE):
         with open(EXEC_TABLE) as fh:
             return json.load(fh)
     return {}
 
 
+def tiers(table: dict) -> list:
+    """Memory tiers; the host tier's bandwidth/overhead are measured when available."""
+    out = [dict(t) for t in TIERS]
+    host = table.get("host_tier")
+    if host:
+        out[1]["read_bandwidth_bytes_per_s"] = float(host["read_bandwidth_bytes_per_s"])
+        out[1]["fixed_load_overhead_s"] = float(host["fixed_load_overhead_s"])
+    return out
+
+
 def device_doc(shapes: dict, table: dict) -> dict:
     """Device document with one gpu exec-constant entry per arch (shape)."""
     consts = []
+    measured = table.get("shapes", {})
     for arch, (d, h, T) in sorted(shapes.items()):
-        entry = table.get(shape_key(d, h, T)) or estimate_exec(d, h, T)
+        entry = measured.get(shape_key(d, h, T)) or estimate_exec(d, h, T)
         consts.append({
             "arch": arch, "proc": "gpu", "k_s": float(entry["k_s"]), "b_s": float(entry["b_s"]),
             "n_sat": 1_000_000, "gamma": 1.0, "intermediate_base_bytes": 0,
             "intermediate_per_item_bytes": T * (d + h) * 2,
         })
-    return {"schema_version": 1, "name": "b200-hgx", "architecture": "numa", "tiers": list(TIERS),
+    return {"schema_version": 1, "name": "b200-hgx", "architecture": "numa", "tiers": tiers(table),
             "exec_constants": consts}
 
 

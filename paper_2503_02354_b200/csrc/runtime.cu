@@ -72,13 +72,13 @@ __global__ void gather_outputs(const __nv_bfloat16 *p0, const __nv_bfloat16 *p1,
 struct CopyAct {
   int32_t expert;
   int32_t slot;
-  int32_t wait_wave;     // last wave of this step reading the slot (-1: none)
-  bool wait_prev_step;   // first write of the slot this step: wait for last step's readers
   bool restore;
+  std::vector<int32_t> wait_waves;  // last issued reader wave of the slot, per stream (this step)
+  bool wait_prev[3] = {false, false, false};  // per stream: wait for last step's readers
 };
 
 struct WaveAct {
-  int32_t cls;  // 0: main compute stream, 1: swap-in (high priority) stream
+  int32_t cls;  // stream: 0 main, 1 release (high priority, reserved SMs)
   int32_t first_group;
   int32_t num_groups;
   int32_t tiles_up;
@@ -87,8 +87,7 @@ struct WaveAct {
   std::vector<int32_t> wait_copies;  // W1 event before the up pass, W2 before the down pass
   std::vector<int32_t> wait_waves;   // other-stream waves producing this wave's inputs
   std::vector<int32_t> wait_recvs;   // hops (local index) this wave consumes
-  int64_t min_send = INT64_MAX;      // smallest global index of a hop this wave produces
-  std::vector<int32_t> frees_slots;  // slots whose last reader this step is this wave
+  std::vector<int32_t> frees_slots;  // slots whose last reader this step, on this stream, is this wave
 };
 
 struct Action {
@@ -142,7 +141,8 @@ struct coe_runtime {
   coe_mlp *mlp[NCLS] = {nullptr, nullptr, nullptr};
   // slot state (persists across steps)
   std::vector<int32_t> slot_expert, expert_slot;
-  std::vector<cudaEvent_t> slot_free_up, slot_free_down;  // last reader of each half, previous step
+  // last reader of each slot half in the previous step, per compute stream ([slot * NCLS + cls])
+  std::vector<cudaEvent_t> slot_free_up, slot_free_down;
   std::vector<uint8_t> slot_free_valid;
   // events
   std::vector<cudaEvent_t> wave_up_ev, wave_down_ev, copy_up_ev, copy_down_ev;
@@ -341,8 +341,8 @@ int coe_runtime_create(const coe_runtime_config *cfg, coe_runtime **out) {
            ok(cudaEventCreateWithFlags(&rt->cls_drained[2], cudaEventDisableTiming), "event") &&
            ok(cudaEventCreate(&rt->t_step_start), "event") && ok(cudaEventCreate(&rt->t_group_end), "event") &&
            ok(cudaEventCreate(&rt->t_step_end), "event") &&
-           rt->ensure_events(rt->slot_free_up, c.num_slots, false) &&
-           rt->ensure_events(rt->slot_free_down, c.num_slots, false);
+           rt->ensure_events(rt->slot_free_up, (size_t)c.num_slots * coe_runtime::NCLS, false) &&
+           rt->ensure_events(rt->slot_free_down, (size_t)c.num_slots * coe_runtime::NCLS, false);
   }
   if (good) {
     coe_mlp_config mc{};
@@ -379,7 +379,7 @@ int coe_runtime_create(const coe_runtime_config *cfg, coe_runtime **out) {
   }
   rt->slot_expert.assign(c.num_slots, -1);
   rt->expert_slot.assign(c.num_experts, -1);
-  rt->slot_free_valid.assign(c.num_slots, 0);
+  rt->slot_free_valid.assign((size_t)c.num_slots * coe_runtime::NCLS, 0);
   *out = rt;
   return COE_CUDA_OK;
 }
@@ -525,6 +525,21 @@ int coe_runtime_timing(coe_runtime *rt, coe_step_timing *out) {
   return COE_CUDA_OK;
 }
 
+int coe_runtime_set_knobs(coe_runtime *rt, int64_t wave_rows_cap, int64_t urgent_rows_cap, int32_t reserve_sms) {
+  rt->cfg.wave_rows_cap = wave_rows_cap;
+  rt->cfg.urgent_rows_cap = urgent_rows_cap;
+  if (reserve_sms >= 0) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int reserve = reserve_sms > 0 ? std::min<int>(reserve_sms, sms / 2) : 0;
+    rt->cfg.reserve_sms = reserve;
+    rt->m_ctas = sms - reserve;
+    rt->r_ctas = reserve > 0 ? reserve : sms;
+  }
+  return COE_CUDA_OK;
+}
+
 int coe_runtime_attach_comm(coe_runtime *rt, coe_comm *comm) {
   rt->comm = comm;
   return COE_CUDA_OK;
@@ -614,11 +629,49 @@ int coe_runtime_counts(coe_runtime *rt, int32_t *copies, int32_t *waves) {
   return COE_CUDA_OK;
 }
 
-int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_step_stats *stats) {
+}  // extern "C"
+
+// ---------------------------------------------------------------------------------------
+// coe_runtime_step: phase A walks the op log in order (slots, copies, data dependencies);
+// phase B list-schedules the physical actions on estimated clocks (copy engine, main
+// stream, release stream) so that no stream blocks behind work whose inputs are not ready
+// while the copy engine -- the bottleneck of budgeted configs -- is kept busy; phase C
+// issues the chosen order.  Every dependency is an explicit event on an earlier-issued
+// action, so estimates only affect speed, never correctness.
+
+namespace {
+
+struct BatchInfo {
+  int32_t op_index;   // index into the op log
+  int32_t expert, slot, count, cls;
+  int32_t copy;       // copy that wrote this batch's slot this step (-1: resident since step start)
+  bool release;       // last reader of a slot a later LOAD overwrites
+  int64_t rows;
+  std::vector<int32_t> producers;  // batches of this executor producing this batch's inputs
+  std::vector<int32_t> recvs;      // my_hops slots consumed
+  std::vector<int32_t> sends;      // my_hops slots produced
+  int64_t max_recv = -1, min_send = INT64_MAX;
+  int32_t wave = -1;
+  double done = 0.0;               // estimated completion
+};
+
+struct CopyInfo {
+  int32_t expert, slot;
+  bool restore;
+  std::vector<int32_t> readers;    // batches reading the slot's previous content this step
+  bool first_write;                // slot not written earlier this step
+  double up_end = 0.0, end = 0.0;  // estimated
+  bool issued = false;
+};
+
+}  // namespace
+
+extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_step_stats *stats) {
   const auto &c = rt->cfg;
   const coe_op *ops = static_cast<const coe_op *>(in->ops);
   const coe_admission *adm = static_cast<const coe_admission *>(in->admissions);
   const int32_t x = in->executor;
+  constexpr int NCLS = coe_runtime::NCLS;
   coe_step_stats st{};
 
   // ---- admissions of this executor (admission order) ----
@@ -645,7 +698,7 @@ int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_step_stats *
   const int passes = (rank_bits + 7) / 8;  // executor field is 0 (one executor per runtime)
   st.rank_bits = rank_bits;
 
-  // ---- lookahead: batches that are the last reader of an expert a later LOAD evicts ----
+  // ---- my ops and the release lookahead ----
   std::vector<int64_t> my_ops;
   for (int64_t i = 0; i < in->num_ops; ++i)
     if (ops[i].executor == x) my_ops.push_back(i);
@@ -666,9 +719,9 @@ int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_step_stats *
 
   // ---- hops touching this executor (global admission order, hops.h) ----
   const std::vector<coe::Hop> all_hops = coe::hop_schedule(adm, in->num_admissions, c.max_requests);
-  std::vector<int32_t> my_hops;                      // indices into all_hops, in global order
-  std::unordered_map<int64_t, int32_t> hop_in, hop_out;  // (request, consumer/producer stage) -> my_hops slot
-  auto hkey = [](int32_t r, int32_t st) { return ((int64_t)r << 8) | st; };
+  std::vector<int32_t> my_hops;
+  std::unordered_map<int64_t, int32_t> hop_in, hop_out;
+  auto hkey = [](int32_t r, int32_t s) { return ((int64_t)r << 8) | s; };
   for (size_t i = 0; i < all_hops.size(); ++i) {
     const coe::Hop &h = all_hops[i];
     if (h.src != x && h.dst != x) continue;
@@ -680,11 +733,12 @@ int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_step_stats *
     coe_set_error("plan moves activations between executors: attach a communicator (coe_runtime_attach_comm)");
     return COE_CUDA_ERR_CONFIG;
   }
-  std::vector<int32_t> hop_producer_wave(my_hops.size(), -1);
+  std::vector<int32_t> hop_batch(my_hops.size(), -1);  // producing batch of each send
 
-  // ---- pass 1: slots, copies, waves on two compute streams ----
+  // ---- phase A: slots, copies, batches in op order ----
   std::vector<uint8_t> plan_res(c.num_experts, 0), pending_restore(c.num_experts, 0);
-  std::vector<int32_t> slot_use_wave(c.num_slots, -1), slot_copy(c.num_slots, -1), slot_open_cls(c.num_slots, -1);
+  std::vector<int32_t> slot_copy(c.num_slots, -1);
+  std::vector<std::vector<int32_t>> slot_readers(c.num_slots);
   std::vector<uint8_t> slot_written(c.num_slots, 0);
   for (int32_t i = 0; i < in->num_initial; ++i) plan_res[in->initial[i]] = 1;
   for (int32_t s = 0; s < c.num_slots; ++s) {  // slots outside the initial placement are free again
@@ -697,75 +751,31 @@ int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_step_stats *
   for (int32_t i = 0; i < in->num_initial; ++i)
     if (rt->expert_slot[in->initial[i]] < 0) pending_restore[in->initial[i]] = 1;
 
-  std::vector<int32_t> req_open_cls(c.max_requests, -1), req_writer(c.max_requests, -1);
-  std::vector<CopyAct> copies;
-  std::vector<uint8_t> copy_waited;
-  std::vector<WaveAct> waves;
-  std::vector<Action> actions;
-  std::vector<coe_mlp_group> g_up, g_down;
-  std::vector<int32_t> b_size;
-  struct Open {
-    bool used = false;
-    WaveAct w{};
-    std::vector<coe_mlp_group> gu, gd;
-    std::vector<int32_t> slots, reqs, sends;
-  } open[coe_runtime::NCLS];
-  int64_t waves_by_cls[coe_runtime::NCLS] = {0, 0, 0};
-
-  auto flush = [&](int cls) {
-    Open &o = open[cls];
-    if (!o.used) return;
-    const int32_t id = (int32_t)waves.size();
-    o.w.cls = cls;
-    o.w.first_group = (int32_t)g_up.size();
-    g_up.insert(g_up.end(), o.gu.begin(), o.gu.end());
-    g_down.insert(g_down.end(), o.gd.begin(), o.gd.end());
-    for (int32_t s : o.slots) {
-      slot_use_wave[s] = id;
-      slot_open_cls[s] = -1;
-    }
-    for (int32_t r : o.reqs) {
-      req_writer[r] = id;
-      req_open_cls[r] = -1;
-    }
-    for (int32_t hslot : o.sends) hop_producer_wave[hslot] = id;
-    st.max_wave_groups = std::max(st.max_wave_groups, o.w.num_groups);
-    st.max_wave_rows = std::max(st.max_wave_rows, o.w.rows);
-    waves.push_back(o.w);
-    actions.push_back(Action{false, id});
-    waves_by_cls[cls] += 1;
-    o = Open();
-  };
-  auto alloc_slot = [&](int32_t &slot) -> bool {
-    int32_t best = -1;
+  std::vector<CopyInfo> copies;
+  std::vector<BatchInfo> batches;
+  std::vector<int32_t> req_last(c.max_requests, -1);  // latest batch of each request on this executor
+  auto issue_copy = [&](int32_t e, bool restore) -> bool {
+    int32_t best = -1;  // free slot whose readers were issued earliest in op order
     for (int32_t s = 0; s < c.num_slots; ++s) {
       if (rt->slot_expert[s] >= 0) continue;
-      auto age = [&](int32_t q) { return slot_open_cls[q] >= 0 ? INT32_MAX : slot_use_wave[q]; };
+      auto age = [&](int32_t q) { return slot_readers[q].empty() ? -1 : slot_readers[q].back(); };
       if (best < 0 || age(s) < age(best)) best = s;
     }
-    if (best < 0) return false;
-    if (slot_open_cls[best] >= 0) flush(slot_open_cls[best]);
-    slot = best;
-    return true;
-  };
-  auto issue_copy = [&](int32_t e, bool restore) -> bool {
-    int32_t s;
-    if (!alloc_slot(s)) {
+    if (best < 0) {
       coe_set_error("no free HBM expert slot (planner residency exceeds the slot count)");
       return false;
     }
-    copies.push_back(CopyAct{e, s, slot_use_wave[s], !slot_written[s] && rt->slot_free_valid[s] != 0, restore});
-    copy_waited.push_back(0);
-    actions.push_back(Action{true, (int32_t)copies.size() - 1});
-    slot_written[s] = 1;
-    rt->slot_expert[s] = e;
-    rt->expert_slot[e] = s;
-    slot_copy[s] = (int32_t)copies.size() - 1;
+    CopyInfo ci{e, best, restore, slot_readers[best], !slot_written[best]};
+    copies.push_back(ci);
+    slot_readers[best].clear();
+    slot_written[best] = 1;
+    rt->slot_expert[best] = e;
+    rt->expert_slot[e] = best;
+    slot_copy[best] = (int32_t)copies.size() - 1;
     (restore ? st.restores : st.loads) += 1;
     (restore ? st.restore_bytes : st.load_bytes) += rt->expert_bytes;
     return true;
   };
-
   for (size_t k = 0; k < my_ops.size(); ++k) {
     const coe_op &op = ops[my_ops[k]];
     if (op.kind == COE_OP_LOAD) {
@@ -797,103 +807,269 @@ int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_step_stats *
       pending_restore[e] = 0;
       if (!issue_copy(e, true)) return COE_CUDA_ERR_CHECK;
     }
-    const int32_t s = rt->expert_slot[e];
-    // the swap-in stream runs only the last readers of slots a later load overwrites: their
-    // completion gates the copy engine, which is the bottleneck of budgeted configs
-    // class 2 (a separate stream for experts swapped in this step) measured slower than
-    // sharing the main stream (c3: 1117 vs 1068 ms/step): the two low-priority streams
-    // starve each other's cross-stream producers.  Kept selectable for experiments.
-    const int cls = releases[k] ? 1 : ((slot_copy[s] >= 0 && c.swapped_stream) ? 2 : 0);
-    const int64_t rows = (int64_t)op.count * c.T;
-    if (rows > c.max_wave_rows) {
+    BatchInfo b;
+    b.op_index = (int32_t)my_ops[k];
+    b.expert = e;
+    b.slot = rt->expert_slot[e];
+    b.count = op.count;
+    b.rows = (int64_t)op.count * c.T;
+    b.copy = slot_copy[b.slot];
+    b.release = releases[k] != 0;
+    b.cls = b.release ? 1 : 0;
+    if (b.rows > c.max_wave_rows) {
       coe_set_error("a single batch exceeds the H scratch rows");
       return COE_CUDA_ERR_CONFIG;
     }
-    // incoming hops: every open wave producing an earlier hop must be issued first, so the
-    // hop stream (global order) never waits on a wave that waits on it
-    int64_t need_recv = -1;
-    std::vector<int32_t> recvs;
+    const int32_t bi = (int32_t)batches.size();
     for (int32_t j = 0; j < op.count; ++j) {
-      auto it = hop_in.find(hkey(in->op_args[op.offset + 2 * j], in->op_args[op.offset + 2 * j + 1]));
-      if (it != hop_in.end()) {
-        recvs.push_back(it->second);
-        need_recv = std::max<int64_t>(need_recv, all_hops[my_hops[it->second]].index);
+      const int32_t r = in->op_args[op.offset + 2 * j], s = in->op_args[op.offset + 2 * j + 1];
+      if (req_last[r] >= 0 && std::find(b.producers.begin(), b.producers.end(), req_last[r]) == b.producers.end())
+        b.producers.push_back(req_last[r]);
+      auto hi = hop_in.find(hkey(r, s));
+      if (hi != hop_in.end()) {
+        b.recvs.push_back(hi->second);
+        b.max_recv = std::max<int64_t>(b.max_recv, all_hops[my_hops[hi->second]].index);
       }
-    }
-    if (need_recv >= 0)
-      for (int k2 = 0; k2 < coe_runtime::NCLS; ++k2)
-        if (open[k2].used && open[k2].w.min_send < need_recv) flush(k2);
-    bool clash = false;
-    for (int32_t j = 0; j < op.count; ++j) {
-      const int32_t r = in->op_args[op.offset + 2 * j];
-      if (req_open_cls[r] >= 0 && req_open_cls[r] != cls) flush(req_open_cls[r]);  // producer needs a wave id
-      if (req_open_cls[r] == cls) clash = true;
-    }
-    const int32_t cp = slot_copy[s];
-    const bool need_wait = cp >= 0 && !(copy_waited[cp] & (1 << cls));
-    Open &o = open[cls];
-    if (o.used && (need_wait || clash || releases[k] || o.w.rows + rows > c.max_wave_rows ||
-                   o.w.num_groups >= coe_mlp_max_groups()))
-      flush(cls);
-    Open &w = open[cls];
-    if (need_wait) {
-      w.w.wait_copies.push_back(cp);
-      copy_waited[cp] |= (1 << cls);
-    }
-    for (int32_t hslot : recvs) w.w.wait_recvs.push_back(hslot);
-    for (int32_t j = 0; j < op.count; ++j) {
-      auto it = hop_out.find(hkey(in->op_args[op.offset + 2 * j], in->op_args[op.offset + 2 * j + 1]));
-      if (it != hop_out.end()) {
-        w.sends.push_back(it->second);
-        w.w.min_send = std::min<int64_t>(w.w.min_send, all_hops[my_hops[it->second]].index);
+      auto ho = hop_out.find(hkey(r, s));
+      if (ho != hop_out.end()) {
+        b.sends.push_back(ho->second);
+        b.min_send = std::min<int64_t>(b.min_send, all_hops[my_hops[ho->second]].index);
+        hop_batch[ho->second] = bi;
       }
+      req_last[r] = bi;
     }
-    for (int32_t j = 0; j < op.count; ++j) {
-      const int32_t r = in->op_args[op.offset + 2 * j];
-      const int32_t wr = req_writer[r];
-      if (wr >= 0 && waves[wr].cls != cls &&
-          std::find(w.w.wait_waves.begin(), w.w.wait_waves.end(), wr) == w.w.wait_waves.end())
-        w.w.wait_waves.push_back(wr);
-    }
-    const int32_t m_tiles = (int32_t)((rows + BM - 1) / BM);
-    coe_mlp_group gu{};
-    gu.rows = (int32_t)rows;
-    gu.slot = s;
-    gu.batch = (int32_t)b_size.size();
-    gu.h_row = (int32_t)w.w.rows;
-    gu.tile_start = w.w.tiles_up;
-    coe_mlp_group gd = gu;
-    gd.tile_start = w.w.tiles_down;
-    w.gu.push_back(gu);
-    w.gd.push_back(gd);
-    b_size.push_back(op.count);
-    w.w.num_groups += 1;
-    w.w.rows += rows;
-    w.w.tiles_up += m_tiles * (c.h / BN);
-    w.w.tiles_down += m_tiles * (c.d / BN);
-    w.used = true;
-    w.slots.push_back(s);
-    slot_open_cls[s] = cls;
-    for (int32_t j = 0; j < op.count; ++j) {
-      const int32_t r = in->op_args[op.offset + 2 * j];
-      w.reqs.push_back(r);
-      req_open_cls[r] = cls;
-    }
-    if (releases[k]) flush(cls);  // the slot's next writer waits for this wave only
+    slot_readers[b.slot].push_back(bi);
+    batches.push_back(std::move(b));
   }
-  for (int k = 0; k < coe_runtime::NCLS; ++k) flush(k);
-  for (int32_t s = 0; s < c.num_slots; ++s)  // per-slot last reader this step -> event after that wave
-    if (slot_use_wave[s] >= 0) waves[slot_use_wave[s]].frees_slots.push_back(s);
-  const int64_t n_batches = (int64_t)b_size.size();
+  const int64_t n_batches = (int64_t)batches.size();
   if (n_batches > c.max_batches) {
     coe_set_error("more batches than the runtime was sized for");
     return COE_CUDA_ERR_CONFIG;
+  }
+  // sends ordered by global index: a batch needing recv h may only be issued once every
+  // send of this executor with a smaller index has its producer issued
+  std::vector<int32_t> send_slots;
+  for (size_t i = 0; i < my_hops.size(); ++i)
+    if (all_hops[my_hops[i]].src == x) send_slots.push_back((int32_t)i);
+
+  // ---- phase B: list schedule ----
+  const double copy_half_s = (double)rt->half_bytes / 55.0e9;
+  const double flops_per_row = 4.0 * c.d * c.h;
+  const double f_main = 1.2e15 * (double)rt->m_ctas / 148.0, f_rel = 1.2e15 * (double)rt->r_ctas / 148.0;
+  const double launch_s = 12e-6;
+  std::vector<uint8_t> issued(n_batches, 0);
+  std::vector<int32_t> main_pending, rel_order;
+  for (int32_t i = 0; i < (int32_t)n_batches; ++i) (batches[i].cls ? rel_order : main_pending).push_back(i);
+  size_t next_rel = 0, next_copy = 0, send_ptr = 0;
+  double t_copy = 0.0, t_stream[NCLS] = {0.0, 0.0, 0.0};
+  std::vector<WaveAct> waves;
+  std::vector<Action> actions;
+  std::vector<coe_mlp_group> g_up, g_down;
+  std::vector<int32_t> batch_of_group;  // group position -> batch (K2 batch index = op-order batch)
+  std::vector<int32_t> slot_last_wave(c.num_slots * NCLS, -1);
+  std::vector<int32_t> copy_action(copies.size(), -1);
+
+  auto sends_ready_before = [&](int64_t hop_index) {
+    while (send_ptr < send_slots.size() && hop_batch[send_slots[send_ptr]] >= 0 &&
+           issued[hop_batch[send_slots[send_ptr]]])
+      ++send_ptr;
+    return send_ptr >= send_slots.size() || all_hops[my_hops[send_slots[send_ptr]]].index > hop_index;
+  };
+  auto issuable = [&](const BatchInfo &b) {
+    for (int32_t p : b.producers)
+      if (!issued[p]) return false;
+    if (b.copy >= 0 && !copies[b.copy].issued) return false;
+    if (b.max_recv >= 0 && !sends_ready_before(b.max_recv)) return false;
+    return true;
+  };
+  auto ready_time = [&](const BatchInfo &b) {
+    double t = 0.0;
+    for (int32_t p : b.producers) t = std::max(t, batches[p].done);
+    if (b.copy >= 0) t = std::max(t, copies[b.copy].up_end);
+    return t;
+  };
+  auto copy_ready = [&](const CopyInfo &ci) {
+    for (int32_t r : ci.readers)
+      if (!issued[r]) return false;
+    return true;
+  };
+  auto wave_time = [&](int64_t rows, int cls) {
+    const double padded = (double)((rows + BM - 1) / BM * BM);
+    return padded * flops_per_row / (cls ? f_rel : f_main) + 2 * launch_s;
+  };
+  auto emit_wave = [&](const std::vector<int32_t> &members, int cls, double start) {
+    WaveAct w{};
+    w.cls = cls;
+    w.first_group = (int32_t)g_up.size();
+    const int32_t id = (int32_t)waves.size();
+    for (int32_t bi : members) {
+      BatchInfo &b = batches[bi];
+      const int32_t m_tiles = (int32_t)((b.rows + BM - 1) / BM);
+      coe_mlp_group gu{};
+      gu.rows = (int32_t)b.rows;
+      gu.slot = b.slot;
+      gu.batch = bi;
+      gu.h_row = (int32_t)w.rows;
+      gu.tile_start = w.tiles_up;
+      coe_mlp_group gd = gu;
+      gd.tile_start = w.tiles_down;
+      g_up.push_back(gu);
+      g_down.push_back(gd);
+      w.num_groups += 1;
+      w.rows += b.rows;
+      w.tiles_up += m_tiles * (c.h / BN);
+      w.tiles_down += m_tiles * (c.d / BN);
+      if (b.copy >= 0 && std::find(w.wait_copies.begin(), w.wait_copies.end(), b.copy) == w.wait_copies.end())
+        w.wait_copies.push_back(b.copy);
+      for (int32_t p : b.producers) {
+        const int32_t pw = batches[p].wave;
+        if (waves[pw].cls != cls && std::find(w.wait_waves.begin(), w.wait_waves.end(), pw) == w.wait_waves.end())
+          w.wait_waves.push_back(pw);
+      }
+      for (int32_t h : b.recvs) w.wait_recvs.push_back(h);
+      b.wave = id;
+      issued[bi] = 1;
+      slot_last_wave[b.slot * NCLS + cls] = id;
+    }
+    const double end = start + wave_time(w.rows, cls);
+    for (int32_t bi : members) batches[bi].done = end;
+    t_stream[cls] = end;
+    st.max_wave_groups = std::max(st.max_wave_groups, w.num_groups);
+    st.max_wave_rows = std::max(st.max_wave_rows, w.rows);
+    waves.push_back(std::move(w));
+    actions.push_back(Action{false, id});
+  };
+
+  const size_t kWindow = 256;
+  const double kSlack = 50e-6;
+  const int max_groups = coe_mlp_max_groups();
+  // urgency: a main batch that reads a slot an upcoming swap-in overwrites goes first, and
+  // a wave carrying urgent work is capped so that swap-in waits for little else
+  std::vector<int32_t> needed_by_copy(n_batches, -1);
+  for (int32_t ci = 0; ci < (int32_t)copies.size(); ++ci)
+    for (int32_t r : copies[ci].readers) needed_by_copy[r] = ci;
+  const int64_t wave_rows_cap = c.wave_rows_cap > 0 ? std::min<int64_t>(c.wave_rows_cap, c.max_wave_rows)
+                                                    : c.max_wave_rows;
+  const int64_t urgent_rows_cap = c.urgent_rows_cap > 0 ? c.urgent_rows_cap : wave_rows_cap;
+  const int urgent_horizon = 2;
+  while (next_copy < copies.size() || next_rel < rel_order.size() || !main_pending.empty()) {
+    const double INF = 1e30;
+    // candidate: next swap-in
+    double c_start = INF;
+    if (next_copy < copies.size() && copy_ready(copies[next_copy])) {
+      c_start = t_copy;
+      for (int32_t r : copies[next_copy].readers) c_start = std::max(c_start, batches[r].done);
+    }
+    // candidate: next release wave (singleton, in order)
+    double r_start = INF;
+    if (next_rel < rel_order.size() && issuable(batches[rel_order[next_rel]]))
+      r_start = std::max(t_stream[1], ready_time(batches[rel_order[next_rel]]));
+    // candidate: a main wave -- earliest estimated-ready issuable batch in the window
+    double m_start = INF;
+    const size_t win = std::min(kWindow, main_pending.size());
+    for (size_t i = 0; i < win; ++i) {
+      const BatchInfo &b = batches[main_pending[i]];
+      if (issuable(b)) m_start = std::min(m_start, std::max(t_stream[0], ready_time(b)));
+    }
+    if (c_start == INF && r_start == INF && m_start == INF) {
+      coe_set_error("internal: runtime list scheduler found no issuable action");
+      return COE_CUDA_ERR_CHECK;
+    }
+    if (c_start <= r_start && c_start <= m_start) {
+      CopyInfo &ci = copies[next_copy];
+      ci.issued = true;
+      ci.up_end = c_start + copy_half_s;
+      ci.end = c_start + 2 * copy_half_s;
+      t_copy = ci.end;
+      copy_action[next_copy] = (int32_t)actions.size();
+      actions.push_back(Action{true, (int32_t)next_copy});
+      ++next_copy;
+    } else if (r_start <= m_start) {
+      emit_wave({rel_order[next_rel]}, 1, r_start);
+      ++next_rel;
+    } else {
+      // greedy wave at m_start: ready (by estimate) issuable batches in op order
+      std::vector<int32_t> members;
+      std::unordered_set<int32_t> reqs;
+      int64_t rows = 0, wave_max_recv = -1, wave_min_send = INT64_MAX;
+      std::vector<size_t> taken;
+      // candidate order: urgent (slot needed by one of the next swap-ins) first, then op order
+      std::vector<size_t> order;
+      bool urgent_present = false;
+      for (size_t i = 0; i < win; ++i) {
+        const int32_t nb = needed_by_copy[main_pending[i]];
+        if (nb >= 0 && nb <= (int32_t)next_copy + urgent_horizon) {
+          order.push_back(i);
+          urgent_present = true;
+        }
+      }
+      for (size_t i = 0; i < win; ++i) {
+        const int32_t nb = needed_by_copy[main_pending[i]];
+        if (!(nb >= 0 && nb <= (int32_t)next_copy + urgent_horizon)) order.push_back(i);
+      }
+      const int64_t cap = urgent_present ? urgent_rows_cap : wave_rows_cap;
+      for (size_t oi = 0; oi < order.size() && (int)members.size() < max_groups; ++oi) {
+        const size_t i = order[oi];
+        const int32_t bi = main_pending[i];
+        const BatchInfo &b = batches[bi];
+        if (!issuable(b) || ready_time(b) > m_start + kSlack) continue;
+        if (!members.empty() && rows + b.rows > cap) break;
+        bool clash = false;
+        for (int32_t j = 0; j < b.count && !clash; ++j)
+          clash = reqs.count(in->op_args[ops[b.op_index].offset + 2 * j]) > 0;
+        if (clash) continue;
+        const int64_t mr = std::max(wave_max_recv, b.max_recv), ms = std::min(wave_min_send, b.min_send);
+        if (mr >= 0 && ms < mr) continue;  // a wave may not wait on a hop its own sends precede
+        members.push_back(bi);
+        taken.push_back(i);
+        rows += b.rows;
+        wave_max_recv = mr;
+        wave_min_send = ms;
+        for (int32_t j = 0; j < b.count; ++j) reqs.insert(in->op_args[ops[b.op_index].offset + 2 * j]);
+      }
+      if (members.empty()) {
+        coe_set_error("internal: empty main wave");
+        return COE_CUDA_ERR_CHECK;
+      }
+      emit_wave(members, 0, m_start);
+      std::sort(taken.begin(), taken.end());
+      for (size_t t = taken.size(); t-- > 0;) main_pending.erase(main_pending.begin() + (std::ptrdiff_t)taken[t]);
+    }
+  }
+  // copy waits: the last issued reader wave of the slot's previous content, per stream
+  std::vector<CopyAct> copy_acts(copies.size());
+  {
+    std::vector<int32_t> last_reader_wave(c.num_slots * NCLS, -1);
+    std::vector<uint8_t> written(c.num_slots, 0);
+    for (const Action &a : actions) {
+      if (a.is_copy) {
+        const CopyInfo &ci = copies[a.index];
+        CopyAct &ca = copy_acts[a.index];
+        ca.expert = ci.expert;
+        ca.slot = ci.slot;
+        ca.restore = ci.restore;
+        for (int k = 0; k < NCLS; ++k) {
+          const int32_t wv = last_reader_wave[ci.slot * NCLS + k];
+          if (wv >= 0) ca.wait_waves.push_back(wv);
+          else if (!written[ci.slot]) ca.wait_prev[k] = rt->slot_free_valid[(size_t)ci.slot * NCLS + k] != 0;
+          last_reader_wave[ci.slot * NCLS + k] = -1;
+        }
+        written[ci.slot] = 1;
+      } else {
+        const WaveAct &w = waves[a.index];
+        for (int32_t gi = w.first_group; gi < w.first_group + w.num_groups; ++gi)
+          last_reader_wave[g_up[gi].slot * NCLS + w.cls] = a.index;
+      }
+    }
+    for (int32_t s = 0; s < c.num_slots; ++s)
+      for (int k = 0; k < NCLS; ++k)
+        if (last_reader_wave[s * NCLS + k] >= 0) waves[last_reader_wave[s * NCLS + k]].frees_slots.push_back(s * NCLS + k);
   }
   st.admissions = n_adm;
   st.batches = n_batches;
   st.waves = (int64_t)waves.size();
 
-  // ---- pass 2: issue ----
+  // ---- phase C: issue ----
   const size_t nw = waves.size(), nc = copies.size();
   if (!rt->ensure_events(rt->wave_up_ev, nw, false) || !rt->ensure_events(rt->wave_down_ev, nw, false) ||
       !rt->ensure_events(rt->copy_up_ev, nc, false) || !rt->ensure_events(rt->copy_down_ev, nc, false) ||
@@ -918,7 +1094,7 @@ int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_step_stats *
   int32_t *s_batch = s_adm + 4 * n_adm;
   for (int64_t b = 0; b < n_batches; ++b) {
     s_batch[b] = 0;
-    s_batch[n_batches + b] = b_size[b];
+    s_batch[n_batches + b] = batches[b].count;
   }
   coe_mlp_group *s_groups = reinterpret_cast<coe_mlp_group *>(
       (reinterpret_cast<uintptr_t>(s_batch + 2 * n_batches) + 31) & ~uintptr_t(31));
@@ -929,8 +1105,6 @@ int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_step_stats *
 
   cudaStream_t cs = rt->compute, ks = rt->copy;
   if (c.profile && !ok(cudaEventRecord(rt->t_step_start, cs), "record")) return fail_cuda();
-  // plan upload first on the copy stream (ahead of this step's swap-ins), into the set
-  // the step before last used -- wait until that step released it
   if (sb.used && !ok(cudaStreamWaitEvent(ks, sb.free_ev, 0), "set reuse")) return fail_cuda();
   if (n_adm && !ok(cudaMemcpyAsync(sb.adm, s_adm, 16 * (size_t)n_adm, cudaMemcpyHostToDevice, ks), "adm H2D"))
     return fail_cuda();
@@ -943,7 +1117,6 @@ int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_step_stats *
   if (!ok(cudaEventRecord(rt->staging_done[set_idx], ks), "record") || !ok(cudaEventRecord(rt->staged, ks), "record") ||
       !ok(cudaStreamWaitEvent(cs, rt->staged, 0), "compute waits upload"))
     return fail_cuda();
-  // K1 + K2 on the main compute stream (executor field 0: this runtime's admissions only)
   int32_t *d_exec = sb.adm, *d_rank = sb.adm + n_adm, *d_req = sb.adm + 2 * n_adm, *d_stage = sb.adm + 3 * n_adm;
   if (n_adm) {
     int rc = coe_group_sort(d_exec, d_rank, n_adm, rank_bits, passes, rt->d_perm, rt->d_keys, rt->d_sort_scratch, cs);
@@ -957,27 +1130,24 @@ int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_step_stats *
   }
   if (c.profile && !ok(cudaEventRecord(rt->t_group_end, cs), "record")) return fail_cuda();
   if (!ok(cudaEventRecord(rt->grouped, cs), "record")) return fail_cuda();
-  for (int k = 1; k < coe_runtime::NCLS; ++k)
+  for (int k = 1; k < NCLS; ++k)
     if (!ok(cudaStreamWaitEvent(rt->cls_stream[k], rt->grouped, 0), "class stream waits K2")) return fail_cuda();
 
-  // hop stream: starts after the previous step (its receives overwrite P rows) and issues
-  // this executor's sends / receives strictly in global hop order
   if (!my_hops.empty() && rt->have_step_end && !ok(cudaStreamWaitEvent(rt->hop, rt->step_end, 0), "hop waits step"))
     return fail_cuda();
   size_t hop_cursor = 0;
-  int32_t waves_issued = 0;
   const size_t row_elems = (size_t)rt->row_elems;
   auto issue_hops_until = [&](int64_t limit) -> bool {
     while (hop_cursor < my_hops.size() && all_hops[my_hops[hop_cursor]].index <= limit) {
       const coe::Hop &h = all_hops[my_hops[hop_cursor]];
       __nv_bfloat16 *row = ((h.stage & 1) ? rt->p1 : rt->p0) + (size_t)h.request * row_elems;
       if (h.src == x) {
-        const int32_t pw = hop_producer_wave[hop_cursor];
-        if (pw < 0 || pw >= waves_issued) {
+        const int32_t pb = hop_batch[hop_cursor];
+        if (pb < 0 || !issued[pb] || batches[pb].wave < 0) {
           coe_set_error("internal: hop send issued before its producer wave");
           return false;
         }
-        if (!ok(cudaStreamWaitEvent(rt->hop, rt->wave_down_ev[pw], 0), "send waits producer") ||
+        if (!ok(cudaStreamWaitEvent(rt->hop, rt->wave_down_ev[batches[pb].wave], 0), "send waits producer") ||
             !coe_comm_send_bf16(rt->comm, row, row_elems, h.dst, rt->hop))
           return false;
       } else {
@@ -989,78 +1159,81 @@ int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_step_stats *
     }
     return true;
   };
+  // issue() for sends must only see producers already issued in phase C
+  std::fill(issued.begin(), issued.end(), 0);
 
   const coe_mlp_group *dg_up = sb.groups, *dg_down = sb.groups + n_batches;
   for (const Action &a : actions) {
     if (a.is_copy) {
-      const CopyAct &cp = copies[a.index];
+      const CopyAct &cp = copy_acts[a.index];
       char *dst = rt->slab + (int64_t)cp.slot * rt->expert_bytes;
       const char *src = rt->host_store + (int64_t)cp.expert * rt->expert_bytes;
-      cudaEvent_t wait_up = nullptr, wait_down = nullptr;
-      if (cp.wait_wave >= 0) {
-        wait_up = rt->wave_up_ev[cp.wait_wave];
-        wait_down = rt->wave_down_ev[cp.wait_wave];
-      } else if (cp.wait_prev_step) {
-        wait_up = rt->slot_free_up[cp.slot];
-        wait_down = rt->slot_free_down[cp.slot];
-      }
-      if (wait_up && !ok(cudaStreamWaitEvent(ks, wait_up, 0), "copy waits W1 readers")) return fail_cuda();
+      for (int32_t wv : cp.wait_waves)
+        if (!ok(cudaStreamWaitEvent(ks, rt->wave_up_ev[wv], 0), "copy waits W1 readers")) return fail_cuda();
+      for (int k = 0; k < NCLS; ++k)
+        if (cp.wait_prev[k] &&
+            !ok(cudaStreamWaitEvent(ks, rt->slot_free_up[(size_t)cp.slot * NCLS + k], 0), "copy waits last step"))
+          return fail_cuda();
       if (c.profile && !ok(cudaEventRecord(rt->t_copy_start[a.index], ks), "record")) return fail_cuda();
       if (!ok(cudaMemcpyAsync(dst, src, rt->half_bytes, cudaMemcpyHostToDevice, ks), "swap-in W1") ||
           !ok(cudaEventRecord(rt->copy_up_ev[a.index], ks), "record"))
         return fail_cuda();
-      if (wait_down && !ok(cudaStreamWaitEvent(ks, wait_down, 0), "copy waits W2 readers")) return fail_cuda();
+      for (int32_t wv : cp.wait_waves)
+        if (!ok(cudaStreamWaitEvent(ks, rt->wave_down_ev[wv], 0), "copy waits W2 readers")) return fail_cuda();
+      for (int k = 0; k < NCLS; ++k)
+        if (cp.wait_prev[k] &&
+            !ok(cudaStreamWaitEvent(ks, rt->slot_free_down[(size_t)cp.slot * NCLS + k], 0), "copy waits last step"))
+          return fail_cuda();
       if (!ok(cudaMemcpyAsync(dst + rt->half_bytes, src + rt->half_bytes, rt->half_bytes, cudaMemcpyHostToDevice, ks),
               "swap-in W2") ||
           !ok(cudaEventRecord(rt->copy_down_ev[a.index], ks), "record"))
         return fail_cuda();
       if (c.profile && !ok(cudaEventRecord(rt->t_copy_end[a.index], ks), "record")) return fail_cuda();
-    } else {
-      const WaveAct &w = waves[a.index];
-      cudaStream_t ws = rt->cls_stream[w.cls];
-      coe_mlp *m = rt->mlp[w.cls];
-      if (!w.wait_recvs.empty()) {
-        int64_t limit = -1;
-        for (int32_t hslot : w.wait_recvs) limit = std::max<int64_t>(limit, all_hops[my_hops[hslot]].index);
-        if (!issue_hops_until(limit)) return COE_CUDA_ERR_CUDA;
-        for (int32_t hslot : w.wait_recvs)
-          if (!ok(cudaStreamWaitEvent(ws, rt->recv_ev[hslot], 0), "wave waits hop")) return fail_cuda();
-      }
-      for (int32_t wid : w.wait_waves)
-        if (!ok(cudaStreamWaitEvent(ws, rt->wave_down_ev[wid], 0), "wave waits producer")) return fail_cuda();
-      for (int32_t cid : w.wait_copies)
-        if (!ok(cudaStreamWaitEvent(ws, rt->copy_up_ev[cid], 0), "wave waits W1")) return fail_cuda();
-      if (c.profile && !ok(cudaEventRecord(rt->t_wave_start[a.index], ws), "record")) return fail_cuda();
-      const int ctas = w.cls == 1 ? rt->r_ctas : rt->m_ctas;
-      int rc = coe_grouped_mlp(m, dg_up + w.first_group, dg_down + w.first_group, w.num_groups, w.tiles_up,
-                               w.tiles_down, sb.boff, sb.mreq, sb.mstage, 1, ctas, ws);
-      if (rc) return rc;
-      if (!ok(cudaEventRecord(rt->wave_up_ev[a.index], ws), "record")) return fail_cuda();
-      for (int32_t s : w.frees_slots)
-        if (!ok(cudaEventRecord(rt->slot_free_up[s], ws), "record")) return fail_cuda();
-      for (int32_t cid : w.wait_copies)
-        if (!ok(cudaStreamWaitEvent(ws, rt->copy_down_ev[cid], 0), "wave waits W2")) return fail_cuda();
-      rc = coe_grouped_mlp(m, dg_up + w.first_group, dg_down + w.first_group, w.num_groups, w.tiles_up,
-                           w.tiles_down, sb.boff, sb.mreq, sb.mstage, 2, ctas, ws);
-      if (rc) return rc;
-      st.launches += 2;
-      if (!ok(cudaEventRecord(rt->wave_down_ev[a.index], ws), "record")) return fail_cuda();
-      for (int32_t s : w.frees_slots) {
-        if (!ok(cudaEventRecord(rt->slot_free_down[s], ws), "record")) return fail_cuda();
-        rt->slot_free_valid[s] = 1;
-      }
-      if (c.profile && !ok(cudaEventRecord(rt->t_wave_end[a.index], ws), "record")) return fail_cuda();
-      waves_issued = a.index + 1;
+      continue;
     }
+    const WaveAct &w = waves[a.index];
+    cudaStream_t ws = rt->cls_stream[w.cls];
+    coe_mlp *m = rt->mlp[w.cls];
+    if (!w.wait_recvs.empty()) {
+      int64_t limit = -1;
+      for (int32_t hslot : w.wait_recvs) limit = std::max<int64_t>(limit, all_hops[my_hops[hslot]].index);
+      if (!issue_hops_until(limit)) return COE_CUDA_ERR_CUDA;
+      for (int32_t hslot : w.wait_recvs)
+        if (!ok(cudaStreamWaitEvent(ws, rt->recv_ev[hslot], 0), "wave waits hop")) return fail_cuda();
+    }
+    for (int32_t wid : w.wait_waves)
+      if (!ok(cudaStreamWaitEvent(ws, rt->wave_down_ev[wid], 0), "wave waits producer")) return fail_cuda();
+    for (int32_t cid : w.wait_copies)
+      if (!ok(cudaStreamWaitEvent(ws, rt->copy_up_ev[cid], 0), "wave waits W1")) return fail_cuda();
+    if (c.profile && !ok(cudaEventRecord(rt->t_wave_start[a.index], ws), "record")) return fail_cuda();
+    const int ctas = w.cls == 1 ? rt->r_ctas : rt->m_ctas;
+    int rc = coe_grouped_mlp(m, dg_up + w.first_group, dg_down + w.first_group, w.num_groups, w.tiles_up, w.tiles_down,
+                             sb.boff, sb.mreq, sb.mstage, 1, ctas, ws);
+    if (rc) return rc;
+    if (!ok(cudaEventRecord(rt->wave_up_ev[a.index], ws), "record")) return fail_cuda();
+    for (int32_t sk : w.frees_slots)
+      if (!ok(cudaEventRecord(rt->slot_free_up[sk], ws), "record")) return fail_cuda();
+    for (int32_t cid : w.wait_copies)
+      if (!ok(cudaStreamWaitEvent(ws, rt->copy_down_ev[cid], 0), "wave waits W2")) return fail_cuda();
+    rc = coe_grouped_mlp(m, dg_up + w.first_group, dg_down + w.first_group, w.num_groups, w.tiles_up, w.tiles_down,
+                         sb.boff, sb.mreq, sb.mstage, 2, ctas, ws);
+    if (rc) return rc;
+    st.launches += 2;
+    if (!ok(cudaEventRecord(rt->wave_down_ev[a.index], ws), "record")) return fail_cuda();
+    for (int32_t sk : w.frees_slots) {
+      if (!ok(cudaEventRecord(rt->slot_free_down[sk], ws), "record")) return fail_cuda();
+      rt->slot_free_valid[sk] = 1;
+    }
+    for (int32_t gi = w.first_group; gi < w.first_group + w.num_groups; ++gi) issued[g_up[gi].batch] = 1;
+    if (c.profile && !ok(cudaEventRecord(rt->t_wave_end[a.index], ws), "record")) return fail_cuda();
   }
   if (!issue_hops_until(INT64_MAX)) return COE_CUDA_ERR_CUDA;
   if (!my_hops.empty() && (!ok(cudaEventRecord(rt->hop_drained, rt->hop), "record") ||
                            !ok(cudaStreamWaitEvent(cs, rt->hop_drained, 0), "join hop")))
     return fail_cuda();
-  // join: the main stream waits for the swap-in stream and the copy stream; set released at step end
   if (!ok(cudaEventRecord(rt->copy_drained, ks), "record") || !ok(cudaStreamWaitEvent(cs, rt->copy_drained, 0), "join"))
     return fail_cuda();
-  for (int k = 1; k < coe_runtime::NCLS; ++k)
+  for (int k = 1; k < NCLS; ++k)
     if (!ok(cudaEventRecord(rt->cls_drained[k], rt->cls_stream[k]), "record") ||
         !ok(cudaStreamWaitEvent(cs, rt->cls_drained[k], 0), "join"))
       return fail_cuda();
@@ -1082,10 +1255,6 @@ int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_step_stats *
   rt->last_adm = n_adm;
   rt->last_batches = n_batches;
   rt->last_set = set_idx;
-  st.max_wave_groups = std::max(st.max_wave_groups, 0);
-  (void)waves_by_cls;
   if (stats) *stats = st;
   return COE_CUDA_OK;
 }
-
-}  // extern "C"

@@ -60,7 +60,8 @@ class RuntimeConfig(ctypes.Structure):
                 ("num_experts", ctypes.c_int32), ("num_slots", ctypes.c_int32), ("max_requests", ctypes.c_int32),
                 ("max_wave_rows", ctypes.c_int64), ("max_admissions", ctypes.c_int64),
                 ("max_batches", ctypes.c_int64), ("weight_seed", ctypes.c_uint64), ("profile", ctypes.c_int32),
-                ("reserve_sms", ctypes.c_int32), ("swapped_stream", ctypes.c_int32), ("store_path", ctypes.c_char_p)]
+                ("reserve_sms", ctypes.c_int32), ("swapped_stream", ctypes.c_int32), ("store_path", ctypes.c_char_p),
+                ("wave_rows_cap", ctypes.c_int64), ("urgent_rows_cap", ctypes.c_int64)]
 
 
 _declared = False
@@ -94,6 +95,8 @@ def _lib():
         lib.coe_comm_create.restype = ctypes.c_int
         lib.coe_comm_destroy.argtypes = [V]
         lib.coe_comm_destroy.restype = None
+        lib.coe_runtime_set_knobs.argtypes = [V, I64, I64, I32]
+        lib.coe_runtime_set_knobs.restype = ctypes.c_int
         lib.coe_runtime_attach_comm.argtypes = [V, V]
         lib.coe_runtime_attach_comm.restype = ctypes.c_int
         lib.coe_runtime_counts.argtypes = [V, P(I32), P(I32)]
@@ -144,8 +147,9 @@ class B200Runtime:
 
     def __init__(self, shape: RuntimeShape, num_experts: int, num_slots: int, max_requests: int,
                  max_admissions: int, max_wave_rows: int | None = None, weight_seed: int = DEFAULT_WEIGHT_SEED,
-                 profile: bool = False, init_experts: bool = True, reserve_sms: int = 16,
-                 store_path: str | None = None):
+                 profile: bool = False, init_experts: bool = True, reserve_sms: int = 0,
+                 store_path: str | None = None, wave_rows_cap: int | None = None,
+                 urgent_rows_cap: int | None = 8192):
         import torch
 
         if not torch.cuda.is_available():
@@ -159,8 +163,11 @@ class B200Runtime:
         self.weight_seed = weight_seed
         rows = max_wave_rows or max(128, min(32768, max_admissions * shape.T))
         cfg = RuntimeConfig(shape.d, shape.h, shape.T, num_experts, num_slots, max_requests, rows, max_admissions,
-                            max_admissions, weight_seed, 1 if profile else 0, reserve_sms, 0,
-                            store_path.encode() if store_path else None)
+                            max_admissions, weight_seed, 1 if profile else 0,
+                            int(os.environ.get("COE_RESERVE_SMS", reserve_sms)), 0,
+                            store_path.encode() if store_path else None,
+                            int(os.environ.get("COE_WAVE_ROWS", wave_rows_cap or 0)),
+                            int(os.environ.get("COE_URGENT_ROWS", urgent_rows_cap or 0)))
         self.profile = profile
         self.handle = ctypes.c_void_p()
         _check(self.lib, self.lib.coe_runtime_create(ctypes.byref(cfg), ctypes.byref(self.handle)), "runtime create")
@@ -265,6 +272,10 @@ class B200Runtime:
         _check(self.lib, self.lib.coe_runtime_members(self.handle, req.ctypes.data, stage.ctypes.data,
                                                       boff.ctypes.data), "members")
         return req[:num_admissions], stage[:num_admissions], boff[:num_batches]
+
+    def set_knobs(self, wave_rows_cap: int = 0, urgent_rows_cap: int = 0, reserve_sms: int = -1) -> None:
+        _check(self.lib, self.lib.coe_runtime_set_knobs(self.handle, wave_rows_cap, urgent_rows_cap, reserve_sms),
+               "set knobs")
 
     def intervals(self) -> dict:
         nc, nw = ctypes.c_int32(), ctypes.c_int32()

@@ -127,8 +127,8 @@ def main(only=None):
         if doc["trace_lines"] <= FULL_TRACE_LIMIT:
             doc["trace_jsonl"] = trace_text
         path = os.path.join(HERE, f"{name}.json.gz")
-        with gzip.open(path, "wt", compresslevel=9) as fh:
-            json.dump(doc, fh, sort_keys=True)
+        with open(path, "wb") as raw, gzip.GzipFile(fileobj=raw, mode="wb", compresslevel=9, mtime=0) as fh:
+            fh.write(json.dumps(doc, sort_keys=True).encode("utf-8"))
         print(f"{name}: {doc['trace_lines']} trace lines, {os.path.getsize(path) / 1024:.0f} KiB")
 
 

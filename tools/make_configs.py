@@ -39,8 +39,8 @@ def write(path, doc, gz=False):
     os.makedirs(os.path.dirname(path), exist_ok=True)
     text = json.dumps(doc, sort_keys=True, separators=(",", ":") if gz else None, indent=None if gz else 1)
     if gz:
-        with gzip.open(path, "wt", encoding="utf-8", compresslevel=9) as fh:
-            fh.write(text)
+        with open(path, "wb") as raw, gzip.GzipFile(fileobj=raw, mode="wb", compresslevel=9, mtime=0) as fh:
+            fh.write(text.encode("utf-8"))
     else:
         with open(path, "w") as fh:
             fh.write(text + "\n")
