@@ -255,17 +255,15 @@ def main() -> None:
         host_in = torch.empty(n_req * row, dtype=torch.bfloat16).pin_memory()
         host_out = torch.empty(n_req * row, dtype=torch.bfloat16).pin_memory()
         rt.read_buffer(0, host_in.data_ptr(), n_req * row * 2)  # the seeded inputs, copied once (untimed)
-        last = runtime.last_stages(plan0)
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
+        io = None
         for i in range(1 + args.e2e_steps):
             if i == 1:
                 barrier()
                 e0.record(stream)
-            rt.upload_inputs(host_in.data_ptr(), n_req)
-            p = engine.plan(cfg)
-            rt.step(p, rank)
-            rt.download_outputs(last, host_out.data_ptr())
+            p = engine.plan(cfg)  # the public call: plan + serve with pinned host buffers
+            io = rt.step(p, rank, host_inputs=host_in.data_ptr(), host_outputs=host_out.data_ptr())
             keep.append(p)
         e1.record(stream)
         rt.synchronize()
@@ -276,8 +274,10 @@ def main() -> None:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_ms = float(t.item())
         e2e = {"value": n_req * args.e2e_steps / (e2e_ms / 1e3), "unit": "requests/s",
-               "h2d_bytes_per_step": n_req * row * 2, "d2h_bytes_per_step": n_req * row * 2,
-               "ms_per_step": e2e_ms / args.e2e_steps}
+               "h2d_bytes_per_step": io["h2d_input_bytes"], "d2h_bytes_per_step": io["d2h_output_bytes"],
+               "ms_per_step": e2e_ms / args.e2e_steps,
+               "note": "planner + stage-0 inputs streamed H2D just in time + final outputs streamed D2H per wave, "
+                       "all inside the timed region; swap-ins share the same PCIe H2D link"}
 
     # ---- CPU baseline (rank 0, N=1) ----
     cpu = None

@@ -131,10 +131,16 @@ typedef struct coe_step_input {
   const int32_t *op_args;
   int32_t num_initial;                      /* initial residency of this executor          */
   const int32_t *initial;
+  /* end-to-end serving (optional, pinned host memory, [requests][T][d] bf16 by request
+   * index): stage-0 inputs are uploaded just in time on an input stream, each final
+   * stage output is downloaded as soon as its wave completes */
+  const void *host_inputs;
+  void *host_outputs;
 } coe_step_input;
 
 typedef struct coe_step_stats {
   int64_t admissions, batches, waves, launches;
+  int64_t h2d_input_bytes, d2h_output_bytes;
   int64_t loads, load_bytes, restores, restore_bytes;
   int64_t max_wave_rows;
   int32_t max_wave_groups;

@@ -154,6 +154,10 @@ struct coe_runtime {
   std::vector<int32_t> last_wave_cls, last_wave_rows, last_wave_groups;
   int64_t last_adm = 0, last_batches = 0;
   int last_set = 0;
+  cudaStream_t in_stream = nullptr, out_stream = nullptr;  // e2e input uploads / output downloads
+  std::vector<cudaEvent_t> in_ev;
+  cudaEvent_t out_drained = nullptr;
+  bool have_out = false;
   coe_comm *comm = nullptr;            // hop transport (N > 1)
   cudaStream_t hop = nullptr;
   std::vector<cudaEvent_t> recv_ev;
@@ -166,6 +170,8 @@ struct coe_runtime {
       if (st) cudaStreamSynchronize(st);
     if (copy) cudaStreamSynchronize(copy);
     if (hop) cudaStreamSynchronize(hop);
+    if (in_stream) cudaStreamSynchronize(in_stream);
+    if (out_stream) cudaStreamSynchronize(out_stream);
     for (auto m : mlp)
       if (m) coe_mlp_destroy(m);
     std::vector<void *> dev = {slab, x, p0, p1, hbuf[0], hbuf[1], hbuf[2], outbuf, d_perm, d_keys, d_flags, d_last, d_sort_scratch,
@@ -186,18 +192,20 @@ struct coe_runtime {
     } else if (host_store) {
       cudaFreeHost(host_store);
     }
-    for (auto *v : {&recv_ev, &slot_free_up, &slot_free_down, &wave_up_ev, &wave_down_ev, &copy_up_ev, &copy_down_ev,
+    for (auto *v : {&in_ev, &recv_ev, &slot_free_up, &slot_free_down, &wave_up_ev, &wave_down_ev, &copy_up_ev, &copy_down_ev,
                     &t_copy_start, &t_copy_end, &t_wave_start, &t_wave_end}) {
       for (auto e : *v) cudaEventDestroy(e);
       v->clear();
     }
-    for (cudaEvent_t e : {hop_drained, step_end, staged, copy_drained, grouped, cls_drained[0], cls_drained[1], cls_drained[2], t_step_start, t_group_end, t_step_end, staging_done[0],
+    for (cudaEvent_t e : {out_drained, hop_drained, step_end, staged, copy_drained, grouped, cls_drained[0], cls_drained[1], cls_drained[2], t_step_start, t_group_end, t_step_end, staging_done[0],
                           staging_done[1]})
       if (e) cudaEventDestroy(e);
     for (auto st : cls_stream)
       if (st) cudaStreamDestroy(st);
     if (copy) cudaStreamDestroy(copy);
     if (hop) cudaStreamDestroy(hop);
+    if (in_stream) cudaStreamDestroy(in_stream);
+    if (out_stream) cudaStreamDestroy(out_stream);
   }
 
   bool ensure_events(std::vector<cudaEvent_t> &v, size_t n, bool timing) {
@@ -306,6 +314,8 @@ int coe_runtime_create(const coe_runtime_config *cfg, coe_runtime **out) {
               ok(cudaStreamCreateWithPriority(&rt->cls_stream[2], cudaStreamNonBlocking, prio_low), "stream") &&
               ok(cudaStreamCreateWithFlags(&rt->copy, cudaStreamNonBlocking), "stream") &&
               ok(cudaStreamCreateWithFlags(&rt->hop, cudaStreamNonBlocking), "stream") &&
+              ok(cudaStreamCreateWithFlags(&rt->in_stream, cudaStreamNonBlocking), "stream") &&
+              ok(cudaStreamCreateWithFlags(&rt->out_stream, cudaStreamNonBlocking), "stream") &&
               dmalloc(&rt->slab, (size_t)rt->expert_bytes * c.num_slots, "slab alloc") &&
               dmalloc(&rt->x, act_bytes, "X alloc") && dmalloc(&rt->p0, act_bytes, "P0 alloc") &&
               dmalloc(&rt->p1, act_bytes, "P1 alloc") && dmalloc(&rt->outbuf, act_bytes, "out alloc") &&
@@ -335,6 +345,7 @@ int coe_runtime_create(const coe_runtime_config *cfg, coe_runtime **out) {
            ok(cudaEventCreateWithFlags(&rt->copy_drained, cudaEventDisableTiming), "event") &&
            ok(cudaEventCreateWithFlags(&rt->grouped, cudaEventDisableTiming), "event") &&
            ok(cudaEventCreateWithFlags(&rt->hop_drained, cudaEventDisableTiming), "event") &&
+           ok(cudaEventCreateWithFlags(&rt->out_drained, cudaEventDisableTiming), "event") &&
            ok(cudaEventCreateWithFlags(&rt->step_end, cudaEventDisableTiming), "event") &&
            ok(cudaEventCreateWithFlags(&rt->cls_drained[0], cudaEventDisableTiming), "event") &&
            ok(cudaEventCreateWithFlags(&rt->cls_drained[1], cudaEventDisableTiming), "event") &&
@@ -481,7 +492,8 @@ int coe_runtime_download_outputs(coe_runtime *rt, const int32_t *last_stage_host
 }
 
 int coe_runtime_synchronize(coe_runtime *rt) {
-  bool good = ok(cudaStreamSynchronize(rt->copy), "sync copy") && ok(cudaStreamSynchronize(rt->hop), "sync hop");
+  bool good = ok(cudaStreamSynchronize(rt->copy), "sync copy") && ok(cudaStreamSynchronize(rt->hop), "sync hop") &&
+              ok(cudaStreamSynchronize(rt->in_stream), "sync in") && ok(cudaStreamSynchronize(rt->out_stream), "sync out");
   for (int k = coe_runtime::NCLS - 1; k >= 0; --k) good = ok(cudaStreamSynchronize(rt->cls_stream[k]), "sync") && good;
   return good ? COE_CUDA_OK : fail_cuda();
 }
@@ -653,6 +665,9 @@ struct BatchInfo {
   int64_t max_recv = -1, min_send = INT64_MAX;
   int32_t wave = -1;
   double done = 0.0;               // estimated completion
+  std::vector<int32_t> inputs;     // e2e: stage-0 requests whose inputs this batch uploads
+  std::vector<int32_t> finals;     // e2e: requests whose final output this batch produces
+  int32_t input_event = -1;
 };
 
 struct CopyInfo {
@@ -754,6 +769,13 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
   std::vector<CopyInfo> copies;
   std::vector<BatchInfo> batches;
   std::vector<int32_t> req_last(c.max_requests, -1);  // latest batch of each request on this executor
+  const bool e2e_in = in->host_inputs != nullptr, e2e_out = in->host_outputs != nullptr;
+  std::vector<int32_t> final_stage;
+  if (e2e_out) {
+    final_stage.assign(c.max_requests, -1);
+    for (int64_t i = 0; i < in->num_admissions; ++i)
+      final_stage[adm[i].request] = std::max(final_stage[adm[i].request], adm[i].stage);
+  }
   auto issue_copy = [&](int32_t e, bool restore) -> bool {
     int32_t best = -1;  // free slot whose readers were issued earliest in op order
     for (int32_t s = 0; s < c.num_slots; ++s) {
@@ -837,6 +859,8 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
         hop_batch[ho->second] = bi;
       }
       req_last[r] = bi;
+      if (e2e_in && s == 0) b.inputs.push_back(r);
+      if (e2e_out && s == final_stage[r]) b.finals.push_back(r);
     }
     slot_readers[b.slot].push_back(bi);
     batches.push_back(std::move(b));
@@ -1135,6 +1159,39 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
 
   if (!my_hops.empty() && rt->have_step_end && !ok(cudaStreamWaitEvent(rt->hop, rt->step_end, 0), "hop waits step"))
     return fail_cuda();
+  // e2e: this step's P writes follow last step's output downloads; its X uploads follow last
+  // step's readers of X; uploads are issued in op order (just in time), one event per batch
+  if (rt->have_out)
+    for (int k = 0; k < NCLS; ++k)
+      if (!ok(cudaStreamWaitEvent(rt->cls_stream[k], rt->out_drained, 0), "P reuse waits downloads"))
+        return fail_cuda();
+  if (e2e_in) {
+    int32_t n_in = 0;
+    for (const BatchInfo &b : batches) n_in += b.inputs.empty() ? 0 : 1;
+    if (!rt->ensure_events(rt->in_ev, (size_t)n_in, false)) return fail_cuda();
+    if (rt->have_step_end && !ok(cudaStreamWaitEvent(rt->in_stream, rt->step_end, 0), "X reuse waits step"))
+      return fail_cuda();
+    const size_t rb = (size_t)rt->row_elems * 2;
+    const char *hin = static_cast<const char *>(in->host_inputs);
+    int32_t ev = 0;
+    for (BatchInfo &b : batches) {
+      if (b.inputs.empty()) continue;
+      std::vector<int32_t> rq = b.inputs;
+      std::sort(rq.begin(), rq.end());
+      for (size_t i = 0; i < rq.size();) {  // coalesce consecutive request rows
+        size_t j = i + 1;
+        while (j < rq.size() && rq[j] == rq[j - 1] + 1) ++j;
+        if (!ok(cudaMemcpyAsync(reinterpret_cast<char *>(rt->x) + rq[i] * rb, hin + rq[i] * rb, (j - i) * rb,
+                                cudaMemcpyHostToDevice, rt->in_stream),
+                "input H2D"))
+          return fail_cuda();
+        st.h2d_input_bytes += (int64_t)((j - i) * rb);
+        i = j;
+      }
+      if (!ok(cudaEventRecord(rt->in_ev[ev], rt->in_stream), "record")) return fail_cuda();
+      b.input_event = ev++;
+    }
+  }
   size_t hop_cursor = 0;
   const size_t row_elems = (size_t)rt->row_elems;
   auto issue_hops_until = [&](int64_t limit) -> bool {
@@ -1205,6 +1262,10 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
       if (!ok(cudaStreamWaitEvent(ws, rt->wave_down_ev[wid], 0), "wave waits producer")) return fail_cuda();
     for (int32_t cid : w.wait_copies)
       if (!ok(cudaStreamWaitEvent(ws, rt->copy_up_ev[cid], 0), "wave waits W1")) return fail_cuda();
+    for (int32_t gi = w.first_group; gi < w.first_group + w.num_groups; ++gi) {
+      const int32_t ie = batches[g_up[gi].batch].input_event;
+      if (ie >= 0 && !ok(cudaStreamWaitEvent(ws, rt->in_ev[ie], 0), "wave waits inputs")) return fail_cuda();
+    }
     if (c.profile && !ok(cudaEventRecord(rt->t_wave_start[a.index], ws), "record")) return fail_cuda();
     const int ctas = w.cls == 1 ? rt->r_ctas : rt->m_ctas;
     int rc = coe_grouped_mlp(m, dg_up + w.first_group, dg_down + w.first_group, w.num_groups, w.tiles_up, w.tiles_down,
@@ -1226,6 +1287,31 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     }
     for (int32_t gi = w.first_group; gi < w.first_group + w.num_groups; ++gi) issued[g_up[gi].batch] = 1;
     if (c.profile && !ok(cudaEventRecord(rt->t_wave_end[a.index], ws), "record")) return fail_cuda();
+    if (e2e_out) {  // final outputs of this wave stream back while later waves run
+      std::vector<int32_t> fin;
+      for (int32_t gi = w.first_group; gi < w.first_group + w.num_groups; ++gi)
+        for (int32_t r : batches[g_up[gi].batch].finals) fin.push_back(r);
+      if (!fin.empty()) {
+        if (!ok(cudaStreamWaitEvent(rt->out_stream, rt->wave_down_ev[a.index], 0), "download waits wave"))
+          return fail_cuda();
+        const size_t rb = (size_t)rt->row_elems * 2;
+        char *hout = static_cast<char *>(in->host_outputs);
+        for (int32_t r : fin) {
+          const int32_t fs = final_stage[r];
+          const char *src = reinterpret_cast<const char *>((fs & 1) ? rt->p1 : rt->p0) + (size_t)r * rb;
+          if (!ok(cudaMemcpyAsync(hout + (size_t)r * rb, src, rb, cudaMemcpyDeviceToHost, rt->out_stream),
+                  "output D2H"))
+            return fail_cuda();
+          st.d2h_output_bytes += (int64_t)rb;
+        }
+      }
+    }
+  }
+  if (e2e_out) {
+    if (!ok(cudaEventRecord(rt->out_drained, rt->out_stream), "record") ||
+        !ok(cudaStreamWaitEvent(cs, rt->out_drained, 0), "join downloads"))
+      return fail_cuda();
+    rt->have_out = true;
   }
   if (!issue_hops_until(INT64_MAX)) return COE_CUDA_ERR_CUDA;
   if (!my_hops.empty() && (!ok(cudaEventRecord(rt->hop_drained, rt->hop), "record") ||

@@ -35,11 +35,13 @@ class StepInput(ctypes.Structure):
         ("num_ops", ctypes.c_int64), ("ops", ctypes.c_void_p),
         ("num_op_args", ctypes.c_int64), ("op_args", ctypes.c_void_p),
         ("num_initial", ctypes.c_int32), ("initial", ctypes.c_void_p),
+        ("host_inputs", ctypes.c_void_p), ("host_outputs", ctypes.c_void_p),
     ]
 
 
 class StepStats(ctypes.Structure):
-    _fields_ = [(n, ctypes.c_int64) for n in ("admissions", "batches", "waves", "launches", "loads", "load_bytes",
+    _fields_ = [(n, ctypes.c_int64) for n in ("admissions", "batches", "waves", "launches", "h2d_input_bytes",
+                                               "d2h_output_bytes", "loads", "load_bytes",
                                                "restores", "restore_bytes", "max_wave_rows")] + \
                [("max_wave_groups", ctypes.c_int32), ("rank_bits", ctypes.c_int32)]
 
@@ -241,7 +243,9 @@ class B200Runtime:
         return int(self.lib.coe_runtime_stream(self.handle, which) or 0)
 
     # -- execution ---------------------------------------------------------
-    def step(self, plan, executor: int = 0) -> dict:
+    def step(self, plan, executor: int = 0, host_inputs: int | None = None, host_outputs: int | None = None) -> dict:
+        """Execute ``plan``'s op log for ``executor``.  With pinned host buffers the step is
+        end to end: inputs stream in just in time, final outputs stream out per wave."""
         lib = plan.lib
         h = plan.handle
         init = np.ascontiguousarray(plan.initial_residency()[executor], dtype=np.int32)
@@ -251,7 +255,7 @@ class B200Runtime:
             lib.coe_plan_num_admissions(h), ctypes.cast(lib.coe_plan_admissions(h), ctypes.c_void_p),
             lib.coe_plan_num_ops(h), ctypes.cast(lib.coe_plan_ops(h), ctypes.c_void_p),
             lib.coe_plan_num_op_args(h), ctypes.cast(lib.coe_plan_op_args(h), ctypes.c_void_p),
-            len(init), init.ctypes.data if len(init) else None,
+            len(init), init.ctypes.data if len(init) else None, host_inputs, host_outputs,
         )
         stats = StepStats()
         _check(self.lib, self.lib.coe_runtime_step(self.handle, ctypes.byref(inp), ctypes.byref(stats)), "step")

@@ -132,3 +132,24 @@ def test_c3_budgeted_swaps_mini_shape():
     _check_grouping(plan, rt, stats[-1])
     _check_outputs(plan, outs, shape, sample=16)
     assert np.array_equal(outs[0], outs[1])
+
+
+def test_streamed_end_to_end_io_matches_device_path():
+    """Pinned host inputs in, final outputs out, inside one step (the e2e API):
+    identical bytes to the device-resident path for every request."""
+    import torch
+
+    w = _trim(configs.load("c2", 1000), 200)
+    shape = runtime.shape_of(w)
+    plan, rt, stats, outs = _serve(w, shape, steps=1)
+    n = len(plan.resolved.request_ids)
+    row = shape.T * shape.d
+    host_in = torch.empty(n * row, dtype=torch.bfloat16).pin_memory()
+    rt.read_buffer(0, host_in.data_ptr(), n * row * 2)
+    host_out = torch.zeros(n * row, dtype=torch.bfloat16).pin_memory()
+    p2 = engine.plan(configs.run_config(w, trace=False))
+    st = rt.step(p2, host_inputs=host_in.data_ptr(), host_outputs=host_out.data_ptr())
+    rt.synchronize()
+    assert st["h2d_input_bytes"] == n * row * 2 and st["d2h_output_bytes"] == n * row * 2
+    got = host_out.view(n, shape.T, shape.d).float().numpy()
+    assert np.array_equal(got, outs[0])
