@@ -97,6 +97,25 @@ struct Action {
 
 bool ok(cudaError_t e, const char *what) { return coe_cuda_ok(e, what); }
 
+// Many row copies as one cudaMemcpyBatchAsync (CUDA 12.8+): the e2e path moves one
+// T x d row block per request, and per-call launch cost would dominate small rows.
+bool batched_copy(std::vector<void *> &dsts, std::vector<void *> &srcs, std::vector<size_t> &sizes,
+                  cudaStream_t stream, const char *what) {
+  if (dsts.empty()) return true;
+  if (dsts.size() > 1) {
+    cudaMemcpyAttributes attr{};
+    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+    size_t attr_idx = 0, fail = 0;
+    cudaError_t e = cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), dsts.size(), &attr, &attr_idx, 1,
+                                         &fail, stream);
+    if (e == cudaSuccess) return true;
+    cudaGetLastError();  // unsupported driver: fall back to one call per copy
+  }
+  for (size_t i = 0; i < dsts.size(); ++i)
+    if (!ok(cudaMemcpyAsync(dsts[i], srcs[i], sizes[i], cudaMemcpyDefault, stream), what)) return false;
+  return true;
+}
+
 }  // namespace
 
 void coe_set_error(const std::string &msg) { g_last_error = msg; }
@@ -1178,16 +1197,18 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
       if (b.inputs.empty()) continue;
       std::vector<int32_t> rq = b.inputs;
       std::sort(rq.begin(), rq.end());
+      std::vector<void *> dsts, srcs;
+      std::vector<size_t> sizes;
       for (size_t i = 0; i < rq.size();) {  // coalesce consecutive request rows
         size_t j = i + 1;
         while (j < rq.size() && rq[j] == rq[j - 1] + 1) ++j;
-        if (!ok(cudaMemcpyAsync(reinterpret_cast<char *>(rt->x) + rq[i] * rb, hin + rq[i] * rb, (j - i) * rb,
-                                cudaMemcpyHostToDevice, rt->in_stream),
-                "input H2D"))
-          return fail_cuda();
+        dsts.push_back(reinterpret_cast<char *>(rt->x) + rq[i] * rb);
+        srcs.push_back(const_cast<char *>(hin) + rq[i] * rb);
+        sizes.push_back((j - i) * rb);
         st.h2d_input_bytes += (int64_t)((j - i) * rb);
         i = j;
       }
+      if (!batched_copy(dsts, srcs, sizes, rt->in_stream, "input H2D")) return fail_cuda();
       if (!ok(cudaEventRecord(rt->in_ev[ev], rt->in_stream), "record")) return fail_cuda();
       b.input_event = ev++;
     }
@@ -1296,14 +1317,16 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
           return fail_cuda();
         const size_t rb = (size_t)rt->row_elems * 2;
         char *hout = static_cast<char *>(in->host_outputs);
+        std::vector<void *> dsts, srcs;
+        std::vector<size_t> sizes;
         for (int32_t r : fin) {
           const int32_t fs = final_stage[r];
-          const char *src = reinterpret_cast<const char *>((fs & 1) ? rt->p1 : rt->p0) + (size_t)r * rb;
-          if (!ok(cudaMemcpyAsync(hout + (size_t)r * rb, src, rb, cudaMemcpyDeviceToHost, rt->out_stream),
-                  "output D2H"))
-            return fail_cuda();
+          dsts.push_back(hout + (size_t)r * rb);
+          srcs.push_back(reinterpret_cast<char *>((fs & 1) ? rt->p1 : rt->p0) + (size_t)r * rb);
+          sizes.push_back(rb);
           st.d2h_output_bytes += (int64_t)rb;
         }
+        if (!batched_copy(dsts, srcs, sizes, rt->out_stream, "output D2H")) return fail_cuda();
       }
     }
   }
