@@ -70,6 +70,8 @@ typedef struct coe_mlp_config {
   void *slab;                   /* expert slots: [num_slots][W1 h*d | W2 d*h]    */
   int32_t num_slots;
   int64_t slot_stride_bytes;
+  int32_t act_ld;               /* row stride of X / P0 / P1 in elements (0: d);
+                                   > d when experts of several widths share them */
 } coe_mlp_config;
 
 /* One planned batch inside a wave.  tile_start is the wave-relative prefix of
@@ -119,6 +121,12 @@ typedef struct coe_runtime_config {
   int64_t wave_rows_cap;    /* main-stream wave size cap (0: max_wave_rows)          */
   int64_t urgent_rows_cap;  /* cap when a wave carries reads an imminent swap-in
                                waits for (0: wave_rows_cap)                          */
+  /* heterogeneous experts: per-shape (d, h) slabs; activations are [requests][T][max d]
+   * and an expert of width d uses the first d columns (d is constant along a chain) */
+  int32_t num_shapes;       /* 0: a single shape (d, h, num_slots above)            */
+  const int32_t *shape_d, *shape_h, *shape_slots;   /* [num_shapes]                  */
+  const int32_t *expert_shape;                       /* [num_experts] shape index     */
+  const uint8_t *store_mask; /* [num_experts] experts held in the host store (NULL: all) */
 } coe_runtime_config;
 
 typedef struct coe_step_input {

@@ -26,9 +26,6 @@ CONFIG_DIR = os.path.join(DATA, "configs")
 EXEC_TABLE = os.path.join(DATA, "b200_exec.json")
 NAMES = ("c1", "c2", "c3", "c4", "c5")
 
-# (d, h) size buckets of the heterogeneous config (10M .. 1B parameters)
-C5_BUCKETS = ((1024, 4096), (1024, 8192), (2048, 8192), (2048, 16384), (4096, 16384), (4096, 32768),
-              (8192, 32768), (8192, 61440))
 
 # B200 memory tiers (measured on the pool: pinned H2D 55.6 GB/s, gpurun_out/probe_box.json);
 # the host tier holds every expert, so swap-ins are always host-tier DMA.

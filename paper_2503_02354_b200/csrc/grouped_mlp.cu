@@ -59,6 +59,7 @@ struct GemmArgs {
   int T;
   int K;
   int N;
+  int ld;  // row stride (elements) of the activation buffers X / P0 / P1
   int n_blocks;
   int mode;
   int a_box_rows;
@@ -248,7 +249,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const int req = args.member_req[boff + j];
           const int st = args.member_stage[boff + j];
           __nv_bfloat16 *dst = (st & 1) ? args.out_act1 : args.out_act0;
-          out_row = dst + ((size_t)req * args.T + (row - j * args.T)) * args.N;
+          out_row = dst + ((size_t)req * args.T + (row - j * args.T)) * args.ld;
         }
         out_row += c.n_blk * BN;
       }
@@ -313,12 +314,13 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-// 2-D bf16 row-major [rows, cols] map, box {64, box_rows}, 128B swizzle.
-bool make_map_2d(CUtensorMap *map, void *base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+// 2-D bf16 row-major [rows, cols] map (row stride ld >= cols elements), box {64, box_rows},
+// 128B swizzle.
+bool make_map_2d(CUtensorMap *map, void *base, uint64_t rows, uint64_t cols, uint32_t box_rows, uint64_t ld = 0) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[2] = {cols, rows};
-  cuuint64_t strides[1] = {cols * 2};
+  cuuint64_t strides[1] = {(ld ? ld : cols) * 2};
   cuuint32_t box[2] = {BK, box_rows};
   cuuint32_t estr[2] = {1, 1};
   return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -351,6 +353,10 @@ struct coe_mlp {
 extern "C" {
 
 int coe_mlp_create(const coe_mlp_config *cfg, coe_mlp **out) {
+  if (cfg->act_ld > 0 && (cfg->act_ld < cfg->d || cfg->act_ld % 8)) {
+    coe_set_error("grouped MLP: act_ld must be >= d and a multiple of 8");
+    return COE_CUDA_ERR_CONFIG;
+  }
   if (cfg->d % BN || cfg->h % BN || cfg->d % BK || cfg->h % BK) {
     coe_set_error("grouped MLP needs d and h to be multiples of 256");
     return COE_CUDA_ERR_CONFIG;
@@ -363,9 +369,10 @@ int coe_mlp_create(const coe_mlp_config *cfg, coe_mlp **out) {
   m->cfg = *cfg;
   m->a_box_rows = cfg->T < BM ? cfg->T : BM;
   bool ok = true;
-  ok &= make_map_2d(&m->xmap, cfg->x, (uint64_t)cfg->act_rows, cfg->d, m->a_box_rows);
-  ok &= make_map_2d(&m->act0, cfg->act0, (uint64_t)cfg->act_rows, cfg->d, m->a_box_rows);
-  ok &= make_map_2d(&m->act1, cfg->act1, (uint64_t)cfg->act_rows, cfg->d, m->a_box_rows);
+  const uint64_t ld = cfg->act_ld > 0 ? (uint64_t)cfg->act_ld : (uint64_t)cfg->d;
+  ok &= make_map_2d(&m->xmap, cfg->x, (uint64_t)cfg->act_rows, cfg->d, m->a_box_rows, ld);
+  ok &= make_map_2d(&m->act0, cfg->act0, (uint64_t)cfg->act_rows, cfg->d, m->a_box_rows, ld);
+  ok &= make_map_2d(&m->act1, cfg->act1, (uint64_t)cfg->act_rows, cfg->d, m->a_box_rows, ld);
   ok &= make_map_2d(&m->hmap, cfg->h_scratch, (uint64_t)cfg->h_rows, cfg->h, BM);
   // slot layout: [W1: h x d][W2: d x h]
   ok &= make_map_3d(&m->w1, cfg->slab, cfg->num_slots, cfg->h, cfg->d, cfg->slot_stride_bytes);
@@ -414,6 +421,7 @@ int coe_grouped_mlp(coe_mlp *m, const coe_mlp_group *groups_up, const coe_mlp_gr
     a.T = c.T;
     a.K = pass == 0 ? c.d : c.h;
     a.N = pass == 0 ? c.h : c.d;
+    a.ld = c.act_ld > 0 ? c.act_ld : c.d;
     a.n_blocks = a.N / BN;
     a.mode = pass;
     a.a_box_rows = m->a_box_rows;

@@ -33,6 +33,7 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <array>
 #include <cstring>
 #include <climits>
 #include <string>
@@ -79,6 +80,7 @@ struct CopyAct {
 
 struct WaveAct {
   int32_t cls;  // stream: 0 main, 1 release (high priority, reserved SMs)
+  int32_t shape = 0;  // expert shape (one K3 tensor-map set per wave)
   int32_t first_group;
   int32_t num_groups;
   int32_t tiles_up;
@@ -132,8 +134,19 @@ struct StepBuffers {  // device arrays one step uses; two sets alternate
 
 struct coe_runtime {
   coe_runtime_config cfg{};
-  int64_t expert_bytes = 0, half_bytes = 0;
-  int64_t row_elems = 0;  // T * d
+  // expert shapes: shape k owns global slots [slot_base[k], slot_base[k] + slot_count[k]) in
+  // its own slab of sbytes[k]-sized slots; act_ld = widest d (activation row stride)
+  int S = 1;
+  std::vector<int32_t> sd, sh, slot_base, slot_count, slot_shape, expert_shape;
+  std::vector<int64_t> sbytes, store_off;
+  std::vector<char *> slabs;
+  int32_t act_ld = 0, h_max = 0, total_slots = 0;
+  int64_t row_elems = 0;  // T * act_ld
+
+  char *slot_ptr(int32_t s) const {
+    const int k = slot_shape[s];
+    return slabs[k] + (int64_t)(s - slot_base[k]) * sbytes[k];
+  }
   // wave classes, one stream each: 0 main (experts resident since step start; also runs K1/K2
   // and the step join), 1 release (last readers of slots a later swap-in overwrites: high
   // priority on reserved SMs -- they gate the copy engine), 2 swapped (experts copied this
@@ -142,7 +155,6 @@ struct coe_runtime {
   cudaStream_t cls_stream[NCLS] = {nullptr, nullptr, nullptr};
   cudaStream_t compute = nullptr, copy = nullptr;  // compute == cls_stream[0]
   // device memory
-  char *slab = nullptr;
   __nv_bfloat16 *x = nullptr, *p0 = nullptr, *p1 = nullptr, *outbuf = nullptr;
   __nv_bfloat16 *hbuf[NCLS] = {nullptr, nullptr, nullptr};
   StepBuffers sets[2];
@@ -157,7 +169,7 @@ struct coe_runtime {
   int64_t staging_bytes = 0;
   cudaEvent_t staging_done[2] = {nullptr, nullptr};
   int32_t *h_last = nullptr;
-  coe_mlp *mlp[NCLS] = {nullptr, nullptr, nullptr};
+  std::vector<std::array<coe_mlp *, NCLS>> mlps;  // [shape][stream class]
   // slot state (persists across steps)
   std::vector<int32_t> slot_expert, expert_slot;
   // last reader of each slot half in the previous step, per compute stream ([slot * NCLS + cls])
@@ -191,10 +203,12 @@ struct coe_runtime {
     if (hop) cudaStreamSynchronize(hop);
     if (in_stream) cudaStreamSynchronize(in_stream);
     if (out_stream) cudaStreamSynchronize(out_stream);
-    for (auto m : mlp)
-      if (m) coe_mlp_destroy(m);
-    std::vector<void *> dev = {slab, x, p0, p1, hbuf[0], hbuf[1], hbuf[2], outbuf, d_perm, d_keys, d_flags, d_last, d_sort_scratch,
+    for (auto &per : mlps)
+      for (auto m : per)
+        if (m) coe_mlp_destroy(m);
+    std::vector<void *> dev = {x, p0, p1, hbuf[0], hbuf[1], hbuf[2], outbuf, d_perm, d_keys, d_flags, d_last, d_sort_scratch,
                                d_compact_scratch};
+    for (char *sl : slabs) dev.push_back(sl);
     for (auto &s : sets) {
       for (void *p : {(void *)s.adm, (void *)s.batch, (void *)s.boff, (void *)s.mreq, (void *)s.mstage,
                       (void *)s.groups})
@@ -288,7 +302,12 @@ float intersect_len(const std::vector<std::pair<float, float>> &a0, const std::v
 // node) the copy lives in a shared file mapping registered with every process's CUDA
 // context, so N ranks share one 60 GB store instead of pinning N copies.
 static bool rt_alloc_store(coe_runtime *rt, const char *path) {
-  rt->store_bytes = (size_t)rt->expert_bytes * rt->cfg.num_experts;
+  rt->store_bytes = 0;
+  for (int64_t off : rt->store_off) rt->store_bytes = std::max<size_t>(rt->store_bytes, (size_t)(off >= 0 ? off : 0));
+  rt->store_bytes = 0;
+  for (int32_t e = 0; e < rt->cfg.num_experts; ++e)
+    if (rt->store_off[e] >= 0) rt->store_bytes = std::max<size_t>(rt->store_bytes, (size_t)rt->store_off[e] + rt->sbytes[rt->expert_shape[e]]);
+  if (rt->store_bytes == 0) rt->store_bytes = 16;
   if (!path || !*path)
     return ok(cudaHostAlloc(reinterpret_cast<void **>(&rt->host_store), rt->store_bytes, cudaHostAllocDefault),
               "pinned expert store");
@@ -321,9 +340,40 @@ int coe_runtime_create(const coe_runtime_config *cfg, coe_runtime **out) {
   auto *rt = new coe_runtime();
   rt->cfg = *cfg;
   const auto &c = rt->cfg;
-  rt->expert_bytes = 2LL * c.d * c.h * 2;
-  rt->half_bytes = rt->expert_bytes / 2;
-  rt->row_elems = (int64_t)c.T * c.d;
+  if (c.num_shapes > 0) {
+    rt->S = c.num_shapes;
+    for (int k = 0; k < rt->S; ++k) {
+      rt->sd.push_back(c.shape_d[k]);
+      rt->sh.push_back(c.shape_h[k]);
+      rt->slot_count.push_back(c.shape_slots[k]);
+    }
+  } else {
+    rt->S = 1;
+    rt->sd = {c.d};
+    rt->sh = {c.h};
+    rt->slot_count = {c.num_slots};
+  }
+  for (int k = 0; k < rt->S; ++k) {
+    rt->sbytes.push_back(2LL * rt->sd[k] * rt->sh[k] * 2);
+    rt->slot_base.push_back(rt->total_slots);
+    rt->total_slots += rt->slot_count[k];
+    for (int32_t q = 0; q < rt->slot_count[k]; ++q) rt->slot_shape.push_back(k);
+    rt->act_ld = std::max(rt->act_ld, rt->sd[k]);
+    rt->h_max = std::max(rt->h_max, rt->sh[k]);
+  }
+  rt->expert_shape.assign(c.num_experts, 0);
+  if (c.num_shapes > 0 && c.expert_shape)
+    for (int32_t e = 0; e < c.num_experts; ++e) rt->expert_shape[e] = c.expert_shape[e];
+  rt->store_off.assign(c.num_experts, -1);
+  {
+    int64_t off = 0;
+    for (int32_t e = 0; e < c.num_experts; ++e)
+      if (!c.store_mask || c.store_mask[e]) {
+        rt->store_off[e] = off;
+        off += rt->sbytes[rt->expert_shape[e]];
+      }
+  }
+  rt->row_elems = (int64_t)c.T * rt->act_ld;
   const int64_t act_bytes = (int64_t)c.max_requests * rt->row_elems * 2;
   const size_t A = (size_t)c.max_admissions, B = (size_t)c.max_batches;
   int prio_low = 0, prio_high = 0;
@@ -335,17 +385,19 @@ int coe_runtime_create(const coe_runtime_config *cfg, coe_runtime **out) {
               ok(cudaStreamCreateWithFlags(&rt->hop, cudaStreamNonBlocking), "stream") &&
               ok(cudaStreamCreateWithFlags(&rt->in_stream, cudaStreamNonBlocking), "stream") &&
               ok(cudaStreamCreateWithFlags(&rt->out_stream, cudaStreamNonBlocking), "stream") &&
-              dmalloc(&rt->slab, (size_t)rt->expert_bytes * c.num_slots, "slab alloc") &&
               dmalloc(&rt->x, act_bytes, "X alloc") && dmalloc(&rt->p0, act_bytes, "P0 alloc") &&
               dmalloc(&rt->p1, act_bytes, "P1 alloc") && dmalloc(&rt->outbuf, act_bytes, "out alloc") &&
-              dmalloc(&rt->hbuf[0], (size_t)c.max_wave_rows * c.h * 2, "H alloc") &&
-              dmalloc(&rt->hbuf[1], (size_t)c.max_wave_rows * c.h * 2, "H alloc") &&
-              dmalloc(&rt->hbuf[2], (size_t)c.max_wave_rows * c.h * 2, "H alloc") &&
+              dmalloc(&rt->hbuf[0], (size_t)c.max_wave_rows * rt->h_max * 2, "H alloc") &&
+              dmalloc(&rt->hbuf[1], (size_t)c.max_wave_rows * rt->h_max * 2, "H alloc") &&
+              dmalloc(&rt->hbuf[2], (size_t)c.max_wave_rows * rt->h_max * 2, "H alloc") &&
               dmalloc(&rt->d_perm, 4 * A, "perm alloc") && dmalloc(&rt->d_keys, 4 * A, "keys alloc") &&
               dmalloc(&rt->d_flags, 64, "flags alloc") && dmalloc(&rt->d_last, 4 * (size_t)c.max_requests, "last") &&
               dmalloc(&rt->d_sort_scratch, (size_t)coe_group_sort_scratch_bytes(c.max_admissions), "sort scratch") &&
               dmalloc(&rt->d_compact_scratch, (size_t)coe_run_compact_scratch_bytes(c.max_admissions, (int)B, 1),
                       "compact scratch");
+  rt->slabs.assign(rt->S, nullptr);
+  for (int k = 0; k < rt->S; ++k)
+    good = good && dmalloc(&rt->slabs[k], (size_t)rt->sbytes[k] * std::max(1, rt->slot_count[k]), "slab alloc");
   for (auto &s : rt->sets)
     good = good && dmalloc(&s.adm, 16 * A, "adm alloc") && dmalloc(&s.batch, 8 * B, "batch alloc") &&
            dmalloc(&s.boff, 4 * B, "boff alloc") && dmalloc(&s.mreq, 4 * A, "member alloc") &&
@@ -371,26 +423,29 @@ int coe_runtime_create(const coe_runtime_config *cfg, coe_runtime **out) {
            ok(cudaEventCreateWithFlags(&rt->cls_drained[2], cudaEventDisableTiming), "event") &&
            ok(cudaEventCreate(&rt->t_step_start), "event") && ok(cudaEventCreate(&rt->t_group_end), "event") &&
            ok(cudaEventCreate(&rt->t_step_end), "event") &&
-           rt->ensure_events(rt->slot_free_up, (size_t)c.num_slots * coe_runtime::NCLS, false) &&
-           rt->ensure_events(rt->slot_free_down, (size_t)c.num_slots * coe_runtime::NCLS, false);
+           rt->ensure_events(rt->slot_free_up, (size_t)rt->total_slots * coe_runtime::NCLS, false) &&
+           rt->ensure_events(rt->slot_free_down, (size_t)rt->total_slots * coe_runtime::NCLS, false);
   }
   if (good) {
-    coe_mlp_config mc{};
-    mc.d = c.d;
-    mc.h = c.h;
-    mc.T = c.T;
-    mc.x = rt->x;
-    mc.act0 = rt->p0;
-    mc.act1 = rt->p1;
-    mc.act_rows = (int64_t)c.max_requests * c.T;
-    mc.h_scratch = rt->hbuf[0];
-    mc.h_rows = c.max_wave_rows;
-    mc.slab = rt->slab;
-    mc.num_slots = c.num_slots;
-    mc.slot_stride_bytes = rt->expert_bytes;
-    for (int k = 0; k < coe_runtime::NCLS && good; ++k) {
-      mc.h_scratch = rt->hbuf[k];
-      if (coe_mlp_create(&mc, &rt->mlp[k]) != COE_CUDA_OK) good = false;
+    rt->mlps.assign(rt->S, std::array<coe_mlp *, coe_runtime::NCLS>{nullptr, nullptr, nullptr});
+    for (int sk = 0; sk < rt->S && good; ++sk) {
+      coe_mlp_config mc{};
+      mc.d = rt->sd[sk];
+      mc.h = rt->sh[sk];
+      mc.T = c.T;
+      mc.x = rt->x;
+      mc.act0 = rt->p0;
+      mc.act1 = rt->p1;
+      mc.act_rows = (int64_t)c.max_requests * c.T;
+      mc.act_ld = rt->act_ld;
+      mc.h_rows = c.max_wave_rows;
+      mc.slab = rt->slabs[sk];
+      mc.num_slots = std::max(1, rt->slot_count[sk]);
+      mc.slot_stride_bytes = rt->sbytes[sk];
+      for (int k = 0; k < coe_runtime::NCLS && good; ++k) {
+        mc.h_scratch = rt->hbuf[k];
+        if (coe_mlp_create(&mc, &rt->mlps[sk][k]) != COE_CUDA_OK) good = false;
+      }
     }
   }
   if (!good) {
@@ -407,9 +462,9 @@ int coe_runtime_create(const coe_runtime_config *cfg, coe_runtime **out) {
     rt->m_ctas = sms - reserve;
     rt->r_ctas = reserve > 0 ? reserve : sms;
   }
-  rt->slot_expert.assign(c.num_slots, -1);
+  rt->slot_expert.assign(rt->total_slots, -1);
   rt->expert_slot.assign(c.num_experts, -1);
-  rt->slot_free_valid.assign((size_t)c.num_slots * coe_runtime::NCLS, 0);
+  rt->slot_free_valid.assign((size_t)rt->total_slots * coe_runtime::NCLS, 0);
   *out = rt;
   return COE_CUDA_OK;
 }
@@ -422,7 +477,7 @@ void *coe_runtime_buffer(coe_runtime *rt, int which) {
     case 1: return rt->p0;
     case 2: return rt->p1;
     case 3: return rt->hbuf[0];
-    case 4: return rt->slab;
+    case 4: return rt->slabs[0];
     case 5: return rt->host_store;
     case 6: return rt->outbuf;
     default: return nullptr;
@@ -452,15 +507,22 @@ int coe_runtime_slot_of(coe_runtime *rt, int32_t expert) {
 
 int coe_runtime_init_experts(coe_runtime *rt) {
   const auto &c = rt->cfg;
-  const int64_t half = (int64_t)c.d * c.h;  // elements per matrix
   if (!ok(cudaDeviceSynchronize(), "init experts sync")) return fail_cuda();
-  for (int32_t e = 0; e < c.num_experts; ++e) {  // generate into slot 0, stage to the pinned store
-    __nv_bfloat16 *w = reinterpret_cast<__nv_bfloat16 *>(rt->slab);
-    if (coe_fill_uniform_bf16(w, half, coe_expert_seed(c.weight_seed, e, 0), sqrtf(3.0f / c.d), rt->compute) ||
-        coe_fill_uniform_bf16(w + half, half, coe_expert_seed(c.weight_seed, e, 1), sqrtf(3.0f / c.h), rt->compute))
+  for (int32_t e = 0; e < c.num_experts; ++e) {  // generate into the shape's first slot, stage to the store
+    if (rt->store_off[e] < 0) continue;
+    const int k = rt->expert_shape[e];
+    if (rt->slot_count[k] < 1) {
+      coe_set_error("init_experts: a stored expert's shape has no HBM slot");
+      return COE_CUDA_ERR_CONFIG;
+    }
+    const int64_t half = (int64_t)rt->sd[k] * rt->sh[k];  // elements per matrix
+    __nv_bfloat16 *w = reinterpret_cast<__nv_bfloat16 *>(rt->slabs[k]);
+    if (coe_fill_uniform_bf16(w, half, coe_expert_seed(c.weight_seed, e, 0), sqrtf(3.0f / rt->sd[k]), rt->compute) ||
+        coe_fill_uniform_bf16(w + half, half, coe_expert_seed(c.weight_seed, e, 1), sqrtf(3.0f / rt->sh[k]),
+                              rt->compute))
       return COE_CUDA_ERR_CUDA;
-    if (!ok(cudaMemcpyAsync(rt->host_store + e * rt->expert_bytes, rt->slab, rt->expert_bytes,
-                            cudaMemcpyDeviceToHost, rt->compute),
+    if (!ok(cudaMemcpyAsync(rt->host_store + rt->store_off[e], rt->slabs[k], rt->sbytes[k], cudaMemcpyDeviceToHost,
+                            rt->compute),
             "expert store D2H"))
       return fail_cuda();
   }
@@ -591,11 +653,11 @@ int coe_runtime_bench_mlp(coe_runtime *rt, int32_t groups, int32_t requests_per_
   int tu = 0, td = 0;
   for (int32_t g = 0; g < groups; ++g) {
     const int32_t mt = (int32_t)((rows + BM - 1) / BM);
-    gu[g] = coe_mlp_group{(int32_t)rows, g % c.num_slots, g, (int32_t)(g * rows), tu, {0, 0, 0}};
+    gu[g] = coe_mlp_group{(int32_t)rows, g % std::max(1, rt->slot_count[0]), g, (int32_t)(g * rows), tu, {0, 0, 0}};
     gd[g] = gu[g];
     gd[g].tile_start = td;
-    tu += mt * (c.h / BN);
-    td += mt * (c.d / BN);
+    tu += mt * (rt->sh[0] / BN);
+    td += mt * (rt->sd[0] / BN);
     boff[g] = g * requests_per_group;
   }
   for (int32_t r = 0; r < nreq; ++r) mreq[r] = r;
@@ -614,10 +676,10 @@ int coe_runtime_bench_mlp(coe_runtime *rt, int32_t groups, int32_t requests_per_
   float tot_up = 0.f, tot_down = 0.f;
   for (int it = -2; good && it < iters; ++it) {  // two untimed warm-up launches
     good = ok(cudaEventRecord(e0, cs), "record") &&
-           coe_grouped_mlp(rt->mlp[0], d_g, d_g + groups, groups, tu, td, d_i, d_i + groups, d_i + groups + nreq, 1, 0,
+           coe_grouped_mlp(rt->mlps[0][0], d_g, d_g + groups, groups, tu, td, d_i, d_i + groups, d_i + groups + nreq, 1, 0,
                            cs) == COE_CUDA_OK &&
            ok(cudaEventRecord(e1, cs), "record") &&
-           coe_grouped_mlp(rt->mlp[0], d_g, d_g + groups, groups, tu, td, d_i, d_i + groups, d_i + groups + nreq, 2, 0,
+           coe_grouped_mlp(rt->mlps[0][0], d_g, d_g + groups, groups, tu, td, d_i, d_i + groups, d_i + groups + nreq, 2, 0,
                            cs) == COE_CUDA_OK &&
            ok(cudaEventRecord(e2, cs), "record") && ok(cudaEventSynchronize(e2), "sync");
     if (good && it >= 0) {
@@ -771,11 +833,12 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
 
   // ---- phase A: slots, copies, batches in op order ----
   std::vector<uint8_t> plan_res(c.num_experts, 0), pending_restore(c.num_experts, 0);
-  std::vector<int32_t> slot_copy(c.num_slots, -1);
-  std::vector<std::vector<int32_t>> slot_readers(c.num_slots);
-  std::vector<uint8_t> slot_written(c.num_slots, 0);
+  const int32_t NS = rt->total_slots;
+  std::vector<int32_t> slot_copy(NS, -1);
+  std::vector<std::vector<int32_t>> slot_readers(NS);
+  std::vector<uint8_t> slot_written(NS, 0);
   for (int32_t i = 0; i < in->num_initial; ++i) plan_res[in->initial[i]] = 1;
-  for (int32_t s = 0; s < c.num_slots; ++s) {  // slots outside the initial placement are free again
+  for (int32_t s = 0; s < NS; ++s) {  // slots outside the initial placement are free again
     int32_t e = rt->slot_expert[s];
     if (e >= 0 && !plan_res[e]) {
       rt->expert_slot[e] = -1;
@@ -796,8 +859,13 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
       final_stage[adm[i].request] = std::max(final_stage[adm[i].request], adm[i].stage);
   }
   auto issue_copy = [&](int32_t e, bool restore) -> bool {
-    int32_t best = -1;  // free slot whose readers were issued earliest in op order
-    for (int32_t s = 0; s < c.num_slots; ++s) {
+    if (rt->store_off[e] < 0) {
+      coe_set_error("swap-in of an expert that is not in the host store");
+      return false;
+    }
+    const int k = rt->expert_shape[e];
+    int32_t best = -1;  // free slot of the expert's shape whose readers were issued earliest
+    for (int32_t s = rt->slot_base[k]; s < rt->slot_base[k] + rt->slot_count[k]; ++s) {
       if (rt->slot_expert[s] >= 0) continue;
       auto age = [&](int32_t q) { return slot_readers[q].empty() ? -1 : slot_readers[q].back(); };
       if (best < 0 || age(s) < age(best)) best = s;
@@ -814,7 +882,7 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     rt->expert_slot[e] = best;
     slot_copy[best] = (int32_t)copies.size() - 1;
     (restore ? st.restores : st.loads) += 1;
-    (restore ? st.restore_bytes : st.load_bytes) += rt->expert_bytes;
+    (restore ? st.restore_bytes : st.load_bytes) += rt->sbytes[k];
     return true;
   };
   for (size_t k = 0; k < my_ops.size(); ++k) {
@@ -896,8 +964,7 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     if (all_hops[my_hops[i]].src == x) send_slots.push_back((int32_t)i);
 
   // ---- phase B: list schedule ----
-  const double copy_half_s = (double)rt->half_bytes / 55.0e9;
-  const double flops_per_row = 4.0 * c.d * c.h;
+  auto copy_half_s = [&](int32_t e) { return (double)rt->sbytes[rt->expert_shape[e]] / 2 / 55.0e9; };
   const double f_main = 1.2e15 * (double)rt->m_ctas / 148.0, f_rel = 1.2e15 * (double)rt->r_ctas / 148.0;
   const double launch_s = 12e-6;
   std::vector<uint8_t> issued(n_batches, 0);
@@ -909,7 +976,7 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
   std::vector<Action> actions;
   std::vector<coe_mlp_group> g_up, g_down;
   std::vector<int32_t> batch_of_group;  // group position -> batch (K2 batch index = op-order batch)
-  std::vector<int32_t> slot_last_wave(c.num_slots * NCLS, -1);
+  std::vector<int32_t> slot_last_wave(NS * NCLS, -1);
   std::vector<int32_t> copy_action(copies.size(), -1);
 
   auto sends_ready_before = [&](int64_t hop_index) {
@@ -936,13 +1003,14 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
       if (!issued[r]) return false;
     return true;
   };
-  auto wave_time = [&](int64_t rows, int cls) {
+  auto wave_time = [&](int64_t rows, int cls, int shape) {
     const double padded = (double)((rows + BM - 1) / BM * BM);
-    return padded * flops_per_row / (cls ? f_rel : f_main) + 2 * launch_s;
+    return padded * 4.0 * rt->sd[shape] * rt->sh[shape] / (cls ? f_rel : f_main) + 2 * launch_s;
   };
   auto emit_wave = [&](const std::vector<int32_t> &members, int cls, double start) {
     WaveAct w{};
     w.cls = cls;
+    w.shape = rt->slot_shape[batches[members[0]].slot];
     w.first_group = (int32_t)g_up.size();
     const int32_t id = (int32_t)waves.size();
     for (int32_t bi : members) {
@@ -950,7 +1018,7 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
       const int32_t m_tiles = (int32_t)((b.rows + BM - 1) / BM);
       coe_mlp_group gu{};
       gu.rows = (int32_t)b.rows;
-      gu.slot = b.slot;
+      gu.slot = b.slot - rt->slot_base[w.shape];  // local index in the shape's slab
       gu.batch = bi;
       gu.h_row = (int32_t)w.rows;
       gu.tile_start = w.tiles_up;
@@ -960,8 +1028,8 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
       g_down.push_back(gd);
       w.num_groups += 1;
       w.rows += b.rows;
-      w.tiles_up += m_tiles * (c.h / BN);
-      w.tiles_down += m_tiles * (c.d / BN);
+      w.tiles_up += m_tiles * (rt->sh[w.shape] / BN);
+      w.tiles_down += m_tiles * (rt->sd[w.shape] / BN);
       if (b.copy >= 0 && std::find(w.wait_copies.begin(), w.wait_copies.end(), b.copy) == w.wait_copies.end())
         w.wait_copies.push_back(b.copy);
       for (int32_t p : b.producers) {
@@ -974,7 +1042,7 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
       issued[bi] = 1;
       slot_last_wave[b.slot * NCLS + cls] = id;
     }
-    const double end = start + wave_time(w.rows, cls);
+    const double end = start + wave_time(w.rows, cls, w.shape);
     for (int32_t bi : members) batches[bi].done = end;
     t_stream[cls] = end;
     st.max_wave_groups = std::max(st.max_wave_groups, w.num_groups);
@@ -1021,8 +1089,8 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     if (c_start <= r_start && c_start <= m_start) {
       CopyInfo &ci = copies[next_copy];
       ci.issued = true;
-      ci.up_end = c_start + copy_half_s;
-      ci.end = c_start + 2 * copy_half_s;
+      ci.up_end = c_start + copy_half_s(ci.expert);
+      ci.end = c_start + 2 * copy_half_s(ci.expert);
       t_copy = ci.end;
       copy_action[next_copy] = (int32_t)actions.size();
       actions.push_back(Action{true, (int32_t)next_copy});
@@ -1056,6 +1124,7 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
         const int32_t bi = main_pending[i];
         const BatchInfo &b = batches[bi];
         if (!issuable(b) || ready_time(b) > m_start + kSlack) continue;
+        if (!members.empty() && rt->slot_shape[b.slot] != rt->slot_shape[batches[members[0]].slot]) continue;
         if (!members.empty() && rows + b.rows > cap) break;
         bool clash = false;
         for (int32_t j = 0; j < b.count && !clash; ++j)
@@ -1082,8 +1151,8 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
   // copy waits: the last issued reader wave of the slot's previous content, per stream
   std::vector<CopyAct> copy_acts(copies.size());
   {
-    std::vector<int32_t> last_reader_wave(c.num_slots * NCLS, -1);
-    std::vector<uint8_t> written(c.num_slots, 0);
+    std::vector<int32_t> last_reader_wave(NS * NCLS, -1);
+    std::vector<uint8_t> written(NS, 0);
     for (const Action &a : actions) {
       if (a.is_copy) {
         const CopyInfo &ci = copies[a.index];
@@ -1104,7 +1173,7 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
           last_reader_wave[g_up[gi].slot * NCLS + w.cls] = a.index;
       }
     }
-    for (int32_t s = 0; s < c.num_slots; ++s)
+    for (int32_t s = 0; s < NS; ++s)
       for (int k = 0; k < NCLS; ++k)
         if (last_reader_wave[s * NCLS + k] >= 0) waves[last_reader_wave[s * NCLS + k]].frees_slots.push_back(s * NCLS + k);
   }
@@ -1244,8 +1313,9 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
   for (const Action &a : actions) {
     if (a.is_copy) {
       const CopyAct &cp = copy_acts[a.index];
-      char *dst = rt->slab + (int64_t)cp.slot * rt->expert_bytes;
-      const char *src = rt->host_store + (int64_t)cp.expert * rt->expert_bytes;
+      char *dst = rt->slot_ptr(cp.slot);
+      const char *src = rt->host_store + rt->store_off[cp.expert];
+      const int64_t half_bytes = rt->sbytes[rt->slot_shape[cp.slot]] / 2;
       for (int32_t wv : cp.wait_waves)
         if (!ok(cudaStreamWaitEvent(ks, rt->wave_up_ev[wv], 0), "copy waits W1 readers")) return fail_cuda();
       for (int k = 0; k < NCLS; ++k)
@@ -1253,7 +1323,7 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
             !ok(cudaStreamWaitEvent(ks, rt->slot_free_up[(size_t)cp.slot * NCLS + k], 0), "copy waits last step"))
           return fail_cuda();
       if (c.profile && !ok(cudaEventRecord(rt->t_copy_start[a.index], ks), "record")) return fail_cuda();
-      if (!ok(cudaMemcpyAsync(dst, src, rt->half_bytes, cudaMemcpyHostToDevice, ks), "swap-in W1") ||
+      if (!ok(cudaMemcpyAsync(dst, src, half_bytes, cudaMemcpyHostToDevice, ks), "swap-in W1") ||
           !ok(cudaEventRecord(rt->copy_up_ev[a.index], ks), "record"))
         return fail_cuda();
       for (int32_t wv : cp.wait_waves)
@@ -1262,7 +1332,7 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
         if (cp.wait_prev[k] &&
             !ok(cudaStreamWaitEvent(ks, rt->slot_free_down[(size_t)cp.slot * NCLS + k], 0), "copy waits last step"))
           return fail_cuda();
-      if (!ok(cudaMemcpyAsync(dst + rt->half_bytes, src + rt->half_bytes, rt->half_bytes, cudaMemcpyHostToDevice, ks),
+      if (!ok(cudaMemcpyAsync(dst + half_bytes, src + half_bytes, half_bytes, cudaMemcpyHostToDevice, ks),
               "swap-in W2") ||
           !ok(cudaEventRecord(rt->copy_down_ev[a.index], ks), "record"))
         return fail_cuda();
@@ -1271,7 +1341,7 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     }
     const WaveAct &w = waves[a.index];
     cudaStream_t ws = rt->cls_stream[w.cls];
-    coe_mlp *m = rt->mlp[w.cls];
+    coe_mlp *m = rt->mlps[w.shape][w.cls];
     if (!w.wait_recvs.empty()) {
       int64_t limit = -1;
       for (int32_t hslot : w.wait_recvs) limit = std::max<int64_t>(limit, all_hops[my_hops[hslot]].index);

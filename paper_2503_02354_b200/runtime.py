@@ -63,7 +63,9 @@ class RuntimeConfig(ctypes.Structure):
                 ("max_wave_rows", ctypes.c_int64), ("max_admissions", ctypes.c_int64),
                 ("max_batches", ctypes.c_int64), ("weight_seed", ctypes.c_uint64), ("profile", ctypes.c_int32),
                 ("reserve_sms", ctypes.c_int32), ("swapped_stream", ctypes.c_int32), ("store_path", ctypes.c_char_p),
-                ("wave_rows_cap", ctypes.c_int64), ("urgent_rows_cap", ctypes.c_int64)]
+                ("wave_rows_cap", ctypes.c_int64), ("urgent_rows_cap", ctypes.c_int64),
+                ("num_shapes", ctypes.c_int32), ("shape_d", ctypes.c_void_p), ("shape_h", ctypes.c_void_p),
+                ("shape_slots", ctypes.c_void_p), ("expert_shape", ctypes.c_void_p), ("store_mask", ctypes.c_void_p)]
 
 
 _declared = False
@@ -124,7 +126,7 @@ def expert_seed(weight_seed: int, expert: int, matrix: int) -> int:
     return int(_lib().coe_expert_seed(weight_seed, expert, matrix))
 
 
-@dataclass
+@dataclass(frozen=True)
 class RuntimeShape:
     d: int
     h: int
@@ -135,41 +137,60 @@ class RuntimeShape:
         return 2 * self.d * self.h * 2
 
 
-def shape_of(workload) -> RuntimeShape:
+def shape_of(workload):
+    """The workload's expert shape: one ``RuntimeShape`` when every arch shares it, else the
+    ``{arch: (d, h, T)}`` map (heterogeneous experts; ``B200Runtime.for_plan`` accepts both)."""
     shapes = set(workload.shapes.values())
-    if len(shapes) != 1:
-        raise NotImplementedError(
-            f"{workload.name}: the single-shape runtime serves one (d, h, T) per executor, got {sorted(shapes)}")
-    d, h, T = shapes.pop()
-    return RuntimeShape(d, h, T)
+    if len(shapes) == 1:
+        d, h, T = shapes.pop()
+        return RuntimeShape(d, h, T)
+    return dict(workload.shapes)
 
 
 class B200Runtime:
     """One executor's GPU serving state (see module docstring)."""
 
-    def __init__(self, shape: RuntimeShape, num_experts: int, num_slots: int, max_requests: int,
+    def __init__(self, shape, num_experts: int, num_slots, max_requests: int,
                  max_admissions: int, max_wave_rows: int | None = None, weight_seed: int = DEFAULT_WEIGHT_SEED,
                  profile: bool = False, init_experts: bool = True, reserve_sms: int = 0,
                  store_path: str | None = None, wave_rows_cap: int | None = None,
-                 urgent_rows_cap: int | None = 8192):
+                 urgent_rows_cap: int | None = 8192, expert_shape=None, store_mask=None):
+        """``shape``: one ``RuntimeShape`` or a list (heterogeneous experts, ``expert_shape``
+        maps each expert to its index); ``num_slots``: HBM slots (per shape for a list)."""
         import torch
 
         if not torch.cuda.is_available():
             raise RuntimeError("B200Runtime needs a CUDA device (no CPU fallback)")
         torch.cuda.init()
         self.lib = _lib()
-        self.shape = shape
+        shapes = list(shape) if isinstance(shape, (list, tuple)) else [shape]
+        slots = list(num_slots) if isinstance(num_slots, (list, tuple)) else [num_slots]
+        if len({s.T for s in shapes}) != 1 or len(slots) != len(shapes):
+            raise ValueError("one T for all shapes and one slot count per shape")
+        self.shapes = shapes
+        self.shape = shapes[0]
+        self.act_ld = max(s.d for s in shapes)
         self.num_experts = num_experts
-        self.num_slots = num_slots
+        self.num_slots = sum(slots)
         self.max_requests = max_requests
         self.weight_seed = weight_seed
-        rows = max_wave_rows or max(128, min(32768, max_admissions * shape.T))
-        cfg = RuntimeConfig(shape.d, shape.h, shape.T, num_experts, num_slots, max_requests, rows, max_admissions,
+        T = shapes[0].T
+        rows = max_wave_rows or max(128, min(32768, max_admissions * T))
+        self._keep = {
+            "d": np.array([s.d for s in shapes], np.int32), "h": np.array([s.h for s in shapes], np.int32),
+            "slots": np.array(slots, np.int32),
+            "es": np.ascontiguousarray(expert_shape if expert_shape is not None else np.zeros(num_experts), np.int32),
+            "mask": None if store_mask is None else np.ascontiguousarray(store_mask, np.uint8),
+        }
+        k = self._keep
+        cfg = RuntimeConfig(shapes[0].d, shapes[0].h, T, num_experts, slots[0], max_requests, rows, max_admissions,
                             max_admissions, weight_seed, 1 if profile else 0,
                             int(os.environ.get("COE_RESERVE_SMS", reserve_sms)), 0,
                             store_path.encode() if store_path else None,
                             int(os.environ.get("COE_WAVE_ROWS", wave_rows_cap or 0)),
-                            int(os.environ.get("COE_URGENT_ROWS", urgent_rows_cap or 0)))
+                            int(os.environ.get("COE_URGENT_ROWS", urgent_rows_cap or 0)),
+                            len(shapes), k["d"].ctypes.data, k["h"].ctypes.data, k["slots"].ctypes.data,
+                            k["es"].ctypes.data, None if k["mask"] is None else k["mask"].ctypes.data)
         self.profile = profile
         self.handle = ctypes.c_void_p()
         _check(self.lib, self.lib.coe_runtime_create(ctypes.byref(cfg), ctypes.byref(self.handle)), "runtime create")
@@ -177,18 +198,40 @@ class B200Runtime:
             _check(self.lib, self.lib.coe_runtime_init_experts(self.handle), "init experts")
 
     @classmethod
-    def for_plan(cls, plan, shape: RuntimeShape, executor: int = 0, **kw) -> "B200Runtime":
-        """Size a runtime for a resolved plan: slots = expert budget / expert bytes."""
+    def for_plan(cls, plan, shape, executor: int = 0, **kw) -> "B200Runtime":
+        """Size a runtime for a resolved plan.
+
+        Slots per shape = min(experts of that shape this executor touches, expert budget //
+        shape bytes): the planner's byte accounting (ModelPool, expert_pool.py:27-59) bounds
+        how many can be resident at once.  ``shape``: a RuntimeShape (every expert that
+        shape -- the committed configs, or a smaller physical stand-in), or the workload's
+        ``{arch: (d, h, T)}`` map (per-expert shapes; heterogeneous configs)."""
         resolved = plan.resolved
         proc, budget, _inf, _k = resolved.executors[executor]
         if proc != "gpu":
             raise ValueError("B200Runtime serves gpu executors only")
-        # slot count follows the planner's byte budget (ModelPool, expert_pool.py:27-59); the
-        # physical slot size is the shape's (equal to param_bytes for the committed configs)
-        largest = max(spec.param_bytes for spec in resolved.config.registry.experts.values())
-        slots = min(int(budget // largest), len(resolved.expert_ids))
+        registry = resolved.config.registry
+        ids = resolved.expert_ids
+        touched = np.zeros(len(ids), np.uint8)
+        for op in plan.ops():
+            if op["executor"] == executor:
+                touched[int(op["expert"])] = 1
         adm = sum(len(c) for c in resolved.chains)
-        return cls(shape, len(resolved.expert_ids), max(1, slots), len(resolved.request_ids), adm, **kw)
+        if isinstance(shape, RuntimeShape):
+            largest = max(spec.param_bytes for spec in registry.experts.values())
+            slots = max(1, min(int(budget // largest), int(touched.sum()) or 1))
+            return cls(shape, len(ids), slots, len(resolved.request_ids), adm, **kw)
+        arch_shapes = shape
+        shapes = sorted({RuntimeShape(*arch_shapes[registry.experts[e].arch]) for e in ids},
+                        key=lambda s: (s.d, s.h))
+        index = {s: i for i, s in enumerate(shapes)}
+        expert_shape = np.array([index[RuntimeShape(*arch_shapes[registry.experts[e].arch])] for e in ids], np.int32)
+        slots = []
+        for i, s in enumerate(shapes):
+            n_touched = int(touched[expert_shape == i].sum())
+            slots.append(max(1, min(n_touched, int(budget // s.expert_bytes))))
+        return cls(shapes, len(ids), slots, len(resolved.request_ids), adm, expert_shape=expert_shape,
+                   store_mask=touched, **kw)
 
     def close(self) -> None:
         if getattr(self, "handle", None):

@@ -153,3 +153,44 @@ def test_streamed_end_to_end_io_matches_device_path():
     assert st["h2d_input_bytes"] == n * row * 2 and st["d2h_output_bytes"] == n * row * 2
     got = host_out.view(n, shape.T, shape.d).float().numpy()
     assert np.array_equal(got, outs[0])
+
+
+def test_c5_heterogeneous_expert_shapes():
+    """Config 5: 11 expert shapes (d in 1k..8k, h up to 61k), 5-stage chains.  Per-shape HBM
+    slabs and K3 tensor maps; activations are [T][max d] rows, a chain of width d uses the
+    first d columns.  Outputs match the numpy fp32 chain within tolerance."""
+    import torch
+
+    w = _trim(configs.load("c5", 1000), 10)
+    plan = engine.plan(configs.run_config(w, trace=False))
+    _check_against_oracle_batches(w, plan)
+    rt = runtime.B200Runtime.for_plan(plan, w.shapes)
+    n = len(plan.resolved.request_ids)
+    rt.fill_inputs(n)
+    stats = rt.step(plan)
+    rt.synchronize()
+    _check_grouping(plan, rt, stats)
+    T, ld = rt.shapes[0].T, rt.act_ld
+    host = torch.empty(n * T * ld, dtype=torch.bfloat16).pin_memory()
+    rt.download_outputs(runtime.last_stages(plan), host.data_ptr())
+    rt.synchronize()
+    out = host.view(n, T, ld).float().numpy()
+    registry = plan.resolved.config.registry
+    ids = plan.resolved.expert_ids
+    shape_of = {e: w.shapes[registry.experts[ids[e]].arch] for e in range(len(ids))}
+    worst = 0.0
+    checked = 0
+    for r in range(n):
+        chain = plan.resolved.chains[r]
+        d = shape_of[chain[0]][0]
+        assert all(shape_of[e][0] == d for e in chain)
+        if d > 2048 or checked >= 4:  # the numpy reference of the 8k-wide experts takes minutes
+            continue
+        checked += 1
+        x = synth.uniform_bf16(runtime.DEFAULT_INPUT_SEED, r * T * ld, T * ld,
+                               float(np.sqrt(np.float32(3.0)))).reshape(T, ld)[:, :d]
+        ref = mlp.chain_forward(x, chain, lambda e: synth.expert_weights(runtime.DEFAULT_WEIGHT_SEED, e,
+                                                                         shape_of[e][0], shape_of[e][1]))
+        worst = max(worst, mlp.rel_l2(out[r, :, :d], ref))
+    assert checked >= 2
+    assert worst <= TOL, worst

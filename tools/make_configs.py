@@ -126,25 +126,31 @@ def main():
     made["c4"] = (reg, None, shapes, {"alloc_override": {"gpu": 59}},
                   "C3 with zipf 1.0 routing; 12 GB expert budget per GPU; 1/2/4/8 GPUs")
 
-    # C5: heterogeneous 10M-1B params, 5-stage chains, full residency
-    buckets = cfgmod.C5_BUCKETS
+    # C5: heterogeneous 8M-1B params, 5-stage chains, full residency.  A request's activation
+    # width d is constant along its chain (each chain draws d, each expert draws h = {4,8,16}*d,
+    # capped at 61440), so stages hand T x d activations to each other without re-projection.
     rng = random.Random(5)
-    arch_of_expert = {}
+    d_choices, d_weights = (1024, 2048, 4096, 8192), (0.3, 0.3, 0.25, 0.15)
     sizes = [60, 60, 60, 60, 60]
-    for k, size in enumerate(sizes):
-        for i in range(size):
-            params = math.exp(rng.uniform(math.log(1e7), math.log(1e9)))
-            best = min(buckets, key=lambda dh: abs(math.log(2 * dh[0] * dh[1]) - math.log(params)))
-            arch_of_expert[f"s{k}-{i:03d}"] = f"mlp-{best[0]}x{best[1]}"
-    arch_kinds = {f"mlp-{a}x{b}": "classification" for a, b in buckets}
-    shape_of = {f"mlp-{a}x{b}": (a, b, 64) for a, b in buckets}
-    reg, routes = stage_chain_registry(sizes, lambda e: arch_of_expert[e],
-                                       lambda e: cfgmod.expert_bytes(*shape_of[arch_of_expert[e]][:2]),
-                                       seed=55, arch_kinds=arch_kinds)
-    used = {s.arch for s in reg.experts.values()}
-    reg.arch_classes = {a: c for a, c in reg.arch_classes.items() if a in used}
-    made["c5"] = (reg, routes, {a: shape_of[a] for a in sorted(used)}, {"alloc_override": None},
-                  "300 heterogeneous MLP experts (10M-1B params, 8 shape buckets), 5-stage chains, full residency")
+    chain_d = [rng.choices(d_choices, weights=d_weights)[0] for _ in range(sizes[0])]
+    # next pointers are a permutation per stage (stage_chain_registry, seed 55), so derive each
+    # expert's chain from the routes after building, then assign shapes
+    reg, routes = stage_chain_registry(sizes, lambda e: "tmp", lambda e: 1, seed=55,
+                                       arch_kinds={"tmp": "classification"})
+    arch_of_expert, bytes_of = {}, {}
+    for comp, route in sorted(routes.items()):
+        d = chain_d[int(comp[1:])]
+        for eid in route["experts"]:
+            h = min(rng.choice((4, 8, 16)) * d, 61440)
+            arch_of_expert[eid] = f"mlp-{d}x{h}"
+            bytes_of[eid] = cfgmod.expert_bytes(d, h)
+    arch_kinds = {a: "classification" for a in set(arch_of_expert.values())}
+    reg, routes = stage_chain_registry(sizes, lambda e: arch_of_expert[e], lambda e: bytes_of[e], seed=55,
+                                       arch_kinds=arch_kinds)
+    shape_of = {a: (int(a[4:].split("x")[0]), int(a.split("x")[1]), 64) for a in arch_kinds}
+    made["c5"] = (reg, routes, shape_of, {"alloc_override": None},
+                  "300 heterogeneous MLP experts (8M-1B params, 11 shapes, d constant per chain), "
+                  "5-stage chains, full residency")
 
     for name, (reg, routes, shapes, run, desc) in made.items():
         base = os.path.join(OUT, name)
