@@ -197,11 +197,13 @@ def main() -> None:
     cfg = configs.run_config(w, trace=False)
     plan0 = engine.plan(cfg)
     n_req = len(plan0.resolved.request_ids)
+    # each rank pins only the experts its executor touches; COE_SHARED_STORE=1 shares one
+    # host copy per node through /dev/shm instead (needs a /dev/shm as large as the store)
     store_path = None
-    if world > 1:  # one shared pinned expert store per node instead of one per rank
+    if world > 1 and os.environ.get("COE_SHARED_STORE") == "1":
         store_path = f"/dev/shm/coe_store_{args.config}_{os.environ.get('MASTER_PORT', '0')}"
     rt = runtime.B200Runtime.for_plan(plan0, shape, executor=rank, profile=True, store_path=store_path,
-                                      init_experts=(local == 0))
+                                      init_experts=(store_path is None or local == 0))
     if dist is not None:
         dist.barrier()  # local rank 0 has filled the shared store
         rt.attach_comm(rank, world)

@@ -220,6 +220,8 @@ class B200Runtime:
         if isinstance(shape, RuntimeShape):
             largest = max(spec.param_bytes for spec in registry.experts.values())
             slots = max(1, min(int(budget // largest), int(touched.sum()) or 1))
+            if not kw.get("store_path"):  # a shared store must hold every expert at fixed offsets
+                kw.setdefault("store_mask", touched)
             return cls(shape, len(ids), slots, len(resolved.request_ids), adm, **kw)
         arch_shapes = shape
         shapes = sorted({RuntimeShape(*arch_shapes[registry.experts[e].arch]) for e in ids},
@@ -230,8 +232,9 @@ class B200Runtime:
         for i, s in enumerate(shapes):
             n_touched = int(touched[expert_shape == i].sum())
             slots.append(max(1, min(n_touched, int(budget // s.expert_bytes))))
-        return cls(shapes, len(ids), slots, len(resolved.request_ids), adm, expert_shape=expert_shape,
-                   store_mask=touched, **kw)
+        if not kw.get("store_path"):
+            kw.setdefault("store_mask", touched)
+        return cls(shapes, len(ids), slots, len(resolved.request_ids), adm, expert_shape=expert_shape, **kw)
 
     def close(self) -> None:
         if getattr(self, "handle", None):
