@@ -206,6 +206,13 @@ typedef struct coe_comm coe_comm;
 int coe_comm_unique_id(const char *nccl_path, void *out128);
 int coe_comm_create(const char *nccl_path, int rank, int world, const void *id128, coe_comm **out);
 void coe_comm_destroy(coe_comm *c);
+/* In-process transport for several runtimes on one device (one host thread each;
+ * synchronise all runtimes and reset the hub between steps). */
+typedef struct coe_local_hub coe_local_hub;
+coe_local_hub *coe_local_hub_create(int world);
+void coe_local_hub_destroy(coe_local_hub *hub);
+void coe_local_hub_reset(coe_local_hub *hub);
+int coe_comm_create_local(coe_local_hub *hub, int rank, coe_comm **out);
 /* Attach to a runtime (rank == the executor it serves); steps then exchange
  * hopped activations on a dedicated hop stream. */
 int coe_runtime_attach_comm(coe_runtime *rt, coe_comm *comm);

@@ -136,6 +136,7 @@ def run_config(w: Workload, **overrides):
     """A ``RunConfig`` for this workload (planner-ready)."""
     from .engine import RunConfig
 
-    kwargs = dict(w.run)
+    kwargs = dict(registry=w.registry, device=w.device, stream=w.stream, routes=w.routes)
+    kwargs.update(w.run)
     kwargs.update(overrides)
-    return RunConfig(registry=w.registry, device=w.device, stream=w.stream, routes=w.routes, **kwargs)
+    return RunConfig(**kwargs)

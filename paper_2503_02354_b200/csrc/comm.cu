@@ -9,8 +9,13 @@
 // global hop order (hops.h).
 #include <dlfcn.h>
 
+#include <condition_variable>
 #include <cstring>
+#include <deque>
+#include <map>
+#include <mutex>
 #include <string>
+#include <vector>
 
 #include "coe_cuda.h"
 #include "comm.h"
@@ -59,16 +64,71 @@ bool nccl_ok(ncclResult_t r, const char *what) {
 
 }  // namespace
 
+// In-process transport: several runtimes on ONE device (one host thread each), e.g. the
+// reference's multiple logical executors per GPU, and the single-GPU test of the hop
+// protocol.  Point-to-point messages match in order per (src, dst) pair like NCCL's; a
+// send publishes (rows, event-after-producer) and returns, a receive blocks on the host
+// until its match is published, then makes its stream wait and copies device to device.
+// Callers synchronise every runtime between steps (the sender does not wait for the copy).
+struct LocalMsg {
+  const void *buf;
+  size_t bytes;
+  cudaEvent_t ready;
+};
+
+struct coe_local_hub {
+  int world = 1;
+  std::mutex mu;
+  std::condition_variable cv;
+  std::map<std::pair<int, int>, std::deque<LocalMsg>> queues;
+  std::vector<cudaEvent_t> events;  // owned, reused round-robin
+  size_t next_event = 0;
+  ~coe_local_hub() {
+    for (auto e : events) cudaEventDestroy(e);
+  }
+};
+
 struct coe_comm {
   ncclComm_t comm = nullptr;
+  coe_local_hub *hub = nullptr;
   int rank = 0, world = 1;
 };
 
 bool coe_comm_send_bf16(coe_comm *c, const void *buf, size_t count, int peer, cudaStream_t stream) {
+  if (c->hub) {
+    std::lock_guard<std::mutex> lk(c->hub->mu);
+    auto &hub = *c->hub;
+    if (hub.next_event >= hub.events.size()) {
+      cudaEvent_t e;
+      if (!coe_cuda_ok(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "local hub event")) return false;
+      hub.events.push_back(e);
+    }
+    cudaEvent_t ev = hub.events[hub.next_event++];
+    if (!coe_cuda_ok(cudaEventRecord(ev, stream), "local send record")) return false;
+    hub.queues[{c->rank, peer}].push_back(LocalMsg{buf, count * 2, ev});
+    hub.cv.notify_all();
+    return true;
+  }
   return nccl_ok(g_nccl.send(buf, count, ncclBfloat16, peer, c->comm, stream), "ncclSend");
 }
 
 bool coe_comm_recv_bf16(coe_comm *c, void *buf, size_t count, int peer, cudaStream_t stream) {
+  if (c->hub) {
+    LocalMsg m;
+    {
+      std::unique_lock<std::mutex> lk(c->hub->mu);
+      auto &q = c->hub->queues[{peer, c->rank}];
+      c->hub->cv.wait(lk, [&] { return !q.empty(); });
+      m = q.front();
+      q.pop_front();
+    }
+    if (m.bytes != count * 2) {
+      coe_set_error("local hop: message size mismatch");
+      return false;
+    }
+    return coe_cuda_ok(cudaStreamWaitEvent(stream, m.ready, 0), "local recv wait") &&
+           coe_cuda_ok(cudaMemcpyAsync(buf, m.buf, m.bytes, cudaMemcpyDeviceToDevice, stream), "local recv copy");
+  }
   return nccl_ok(g_nccl.recv(buf, count, ncclBfloat16, peer, c->comm, stream), "ncclRecv");
 }
 
@@ -103,6 +163,29 @@ void coe_comm_destroy(coe_comm *c) {
   if (!c) return;
   if (c->comm && g_nccl.comm_destroy) g_nccl.comm_destroy(c->comm);
   delete c;
+}
+
+coe_local_hub *coe_local_hub_create(int world) {
+  auto *h = new coe_local_hub();
+  h->world = world;
+  return h;
+}
+
+void coe_local_hub_destroy(coe_local_hub *h) { delete h; }
+
+void coe_local_hub_reset(coe_local_hub *h) {
+  std::lock_guard<std::mutex> lk(h->mu);
+  h->queues.clear();
+  h->next_event = 0;
+}
+
+int coe_comm_create_local(coe_local_hub *hub, int rank, coe_comm **out) {
+  auto *c = new coe_comm();
+  c->hub = hub;
+  c->rank = rank;
+  c->world = hub->world;
+  *out = c;
+  return COE_CUDA_OK;
 }
 
 }  // extern "C"

@@ -99,6 +99,14 @@ def _lib():
         lib.coe_comm_create.restype = ctypes.c_int
         lib.coe_comm_destroy.argtypes = [V]
         lib.coe_comm_destroy.restype = None
+        lib.coe_local_hub_create.argtypes = [ctypes.c_int]
+        lib.coe_local_hub_create.restype = V
+        lib.coe_local_hub_destroy.argtypes = [V]
+        lib.coe_local_hub_destroy.restype = None
+        lib.coe_local_hub_reset.argtypes = [V]
+        lib.coe_local_hub_reset.restype = None
+        lib.coe_comm_create_local.argtypes = [V, ctypes.c_int, P(V)]
+        lib.coe_comm_create_local.restype = ctypes.c_int
         lib.coe_runtime_set_knobs.argtypes = [V, I64, I64, I32]
         lib.coe_runtime_set_knobs.restype = ctypes.c_int
         lib.coe_runtime_attach_comm.argtypes = [V, V]
@@ -244,6 +252,12 @@ class B200Runtime:
             self.lib.coe_comm_destroy(self.comm)
             self.comm = None
 
+    def attach_local(self, hub: "LocalHub", rank: int) -> None:
+        """Join an in-process hop transport (several executors sharing one GPU)."""
+        self.comm = ctypes.c_void_p()
+        _check(self.lib, self.lib.coe_comm_create_local(hub.handle, rank, ctypes.byref(self.comm)), "local comm")
+        _check(self.lib, self.lib.coe_runtime_attach_comm(self.handle, self.comm), "attach comm")
+
     def attach_comm(self, rank: int, world: int) -> None:
         """Create the NCCL hop communicator (one executor per rank) and attach it.
 
@@ -348,6 +362,50 @@ class B200Runtime:
         t = StepTiming()
         _check(self.lib, self.lib.coe_runtime_timing(self.handle, ctypes.byref(t)), "timing")
         return t.as_dict()
+
+
+class LocalHub:
+    """In-process hop transport for several runtimes on one device (coe_local_hub)."""
+
+    def __init__(self, world: int):
+        self.lib = _lib()
+        self.handle = self.lib.coe_local_hub_create(world)
+
+    def reset(self) -> None:
+        self.lib.coe_local_hub_reset(self.handle)
+
+    def __del__(self):
+        try:
+            self.lib.coe_local_hub_destroy(self.handle)
+        except Exception:
+            pass
+
+
+def step_executors(plan, runtimes: list, hub: "LocalHub | None" = None) -> list:
+    """Step every executor's runtime concurrently (one host thread each), then synchronise."""
+    import threading
+
+    results = [None] * len(runtimes)
+    errors = []
+
+    def work(x):
+        try:
+            results[x] = runtimes[x].step(plan, x)
+        except Exception as exc:  # surfaced after join
+            errors.append(exc)
+
+    threads = [threading.Thread(target=work, args=(x,)) for x in range(len(runtimes))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    for rt in runtimes:
+        rt.synchronize()
+    if hub is not None:
+        hub.reset()
+    if errors:
+        raise errors[0]
+    return results
 
 
 def nccl_library() -> str:

@@ -69,9 +69,11 @@ def _check_against_oracle_batches(workload, plan):
     out = des.simulate(docs["registry"], docs["device"], docs["stream"], routes=docs["routes"], trace=False, **run)
     ids = plan.resolved.expert_ids
     rid = plan.resolved.request_ids
-    ours = [(ids[e], [(rid[r], s) for r, s in members]) for e, members in runtime.batches_from_plan(plan)]
-    theirs = [(e, list(m)) for _x, e, m in out["batches"]]
-    assert ours == theirs
+    for x in range(len(plan.resolved.executors)):
+        ours = [(ids[e], [(rid[r], s) for r, s in members])
+                for e, members in runtime.batches_from_plan(plan, executor=x)]
+        theirs = [(e, list(m)) for xx, e, m in out["batches"] if xx == x]
+        assert ours == theirs, f"executor {x}"
     return out
 
 
@@ -193,4 +195,66 @@ def test_c5_heterogeneous_expert_shapes():
                                                                          shape_of[e][0], shape_of[e][1]))
         worst = max(worst, mlp.rel_l2(out[r, :, :d], ref))
     assert checked >= 2
+    assert worst <= TOL, worst
+
+
+@pytest.mark.parametrize("executors", [2, 3])
+def test_multi_executor_hops_on_one_gpu(executors):
+    """Config 4 (Zipf routing) with several executors, each its own runtime on the one GPU,
+    follow-up hops exchanged through the in-process transport in the global hop order
+    (the protocol the NCCL path uses across GPUs).  Grouping is exact per executor and
+    every request's final output, wherever it ran, matches the numpy fp32 chain."""
+    import torch
+
+    w = _trim(configs.load("c4", 1000, gpu_executors=executors), 240)
+    plan = engine.plan(configs.run_config(w, trace=False))
+    _check_against_oracle_batches(w, plan)
+    assert len(runtime.hops_from_plan(plan)) > 0
+    shape = runtime.RuntimeShape(1024, 2048, 64)
+    hub = runtime.LocalHub(executors)
+    rts = []
+    for x in range(executors):
+        rt = runtime.B200Runtime.for_plan(plan, shape, executor=x)
+        rt.attach_local(hub, x)
+        rt.fill_inputs(len(plan.resolved.request_ids))
+        rts.append(rt)
+    n = len(plan.resolved.request_ids)
+    chains = plan.resolved.chains
+    final_exec = {}
+    for x in range(executors):
+        for _e, members in runtime.batches_from_plan(plan, executor=x):
+            for r, s in members:
+                if s == len(chains[r]) - 1:
+                    final_exec[r] = x
+    outs = []
+    for _step in range(2):
+        stats = runtime.step_executors(plan, rts, hub)
+        per_exec = []
+        for x, rt in enumerate(rts):
+            _, violations = rt.check()
+            assert violations == 0
+            req, stage, boff = rt.members(stats[x]["admissions"], stats[x]["batches"])
+            for b, (_e, members) in enumerate(runtime.batches_from_plan(plan, executor=x)):
+                got = list(zip(req[boff[b]:boff[b] + len(members)].tolist(),
+                               stage[boff[b]:boff[b] + len(members)].tolist()))
+                assert got == members
+            host = torch.empty(n * shape.T * shape.d, dtype=torch.bfloat16).pin_memory()
+            rt.download_outputs(runtime.last_stages(plan), host.data_ptr())
+            rt.synchronize()
+            per_exec.append(host.view(n, shape.T, shape.d).float().numpy().copy())
+        outs.append(np.stack([per_exec[final_exec[r]][r] for r in range(n)]))
+    assert np.array_equal(outs[0], outs[1])
+    cache = {}
+
+    def weights(e):
+        if e not in cache:
+            cache[e] = synth.expert_weights(runtime.DEFAULT_WEIGHT_SEED, e, shape.d, shape.h)
+        return cache[e]
+
+    hopped = {h[3] for h in runtime.hops_from_plan(plan)}
+    picks = sorted(hopped)[:8] + [r for r in range(0, n, 37)]
+    worst = 0.0
+    for r in picks:
+        x = synth.request_inputs(runtime.DEFAULT_INPUT_SEED, r, shape.T, shape.d)
+        worst = max(worst, mlp.rel_l2(outs[0][r], mlp.chain_forward(x, chains[r], weights)))
     assert worst <= TOL, worst
