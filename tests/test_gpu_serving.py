@@ -258,3 +258,16 @@ def test_multi_executor_hops_on_one_gpu(executors):
         x = synth.request_inputs(runtime.DEFAULT_INPUT_SEED, r, shape.T, shape.d)
         worst = max(worst, mlp.rel_l2(outs[0][r], mlp.chain_forward(x, chains[r], weights)))
     assert worst <= TOL, worst
+
+
+def test_window_search_with_measured_b200_throughput():
+    """The allocation search (profiler.py:281-419) driven by real serving probes on the GPU."""
+    from paper_2503_02354_b200 import profiler
+
+    w = configs.load("c3", 1000)
+    cfg = configs.run_config(w, trace=False)
+    res = profiler.search_memory_allocation_measured(cfg, runtime.RuntimeShape(1024, 2048, 64), sample_requests=120,
+                                                     steps=1, choose="midpoint")
+    assert res.throughput_samples and all(t > 0 for _, t in res.throughput_samples)
+    counts = [c for c, _ in res.throughput_samples]
+    assert counts == sorted(counts) and res.lower <= res.chosen <= res.upper
