@@ -318,9 +318,14 @@ def main() -> None:
         return
     peaks, peak_src = load_peaks()
     flops = algorithmic_flops(plan_last, shape, rank)
-    achieved = wave_flops / ((up_ms + down_ms) / 1e3) / 1e12
-    peak = float(peaks.get("bf16_tflops"))
-    sustained = float(peaks.get("bf16_tflops_sustained", peak))
+    assert abs(flops - timing["k3_flops"]) <= 1e-6 * max(flops, 1.0), (flops, timing["k3_flops"])
+    burst = float(peaks.get("bf16_tflops"))
+    sustained = float(peaks.get("bf16_tflops_sustained", burst))
+    isolated = wave_flops / ((up_ms + down_ms) / 1e3) / 1e12
+    # headline: K3 inside the timed serving step -- the step's algorithmic FLOPs over the union of
+    # its K3 launch intervals (CUDA events on the launching streams), against the sustained peak
+    achieved = flops / (timing["k3_busy_ms"] / 1e3) / 1e12 if timing["k3_busy_ms"] > 0 else None
+    peak = sustained
     traffic = None
     ncu_path = os.path.join(ROOT, "profiles", "k3_ncu_summary.json")
     if os.path.exists(ncu_path):
@@ -346,19 +351,23 @@ def main() -> None:
         "gb_moved_per_1k_requests": 1000.0 * ps["bytes_moved"] / 1e9 / n_req,
         "planner": {"makespan_virtual_s": metrics.makespan_s, "switches": metrics.expert_switches,
                     "evictions": metrics.evictions, "batches": ps["batches"]},
-        "roofline": {"bound": "tensor", "kernel": "grouped_gemm_kernel (K3, tcgen05; up + down launch)",
-                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
-                     "peak_source": f"{peak_src} bf16_tflops (burst: kernel timed alone, CUDA events)",
+        "roofline": {"bound": "tensor", "kernel": "grouped_gemm_kernel (K3, tcgen05; up + down launch per wave)",
+                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak if (peak and achieved) else None,
+                     "peak_source": f"{peak_src} bf16_tflops_sustained (K3 timed inside the serving step)",
                      "traffic": traffic,
-                     "wave": {"batches": groups, "requests_per_batch": max_batch,
-                              "rows": groups * max_batch * k3_shape.T,
-                              "shape": {"d": k3_shape.d, "h": k3_shape.h, "T": k3_shape.T},
-                              "up_ms": up_ms, "down_ms": down_ms, "flops": wave_flops},
-                     "in_step": {"algorithmic_flops": flops, "compute_busy_ms": timing["compute_busy_ms"],
-                                 "tflops": flops / (timing["compute_busy_ms"] / 1e3) / 1e12
-                                 if timing["compute_busy_ms"] > 0 else None,
-                                 "frac_of_sustained": flops / (timing["compute_busy_ms"] / 1e3) / 1e12 / sustained
-                                 if timing["compute_busy_ms"] > 0 else None}},
+                     "measured_over": {"k3_launches_per_step": timing["k3_launches"],
+                                       "algorithmic_flops_per_step": flops,
+                                       "flops_per_launch": flops / max(1, timing["k3_launches"]),
+                                       "k3_busy_ms_per_step": timing["k3_busy_ms"],
+                                       "avg_launch_ms": timing["k3_busy_ms"] / max(1, timing["k3_launches"]),
+                                       "wave_busy_ms_incl_w2_waits": timing["compute_busy_ms"]},
+                     "isolated_wave": {"batches": groups, "requests_per_batch": max_batch,
+                                       "rows": groups * max_batch * k3_shape.T,
+                                       "shape": {"d": k3_shape.d, "h": k3_shape.h, "T": k3_shape.T},
+                                       "up_ms": up_ms, "down_ms": down_ms, "flops": wave_flops,
+                                       "tflops": isolated, "peak": burst, "frac": isolated / burst,
+                                       "peak_source": f"{peak_src} bf16_tflops (burst: kernel timed alone)"}},
         "swap_in": {"bound": "pcie_h2d", "bytes_per_step": load_bytes, "loads": stats["loads"],
                     "restores": stats["restores"],
                     "achieved_gbs": load_bytes / copy_s / 1e9 if copy_s > 0 else None, "peak_gbs": PCIE_H2D_GBS,

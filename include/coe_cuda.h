@@ -162,6 +162,10 @@ typedef struct coe_step_timing {
   float overlap_ms;         /* intersection of the two                               */
   float mlp_ms;             /* sum of K3 wave durations                              */
   float group_ms;           /* K1 + K2                                                */
+  float k3_busy_ms;         /* union of K3 launch intervals (up and down passes; waits
+                               for a swap-in's W2 half between them excluded)          */
+  int32_t k3_launches;      /* K3 launches in the step (2 per wave)                   */
+  double k3_flops;          /* algorithmic 4*rows*d*h over the step's waves          */
 } coe_step_timing;
 
 typedef struct coe_runtime coe_runtime;
@@ -189,6 +193,9 @@ int coe_runtime_counts(coe_runtime *rt, int32_t *copies, int32_t *waves);
 int coe_runtime_bench_mlp(coe_runtime *rt, int32_t groups, int32_t requests_per_group, int32_t iters,
                           float *up_ms, float *down_ms);
 int coe_runtime_intervals(coe_runtime *rt, float *copy_iv, float *wave_iv, int32_t *wave_info);
+/* profile mode: per wave [up start, up end, down start, down end] ms since step start and
+ * the wave's algorithmic FLOPs (4 * rows * d * h) */
+int coe_runtime_wave_phases(coe_runtime *rt, float *phase_iv, double *wave_flops);
 /* device pointers (tests / benches): 0 X, 1 P0, 2 P1, 3 H scratch, 4 slot slab */
 void *coe_runtime_buffer(coe_runtime *rt, int which);
 /* synchronous device -> host copy of the first `bytes` of buffer `which` */

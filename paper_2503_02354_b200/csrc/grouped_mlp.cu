@@ -27,6 +27,7 @@
 #include <cuda_bf16.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -66,7 +67,10 @@ struct GemmArgs {
   __nv_bfloat16 *out_h;
   __nv_bfloat16 *out_act0;
   __nv_bfloat16 *out_act1;
+  int32_t *tile_counter;  // [next tile, CTAs done]: dynamic tile scheduler, self-resetting
 };
+
+constexpr int TILE_RING = 4;  // tile indices handed from the producer to the MMA / epilogue warps
 
 // A-operand source of a member at chain stage s: 0 = X, 1 = P0, 2 = P1.
 __device__ __forceinline__ int a_source(int stage) { return stage == 0 ? 0 : 1 + ((stage - 1) & 1); }
@@ -116,7 +120,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t *empty_bar = full_bar + STAGES;
   uint64_t *tfull_bar = empty_bar + STAGES;
   uint64_t *tempty_bar = tfull_bar + 2;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty_bar + 2);
+  uint64_t *ring_full = tempty_bar + 2;
+  uint64_t *ring_empty = ring_full + TILE_RING;
+  int32_t *ring_tile = reinterpret_cast<int32_t *>(ring_empty + TILE_RING);
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(ring_tile + TILE_RING);
   int32_t *tile_start = reinterpret_cast<int32_t *>(smem + STAGES * STAGE_BYTES + 256);
 
   const uint32_t warp = sm100::warp_id();
@@ -136,6 +143,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       sm100::mbar_init(&tfull_bar[s], 1);
       sm100::mbar_init(&tempty_bar[s], 128);
     }
+    for (int s = 0; s < TILE_RING; ++s) {
+      sm100::mbar_init(&ring_full[s], 1);
+      sm100::mbar_init(&ring_empty[s], 1 + 4);  // the MMA thread + one lane per epilogue warp
+    }
     sm100::fence_mbar_init();
   }
   if (warp == 2) sm100::tmem_alloc<TMEM_COLS>(tmem_slot);
@@ -150,7 +161,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       // ===== TMA producer =====
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < args.total_tiles; t += gridDim.x) {
+      // dynamic scheduler: tiles are claimed in (group, n-block, m-block) order, so CTAs
+      // running at the same time share weight tiles through L2, and a CTA that starts late
+      // (SMs held by another stream's kernel) simply claims fewer tiles.  The next claim is
+      // issued before the current tile's loads so its latency hides behind them.
+      // (tile_counter == nullptr: static round-robin, tile = blockIdx.x + i * gridDim.x)
+      const bool dyn = args.tile_counter != nullptr;
+      int claim = dyn ? atomicAdd(&args.tile_counter[0], 1) : (int)blockIdx.x;
+      for (int i = 0;; ++i) {
+        const int t = claim < args.total_tiles ? claim : -1;
+        sm100::mbar_wait(&ring_empty[i % TILE_RING], ((i / TILE_RING) & 1) ^ 1);
+        ring_tile[i % TILE_RING] = t;
+        sm100::mbar_arrive(&ring_full[i % TILE_RING]);
+        if (t < 0) break;
+        claim = dyn ? atomicAdd(&args.tile_counter[0], 1) : claim + (int)gridDim.x;
         TileCoord c = decode_tile(t, tile_start, args.num_groups, args.groups, args.n_blocks);
         const coe_mlp_group grp = args.groups[c.g];
         int box_row[BM / 32];
@@ -201,7 +225,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = blockIdx.x; t < args.total_tiles; t += gridDim.x) {
+      for (int i = 0;; ++i) {
+        sm100::mbar_wait(&ring_full[i % TILE_RING], (i / TILE_RING) & 1);
+        const int t = ring_tile[i % TILE_RING];
+        sm100::mbar_arrive(&ring_empty[i % TILE_RING]);
+        if (t < 0) break;
         sm100::mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         sm100::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -234,7 +262,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const uint32_t quarter = warp & 3;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < args.total_tiles; t += gridDim.x) {
+    for (int i = 0;; ++i) {
+      sm100::mbar_wait(&ring_full[i % TILE_RING], (i / TILE_RING) & 1);
+      const int t = ring_tile[i % TILE_RING];
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(&ring_empty[i % TILE_RING]);
+      if (t < 0) break;
       TileCoord c = decode_tile(t, tile_start, args.num_groups, args.groups, args.n_blocks);
       const coe_mlp_group grp = args.groups[c.g];
       const int row = c.m_blk * BM + quarter * 32 + lane;
@@ -294,6 +327,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     sm100::tc_fence_after();
     sm100::tmem_dealloc<TMEM_COLS>(tmem_base);
   }
+  if (threadIdx.x == 0 && args.tile_counter) {
+    // every claim of this CTA precedes its arrival here; the last CTA out re-arms the
+    // counter for the next launch on this stream (launches on a stream are ordered)
+    if (atomicAdd(&args.tile_counter[1], 1) == (int)gridDim.x - 1) {
+      args.tile_counter[0] = 0;
+      args.tile_counter[1] = 0;
+      __threadfence();
+    }
+  }
 }
 
 // ---- host side ---------------------------------------------------------------
@@ -348,6 +390,9 @@ struct coe_mlp {
   CUtensorMap xmap, act0, act1, hmap, w1, w2;
   int num_sms;
   int a_box_rows;
+  int32_t *tile_counter = nullptr;  // device [2]; one per instance = one per stream
+  bool dynamic = false;             // COE_K3_DYNAMIC=1: atomic tile claims instead of the static
+                                    // round-robin (measured 3 % slower on full-GPU waves, r1)
 };
 
 extern "C" {
@@ -367,6 +412,7 @@ int coe_mlp_create(const coe_mlp_config *cfg, coe_mlp **out) {
   }
   auto *m = new coe_mlp();
   m->cfg = *cfg;
+  m->dynamic = getenv("COE_K3_DYNAMIC") && atoi(getenv("COE_K3_DYNAMIC")) != 0;
   m->a_box_rows = cfg->T < BM ? cfg->T : BM;
   bool ok = true;
   const uint64_t ld = cfg->act_ld > 0 ? (uint64_t)cfg->act_ld : (uint64_t)cfg->d;
@@ -387,7 +433,10 @@ int coe_mlp_create(const coe_mlp_config *cfg, coe_mlp **out) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&m->num_sms, cudaDevAttrMultiProcessorCount, dev);
   cudaError_t e = cudaFuncSetAttribute(grouped_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  if (e == cudaSuccess) e = cudaMalloc(&m->tile_counter, 2 * sizeof(int32_t));
+  if (e == cudaSuccess) e = cudaMemset(m->tile_counter, 0, 2 * sizeof(int32_t));
   if (e != cudaSuccess) {
+    if (m->tile_counter) cudaFree(m->tile_counter);
     delete m;
     coe_set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
     return COE_CUDA_ERR_CUDA;
@@ -396,7 +445,11 @@ int coe_mlp_create(const coe_mlp_config *cfg, coe_mlp **out) {
   return COE_CUDA_OK;
 }
 
-void coe_mlp_destroy(coe_mlp *m) { delete m; }
+void coe_mlp_destroy(coe_mlp *m) {
+  if (!m) return;
+  if (m->tile_counter) cudaFree(m->tile_counter);
+  delete m;
+}
 
 int coe_mlp_max_groups(void) { return MAX_GROUPS; }
 
@@ -428,6 +481,7 @@ int coe_grouped_mlp(coe_mlp *m, const coe_mlp_group *groups_up, const coe_mlp_gr
     a.out_h = reinterpret_cast<__nv_bfloat16 *>(c.h_scratch);
     a.out_act0 = reinterpret_cast<__nv_bfloat16 *>(c.act0);
     a.out_act1 = reinterpret_cast<__nv_bfloat16 *>(c.act1);
+    a.tile_counter = m->dynamic ? m->tile_counter : nullptr;
     if (a.total_tiles <= 0) continue;
     int cap = (max_ctas > 0 && max_ctas < m->num_sms) ? max_ctas : m->num_sms;
     int grid = a.total_tiles < cap ? a.total_tiles : cap;

@@ -36,6 +36,7 @@
 #include <array>
 #include <cstring>
 #include <climits>
+#include <cstdlib>
 #include <string>
 #include <unordered_map>
 #include <unordered_set>
@@ -98,6 +99,14 @@ struct Action {
 };
 
 bool ok(cudaError_t e, const char *what) { return coe_cuda_ok(e, what); }
+
+// Release-wave grid: the reserved SMs (static K3 tiles); with COE_K3_DYNAMIC=1 the whole GPU,
+// its CTAs claiming tiles as the main stream's kernels hand SMs back.  COE_RELEASE_CTAS overrides.
+int release_grid(int reserved, int sms) {
+  if (const char *v = getenv("COE_RELEASE_CTAS")) return std::max(1, atoi(v));
+  const bool dyn = getenv("COE_K3_DYNAMIC") && atoi(getenv("COE_K3_DYNAMIC")) != 0;
+  return dyn ? sms : reserved;
+}
 
 // Many row copies as one cudaMemcpyBatchAsync (CUDA 12.8+): the e2e path moves one
 // T x d row block per request, and per-call launch cost would dominate small rows.
@@ -177,7 +186,8 @@ struct coe_runtime {
   std::vector<uint8_t> slot_free_valid;
   // events
   std::vector<cudaEvent_t> wave_up_ev, wave_down_ev, copy_up_ev, copy_down_ev;
-  std::vector<cudaEvent_t> t_copy_start, t_copy_end, t_wave_start, t_wave_end;
+  std::vector<cudaEvent_t> t_copy_start, t_copy_end, t_wave_start, t_wave_end, t_up_end, t_down_start;
+  std::vector<double> last_wave_flops;  // algorithmic 4*rows*d*h per wave
   cudaEvent_t staged = nullptr, copy_drained = nullptr, grouped = nullptr;
   cudaEvent_t cls_drained[NCLS] = {nullptr, nullptr, nullptr};
   cudaEvent_t t_step_start = nullptr, t_group_end = nullptr, t_step_end = nullptr;
@@ -195,6 +205,7 @@ struct coe_runtime {
   cudaEvent_t hop_drained = nullptr, step_end = nullptr;
   bool have_step_end = false;
   int m_ctas = 148, r_ctas = 16;  // SM split: main waves vs the swap-in-gating waves
+  int rel_launch_ctas = 148;      // grid of a release wave (all SMs; see phase C)
 
   ~coe_runtime() {
     for (auto st : cls_stream)
@@ -226,7 +237,7 @@ struct coe_runtime {
       cudaFreeHost(host_store);
     }
     for (auto *v : {&in_ev, &recv_ev, &slot_free_up, &slot_free_down, &wave_up_ev, &wave_down_ev, &copy_up_ev, &copy_down_ev,
-                    &t_copy_start, &t_copy_end, &t_wave_start, &t_wave_end}) {
+                    &t_copy_start, &t_copy_end, &t_wave_start, &t_wave_end, &t_up_end, &t_down_start}) {
       for (auto e : *v) cudaEventDestroy(e);
       v->clear();
     }
@@ -461,6 +472,7 @@ int coe_runtime_create(const coe_runtime_config *cfg, coe_runtime **out) {
     const int reserve = c.reserve_sms > 0 ? std::min(c.reserve_sms, sms / 2) : 0;
     rt->m_ctas = sms - reserve;
     rt->r_ctas = reserve > 0 ? reserve : sms;
+    rt->rel_launch_ctas = release_grid(rt->r_ctas, sms);
   }
   rt->slot_expert.assign(rt->total_slots, -1);
   rt->expert_slot.assign(c.num_experts, -1);
@@ -606,15 +618,22 @@ int coe_runtime_timing(coe_runtime *rt, coe_step_timing *out) {
   std::vector<std::pair<float, float>> cp, wv;
   for (int i = 0; i < rt->last_copies; ++i)
     cp.emplace_back(elapsed(rt->t_step_start, rt->t_copy_start[i]), elapsed(rt->t_step_start, rt->t_copy_end[i]));
+  std::vector<std::pair<float, float>> k3;  // K3 launches only (up, down), W2 waits excluded
   wv.emplace_back(0.f, out->group_ms);
   for (int i = 0; i < rt->last_waves; ++i) {
     float s = elapsed(rt->t_step_start, rt->t_wave_start[i]), e = elapsed(rt->t_step_start, rt->t_wave_end[i]);
+    float ue = elapsed(rt->t_step_start, rt->t_up_end[i]), ds = elapsed(rt->t_step_start, rt->t_down_start[i]);
     wv.emplace_back(s, e);
+    k3.emplace_back(s, ue);
+    k3.emplace_back(ds, e);
     out->mlp_ms += e - s;
+    out->k3_flops += rt->last_wave_flops[i];
   }
   out->copy_busy_ms = union_len(cp);
   out->compute_busy_ms = union_len(wv);
   out->overlap_ms = intersect_len(cp, wv);
+  out->k3_busy_ms = union_len(k3);
+  out->k3_launches = 2 * rt->last_waves;
   return COE_CUDA_OK;
 }
 
@@ -629,6 +648,7 @@ int coe_runtime_set_knobs(coe_runtime *rt, int64_t wave_rows_cap, int64_t urgent
     rt->cfg.reserve_sms = reserve;
     rt->m_ctas = sms - reserve;
     rt->r_ctas = reserve > 0 ? reserve : sms;
+    rt->rel_launch_ctas = release_grid(rt->r_ctas, sms);
   }
   return COE_CUDA_OK;
 }
@@ -712,6 +732,21 @@ int coe_runtime_intervals(coe_runtime *rt, float *copy_iv, float *wave_iv, int32
     wave_info[3 * i] = rt->last_wave_cls[i];
     wave_info[3 * i + 1] = rt->last_wave_rows[i];
     wave_info[3 * i + 2] = rt->last_wave_groups[i];
+  }
+  return COE_CUDA_OK;
+}
+
+int coe_runtime_wave_phases(coe_runtime *rt, float *phase_iv, double *wave_flops) {
+  if (!rt->cfg.profile) {
+    coe_set_error("runtime created without profile events");
+    return COE_CUDA_ERR_CONFIG;
+  }
+  for (int i = 0; i < rt->last_waves; ++i) {
+    phase_iv[4 * i] = elapsed(rt->t_step_start, rt->t_wave_start[i]);
+    phase_iv[4 * i + 1] = elapsed(rt->t_step_start, rt->t_up_end[i]);
+    phase_iv[4 * i + 2] = elapsed(rt->t_step_start, rt->t_down_start[i]);
+    phase_iv[4 * i + 3] = elapsed(rt->t_step_start, rt->t_wave_end[i]);
+    wave_flops[i] = rt->last_wave_flops[i];
   }
   return COE_CUDA_OK;
 }
@@ -1063,13 +1098,30 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
                                                     : c.max_wave_rows;
   const int64_t urgent_rows_cap = c.urgent_rows_cap > 0 ? c.urgent_rows_cap : wave_rows_cap;
   const int urgent_horizon = 2;
+  // Swap-ins may leave op order within a small window: a copy whose victim slot is still
+  // being read (e.g. the expert the previous copy brought in, evicted right after its
+  // batches) must not idle the copy engine while a later copy's slot is already free.  The
+  // planner's decisions are unaffected -- only the physical order of slot writes changes;
+  // two copies into the same slot keep their order.
+  const size_t kCopyWindow = 8;
+  size_t copy_pick = 0;
   while (next_copy < copies.size() || next_rel < rel_order.size() || !main_pending.empty()) {
     const double INF = 1e30;
-    // candidate: next swap-in
+    while (next_copy < copies.size() && copies[next_copy].issued) ++next_copy;
+    // candidate: the earliest-startable swap-in in the window
     double c_start = INF;
-    if (next_copy < copies.size() && copy_ready(copies[next_copy])) {
-      c_start = t_copy;
-      for (int32_t r : copies[next_copy].readers) c_start = std::max(c_start, batches[r].done);
+    for (size_t k = next_copy, seen = 0; k < copies.size() && seen < kCopyWindow; ++k) {
+      if (copies[k].issued) continue;
+      ++seen;
+      bool waw = false;
+      for (size_t m = next_copy; m < k && !waw; ++m) waw = !copies[m].issued && copies[m].slot == copies[k].slot;
+      if (waw || !copy_ready(copies[k])) continue;
+      double t = t_copy;
+      for (int32_t r : copies[k].readers) t = std::max(t, batches[r].done);
+      if (t < c_start) {
+        c_start = t;
+        copy_pick = k;
+      }
     }
     // candidate: next release wave (singleton, in order)
     double r_start = INF;
@@ -1087,14 +1139,13 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
       return COE_CUDA_ERR_CHECK;
     }
     if (c_start <= r_start && c_start <= m_start) {
-      CopyInfo &ci = copies[next_copy];
+      CopyInfo &ci = copies[copy_pick];
       ci.issued = true;
       ci.up_end = c_start + copy_half_s(ci.expert);
       ci.end = c_start + 2 * copy_half_s(ci.expert);
       t_copy = ci.end;
-      copy_action[next_copy] = (int32_t)actions.size();
-      actions.push_back(Action{true, (int32_t)next_copy});
-      ++next_copy;
+      copy_action[copy_pick] = (int32_t)actions.size();
+      actions.push_back(Action{true, (int32_t)copy_pick});
     } else if (r_start <= m_start) {
       emit_wave({rel_order[next_rel]}, 1, r_start);
       ++next_rel;
@@ -1118,14 +1169,22 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
         const int32_t nb = needed_by_copy[main_pending[i]];
         if (!(nb >= 0 && nb <= (int32_t)next_copy + urgent_horizon)) order.push_back(i);
       }
-      const int64_t cap = urgent_present ? urgent_rows_cap : wave_rows_cap;
+      // urgent batches (readers of slots the next swap-ins overwrite) fill a wave up to the
+      // full cap -- one big wave lets the swap-in's W1 half wait for a single up pass instead
+      // of an up/down chain; unrelated work only rides along up to urgent_rows_cap
       for (size_t oi = 0; oi < order.size() && (int)members.size() < max_groups; ++oi) {
         const size_t i = order[oi];
         const int32_t bi = main_pending[i];
         const BatchInfo &b = batches[bi];
         if (!issuable(b) || ready_time(b) > m_start + kSlack) continue;
         if (!members.empty() && rt->slot_shape[b.slot] != rt->slot_shape[batches[members[0]].slot]) continue;
-        if (!members.empty() && rows + b.rows > cap) break;
+        const int32_t nb = needed_by_copy[bi];
+        const bool urgent = nb >= 0 && nb <= (int32_t)next_copy + urgent_horizon;
+        const int64_t cap = (urgent || !urgent_present) ? wave_rows_cap : urgent_rows_cap;
+        if (!members.empty() && rows + b.rows > cap) {
+          if (urgent) continue;  // a smaller urgent batch may still fit
+          break;
+        }
         bool clash = false;
         for (int32_t j = 0; j < b.count && !clash; ++j)
           clash = reqs.count(in->op_args[ops[b.op_index].offset + 2 * j]) > 0;
@@ -1169,8 +1228,8 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
         written[ci.slot] = 1;
       } else {
         const WaveAct &w = waves[a.index];
-        for (int32_t gi = w.first_group; gi < w.first_group + w.num_groups; ++gi)
-          last_reader_wave[g_up[gi].slot * NCLS + w.cls] = a.index;
+        for (int32_t gi = w.first_group; gi < w.first_group + w.num_groups; ++gi)  // global slot index
+          last_reader_wave[batches[g_up[gi].batch].slot * NCLS + w.cls] = a.index;
       }
     }
     for (int32_t s = 0; s < NS; ++s)
@@ -1180,6 +1239,36 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
   st.admissions = n_adm;
   st.batches = n_batches;
   st.waves = (int64_t)waves.size();
+  if (const char *dump = getenv("COE_SCHED_DUMP")) {  // debug: the issue order and its dependencies
+    if (FILE *f = fopen(dump, "w")) {
+      fprintf(f, "{\"actions\": [");
+      for (size_t i = 0; i < actions.size(); ++i)
+        fprintf(f, "%s[%d, %d]", i ? ", " : "", actions[i].is_copy ? 1 : 0, actions[i].index);
+      fprintf(f, "], \"copies\": [");
+      for (size_t i = 0; i < copy_acts.size(); ++i) {
+        fprintf(f, "%s{\"expert\": %d, \"slot\": %d, \"est_start\": %.6f, \"wait_waves\": [", i ? ", " : "",
+                copy_acts[i].expert, copy_acts[i].slot, copies[i].end - 2 * copy_half_s(copies[i].expert));
+        for (size_t j = 0; j < copy_acts[i].wait_waves.size(); ++j)
+          fprintf(f, "%s%d", j ? ", " : "", copy_acts[i].wait_waves[j]);
+        fprintf(f, "]}");
+      }
+      fprintf(f, "], \"waves\": [");
+      for (size_t i = 0; i < waves.size(); ++i) {
+        const WaveAct &w = waves[i];
+        fprintf(f, "%s{\"cls\": %d, \"rows\": %lld, \"est_end\": %.6f, \"wait_copies\": [", i ? ", " : "", w.cls,
+                (long long)w.rows, batches[g_up[w.first_group].batch].done);
+        for (size_t j = 0; j < w.wait_copies.size(); ++j) fprintf(f, "%s%d", j ? ", " : "", w.wait_copies[j]);
+        fprintf(f, "], \"wait_waves\": [");
+        for (size_t j = 0; j < w.wait_waves.size(); ++j) fprintf(f, "%s%d", j ? ", " : "", w.wait_waves[j]);
+        fprintf(f, "], \"batches\": [");
+        for (int32_t gi = w.first_group; gi < w.first_group + w.num_groups; ++gi)
+          fprintf(f, "%s%d", gi > w.first_group ? ", " : "", g_up[gi].batch);
+        fprintf(f, "]}");
+      }
+      fprintf(f, "]}\n");
+      fclose(f);
+    }
+  }
 
   // ---- phase C: issue ----
   const size_t nw = waves.size(), nc = copies.size();
@@ -1188,6 +1277,7 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
       !rt->ensure_events(rt->recv_ev, my_hops.size(), false))
     return fail_cuda();
   if (c.profile && (!rt->ensure_events(rt->t_wave_start, nw, true) || !rt->ensure_events(rt->t_wave_end, nw, true) ||
+                    !rt->ensure_events(rt->t_up_end, nw, true) || !rt->ensure_events(rt->t_down_start, nw, true) ||
                     !rt->ensure_events(rt->t_copy_start, nc, true) || !rt->ensure_events(rt->t_copy_end, nc, true)))
     return fail_cuda();
 
@@ -1358,15 +1448,18 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
       if (ie >= 0 && !ok(cudaStreamWaitEvent(ws, rt->in_ev[ie], 0), "wave waits inputs")) return fail_cuda();
     }
     if (c.profile && !ok(cudaEventRecord(rt->t_wave_start[a.index], ws), "record")) return fail_cuda();
-    const int ctas = w.cls == 1 ? rt->r_ctas : rt->m_ctas;
+    // release waves gate the copy engine: they start on the reserved SMs at once
+    const int ctas = w.cls == 1 ? rt->rel_launch_ctas : rt->m_ctas;
     int rc = coe_grouped_mlp(m, dg_up + w.first_group, dg_down + w.first_group, w.num_groups, w.tiles_up, w.tiles_down,
                              sb.boff, sb.mreq, sb.mstage, 1, ctas, ws);
     if (rc) return rc;
     if (!ok(cudaEventRecord(rt->wave_up_ev[a.index], ws), "record")) return fail_cuda();
+    if (c.profile && !ok(cudaEventRecord(rt->t_up_end[a.index], ws), "record")) return fail_cuda();
     for (int32_t sk : w.frees_slots)
       if (!ok(cudaEventRecord(rt->slot_free_up[sk], ws), "record")) return fail_cuda();
     for (int32_t cid : w.wait_copies)
       if (!ok(cudaStreamWaitEvent(ws, rt->copy_down_ev[cid], 0), "wave waits W2")) return fail_cuda();
+    if (c.profile && !ok(cudaEventRecord(rt->t_down_start[a.index], ws), "record")) return fail_cuda();
     rc = coe_grouped_mlp(m, dg_up + w.first_group, dg_down + w.first_group, w.num_groups, w.tiles_up, w.tiles_down,
                          sb.boff, sb.mreq, sb.mstage, 2, ctas, ws);
     if (rc) return rc;
@@ -1425,10 +1518,12 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
   rt->last_wave_cls.clear();
   rt->last_wave_rows.clear();
   rt->last_wave_groups.clear();
+  rt->last_wave_flops.clear();
   for (const WaveAct &w : waves) {
     rt->last_wave_cls.push_back(w.cls);
     rt->last_wave_rows.push_back((int32_t)w.rows);
     rt->last_wave_groups.push_back(w.num_groups);
+    rt->last_wave_flops.push_back(4.0 * (double)w.rows * rt->sd[w.shape] * rt->sh[w.shape]);
   }
   rt->last_copies = (int32_t)nc;
   rt->last_adm = n_adm;

@@ -51,7 +51,8 @@ class StepStats(ctypes.Structure):
 
 class StepTiming(ctypes.Structure):
     _fields_ = [(n, ctypes.c_float) for n in ("total_ms", "copy_busy_ms", "compute_busy_ms", "overlap_ms", "mlp_ms",
-                                               "group_ms")]
+                                               "group_ms", "k3_busy_ms")] + \
+               [("k3_launches", ctypes.c_int32), ("k3_flops", ctypes.c_double)]
 
     def as_dict(self) -> dict:
         return {name: float(getattr(self, name)) for name, _ in self._fields_}
@@ -115,6 +116,8 @@ def _lib():
         lib.coe_runtime_counts.restype = ctypes.c_int
         lib.coe_runtime_intervals.argtypes = [V, V, V, V]
         lib.coe_runtime_intervals.restype = ctypes.c_int
+        lib.coe_runtime_wave_phases.argtypes = [V, V, V]
+        lib.coe_runtime_wave_phases.restype = ctypes.c_int
         lib.coe_runtime_read_buffer.argtypes = [V, ctypes.c_int, V, I64]
         lib.coe_runtime_read_buffer.restype = ctypes.c_int
         lib.coe_runtime_stream.argtypes = [V, ctypes.c_int]
@@ -183,7 +186,7 @@ class B200Runtime:
         self.max_requests = max_requests
         self.weight_seed = weight_seed
         T = shapes[0].T
-        rows = max_wave_rows or max(128, min(32768, max_admissions * T))
+        rows = max_wave_rows or max(128, min(int(os.environ.get("COE_MAX_WAVE_ROWS", 32768)), max_admissions * T))
         self._keep = {
             "d": np.array([s.d for s in shapes], np.int32), "h": np.array([s.h for s in shapes], np.int32),
             "slots": np.array(slots, np.int32),
@@ -351,6 +354,15 @@ class B200Runtime:
                                                         info.ctypes.data), "intervals")
         return {"copies": cp[:2 * nc.value].reshape(-1, 2).tolist(), "waves": wv[:2 * nw.value].reshape(-1, 2).tolist(),
                 "wave_info": info[:3 * nw.value].reshape(-1, 3).tolist()}
+
+    def wave_phases(self) -> dict:
+        """Per wave: [up start, up end, down start, down end] (ms since step start) and FLOPs."""
+        nc, nw = ctypes.c_int32(), ctypes.c_int32()
+        self.lib.coe_runtime_counts(self.handle, ctypes.byref(nc), ctypes.byref(nw))
+        iv = np.zeros(4 * max(1, nw.value), np.float32)
+        fl = np.zeros(max(1, nw.value), np.float64)
+        _check(self.lib, self.lib.coe_runtime_wave_phases(self.handle, iv.ctypes.data, fl.ctypes.data), "wave_phases")
+        return {"phases": iv[:4 * nw.value].reshape(-1, 4).tolist(), "flops": fl[:nw.value].tolist()}
 
     def bench_mlp(self, groups: int, requests_per_group: int, iters: int = 10) -> tuple:
         up, down = ctypes.c_float(), ctypes.c_float()

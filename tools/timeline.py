@@ -1,22 +1,92 @@
-"""Run a few serving steps of a config and dump the per-copy / per-wave timeline (debug tool)."""
-import json, sys, os
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2503_02354_b200 import configs, engine, runtime
+"""Run a few serving steps of a config and analyse the last step's timeline (debug tool).
 
-name = sys.argv[1] if len(sys.argv) > 1 else "c3"
-nreq = int(sys.argv[2]) if len(sys.argv) > 2 else 10000
-out = sys.argv[3] if len(sys.argv) > 3 else "gpurun_out/timeline.json"
-w = configs.load(name, nreq)
-shape = runtime.shape_of(w)
-cfg = configs.run_config(w, trace=False)
-plan = engine.plan(cfg)
-rt = runtime.B200Runtime.for_plan(plan, shape, profile=True)
-rt.fill_inputs(len(plan.resolved.request_ids))
-res = []
-for i in range(3):
-    p = engine.plan(cfg)
-    st = rt.step(p)
-    rt.synchronize()
-    res.append({"stats": st, "timing": rt.timing(), "iv": rt.intervals()})
-    print(json.dumps(res[-1]["timing"]))
-json.dump(res[-1], open(out, "w"))
+    python tools/timeline.py [config] [requests] [out.json]
+
+Prints one JSON summary: step / copy / K3 busy times, the K3 launch efficiency
+split by wave size, the idle time of the GPU between K3 launches, and the
+W2-wait gaps inside waves.  The raw per-wave phases go to out.json.
+"""
+import json
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2503_02354_b200 import configs, engine, runtime  # noqa: E402
+
+
+def union(iv):
+    iv = sorted(iv)
+    tot, cur_s, cur_e = 0.0, None, None
+    for s, e in iv:
+        if cur_e is None or s > cur_e:
+            if cur_e is not None:
+                tot += cur_e - cur_s
+            cur_s, cur_e = s, e
+        else:
+            cur_e = max(cur_e, e)
+    if cur_e is not None:
+        tot += cur_e - cur_s
+    return tot
+
+
+def main():
+    name = sys.argv[1] if len(sys.argv) > 1 else "c3"
+    nreq = int(sys.argv[2]) if len(sys.argv) > 2 else 10000
+    out = sys.argv[3] if len(sys.argv) > 3 else f"gpurun_out/timeline_{name}_{nreq}.json"
+    w = configs.load(name, nreq)
+    shape = runtime.shape_of(w)
+    cfg = configs.run_config(w, trace=False)
+    plan = engine.plan(cfg)
+    rt = runtime.B200Runtime.for_plan(plan, shape, profile=True)
+    rt.fill_inputs(len(plan.resolved.request_ids))
+    keep = []
+    for _ in range(4):
+        p = engine.plan(cfg)
+        st = rt.step(p)
+        keep.append(p)
+        rt.synchronize()
+    timing = rt.timing()
+    iv = rt.intervals()
+    ph = rt.wave_phases()
+    phases = np.array(ph["phases"])
+    flops = np.array(ph["flops"])
+    info = np.array(iv["wave_info"])
+    up = phases[:, 1] - phases[:, 0]
+    down = phases[:, 3] - phases[:, 2]
+    w2wait = phases[:, 2] - phases[:, 1]
+    k3_iv = [(a, b) for a, b in phases[:, 0:2]] + [(a, b) for a, b in phases[:, 2:4]]
+    busy = union(k3_iv)
+    rows = info[:, 1]
+    buckets = {}
+    for lo, hi in ((0, 2048), (2048, 8192), (8192, 16384), (16384, 1 << 30)):
+        m = (rows >= lo) & (rows < hi)
+        if m.any():
+            t = float((up[m] + down[m]).sum())
+            buckets[f"rows[{lo},{hi})"] = {"waves": int(m.sum()), "sum_launch_ms": t,
+                                           "tflops_serial": float(flops[m].sum() / (t / 1e3) / 1e12) if t > 0 else None}
+    cls = {}
+    for c in sorted(set(info[:, 0].tolist())):
+        m = info[:, 0] == c
+        t = float((up[m] + down[m]).sum())
+        cls[int(c)] = {"waves": int(m.sum()), "rows": int(rows[m].sum()), "sum_launch_ms": t,
+                       "busy_union_ms": union([(a, b) for a, b in phases[m][:, 0:2]] +
+                                              [(a, b) for a, b in phases[m][:, 2:4]]),
+                       "tflops_serial": float(flops[m].sum() / (t / 1e3) / 1e12) if t > 0 else None}
+    summary = {
+        "config": name, "requests": nreq, "timing": timing, "stats": st,
+        "k3": {"busy_ms": busy, "flops": float(flops.sum()), "tflops_busy": float(flops.sum() / (busy / 1e3) / 1e12),
+               "sum_launch_ms": float((up + down).sum()), "w2_wait_ms_sum": float(w2wait.sum()),
+               "waves": int(len(flops)), "mean_rows": float(rows.mean()), "median_rows": float(np.median(rows)),
+               "idle_ms_in_step": timing["total_ms"] - busy, "by_rows": buckets, "by_stream_class": cls},
+        "copies": {"n": len(iv["copies"]), "busy_ms": union([tuple(c) for c in iv["copies"]])},
+    }
+    print(json.dumps(summary))
+    json.dump({"summary": summary, "phases": ph["phases"], "flops": ph["flops"], "wave_info": iv["wave_info"],
+               "copies": iv["copies"]}, open(out, "w"))
+    rt.close()
+
+
+if __name__ == "__main__":
+    main()
