@@ -197,12 +197,22 @@ def main() -> None:
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         world = max(world, 1)
+    # COE_BENCH_SHARE_GPU=1: every rank on cuda:0 with a gloo control group -- exercises the
+    # multi-rank path (fused IPC hops, step fences) on a one-GPU box; its timings are not a
+    # scaling measurement
+    share = os.environ.get("COE_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    red_dev = "cpu" if share else "cuda"
 
     w = configs.load(args.config, args.requests, gpu_executors=world)
     shape = runtime.shape_of(w)
@@ -216,9 +226,13 @@ def main() -> None:
         store_path = f"/dev/shm/coe_store_{args.config}_{os.environ.get('MASTER_PORT', '0')}"
     rt = runtime.B200Runtime.for_plan(plan0, shape, executor=rank, profile=True, store_path=store_path,
                                       init_experts=(store_path is None or local == 0))
+    transport = os.environ.get("COE_HOP_TRANSPORT", "peer")
     if dist is not None:
         dist.barrier()  # local rank 0 has filled the shared store
-        rt.attach_comm(rank, world)
+        if transport == "nccl":
+            rt.attach_comm(rank, world)  # NCCL send/recv pairs on a hop stream
+        else:
+            rt.attach_peers_ipc(rank, world)  # hops fused into K3's down pass (NVLink peer stores)
     rt.fill_inputs(n_req)
     stream = torch.cuda.ExternalStream(rt.stream_handle(0))
 
@@ -261,7 +275,7 @@ def main() -> None:
     elapsed_ms = start.elapsed_time(end)
     timing = rt.timing()
     if dist is not None:
-        t = torch.tensor([elapsed_ms], device="cuda")
+        t = torch.tensor([elapsed_ms], device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         elapsed_ms = float(t.item())
     plan_last = keep[-1]
@@ -292,7 +306,7 @@ def main() -> None:
         barrier()
         e2e_ms = e0.elapsed_time(e1)
         if dist is not None:
-            t = torch.tensor([e2e_ms], device="cuda")
+            t = torch.tensor([e2e_ms], device=red_dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_ms = float(t.item())
         e2e = {"value": n_req * args.e2e_steps / (e2e_ms / 1e3), "unit": "requests/s",
@@ -346,6 +360,7 @@ def main() -> None:
                                     {a: {"d": v[0], "h": v[1], "T": v[2]} for a, v in sorted(shape.items())}),
                    "expert_budget_bytes": plan0.resolved.alloc["gpu"]["expert_budget_bytes"],
                    "hbm_slots": rt.num_slots, "policy": w.run["policy"], "parallelism": f"executor-per-gpu x{world}",
+                   "hop_transport": (transport if world > 1 else None),
                    "l2": "no flush needed: 60 GB of experts and >2 GB of activations per step exceed the 126 MB L2"},
         "swaps_per_1k_requests": 1000.0 * metrics.expert_switches / n_req,
         "gb_moved_per_1k_requests": 1000.0 * ps["bytes_moved"] / 1e9 / n_req,

@@ -94,6 +94,12 @@ int coe_mlp_max_groups(void);
 int coe_grouped_mlp(coe_mlp *m, const coe_mlp_group *groups_up, const coe_mlp_group *groups_down, int num_groups,
                     int tiles_up, int tiles_down, const int32_t *batch_off, const int32_t *member_req,
                     const int32_t *member_stage, int which, int max_ctas, cudaStream_t stream);
+/* Fused follow-up hops for the down projection of later launches: a member whose
+ * hop_dst[req * hop_stride + stage] = r >= 0 has its output rows stored into
+ * peer_act[2 * r + (stage & 1)] (executor r's P0 / P1, same row layout) instead of the
+ * local buffer.  hop_dst == NULL turns it off.  world <= COE_MAX_PEERS. */
+#define COE_MAX_PEERS 8
+int coe_mlp_set_hops(coe_mlp *m, const int8_t *hop_dst, int hop_stride, void *const *peer_act, int world);
 
 /* ---------------- GPU serving runtime (one executor per GPU) --------------- */
 
@@ -193,6 +199,26 @@ int coe_runtime_counts(coe_runtime *rt, int32_t *copies, int32_t *waves);
 int coe_runtime_bench_mlp(coe_runtime *rt, int32_t groups, int32_t requests_per_group, int32_t iters,
                           float *up_ms, float *down_ms);
 int coe_runtime_intervals(coe_runtime *rt, float *copy_iv, float *wave_iv, int32_t *wave_info);
+
+/* ---- fused follow-up hops over peer memory (N executors, N <= COE_MAX_PEERS) ----
+ * Instead of a send / receive pair, the producer's K3 down pass stores a hopping request's
+ * output rows directly into the destination executor's P buffer (NVLink peer stores when
+ * the executors are different GPUs), then its stream publishes the hop's flag in the
+ * destination's flag array (cuStreamWriteValue32, after a memory barrier); the consumer's
+ * wave waits on its own flag (cuStreamWaitValue32) -- no copy, no extra kernel.  Every
+ * executor sees the same global hop order (hops.h), so flags are indexed by hop index and
+ * hold the step sequence number.  A per-step device-side fence keeps a producer from
+ * writing into a destination still running the previous step.
+ * Buffers come from coe_runtime_peer_buffers (same process) or, across processes, from
+ * coe_runtime_ipc_export (3 x 64-byte cudaIpcMemHandle_t) + coe_runtime_ipc_open. */
+typedef struct coe_peer_buffers {
+  void *p0, *p1, *flags;
+} coe_peer_buffers;
+int coe_runtime_peer_buffers(coe_runtime *rt, coe_peer_buffers *out);
+int coe_runtime_ipc_export(coe_runtime *rt, void *handles);
+int coe_runtime_ipc_open(coe_runtime *rt, const void *handles, coe_peer_buffers *out);
+/* peers[world]: every executor's buffers (peers[rank] = this runtime's own) */
+int coe_runtime_attach_peers(coe_runtime *rt, int32_t rank, int32_t world, const coe_peer_buffers *peers);
 /* profile mode: per wave [up start, up end, down start, down end] ms since step start and
  * the wave's algorithmic FLOPs (4 * rows * d * h) */
 int coe_runtime_wave_phases(coe_runtime *rt, float *phase_iv, double *wave_flops);

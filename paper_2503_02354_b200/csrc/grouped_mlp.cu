@@ -68,6 +68,12 @@ struct GemmArgs {
   __nv_bfloat16 *out_act0;
   __nv_bfloat16 *out_act1;
   int32_t *tile_counter;  // [next tile, CTAs done]: dynamic tile scheduler, self-resetting
+  // fused follow-up hops (down pass): hop_dst[req * hop_stride + stage] = executor that runs
+  // the request's next stage when it is not this one (-1 otherwise); those output rows are
+  // stored straight into that executor's activation buffer (NVLink peer stores across GPUs)
+  const int8_t *hop_dst;
+  int hop_stride;
+  __nv_bfloat16 *peer_act[COE_MAX_PEERS][2];
 };
 
 constexpr int TILE_RING = 4;  // tile indices handed from the producer to the MMA / epilogue warps
@@ -282,6 +288,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const int req = args.member_req[boff + j];
           const int st = args.member_stage[boff + j];
           __nv_bfloat16 *dst = (st & 1) ? args.out_act1 : args.out_act0;
+          if (args.hop_dst) {
+            const int hd = args.hop_dst[(size_t)req * args.hop_stride + st];
+            if (hd >= 0) dst = args.peer_act[hd][st & 1];
+          }
           out_row = dst + ((size_t)req * args.T + (row - j * args.T)) * args.ld;
         }
         out_row += c.n_blk * BN;
@@ -391,6 +401,9 @@ struct coe_mlp {
   int num_sms;
   int a_box_rows;
   int32_t *tile_counter = nullptr;  // device [2]; one per instance = one per stream
+  const int8_t *hop_dst = nullptr;   // fused hops (coe_mlp_set_hops)
+  int hop_stride = 0;
+  __nv_bfloat16 *peer_act[COE_MAX_PEERS][2] = {};
   bool dynamic = false;             // COE_K3_DYNAMIC=1: atomic tile claims instead of the static
                                     // round-robin (measured 3 % slower on full-GPU waves, r1)
 };
@@ -453,6 +466,19 @@ void coe_mlp_destroy(coe_mlp *m) {
 
 int coe_mlp_max_groups(void) { return MAX_GROUPS; }
 
+int coe_mlp_set_hops(coe_mlp *m, const int8_t *hop_dst, int hop_stride, void *const *peer_act, int world) {
+  if (world > COE_MAX_PEERS) {
+    coe_set_error("fused hops: more executors than COE_MAX_PEERS");
+    return COE_CUDA_ERR_CONFIG;
+  }
+  m->hop_dst = hop_dst;
+  m->hop_stride = hop_stride;
+  for (int r = 0; r < COE_MAX_PEERS; ++r)
+    for (int b = 0; b < 2; ++b)
+      m->peer_act[r][b] = (hop_dst && r < world) ? static_cast<__nv_bfloat16 *>(peer_act[2 * r + b]) : nullptr;
+  return COE_CUDA_OK;
+}
+
 int coe_grouped_mlp(coe_mlp *m, const coe_mlp_group *groups_up, const coe_mlp_group *groups_down, int num_groups,
                     int tiles_up, int tiles_down, const int32_t *batch_off, const int32_t *member_req,
                     const int32_t *member_stage, int which, int max_ctas, cudaStream_t stream) {
@@ -482,6 +508,9 @@ int coe_grouped_mlp(coe_mlp *m, const coe_mlp_group *groups_up, const coe_mlp_gr
     a.out_act0 = reinterpret_cast<__nv_bfloat16 *>(c.act0);
     a.out_act1 = reinterpret_cast<__nv_bfloat16 *>(c.act1);
     a.tile_counter = m->dynamic ? m->tile_counter : nullptr;
+    a.hop_dst = pass == 1 ? m->hop_dst : nullptr;
+    a.hop_stride = m->hop_stride;
+    std::memcpy(a.peer_act, m->peer_act, sizeof(a.peer_act));
     if (a.total_tiles <= 0) continue;
     int cap = (max_ctas > 0 && max_ctas < m->num_sms) ? max_ctas : m->num_sms;
     int grid = a.total_tiles < cap ? a.total_tiles : cap;

@@ -27,6 +27,7 @@
 // some later LOAD overwrites runs as its own wave, so that swap-in waits for
 // nothing else).  Pass 2 issues them.  Timing never feeds back into decisions.
 
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <fcntl.h>
 #include <sys/mman.h>
@@ -99,6 +100,44 @@ struct Action {
 };
 
 bool ok(cudaError_t e, const char *what) { return coe_cuda_ok(e, what); }
+
+// Stream memory operations (driver API, resolved once): the fused-hop flags.
+using StreamValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+struct StreamMemops {
+  StreamValueFn wait = nullptr, write = nullptr;
+};
+const StreamMemops *stream_memops() {
+  static StreamMemops ops;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void *w = nullptr, *v = nullptr;
+    cudaDriverEntryPointQueryResult q1, q2;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &w, cudaEnableDefault, &q1) == cudaSuccess &&
+        q1 == cudaDriverEntryPointSuccess &&
+        cudaGetDriverEntryPoint("cuStreamWriteValue32", &v, cudaEnableDefault, &q2) == cudaSuccess &&
+        q2 == cudaDriverEntryPointSuccess) {
+      ops.wait = reinterpret_cast<StreamValueFn>(w);
+      ops.write = reinterpret_cast<StreamValueFn>(v);
+    }
+  }
+  return ops.wait ? &ops : nullptr;
+}
+bool wait_flag(cudaStream_t s, const int32_t *addr, uint32_t value) {
+  CUresult r = stream_memops()->wait(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(addr), value,
+                                     CU_STREAM_WAIT_VALUE_GEQ);
+  if (r != CUDA_SUCCESS) coe_set_error("cuStreamWaitValue32 failed (" + std::to_string((int)r) + ")");
+  return r == CUDA_SUCCESS;
+}
+// default flags: the write follows a memory barrier, so the producer kernel's stores (peer
+// stores included) are visible before the flag is
+bool write_flag(cudaStream_t s, int32_t *addr, uint32_t value) {
+  CUresult r = stream_memops()->write(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(addr), value,
+                                      CU_STREAM_WRITE_VALUE_DEFAULT);
+  if (r != CUDA_SUCCESS) coe_set_error("cuStreamWriteValue32 failed (" + std::to_string((int)r) + ")");
+  return r == CUDA_SUCCESS;
+}
+constexpr int HOP_STRIDE = 8;  // hop_dst row per request: one entry per chain stage (<= 8 stages)
 
 // Release-wave grid: the reserved SMs (static K3 tiles); with COE_K3_DYNAMIC=1 the whole GPU,
 // its CTAs claiming tiles as the main stream's kernels hand SMs back.  COE_RELEASE_CTAS overrides.
@@ -204,6 +243,18 @@ struct coe_runtime {
   std::vector<cudaEvent_t> recv_ev;
   cudaEvent_t hop_drained = nullptr, step_end = nullptr;
   bool have_step_end = false;
+  // fused hops over peer memory (coe_runtime_attach_peers): K3's down pass stores a hopping
+  // request's rows into the destination executor's P buffer; flags are published with stream
+  // memory operations.  d_hflags: [max_admissions] hop flags (by global hop index) followed
+  // by COE_MAX_PEERS step flags; each holds the step sequence number that last set it.
+  int32_t *d_hflags = nullptr;
+  int64_t hflag_step_base = 0;
+  std::vector<coe_peer_buffers> peers;  // every executor's buffers as mapped in this process
+  std::vector<void *> ipc_opened;
+  int32_t peer_rank = -1, peer_world = 0;
+  uint32_t step_seq = 0;
+  int8_t *d_hopdst[2] = {nullptr, nullptr};  // per step set: [max_requests][HOP_STRIDE]
+  int8_t *h_hopdst[2] = {nullptr, nullptr};
   int m_ctas = 148, r_ctas = 16;  // SM split: main waves vs the swap-in-gating waves
   int rel_launch_ctas = 148;      // grid of a release wave (all SMs; see phase C)
 
@@ -228,7 +279,10 @@ struct coe_runtime {
     }
     for (void *p : dev)
       if (p) cudaFree(p);
-    for (void *p : {(void *)staging[0], (void *)staging[1], (void *)h_last})
+    for (void *p : ipc_opened) cudaIpcCloseMemHandle(p);
+    for (void *p : {(void *)d_hflags, (void *)d_hopdst[0], (void *)d_hopdst[1]})
+      if (p) cudaFree(p);
+    for (void *p : {(void *)staging[0], (void *)staging[1], (void *)h_last, (void *)h_hopdst[0], (void *)h_hopdst[1]})
       if (p) cudaFreeHost(p);
     if (host_store && store_mapped) {
       cudaHostUnregister(host_store);
@@ -405,7 +459,10 @@ int coe_runtime_create(const coe_runtime_config *cfg, coe_runtime **out) {
               dmalloc(&rt->d_flags, 64, "flags alloc") && dmalloc(&rt->d_last, 4 * (size_t)c.max_requests, "last") &&
               dmalloc(&rt->d_sort_scratch, (size_t)coe_group_sort_scratch_bytes(c.max_admissions), "sort scratch") &&
               dmalloc(&rt->d_compact_scratch, (size_t)coe_run_compact_scratch_bytes(c.max_admissions, (int)B, 1),
-                      "compact scratch");
+                      "compact scratch") &&
+              dmalloc(&rt->d_hflags, 4 * (A + COE_MAX_PEERS), "hop flags") &&
+              ok(cudaMemset(rt->d_hflags, 0, 4 * (A + COE_MAX_PEERS)), "hop flags");
+  rt->hflag_step_base = (int64_t)A;
   rt->slabs.assign(rt->S, nullptr);
   for (int k = 0; k < rt->S; ++k)
     good = good && dmalloc(&rt->slabs[k], (size_t)rt->sbytes[k] * std::max(1, rt->slot_count[k]), "slab alloc");
@@ -658,6 +715,56 @@ int coe_runtime_attach_comm(coe_runtime *rt, coe_comm *comm) {
   return COE_CUDA_OK;
 }
 
+int coe_runtime_peer_buffers(coe_runtime *rt, coe_peer_buffers *out) {
+  out->p0 = rt->p0;
+  out->p1 = rt->p1;
+  out->flags = rt->d_hflags;
+  return COE_CUDA_OK;
+}
+
+int coe_runtime_ipc_export(coe_runtime *rt, void *handles) {
+  auto *h = static_cast<cudaIpcMemHandle_t *>(handles);
+  bool good = ok(cudaIpcGetMemHandle(&h[0], rt->p0), "ipc export P0") &&
+              ok(cudaIpcGetMemHandle(&h[1], rt->p1), "ipc export P1") &&
+              ok(cudaIpcGetMemHandle(&h[2], rt->d_hflags), "ipc export flags");
+  return good ? COE_CUDA_OK : fail_cuda();
+}
+
+int coe_runtime_ipc_open(coe_runtime *rt, const void *handles, coe_peer_buffers *out) {
+  const auto *h = static_cast<const cudaIpcMemHandle_t *>(handles);
+  void *p[3] = {nullptr, nullptr, nullptr};
+  for (int i = 0; i < 3; ++i) {
+    if (!ok(cudaIpcOpenMemHandle(&p[i], h[i], cudaIpcMemLazyEnablePeerAccess), "ipc open")) return fail_cuda();
+    rt->ipc_opened.push_back(p[i]);
+  }
+  out->p0 = p[0];
+  out->p1 = p[1];
+  out->flags = p[2];
+  return COE_CUDA_OK;
+}
+
+int coe_runtime_attach_peers(coe_runtime *rt, int32_t rank, int32_t world, const coe_peer_buffers *peers) {
+  if (world < 1 || world > COE_MAX_PEERS || rank < 0 || rank >= world) {
+    coe_set_error("attach_peers: world must be 1..COE_MAX_PEERS and rank inside it");
+    return COE_CUDA_ERR_CONFIG;
+  }
+  if (!stream_memops()) {
+    coe_set_error("attach_peers: cuStreamWaitValue32 / cuStreamWriteValue32 unavailable");
+    return COE_CUDA_ERR_CUDA;
+  }
+  const size_t bytes = (size_t)rt->cfg.max_requests * HOP_STRIDE;
+  for (int k = 0; k < 2; ++k) {
+    if (!rt->d_hopdst[k] && !dmalloc(&rt->d_hopdst[k], bytes, "hop dst")) return fail_cuda();
+    if (!rt->h_hopdst[k] &&
+        !ok(cudaHostAlloc(reinterpret_cast<void **>(&rt->h_hopdst[k]), bytes, cudaHostAllocDefault), "hop dst"))
+      return fail_cuda();
+  }
+  rt->peers.assign(peers, peers + world);
+  rt->peer_rank = rank;
+  rt->peer_world = world;
+  return COE_CUDA_OK;
+}
+
 int coe_runtime_bench_mlp(coe_runtime *rt, int32_t groups, int32_t requests_per_group, int32_t iters,
                           float *up_ms, float *down_ms) {
   const auto &c = rt->cfg;
@@ -860,8 +967,14 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     if (h.src == x) hop_out[hkey(h.request, h.stage)] = (int32_t)my_hops.size();
     my_hops.push_back((int32_t)i);
   }
-  if (!my_hops.empty() && !rt->comm) {
-    coe_set_error("plan moves activations between executors: attach a communicator (coe_runtime_attach_comm)");
+  const bool peer_mode = rt->peer_world > 0;
+  if (!my_hops.empty() && !rt->comm && !peer_mode) {
+    coe_set_error("plan moves activations between executors: attach a communicator (coe_runtime_attach_comm) "
+                  "or peer buffers (coe_runtime_attach_peers)");
+    return COE_CUDA_ERR_CONFIG;
+  }
+  if (peer_mode && x != rt->peer_rank) {
+    coe_set_error("peer hops: step executor differs from the rank the runtime was attached as");
     return COE_CUDA_ERR_CONFIG;
   }
   std::vector<int32_t> hop_batch(my_hops.size(), -1);  // producing batch of each send
@@ -1286,6 +1399,30 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
   StepBuffers &sb = rt->sets[set_idx];
   if (!ok(cudaEventSynchronize(rt->staging_done[set_idx]), "staging reuse")) return fail_cuda();
   char *stg = rt->staging[set_idx];
+  uint32_t seq = 0;
+  if (peer_mode) {  // fused hops: where each of this executor's hopping rows goes
+    seq = ++rt->step_seq;
+    int8_t *hd = rt->h_hopdst[set_idx];
+    std::memset(hd, 0xFF, (size_t)c.max_requests * HOP_STRIDE);
+    for (int32_t hs : my_hops) {
+      const coe::Hop &h = all_hops[hs];
+      if (h.src != x) continue;
+      if (h.stage >= HOP_STRIDE || h.dst >= rt->peer_world) {
+        coe_set_error("peer hops: chain longer than 8 stages or destination outside the peer group");
+        return COE_CUDA_ERR_CONFIG;
+      }
+      hd[(size_t)h.request * HOP_STRIDE + h.stage] = (int8_t)h.dst;
+    }
+    std::vector<void *> pa(2 * rt->peer_world);
+    for (int r = 0; r < rt->peer_world; ++r) {
+      pa[2 * r] = rt->peers[r].p0;
+      pa[2 * r + 1] = rt->peers[r].p1;
+    }
+    for (auto &per : rt->mlps)
+      for (coe_mlp *m : per)
+        if (m && coe_mlp_set_hops(m, rt->d_hopdst[set_idx], HOP_STRIDE, pa.data(), rt->peer_world))
+          return COE_CUDA_ERR_CONFIG;
+  }
   int32_t *s_adm = reinterpret_cast<int32_t *>(stg);
   for (int64_t i = 0; i < n_adm; ++i) {
     s_adm[i] = 0;
@@ -1316,6 +1453,13 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
                            cudaMemcpyHostToDevice, ks),
            "group H2D")))
     return fail_cuda();
+  if (peer_mode && !ok(cudaMemcpyAsync(rt->d_hopdst[set_idx], rt->h_hopdst[set_idx],
+                                       (size_t)c.max_requests * HOP_STRIDE, cudaMemcpyHostToDevice, ks),
+                       "hop dst H2D"))
+    return fail_cuda();
+  if (peer_mode)  // step fence: every peer has finished the previous step (its P rows are free)
+    for (int r = 0; r < rt->peer_world; ++r)
+      if (r != x && !wait_flag(cs, rt->d_hflags + rt->hflag_step_base + r, seq - 1)) return COE_CUDA_ERR_CUDA;
   if (!ok(cudaEventRecord(rt->staging_done[set_idx], ks), "record") || !ok(cudaEventRecord(rt->staged, ks), "record") ||
       !ok(cudaStreamWaitEvent(cs, rt->staged, 0), "compute waits upload"))
     return fail_cuda();
@@ -1432,7 +1576,10 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     const WaveAct &w = waves[a.index];
     cudaStream_t ws = rt->cls_stream[w.cls];
     coe_mlp *m = rt->mlps[w.shape][w.cls];
-    if (!w.wait_recvs.empty()) {
+    if (peer_mode) {
+      for (int32_t hslot : w.wait_recvs)
+        if (!wait_flag(ws, rt->d_hflags + all_hops[my_hops[hslot]].index, seq)) return COE_CUDA_ERR_CUDA;
+    } else if (!w.wait_recvs.empty()) {
       int64_t limit = -1;
       for (int32_t hslot : w.wait_recvs) limit = std::max<int64_t>(limit, all_hops[my_hops[hslot]].index);
       if (!issue_hops_until(limit)) return COE_CUDA_ERR_CUDA;
@@ -1465,6 +1612,12 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     if (rc) return rc;
     st.launches += 2;
     if (!ok(cudaEventRecord(rt->wave_down_ev[a.index], ws), "record")) return fail_cuda();
+    if (peer_mode)  // publish the hops this wave's down pass just stored into the peers
+      for (int32_t gi = w.first_group; gi < w.first_group + w.num_groups; ++gi)
+        for (int32_t hslot : batches[g_up[gi].batch].sends) {
+          const coe::Hop &h = all_hops[my_hops[hslot]];
+          if (!write_flag(ws, static_cast<int32_t *>(rt->peers[h.dst].flags) + h.index, seq)) return COE_CUDA_ERR_CUDA;
+        }
     for (int32_t sk : w.frees_slots) {
       if (!ok(cudaEventRecord(rt->slot_free_down[sk], ws), "record")) return fail_cuda();
       rt->slot_free_valid[sk] = 1;
@@ -1499,7 +1652,11 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
       return fail_cuda();
     rt->have_out = true;
   }
-  if (!issue_hops_until(INT64_MAX)) return COE_CUDA_ERR_CUDA;
+  if (!peer_mode && !issue_hops_until(INT64_MAX)) return COE_CUDA_ERR_CUDA;
+  if (peer_mode)  // launches captured their arguments; later direct K3 uses run hop-free
+    for (auto &per : rt->mlps)
+      for (coe_mlp *m : per)
+        if (m) coe_mlp_set_hops(m, nullptr, 0, nullptr, 0);
   if (!my_hops.empty() && (!ok(cudaEventRecord(rt->hop_drained, rt->hop), "record") ||
                            !ok(cudaStreamWaitEvent(cs, rt->hop_drained, 0), "join hop")))
     return fail_cuda();
@@ -1509,6 +1666,11 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     if (!ok(cudaEventRecord(rt->cls_drained[k], rt->cls_stream[k]), "record") ||
         !ok(cudaStreamWaitEvent(cs, rt->cls_drained[k], 0), "join"))
       return fail_cuda();
+  if (peer_mode)  // this step is done here: tell every peer (their next step's fence)
+    for (int r = 0; r < rt->peer_world; ++r)
+      if (r != x &&
+          !write_flag(cs, static_cast<int32_t *>(rt->peers[r].flags) + rt->hflag_step_base + x, seq))
+        return COE_CUDA_ERR_CUDA;
   if (c.profile && !ok(cudaEventRecord(rt->t_step_end, cs), "record")) return fail_cuda();
   if (!ok(cudaEventRecord(sb.free_ev, cs), "record") || !ok(cudaEventRecord(rt->step_end, cs), "record"))
     return fail_cuda();

@@ -58,6 +58,13 @@ class StepTiming(ctypes.Structure):
         return {name: float(getattr(self, name)) for name, _ in self._fields_}
 
 
+class PeerBuffers(ctypes.Structure):
+    _fields_ = [("p0", ctypes.c_void_p), ("p1", ctypes.c_void_p), ("flags", ctypes.c_void_p)]
+
+
+IPC_HANDLE_BYTES = 3 * 64  # P0, P1, flags (cudaIpcMemHandle_t each)
+
+
 class RuntimeConfig(ctypes.Structure):
     _fields_ = [("d", ctypes.c_int32), ("h", ctypes.c_int32), ("T", ctypes.c_int32),
                 ("num_experts", ctypes.c_int32), ("num_slots", ctypes.c_int32), ("max_requests", ctypes.c_int32),
@@ -122,6 +129,14 @@ def _lib():
         lib.coe_runtime_read_buffer.restype = ctypes.c_int
         lib.coe_runtime_stream.argtypes = [V, ctypes.c_int]
         lib.coe_runtime_stream.restype = V
+        lib.coe_runtime_peer_buffers.argtypes = [V, P(PeerBuffers)]
+        lib.coe_runtime_peer_buffers.restype = ctypes.c_int
+        lib.coe_runtime_ipc_export.argtypes = [V, V]
+        lib.coe_runtime_ipc_export.restype = ctypes.c_int
+        lib.coe_runtime_ipc_open.argtypes = [V, V, P(PeerBuffers)]
+        lib.coe_runtime_ipc_open.restype = ctypes.c_int
+        lib.coe_runtime_attach_peers.argtypes = [V, I32, I32, V]
+        lib.coe_runtime_attach_peers.restype = ctypes.c_int
         lib.coe_expert_seed.argtypes = [ctypes.c_uint64, I32, I32]
         lib.coe_expert_seed.restype = ctypes.c_uint64
         for name in ("coe_runtime_create", "coe_runtime_init_experts", "coe_runtime_fill_inputs",
@@ -278,6 +293,36 @@ class B200Runtime:
         _check(self.lib, self.lib.coe_comm_create(path, rank, world, uid, ctypes.byref(self.comm)), "nccl comm")
         _check(self.lib, self.lib.coe_runtime_attach_comm(self.handle, self.comm), "attach comm")
 
+    def peer_buffers(self) -> PeerBuffers:
+        pb = PeerBuffers()
+        _check(self.lib, self.lib.coe_runtime_peer_buffers(self.handle, ctypes.byref(pb)), "peer buffers")
+        return pb
+
+    def _attach_peers(self, rank: int, peers: list) -> None:
+        arr = (PeerBuffers * len(peers))(*peers)
+        _check(self.lib, self.lib.coe_runtime_attach_peers(self.handle, rank, len(peers), arr), "attach peers")
+
+    def attach_peers_ipc(self, rank: int, world: int) -> None:
+        """Fused hops across processes (one executor per rank, normally one GPU each): every
+        rank exports its P0 / P1 / flag buffers as CUDA IPC handles, the handles travel over
+        the default torch.distributed group, and each rank maps every peer's buffers."""
+        import torch.distributed as dist
+
+        mine = (ctypes.c_char * IPC_HANDLE_BYTES)()
+        _check(self.lib, self.lib.coe_runtime_ipc_export(self.handle, mine), "ipc export")
+        gathered = [None] * world
+        dist.all_gather_object(gathered, bytes(mine))
+        peers = []
+        for r in range(world):
+            if r == rank:
+                peers.append(self.peer_buffers())
+                continue
+            h = (ctypes.c_char * IPC_HANDLE_BYTES).from_buffer_copy(gathered[r])
+            pb = PeerBuffers()
+            _check(self.lib, self.lib.coe_runtime_ipc_open(self.handle, h, ctypes.byref(pb)), "ipc open")
+            peers.append(pb)
+        self._attach_peers(rank, peers)
+
     def __del__(self):
         try:
             self.close()
@@ -391,6 +436,14 @@ class LocalHub:
             self.lib.coe_local_hub_destroy(self.handle)
         except Exception:
             pass
+
+
+def attach_peers_local(runtimes: list) -> None:
+    """Fused hops between runtimes of ONE process (several executors on one GPU): each maps
+    the others' buffers directly."""
+    peers = [rt.peer_buffers() for rt in runtimes]
+    for x, rt in enumerate(runtimes):
+        rt._attach_peers(x, peers)
 
 
 def step_executors(plan, runtimes: list, hub: "LocalHub | None" = None) -> list:

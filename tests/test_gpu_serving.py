@@ -198,12 +198,15 @@ def test_c5_heterogeneous_expert_shapes():
     assert worst <= TOL, worst
 
 
+@pytest.mark.parametrize("transport", ["peer", "hub"])
 @pytest.mark.parametrize("executors", [2, 3])
-def test_multi_executor_hops_on_one_gpu(executors):
-    """Config 4 (Zipf routing) with several executors, each its own runtime on the one GPU,
-    follow-up hops exchanged through the in-process transport in the global hop order
-    (the protocol the NCCL path uses across GPUs).  Grouping is exact per executor and
-    every request's final output, wherever it ran, matches the numpy fp32 chain."""
+def test_multi_executor_hops_on_one_gpu(executors, transport):
+    """Config 4 (Zipf routing) with several executors, each its own runtime on the one GPU.
+    transport "peer": fused hops -- K3's down pass stores hopping rows straight into the
+    destination runtime's buffers, flags via stream memory operations (the path used across
+    GPUs); "hub": send/receive pairs in the global hop order through the in-process
+    transport (the protocol the NCCL path uses).  Grouping is exact per executor and every
+    request's final output, wherever it ran, matches the numpy fp32 chain."""
     import torch
 
     w = _trim(configs.load("c4", 1000, gpu_executors=executors), 240)
@@ -211,13 +214,16 @@ def test_multi_executor_hops_on_one_gpu(executors):
     _check_against_oracle_batches(w, plan)
     assert len(runtime.hops_from_plan(plan)) > 0
     shape = runtime.RuntimeShape(1024, 2048, 64)
-    hub = runtime.LocalHub(executors)
+    hub = runtime.LocalHub(executors) if transport == "hub" else None
     rts = []
     for x in range(executors):
         rt = runtime.B200Runtime.for_plan(plan, shape, executor=x)
-        rt.attach_local(hub, x)
+        if hub is not None:
+            rt.attach_local(hub, x)
         rt.fill_inputs(len(plan.resolved.request_ids))
         rts.append(rt)
+    if hub is None:
+        runtime.attach_peers_local(rts)
     n = len(plan.resolved.request_ids)
     chains = plan.resolved.chains
     final_exec = {}
@@ -271,3 +277,61 @@ def test_window_search_with_measured_b200_throughput():
     assert res.throughput_samples and all(t > 0 for _, t in res.throughput_samples)
     counts = [c for c, _ in res.throughput_samples]
     assert counts == sorted(counts) and res.lower <= res.chosen <= res.upper
+
+
+def test_fused_hops_across_processes_ipc():
+    """Two processes, one executor each (the multi-GPU layout, here sharing the one GPU):
+    buffers exchanged as CUDA IPC handles over a gloo group, hops fused into K3's down pass
+    (cross-process stores + stream-memop flags).  Each rank's final outputs must match the
+    numpy fp32 chain for the requests that finished there, hopped ones included."""
+    import os
+    import socket
+    import subprocess
+    import sys
+    import tempfile
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    with tempfile.TemporaryDirectory() as tmp:
+        procs = []
+        for rank in range(2):
+            env = dict(os.environ, RANK=str(rank), WORLD_SIZE="2", MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port),
+                       PYTHONPATH=root)
+            procs.append(subprocess.Popen([sys.executable, os.path.join(root, "tests", "ipc_hop_worker.py"), tmp],
+                                          env=env, stdout=subprocess.PIPE, stderr=subprocess.STDOUT))
+        logs = []
+        for p in procs:
+            out, _ = p.communicate(timeout=600)
+            logs.append(out.decode(errors="replace"))
+        assert all(p.returncode == 0 for p in procs), "\n".join(l[-3000:] for l in logs)
+        parts = [np.load(os.path.join(tmp, f"rank{r}.npz")) for r in range(2)]
+    w = _trim(configs.load("c4", 1000, gpu_executors=2), 240)
+    plan = engine.plan(configs.run_config(w, trace=False))
+    hopped = {h[3] for h in runtime.hops_from_plan(plan)}
+    assert hopped
+    shape = runtime.RuntimeShape(1024, 2048, 64)
+    chains = plan.resolved.chains
+    cache = {}
+
+    def weights(e):
+        if e not in cache:
+            cache[e] = synth.expert_weights(runtime.DEFAULT_WEIGHT_SEED, e, shape.d, shape.h)
+        return cache[e]
+
+    seen = 0
+    worst = 0.0
+    hopped_checked = 0
+    for part in parts:
+        reqs, outs = part["requests"], part["outputs"]
+        assert np.array_equal(outs[0], outs[1])  # two steps, identical results
+        for i, r in enumerate(reqs.tolist()):
+            if r in hopped and hopped_checked >= 6 and r % 23:
+                continue
+            x = synth.request_inputs(runtime.DEFAULT_INPUT_SEED, r, shape.T, shape.d)
+            worst = max(worst, mlp.rel_l2(outs[0][i], mlp.chain_forward(x, chains[r], weights)))
+            hopped_checked += r in hopped
+            seen += 1
+    assert hopped_checked >= 6 and seen >= 10
+    assert worst <= TOL, worst
