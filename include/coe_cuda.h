@@ -211,14 +211,19 @@ int coe_runtime_intervals(coe_runtime *rt, float *copy_iv, float *wave_iv, int32
  * writing into a destination still running the previous step.
  * Buffers come from coe_runtime_peer_buffers (same process) or, across processes, from
  * coe_runtime_ipc_export (3 x 64-byte cudaIpcMemHandle_t) + coe_runtime_ipc_open. */
+typedef struct coe_local_hub coe_local_hub;  /* in-process transport, declared below */
 typedef struct coe_peer_buffers {
   void *p0, *p1, *flags;
 } coe_peer_buffers;
 int coe_runtime_peer_buffers(coe_runtime *rt, coe_peer_buffers *out);
 int coe_runtime_ipc_export(coe_runtime *rt, void *handles);
 int coe_runtime_ipc_open(coe_runtime *rt, const void *handles, coe_peer_buffers *out);
-/* peers[world]: every executor's buffers (peers[rank] = this runtime's own) */
-int coe_runtime_attach_peers(coe_runtime *rt, int32_t rank, int32_t world, const coe_peer_buffers *peers);
+/* peers[world]: every executor's buffers (peers[rank] = this runtime's own).  hub != NULL:
+ * the peers are runtimes of THIS process (several executors on one GPU, stepped together):
+ * hops are handed over as events through the hub instead of stream-memop flags, since a
+ * flag-waiting stream may share a hardware queue with the stream that would write it. */
+int coe_runtime_attach_peers(coe_runtime *rt, int32_t rank, int32_t world, const coe_peer_buffers *peers,
+                             coe_local_hub *hub);
 /* profile mode: per wave [up start, up end, down start, down end] ms since step start and
  * the wave's algorithmic FLOPs (4 * rows * d * h) */
 int coe_runtime_wave_phases(coe_runtime *rt, float *phase_iv, double *wave_flops);

@@ -81,6 +81,7 @@ struct coe_local_hub {
   std::mutex mu;
   std::condition_variable cv;
   std::map<std::pair<int, int>, std::deque<LocalMsg>> queues;
+  std::map<int64_t, cudaEvent_t> published;  // fused peer hops in one process: hop index -> event
   std::vector<cudaEvent_t> events;  // owned, reused round-robin
   size_t next_event = 0;
   ~coe_local_hub() {
@@ -134,6 +135,35 @@ bool coe_comm_recv_bf16(coe_comm *c, void *buf, size_t count, int peer, cudaStre
 
 int coe_comm_rank(const coe_comm *c) { return c->rank; }
 
+// Fused peer hops between runtimes of one process: the producer publishes an event recorded
+// after the down pass that stored the rows; the consumer blocks on the host until it is
+// published and makes its stream wait on it.  (Stream memory-op flags are not used in one
+// process: a waiting stream can share a hardware queue with the stream that would write the
+// flag.)
+bool coe_hub_publish(coe_local_hub *hub, int64_t key, cudaStream_t stream) {
+  std::lock_guard<std::mutex> lk(hub->mu);
+  if (hub->next_event >= hub->events.size()) {
+    cudaEvent_t e;
+    if (!coe_cuda_ok(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "hub event")) return false;
+    hub->events.push_back(e);
+  }
+  cudaEvent_t ev = hub->events[hub->next_event++];
+  if (!coe_cuda_ok(cudaEventRecord(ev, stream), "hub publish")) return false;
+  hub->published[key] = ev;
+  hub->cv.notify_all();
+  return true;
+}
+
+bool coe_hub_wait(coe_local_hub *hub, int64_t key, cudaStream_t stream) {
+  cudaEvent_t ev;
+  {
+    std::unique_lock<std::mutex> lk(hub->mu);
+    hub->cv.wait(lk, [&] { return hub->published.count(key) > 0; });
+    ev = hub->published[key];
+  }
+  return coe_cuda_ok(cudaStreamWaitEvent(stream, ev, 0), "hub wait");
+}
+
 extern "C" {
 
 int coe_comm_unique_id(const char *nccl_path, void *out128) {
@@ -176,6 +206,7 @@ void coe_local_hub_destroy(coe_local_hub *h) { delete h; }
 void coe_local_hub_reset(coe_local_hub *h) {
   std::lock_guard<std::mutex> lk(h->mu);
   h->queues.clear();
+  h->published.clear();
   h->next_event = 0;
 }
 

@@ -26,6 +26,7 @@
 
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -37,23 +38,33 @@
 
 namespace {
 
-constexpr int BM = 128;
-constexpr int BN = 256;
-constexpr int BK = 64;
-constexpr int STAGES = 4;
-constexpr int A_BYTES = BM * BK * 2;
-constexpr int B_BYTES = BN * BK * 2;
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int BM = 128;  // rows per CTA tile (TMEM lanes)
+constexpr int BN = 256;  // output columns per tile (one 256-column TMEM accumulator)
+constexpr int BK = 64;   // K per stage (one 128-byte swizzle row of bf16)
 constexpr int TMEM_COLS = 512;  // 2 accumulator buffers x BN fp32 columns
 constexpr int NUM_THREADS = 256;
 constexpr int EPI_WARP0 = 4;
 constexpr int MAX_GROUPS = 1024;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + MAX_GROUPS * 4;
+
+// CG = CTAs per MMA: 1 -- one CTA computes a 128 x 256 tile and loads A (128 x 64) and B
+// (256 x 64) per stage; 2 -- a CTA pair (cluster of 2 on one TPC) computes a 256 x 256 tile
+// with tcgen05.mma.cta_group::2: each CTA loads its own 128 A rows and HALF of B (128 x 64),
+// so per-CTA operand traffic per stage drops from 48 KB to 32 KB for the same MMA work.
+template <int CG>
+struct Tiling {
+  static constexpr int TILE_M = BM * CG;
+  static constexpr int B_ROWS = BN / CG;
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = B_ROWS * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = CG == 1 ? 4 : 6;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + MAX_GROUPS * 4;
+};
 
 struct GemmArgs {
   const coe_mlp_group *groups;
   int num_groups;
-  int total_tiles;
+  int total_tiles;  // CG == 1: host-computed; CG == 2: recomputed in the prologue
   const int32_t *batch_off;
   const int32_t *member_req;
   const int32_t *member_stage;
@@ -67,7 +78,6 @@ struct GemmArgs {
   __nv_bfloat16 *out_h;
   __nv_bfloat16 *out_act0;
   __nv_bfloat16 *out_act1;
-  int32_t *tile_counter;  // [next tile, CTAs done]: dynamic tile scheduler, self-resetting
   // fused follow-up hops (down pass): hop_dst[req * hop_stride + stage] = executor that runs
   // the request's next stage when it is not this one (-1 otherwise); those output rows are
   // stored straight into that executor's activation buffer (NVLink peer stores across GPUs)
@@ -75,8 +85,6 @@ struct GemmArgs {
   int hop_stride;
   __nv_bfloat16 *peer_act[COE_MAX_PEERS][2];
 };
-
-constexpr int TILE_RING = 4;  // tile indices handed from the producer to the MMA / epilogue warps
 
 // A-operand source of a member at chain stage s: 0 = X, 1 = P0, 2 = P1.
 __device__ __forceinline__ int a_source(int stage) { return stage == 0 ? 0 : 1 + ((stage - 1) & 1); }
@@ -94,11 +102,12 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 }
 
 struct TileCoord {
-  int g, m_blk, n_blk;
+  int g, m_blk, n_blk;  // m_blk in units of the (pair) tile height
 };
 
+template <int CG>
 __device__ __forceinline__ TileCoord decode_tile(int t, const int32_t *tile_start, int num_groups,
-                                                 const coe_mlp_group *groups, int n_blocks) {
+                                                 const coe_mlp_group *groups) {
   int lo = 0, hi = num_groups - 1;
   while (lo < hi) {  // last group with tile_start <= t
     int mid = (lo + hi + 1) >> 1;
@@ -106,117 +115,142 @@ __device__ __forceinline__ TileCoord decode_tile(int t, const int32_t *tile_star
     else hi = mid - 1;
   }
   int local = t - tile_start[lo];
-  int m_tiles = (groups[lo].rows + BM - 1) / BM;
+  int m_tiles = (groups[lo].rows + Tiling<CG>::TILE_M - 1) / Tiling<CG>::TILE_M;
   TileCoord c;
   c.g = lo;
   c.n_blk = local / m_tiles;
   c.m_blk = local - c.n_blk * m_tiles;
-  (void)n_blocks;
   return c;
 }
 
+template <int CG>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tm_a0, const __grid_constant__ CUtensorMap tm_a1,
                         const __grid_constant__ CUtensorMap tm_a2, const __grid_constant__ CUtensorMap tm_b,
                         GemmArgs args) {
+  using TL = Tiling<CG>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *stage_base = smem;
-  uint64_t *full_bar = reinterpret_cast<uint64_t *>(smem + STAGES * STAGE_BYTES);
-  uint64_t *empty_bar = full_bar + STAGES;
-  uint64_t *tfull_bar = empty_bar + STAGES;
+  uint64_t *full_bar = reinterpret_cast<uint64_t *>(smem + TL::STAGES * TL::STAGE_BYTES);
+  uint64_t *empty_bar = full_bar + TL::STAGES;
+  uint64_t *tfull_bar = empty_bar + TL::STAGES;
   uint64_t *tempty_bar = tfull_bar + 2;
-  uint64_t *ring_full = tempty_bar + 2;
-  uint64_t *ring_empty = ring_full + TILE_RING;
-  int32_t *ring_tile = reinterpret_cast<int32_t *>(ring_empty + TILE_RING);
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(ring_tile + TILE_RING);
-  int32_t *tile_start = reinterpret_cast<int32_t *>(smem + STAGES * STAGE_BYTES + 256);
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty_bar + 2);
+  int32_t *total_slot = reinterpret_cast<int32_t *>(tmem_slot + 1);
+  int32_t *tile_start = reinterpret_cast<int32_t *>(smem + TL::STAGES * TL::STAGE_BYTES + 256);
 
   const uint32_t warp = sm100::warp_id();
   const uint32_t lane = sm100::lane_id();
+  const uint32_t cta_rank = CG == 2 ? sm100::cluster_ctarank() : 0;  // 0 = leader (issues the MMAs)
+  const int tile0 = blockIdx.x / CG, tile_step = gridDim.x / CG;
 
-  for (int i = threadIdx.x; i < args.num_groups; i += NUM_THREADS) tile_start[i] = args.groups[i].tile_start;
+  if constexpr (CG == 1) {
+    for (int i = threadIdx.x; i < args.num_groups; i += NUM_THREADS) tile_start[i] = args.groups[i].tile_start;
+  } else if (warp == 3) {
+    // pair tiles per group (256-row tiles): exclusive scan across the warp, chunk per lane
+    const int per = (args.num_groups + 31) / 32;
+    const int lo = min((int)lane * per, args.num_groups), hi = min(lo + per, args.num_groups);
+    auto tiles_of = [&](int g) { return (args.groups[g].rows + TL::TILE_M - 1) / TL::TILE_M * args.n_blocks; };
+    int sum = 0;
+    for (int g = lo; g < hi; ++g) sum += tiles_of(g);
+    int incl = sum;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, off);
+      if ((int)lane >= off) incl += v;
+    }
+    int run = incl - sum;
+    for (int g = lo; g < hi; ++g) {
+      tile_start[g] = run;
+      run += tiles_of(g);
+    }
+    if (lane == 31) *total_slot = incl;
+  }
   if (warp == 0 && lane == 0) {
     sm100::prefetch_tmap(&tm_a0);
     sm100::prefetch_tmap(&tm_a1);
     sm100::prefetch_tmap(&tm_a2);
     sm100::prefetch_tmap(&tm_b);
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < TL::STAGES; ++s) {
       sm100::mbar_init(&full_bar[s], 1);
       sm100::mbar_init(&empty_bar[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
       sm100::mbar_init(&tfull_bar[s], 1);
-      sm100::mbar_init(&tempty_bar[s], 128);
-    }
-    for (int s = 0; s < TILE_RING; ++s) {
-      sm100::mbar_init(&ring_full[s], 1);
-      sm100::mbar_init(&ring_empty[s], 1 + 4);  // the MMA thread + one lane per epilogue warp
+      // CG 1: every epilogue thread arrives; CG 2: one lane per epilogue warp of both CTAs
+      sm100::mbar_init(&tempty_bar[s], CG == 1 ? 128 : 8);
     }
     sm100::fence_mbar_init();
   }
-  if (warp == 2) sm100::tmem_alloc<TMEM_COLS>(tmem_slot);
+  if (warp == 2) sm100::tmem_alloc<TMEM_COLS, CG>(tmem_slot);
   sm100::tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) sm100::cluster_sync();  // peer barriers initialised, TMEM allocated in both
+  else __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  const int total_tiles = CG == 1 ? args.total_tiles : *total_slot;
   const int k_blocks = args.K / BK;
 
   if (warp == 0) {
     if (lane == 0) {
-      // ===== TMA producer =====
+      // ===== TMA producer (both CTAs of a pair: own A rows, own half of B) =====
       int stage = 0;
       uint32_t phase = 0;
-      // dynamic scheduler: tiles are claimed in (group, n-block, m-block) order, so CTAs
-      // running at the same time share weight tiles through L2, and a CTA that starts late
-      // (SMs held by another stream's kernel) simply claims fewer tiles.  The next claim is
-      // issued before the current tile's loads so its latency hides behind them.
-      // (tile_counter == nullptr: static round-robin, tile = blockIdx.x + i * gridDim.x)
-      const bool dyn = args.tile_counter != nullptr;
-      int claim = dyn ? atomicAdd(&args.tile_counter[0], 1) : (int)blockIdx.x;
-      for (int i = 0;; ++i) {
-        const int t = claim < args.total_tiles ? claim : -1;
-        sm100::mbar_wait(&ring_empty[i % TILE_RING], ((i / TILE_RING) & 1) ^ 1);
-        ring_tile[i % TILE_RING] = t;
-        sm100::mbar_arrive(&ring_full[i % TILE_RING]);
-        if (t < 0) break;
-        claim = dyn ? atomicAdd(&args.tile_counter[0], 1) : claim + (int)gridDim.x;
-        TileCoord c = decode_tile(t, tile_start, args.num_groups, args.groups, args.n_blocks);
+      for (int t = tile0; t < total_tiles; t += tile_step) {
+        TileCoord c = decode_tile<CG>(t, tile_start, args.num_groups, args.groups);
         const coe_mlp_group grp = args.groups[c.g];
+        const int m0 = c.m_blk * TL::TILE_M + (int)cta_rank * BM;  // first row of this CTA's half
         int box_row[BM / 32];
         int box_par[BM / 32];
         int nboxes;
         uint32_t a_bytes;
         if (args.mode == 0) {
           const int boff = args.batch_off[grp.batch];
-          const int rows_left = grp.rows - c.m_blk * BM;
-          const int rows_here = rows_left < BM ? rows_left : BM;
-          nboxes = (rows_here + args.a_box_rows - 1) / args.a_box_rows;
+          const int members = grp.rows / args.T;
+          if constexpr (CG == 1) {
+            const int rows_here = min(grp.rows - m0, BM);
+            nboxes = (rows_here + args.a_box_rows - 1) / args.a_box_rows;
+          } else {
+            nboxes = BM / args.a_box_rows;  // full boxes: the leader expects a fixed byte count
+          }
           for (int b = 0; b < nboxes; ++b) {
-            int r = c.m_blk * BM + b * args.a_box_rows;
+            const int r = m0 + b * args.a_box_rows;
             int j = r / args.T;
-            int req = args.member_req[boff + j];
-            box_row[b] = req * args.T + (r - j * args.T);
+            const int within = r - j * args.T;
+            j = min(j, members - 1);  // rows past the group (pair tail): any valid member, discarded
+            box_row[b] = args.member_req[boff + j] * args.T + within;
             box_par[b] = a_source(args.member_stage[boff + j]);
           }
           a_bytes = (uint32_t)(nboxes * args.a_box_rows * BK * 2);
         } else {
           nboxes = 1;
-          box_row[0] = grp.h_row + c.m_blk * BM;
+          box_row[0] = grp.h_row + m0;  // past the H scratch end TMA fills zeros (bytes still counted)
           box_par[0] = 0;
-          a_bytes = A_BYTES;
+          a_bytes = TL::A_BYTES;
         }
+        const int b_row = c.n_blk * BN + (int)cta_rank * TL::B_ROWS;
         for (int kb = 0; kb < k_blocks; ++kb) {
           sm100::mbar_wait(&empty_bar[stage], phase ^ 1);
-          uint8_t *sa = stage_base + stage * STAGE_BYTES;
-          uint8_t *sb = sa + A_BYTES;
-          sm100::mbar_arrive_expect_tx(&full_bar[stage], a_bytes + B_BYTES);
-          for (int b = 0; b < nboxes; ++b)
-            sm100::tma_load_2d(sa + b * args.a_box_rows * 128,
-                               box_par[b] == 0 ? &tm_a0 : (box_par[b] == 1 ? &tm_a1 : &tm_a2), &full_bar[stage],
-                               kb * BK, box_row[b]);
-          sm100::tma_load_3d(sb, &tm_b, &full_bar[stage], kb * BK, c.n_blk * BN, grp.slot);
-          if (++stage == STAGES) {
+          uint8_t *sa = stage_base + stage * TL::STAGE_BYTES;
+          uint8_t *sb = sa + TL::A_BYTES;
+          if constexpr (CG == 1) {
+            sm100::mbar_arrive_expect_tx(&full_bar[stage], a_bytes + TL::B_BYTES);
+            for (int b = 0; b < nboxes; ++b)
+              sm100::tma_load_2d(sa + b * args.a_box_rows * 128,
+                                 box_par[b] == 0 ? &tm_a0 : (box_par[b] == 1 ? &tm_a1 : &tm_a2), &full_bar[stage],
+                                 kb * BK, box_row[b]);
+            sm100::tma_load_3d(sb, &tm_b, &full_bar[stage], kb * BK, b_row, grp.slot);
+          } else {
+            const uint32_t bar = sm100::mapa_shared(sm100::smem_u32(&full_bar[stage]), 0);
+            if (cta_rank == 0) sm100::mbar_arrive_expect_tx(&full_bar[stage], 2 * TL::STAGE_BYTES);
+            for (int b = 0; b < nboxes; ++b)
+              sm100::tma_load_2d_pair(sa + b * args.a_box_rows * 128,
+                                      box_par[b] == 0 ? &tm_a0 : (box_par[b] == 1 ? &tm_a1 : &tm_a2), bar, kb * BK,
+                                      box_row[b]);
+            sm100::tma_load_3d_pair(sb, &tm_b, bar, kb * BK, b_row, grp.slot);
+          }
+          if (++stage == TL::STAGES) {
             stage = 0;
             phase ^= 1;
           }
@@ -224,39 +258,38 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ===== MMA issuer =====
-      constexpr uint32_t idesc = sm100::make_idesc_bf16_f32(BM, BN);
+    if (lane == 0 && cta_rank == 0) {
+      // ===== MMA issuer (the leader CTA of a pair issues for both) =====
+      constexpr uint32_t idesc = sm100::make_idesc_bf16_f32(TL::TILE_M, BN);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int i = 0;; ++i) {
-        sm100::mbar_wait(&ring_full[i % TILE_RING], (i / TILE_RING) & 1);
-        const int t = ring_tile[i % TILE_RING];
-        sm100::mbar_arrive(&ring_empty[i % TILE_RING]);
-        if (t < 0) break;
+      for (int t = tile0; t < total_tiles; t += tile_step) {
         sm100::mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         sm100::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = 0; kb < k_blocks; ++kb) {
           sm100::mbar_wait(&full_bar[stage], phase);
           sm100::tc_fence_after();
-          const uint32_t sa = sm100::smem_u32(stage_base + stage * STAGE_BYTES);
-          const uint32_t sb = sa + A_BYTES;
+          const uint32_t sa = sm100::smem_u32(stage_base + stage * TL::STAGE_BYTES);
+          const uint32_t sb = sa + TL::A_BYTES;
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
             uint64_t adesc = sm100::make_desc_k_sw128(sa + k * 32);
             uint64_t bdesc = sm100::make_desc_k_sw128(sb + k * 32);
-            sm100::mma_bf16_ss(d_tmem, adesc, bdesc, idesc, (kb | k) != 0);
+            if constexpr (CG == 1) sm100::mma_bf16_ss(d_tmem, adesc, bdesc, idesc, (kb | k) != 0);
+            else sm100::mma_bf16_ss_pair(d_tmem, adesc, bdesc, idesc, (kb | k) != 0);
           }
-          sm100::mma_commit(&empty_bar[stage]);
-          if (++stage == STAGES) {
+          if constexpr (CG == 1) sm100::mma_commit(&empty_bar[stage]);
+          else sm100::mma_commit_pair(&empty_bar[stage], 0x3);  // frees the stage in both CTAs
+          if (++stage == TL::STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        sm100::mma_commit(&tfull_bar[acc]);
+        if constexpr (CG == 1) sm100::mma_commit(&tfull_bar[acc]);
+        else sm100::mma_commit_pair(&tfull_bar[acc], 0x3);
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -264,19 +297,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else if (warp >= EPI_WARP0) {
-    // ===== epilogue =====
+    // ===== epilogue (each CTA drains its own 128 TMEM lanes) =====
     const uint32_t quarter = warp & 3;
+    const uint32_t tempty_leader = CG == 2 ? sm100::mapa_shared(sm100::smem_u32(&tempty_bar[0]), 0) : 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int i = 0;; ++i) {
-      sm100::mbar_wait(&ring_full[i % TILE_RING], (i / TILE_RING) & 1);
-      const int t = ring_tile[i % TILE_RING];
-      __syncwarp();
-      if (lane == 0) sm100::mbar_arrive(&ring_empty[i % TILE_RING]);
-      if (t < 0) break;
-      TileCoord c = decode_tile(t, tile_start, args.num_groups, args.groups, args.n_blocks);
+    for (int t = tile0; t < total_tiles; t += tile_step) {
+      TileCoord c = decode_tile<CG>(t, tile_start, args.num_groups, args.groups);
       const coe_mlp_group grp = args.groups[c.g];
-      const int row = c.m_blk * BM + quarter * 32 + lane;
+      const int row = c.m_blk * TL::TILE_M + (int)cta_rank * BM + quarter * 32 + lane;
       const bool valid = row < grp.rows;
       __nv_bfloat16 *out_row = nullptr;
       if (valid) {
@@ -323,7 +352,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
       }
       sm100::tc_fence_before();
-      sm100::mbar_arrive(&tempty_bar[acc]);
+      if constexpr (CG == 1) {
+        sm100::mbar_arrive(&tempty_bar[acc]);
+      } else {
+        __syncwarp();
+        if (lane == 0) sm100::mbar_arrive_cluster(tempty_leader + acc * 8);  // the leader's tempty[acc]
+      }
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
@@ -332,19 +366,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
 
   sm100::tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) sm100::cluster_sync();  // no CTA leaves while its peer may still signal it
+  else __syncthreads();
   if (warp == 2) {
     sm100::tc_fence_after();
-    sm100::tmem_dealloc<TMEM_COLS>(tmem_base);
-  }
-  if (threadIdx.x == 0 && args.tile_counter) {
-    // every claim of this CTA precedes its arrival here; the last CTA out re-arms the
-    // counter for the next launch on this stream (launches on a stream are ordered)
-    if (atomicAdd(&args.tile_counter[1], 1) == (int)gridDim.x - 1) {
-      args.tile_counter[0] = 0;
-      args.tile_counter[1] = 0;
-      __threadfence();
-    }
+    sm100::tmem_dealloc<TMEM_COLS, CG>(tmem_base);
   }
 }
 
@@ -381,12 +407,13 @@ bool make_map_2d(CUtensorMap *map, void *base, uint64_t rows, uint64_t cols, uin
 }
 
 // 3-D bf16 map over expert slots: [slots][rows][cols], slot stride in bytes.
-bool make_map_3d(CUtensorMap *map, void *base, uint64_t slots, uint64_t rows, uint64_t cols, uint64_t slot_stride) {
+bool make_map_3d(CUtensorMap *map, void *base, uint64_t slots, uint64_t rows, uint64_t cols, uint64_t slot_stride,
+                 uint32_t box_rows) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[3] = {cols, rows, slots};
   cuuint64_t strides[2] = {cols * 2, slot_stride};
-  cuuint32_t box[3] = {BK, BN, 1};
+  cuuint32_t box[3] = {BK, box_rows, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -400,12 +427,10 @@ struct coe_mlp {
   CUtensorMap xmap, act0, act1, hmap, w1, w2;
   int num_sms;
   int a_box_rows;
-  int32_t *tile_counter = nullptr;  // device [2]; one per instance = one per stream
+  int cg = 2;                        // CTAs per MMA (COE_K3_CG=1 selects the single-CTA kernel)
   const int8_t *hop_dst = nullptr;   // fused hops (coe_mlp_set_hops)
   int hop_stride = 0;
   __nv_bfloat16 *peer_act[COE_MAX_PEERS][2] = {};
-  bool dynamic = false;             // COE_K3_DYNAMIC=1: atomic tile claims instead of the static
-                                    // round-robin (measured 3 % slower on full-GPU waves, r1)
 };
 
 extern "C" {
@@ -425,7 +450,7 @@ int coe_mlp_create(const coe_mlp_config *cfg, coe_mlp **out) {
   }
   auto *m = new coe_mlp();
   m->cfg = *cfg;
-  m->dynamic = getenv("COE_K3_DYNAMIC") && atoi(getenv("COE_K3_DYNAMIC")) != 0;
+  if (const char *v = getenv("COE_K3_CG")) m->cg = atoi(v) == 1 ? 1 : 2;
   m->a_box_rows = cfg->T < BM ? cfg->T : BM;
   bool ok = true;
   const uint64_t ld = cfg->act_ld > 0 ? (uint64_t)cfg->act_ld : (uint64_t)cfg->d;
@@ -434,9 +459,11 @@ int coe_mlp_create(const coe_mlp_config *cfg, coe_mlp **out) {
   ok &= make_map_2d(&m->act1, cfg->act1, (uint64_t)cfg->act_rows, cfg->d, m->a_box_rows, ld);
   ok &= make_map_2d(&m->hmap, cfg->h_scratch, (uint64_t)cfg->h_rows, cfg->h, BM);
   // slot layout: [W1: h x d][W2: d x h]
-  ok &= make_map_3d(&m->w1, cfg->slab, cfg->num_slots, cfg->h, cfg->d, cfg->slot_stride_bytes);
+  // B box: the whole 256-column n-block (1 CTA) or each pair CTA's half of it
+  const uint32_t b_rows = (uint32_t)(BN / m->cg);
+  ok &= make_map_3d(&m->w1, cfg->slab, cfg->num_slots, cfg->h, cfg->d, cfg->slot_stride_bytes, b_rows);
   ok &= make_map_3d(&m->w2, (char *)cfg->slab + (size_t)cfg->h * cfg->d * 2, cfg->num_slots, cfg->d, cfg->h,
-                    cfg->slot_stride_bytes);
+                    cfg->slot_stride_bytes, b_rows);
   if (!ok) {
     delete m;
     coe_set_error("cuTensorMapEncodeTiled failed (alignment / driver entry point)");
@@ -445,11 +472,11 @@ int coe_mlp_create(const coe_mlp_config *cfg, coe_mlp **out) {
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&m->num_sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaError_t e = cudaFuncSetAttribute(grouped_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-  if (e == cudaSuccess) e = cudaMalloc(&m->tile_counter, 2 * sizeof(int32_t));
-  if (e == cudaSuccess) e = cudaMemset(m->tile_counter, 0, 2 * sizeof(int32_t));
+  cudaError_t e = m->cg == 1 ? cudaFuncSetAttribute(grouped_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                     Tiling<1>::SMEM)
+                              : cudaFuncSetAttribute(grouped_gemm_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                     Tiling<2>::SMEM);
   if (e != cudaSuccess) {
-    if (m->tile_counter) cudaFree(m->tile_counter);
     delete m;
     coe_set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
     return COE_CUDA_ERR_CUDA;
@@ -458,11 +485,7 @@ int coe_mlp_create(const coe_mlp_config *cfg, coe_mlp **out) {
   return COE_CUDA_OK;
 }
 
-void coe_mlp_destroy(coe_mlp *m) {
-  if (!m) return;
-  if (m->tile_counter) cudaFree(m->tile_counter);
-  delete m;
-}
+void coe_mlp_destroy(coe_mlp *m) { delete m; }
 
 int coe_mlp_max_groups(void) { return MAX_GROUPS; }
 
@@ -507,18 +530,35 @@ int coe_grouped_mlp(coe_mlp *m, const coe_mlp_group *groups_up, const coe_mlp_gr
     a.out_h = reinterpret_cast<__nv_bfloat16 *>(c.h_scratch);
     a.out_act0 = reinterpret_cast<__nv_bfloat16 *>(c.act0);
     a.out_act1 = reinterpret_cast<__nv_bfloat16 *>(c.act1);
-    a.tile_counter = m->dynamic ? m->tile_counter : nullptr;
     a.hop_dst = pass == 1 ? m->hop_dst : nullptr;
     a.hop_stride = m->hop_stride;
     std::memcpy(a.peer_act, m->peer_act, sizeof(a.peer_act));
     if (a.total_tiles <= 0) continue;
     int cap = (max_ctas > 0 && max_ctas < m->num_sms) ? max_ctas : m->num_sms;
-    int grid = a.total_tiles < cap ? a.total_tiles : cap;
-    if (pass == 0)
-      grouped_gemm_kernel<<<grid, NUM_THREADS, SMEM_BYTES, stream>>>(m->xmap, m->act0, m->act1, m->w1, a);
-    else
-      grouped_gemm_kernel<<<grid, NUM_THREADS, SMEM_BYTES, stream>>>(m->hmap, m->hmap, m->hmap, m->w2, a);
-    cudaError_t e = cudaGetLastError();
+    const CUtensorMap &ta0 = pass == 0 ? m->xmap : m->hmap, &ta1 = pass == 0 ? m->act0 : m->hmap,
+                      &ta2 = pass == 0 ? m->act1 : m->hmap, &tb = pass == 0 ? m->w1 : m->w2;
+    cudaError_t e;
+    if (m->cg == 1) {
+      const int grid = a.total_tiles < cap ? a.total_tiles : cap;
+      grouped_gemm_kernel<1><<<grid, NUM_THREADS, Tiling<1>::SMEM, stream>>>(ta0, ta1, ta2, tb, a);
+      e = cudaGetLastError();
+    } else {
+      // pairs: at most one per 128-row tile (the kernel recounts 256-row pair tiles itself)
+      const int pairs = std::max(1, std::min(cap / 2, a.total_tiles));
+      cudaLaunchConfig_t lc{};
+      lc.gridDim = dim3(2 * pairs);
+      lc.blockDim = dim3(NUM_THREADS);
+      lc.dynamicSmemBytes = Tiling<2>::SMEM;
+      lc.stream = stream;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = 2;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      lc.attrs = attr;
+      lc.numAttrs = 1;
+      e = cudaLaunchKernelEx(&lc, grouped_gemm_kernel<2>, ta0, ta1, ta2, tb, a);
+    }
     if (e != cudaSuccess) {
       coe_set_error(std::string("grouped_gemm_kernel launch: ") + cudaGetErrorString(e));
       return COE_CUDA_ERR_CUDA;

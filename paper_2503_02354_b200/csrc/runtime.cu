@@ -139,12 +139,10 @@ bool write_flag(cudaStream_t s, int32_t *addr, uint32_t value) {
 }
 constexpr int HOP_STRIDE = 8;  // hop_dst row per request: one entry per chain stage (<= 8 stages)
 
-// Release-wave grid: the reserved SMs (static K3 tiles); with COE_K3_DYNAMIC=1 the whole GPU,
-// its CTAs claiming tiles as the main stream's kernels hand SMs back.  COE_RELEASE_CTAS overrides.
-int release_grid(int reserved, int sms) {
-  if (const char *v = getenv("COE_RELEASE_CTAS")) return std::max(1, atoi(v));
-  const bool dyn = getenv("COE_K3_DYNAMIC") && atoi(getenv("COE_K3_DYNAMIC")) != 0;
-  return dyn ? sms : reserved;
+// Release-wave grid: the reserved SMs (COE_RELEASE_CTAS overrides, for experiments).
+int release_grid(int reserved, int /*sms*/) {
+  if (const char *v = getenv("COE_RELEASE_CTAS")) return std::max(2, atoi(v) & ~1);
+  return reserved;
 }
 
 // Many row copies as one cudaMemcpyBatchAsync (CUDA 12.8+): the e2e path moves one
@@ -252,6 +250,7 @@ struct coe_runtime {
   std::vector<coe_peer_buffers> peers;  // every executor's buffers as mapped in this process
   std::vector<void *> ipc_opened;
   int32_t peer_rank = -1, peer_world = 0;
+  coe_local_hub *peer_hub = nullptr;  // same-process peers: host-side event handoff, no flags
   uint32_t step_seq = 0;
   int8_t *d_hopdst[2] = {nullptr, nullptr};  // per step set: [max_requests][HOP_STRIDE]
   int8_t *h_hopdst[2] = {nullptr, nullptr};
@@ -743,12 +742,13 @@ int coe_runtime_ipc_open(coe_runtime *rt, const void *handles, coe_peer_buffers 
   return COE_CUDA_OK;
 }
 
-int coe_runtime_attach_peers(coe_runtime *rt, int32_t rank, int32_t world, const coe_peer_buffers *peers) {
+int coe_runtime_attach_peers(coe_runtime *rt, int32_t rank, int32_t world, const coe_peer_buffers *peers,
+                             coe_local_hub *hub) {
   if (world < 1 || world > COE_MAX_PEERS || rank < 0 || rank >= world) {
     coe_set_error("attach_peers: world must be 1..COE_MAX_PEERS and rank inside it");
     return COE_CUDA_ERR_CONFIG;
   }
-  if (!stream_memops()) {
+  if (!hub && !stream_memops()) {
     coe_set_error("attach_peers: cuStreamWaitValue32 / cuStreamWriteValue32 unavailable");
     return COE_CUDA_ERR_CUDA;
   }
@@ -760,6 +760,7 @@ int coe_runtime_attach_peers(coe_runtime *rt, int32_t rank, int32_t world, const
       return fail_cuda();
   }
   rt->peers.assign(peers, peers + world);
+  rt->peer_hub = hub;
   rt->peer_rank = rank;
   rt->peer_world = world;
   return COE_CUDA_OK;
@@ -1120,6 +1121,9 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
   for (int32_t i = 0; i < (int32_t)n_batches; ++i) (batches[i].cls ? rel_order : main_pending).push_back(i);
   size_t next_rel = 0, next_copy = 0, send_ptr = 0;
   double t_copy = 0.0, t_stream[NCLS] = {0.0, 0.0, 0.0};
+  // two main streams measured faster than one (r1: C1 -5 %, C3 -3 %, C2 even)
+  const int main_streams = getenv("COE_MAIN_STREAMS") ? atoi(getenv("COE_MAIN_STREAMS")) : 2;
+  int main_flip = 0;
   std::vector<WaveAct> waves;
   std::vector<Action> actions;
   std::vector<coe_mlp_group> g_up, g_down;
@@ -1192,7 +1196,7 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     }
     const double end = start + wave_time(w.rows, cls, w.shape);
     for (int32_t bi : members) batches[bi].done = end;
-    t_stream[cls] = end;
+    t_stream[cls == 2 ? 0 : cls] = end;  // streams 0 and 2 share the main clock
     st.max_wave_groups = std::max(st.max_wave_groups, w.num_groups);
     st.max_wave_rows = std::max(st.max_wave_rows, w.rows);
     waves.push_back(std::move(w));
@@ -1315,7 +1319,9 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
         coe_set_error("internal: empty main wave");
         return COE_CUDA_ERR_CHECK;
       }
-      emit_wave(members, 0, m_start);
+      // main waves alternate between two streams (0, 2) when enabled: the next wave's up
+      // pass fills the SMs the previous wave's down pass leaves idle in its tail
+      emit_wave(members, (main_streams == 2 && (main_flip ^= 1) == 0) ? 2 : 0, m_start);
       std::sort(taken.begin(), taken.end());
       for (size_t t = taken.size(); t-- > 0;) main_pending.erase(main_pending.begin() + (std::ptrdiff_t)taken[t]);
     }
@@ -1457,7 +1463,9 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
                                        (size_t)c.max_requests * HOP_STRIDE, cudaMemcpyHostToDevice, ks),
                        "hop dst H2D"))
     return fail_cuda();
-  if (peer_mode)  // step fence: every peer has finished the previous step (its P rows are free)
+  // step fence: every peer has finished the previous step (its P rows are free).  Same-process
+  // peers (hub) are stepped and synchronised together (runtime.step_executors): no fence.
+  if (peer_mode && !rt->peer_hub)
     for (int r = 0; r < rt->peer_world; ++r)
       if (r != x && !wait_flag(cs, rt->d_hflags + rt->hflag_step_base + r, seq - 1)) return COE_CUDA_ERR_CUDA;
   if (!ok(cudaEventRecord(rt->staging_done[set_idx], ks), "record") || !ok(cudaEventRecord(rt->staged, ks), "record") ||
@@ -1577,8 +1585,11 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     cudaStream_t ws = rt->cls_stream[w.cls];
     coe_mlp *m = rt->mlps[w.shape][w.cls];
     if (peer_mode) {
-      for (int32_t hslot : w.wait_recvs)
-        if (!wait_flag(ws, rt->d_hflags + all_hops[my_hops[hslot]].index, seq)) return COE_CUDA_ERR_CUDA;
+      for (int32_t hslot : w.wait_recvs) {
+        const int64_t hi = all_hops[my_hops[hslot]].index;
+        if (rt->peer_hub ? !coe_hub_wait(rt->peer_hub, hi, ws) : !wait_flag(ws, rt->d_hflags + hi, seq))
+          return COE_CUDA_ERR_CUDA;
+      }
     } else if (!w.wait_recvs.empty()) {
       int64_t limit = -1;
       for (int32_t hslot : w.wait_recvs) limit = std::max<int64_t>(limit, all_hops[my_hops[hslot]].index);
@@ -1616,7 +1627,9 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
       for (int32_t gi = w.first_group; gi < w.first_group + w.num_groups; ++gi)
         for (int32_t hslot : batches[g_up[gi].batch].sends) {
           const coe::Hop &h = all_hops[my_hops[hslot]];
-          if (!write_flag(ws, static_cast<int32_t *>(rt->peers[h.dst].flags) + h.index, seq)) return COE_CUDA_ERR_CUDA;
+          if (rt->peer_hub ? !coe_hub_publish(rt->peer_hub, h.index, ws)
+                           : !write_flag(ws, static_cast<int32_t *>(rt->peers[h.dst].flags) + h.index, seq))
+            return COE_CUDA_ERR_CUDA;
         }
     for (int32_t sk : w.frees_slots) {
       if (!ok(cudaEventRecord(rt->slot_free_down[sk], ws), "record")) return fail_cuda();
@@ -1666,7 +1679,7 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     if (!ok(cudaEventRecord(rt->cls_drained[k], rt->cls_stream[k]), "record") ||
         !ok(cudaStreamWaitEvent(cs, rt->cls_drained[k], 0), "join"))
       return fail_cuda();
-  if (peer_mode)  // this step is done here: tell every peer (their next step's fence)
+  if (peer_mode && !rt->peer_hub)  // this step is done here: tell every peer (their next step's fence)
     for (int r = 0; r < rt->peer_world; ++r)
       if (r != x &&
           !write_flag(cs, static_cast<int32_t *>(rt->peers[r].flags) + rt->hflag_step_base + x, seq))

@@ -135,7 +135,7 @@ def _lib():
         lib.coe_runtime_ipc_export.restype = ctypes.c_int
         lib.coe_runtime_ipc_open.argtypes = [V, V, P(PeerBuffers)]
         lib.coe_runtime_ipc_open.restype = ctypes.c_int
-        lib.coe_runtime_attach_peers.argtypes = [V, I32, I32, V]
+        lib.coe_runtime_attach_peers.argtypes = [V, I32, I32, V, V]
         lib.coe_runtime_attach_peers.restype = ctypes.c_int
         lib.coe_expert_seed.argtypes = [ctypes.c_uint64, I32, I32]
         lib.coe_expert_seed.restype = ctypes.c_uint64
@@ -298,9 +298,11 @@ class B200Runtime:
         _check(self.lib, self.lib.coe_runtime_peer_buffers(self.handle, ctypes.byref(pb)), "peer buffers")
         return pb
 
-    def _attach_peers(self, rank: int, peers: list) -> None:
+    def _attach_peers(self, rank: int, peers: list, hub: "LocalHub | None" = None) -> None:
         arr = (PeerBuffers * len(peers))(*peers)
-        _check(self.lib, self.lib.coe_runtime_attach_peers(self.handle, rank, len(peers), arr), "attach peers")
+        self._peer_hub = hub  # keep the hub alive as long as the runtime uses it
+        _check(self.lib, self.lib.coe_runtime_attach_peers(self.handle, rank, len(peers), arr,
+                                                           hub.handle if hub is not None else None), "attach peers")
 
     def attach_peers_ipc(self, rank: int, world: int) -> None:
         """Fused hops across processes (one executor per rank, normally one GPU each): every
@@ -438,12 +440,15 @@ class LocalHub:
             pass
 
 
-def attach_peers_local(runtimes: list) -> None:
-    """Fused hops between runtimes of ONE process (several executors on one GPU): each maps
-    the others' buffers directly."""
+def attach_peers_local(runtimes: list) -> "LocalHub":
+    """Fused hops between runtimes of ONE process (several executors on one GPU): each stores
+    straight into the others' buffers; readiness is handed over through a LocalHub (pass it
+    to step_executors, which resets it between steps)."""
+    hub = LocalHub(len(runtimes))
     peers = [rt.peer_buffers() for rt in runtimes]
     for x, rt in enumerate(runtimes):
-        rt._attach_peers(x, peers)
+        rt._attach_peers(x, peers, hub)
+    return hub
 
 
 def step_executors(plan, runtimes: list, hub: "LocalHub | None" = None) -> list:

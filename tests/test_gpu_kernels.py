@@ -212,11 +212,16 @@ SPEC = [([(0, 0)], 0), ([(1, 0), (2, 1), (3, 2)], 1), ([(4, 1), (5, 3)], 2), ([(
         ([(7 + i, i % 4) for i in range(9)], 0)]
 
 
+@pytest.mark.parametrize("cg", [2, 1])
 @pytest.mark.parametrize("d, h, T", [(1024, 2048, 128), (1024, 4096, 64), (2048, 1024, 256), (512, 768, 32)])
-def test_grouped_mlp_matches_torch_fp32(lib, d, h, T):
+def test_grouped_mlp_matches_torch_fp32(lib, d, h, T, cg, monkeypatch):
+    """cg 2: the CTA-pair kernel (tcgen05.mma.cta_group::2, 256 x 256 tiles); cg 1: one CTA."""
+    monkeypatch.setenv("COE_K3_CG", str(cg))
     assert _mlp_case(lib, d, h, T, SPEC) <= 1e-2
 
 
-def test_grouped_mlp_single_row_block_and_many_groups(lib):
+@pytest.mark.parametrize("cg", [2, 1])
+def test_grouped_mlp_single_row_block_and_many_groups(lib, cg, monkeypatch):
+    monkeypatch.setenv("COE_K3_CG", str(cg))
     spec = [([(i, i % 2)], i % 3) for i in range(40)]
     assert _mlp_case(lib, 1024, 1024, 64, spec) <= 1e-2

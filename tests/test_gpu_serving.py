@@ -223,7 +223,7 @@ def test_multi_executor_hops_on_one_gpu(executors, transport):
         rt.fill_inputs(len(plan.resolved.request_ids))
         rts.append(rt)
     if hub is None:
-        runtime.attach_peers_local(rts)
+        hub = runtime.attach_peers_local(rts)
     n = len(plan.resolved.request_ids)
     chains = plan.resolved.chains
     final_exec = {}
