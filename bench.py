@@ -340,12 +340,13 @@ def main() -> None:
     # its K3 launch intervals (CUDA events on the launching streams), against the sustained peak
     achieved = flops / (timing["k3_busy_ms"] / 1e3) / 1e12 if timing["k3_busy_ms"] > 0 else None
     peak = sustained
-    traffic = None
+    traffic = traffic_algo = None
     ncu_path = os.path.join(ROOT, "profiles", "k3_ncu_summary.json")
     if os.path.exists(ncu_path):
         with open(ncu_path) as fh:
             ncu = json.load(fh)
-        traffic = ncu.get("dram_bytes_per_wave")
+        traffic = ncu.get("dram_bytes_per_launch")  # the profiled wave's average up/down launch
+        traffic_algo = ncu.get("algorithmic_bytes_per_launch")
     load_bytes = stats["load_bytes"] + stats["restore_bytes"]
     copy_s = timing["copy_busy_ms"] / 1e3
     short = min(timing["copy_busy_ms"], timing["compute_busy_ms"])
@@ -371,6 +372,9 @@ def main() -> None:
                      "frac": achieved / peak if (peak and achieved) else None,
                      "peak_source": f"{peak_src} bf16_tflops_sustained (K3 timed inside the serving step)",
                      "traffic": traffic,
+                     "traffic_note": "dram__bytes_read+write per launch from profiles/k3_ncu_summary.json (ncu --set "
+                                     "full of the isolated wave below); algorithmic bytes per launch "
+                                     f"{traffic_algo}",
                      "measured_over": {"k3_launches_per_step": timing["k3_launches"],
                                        "algorithmic_flops_per_step": flops,
                                        "flops_per_launch": flops / max(1, timing["k3_launches"]),

@@ -69,6 +69,33 @@ def full():
     return out
 
 
+def grouping():
+    """K1/K2 (make_keys, radix passes, scan, compaction) from gpurun_out/k12_full.ncu-rep."""
+    path = os.path.join(OUT, "k12_full.ncu-rep")
+    if not os.path.exists(path):
+        return None
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units, data = rows[0], rows[1], rows[2:]
+    ki = hdr.index("Kernel Name")
+    unit_scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ms": 1, "msecond": 1, "us": 1e-3,
+                  "usecond": 1e-3, "ns": 1e-6, "nsecond": 1e-6}
+
+    def val(r, m):
+        i = hdr.index(m)
+        return float(r[i].replace(",", "")) * unit_scale.get(units[i], 1)
+
+    out = []
+    for r in data:
+        dur = val(r, "gpu__time_duration.sum")
+        byts = val(r, "dram__bytes_read.sum") + val(r, "dram__bytes_write.sum")
+        out.append({"kernel": r[ki].split("(")[0].replace("<unnamed>::", ""), "duration_us": dur * 1e3,
+                    "dram_bytes": byts, "dram_gbs": byts / (dur * 1e-3) / 1e9 if dur > 0 else None,
+                    "dram_throughput_pct": val(r, "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
+                    "grid": val(r, "launch__grid_size")})
+    return out
+
+
 res = launches()
 if res:
     text, table = res
@@ -76,11 +103,26 @@ if res:
     print(text)
 kf = full()
 if kf:
-    k3 = {"launches": kf, "note": "ncu --set full --clock-control none, tools/k3_profile.py 16 8: one wave of 16 "
-                                  "batches x 8 requests x T=256 (32768 rows), d=4096 h=12288; launch 0 = up "
-                                  "projection (gelu), launch 1 = down projection",
-          "flops_per_launch": 2.0 * 32768 * 4096 * 12288}
+    G, R, T, d, h = 16, 6, 256, 4096, 12288  # tools/profile_round.sh: k3_profile.py 16 6 (the bench's wave)
+    rows = G * R * T
+    k3 = {"launches": kf, "note": f"ncu --set full --clock-control none, tools/k3_profile.py {G} {R}: one wave of "
+                                  f"{G} batches x {R} requests x T={T} ({rows} rows), d={d} h={h} (the bench's "
+                                  "isolated wave); launch 0 = up projection (gelu), launch 1 = down projection; "
+                                  "CTA-pair kernel (tcgen05.mma.cta_group::2)",
+          "flops_per_launch": 2.0 * rows * d * h}
     k3["dram_bytes_per_wave"] = sum(l["dram_read"] + l["dram_write"] for l in kf)
-    k3["algorithmic_bytes_per_wave"] = 2 * (16 * 4096 * 12288 * 2) + 2 * (32768 * 4096 * 2) + 2 * (32768 * 12288 * 2)
+    k3["dram_bytes_per_launch"] = k3["dram_bytes_per_wave"] / len(kf)
+    # weights once + activations in/out, per projection: up reads X (rows x d) writes H (rows x h)
+    k3["algorithmic_bytes_per_wave"] = 2 * (G * d * h * 2) + 2 * (rows * d * 2) + 2 * (rows * h * 2)
+    k3["algorithmic_bytes_per_launch"] = k3["algorithmic_bytes_per_wave"] / 2
     json.dump(k3, open(os.path.join(PROF, f"k3_ncu_summary.json"), "w"), indent=1)
     print(json.dumps(k3, indent=1))
+
+kg = grouping()
+if kg:
+    summ = {"launches": kg, "note": "ncu --set full, one bench step of C3 (13,642 admissions): K1 make_keys + "
+                                    "8-bit LSD radix passes (hist / scan / scatter), K2 compaction. Latency-bound: "
+                                    "~218 KB of algorithmic traffic per step (16 B per admission)",
+            "total_us": sum(k["duration_us"] for k in kg), "total_dram_bytes": sum(k["dram_bytes"] for k in kg)}
+    json.dump(summ, open(os.path.join(PROF, f"{tag}_k12_ncu_summary.json"), "w"), indent=1)
+    print(json.dumps(summ, indent=1))
