@@ -227,6 +227,9 @@ int coe_runtime_attach_peers(coe_runtime *rt, int32_t rank, int32_t world, const
 /* profile mode: per wave [up start, up end, down start, down end] ms since step start and
  * the wave's algorithmic FLOPs (4 * rows * d * h) */
 int coe_runtime_wave_phases(coe_runtime *rt, float *phase_iv, double *wave_flops);
+/* profile mode, e2e steps: [start, end] ms of each stage-0 input upload (copy engine) then of
+ * each output download (output stream); iv == NULL queries the counts only */
+int coe_runtime_io_intervals(coe_runtime *rt, float *iv, int32_t *n_in, int32_t *n_out);
 /* device pointers (tests / benches): 0 X, 1 P0, 2 P1, 3 H scratch, 4 slot slab */
 void *coe_runtime_buffer(coe_runtime *rt, int which);
 /* synchronous device -> host copy of the first `bytes` of buffer `which` */

@@ -95,8 +95,9 @@ struct WaveAct {
 };
 
 struct Action {
-  bool is_copy;
+  bool is_copy;      // swap-in (index: copy) ...
   int32_t index;
+  bool is_input = false;  // ... or an e2e stage-0 input upload (index: batch), same copy engine
 };
 
 bool ok(cudaError_t e, const char *what) { return coe_cuda_ok(e, what); }
@@ -224,6 +225,8 @@ struct coe_runtime {
   // events
   std::vector<cudaEvent_t> wave_up_ev, wave_down_ev, copy_up_ev, copy_down_ev;
   std::vector<cudaEvent_t> t_copy_start, t_copy_end, t_wave_start, t_wave_end, t_up_end, t_down_start;
+  std::vector<cudaEvent_t> t_io;    // profile, e2e: [start, end] event pairs of uploads / downloads
+  std::vector<uint8_t> io_kind;      // per pair: 0 input upload, 1 output download
   std::vector<double> last_wave_flops;  // algorithmic 4*rows*d*h per wave
   cudaEvent_t staged = nullptr, copy_drained = nullptr, grouped = nullptr;
   cudaEvent_t cls_drained[NCLS] = {nullptr, nullptr, nullptr};
@@ -290,7 +293,7 @@ struct coe_runtime {
       cudaFreeHost(host_store);
     }
     for (auto *v : {&in_ev, &recv_ev, &slot_free_up, &slot_free_down, &wave_up_ev, &wave_down_ev, &copy_up_ev, &copy_down_ev,
-                    &t_copy_start, &t_copy_end, &t_wave_start, &t_wave_end, &t_up_end, &t_down_start}) {
+                    &t_copy_start, &t_copy_end, &t_wave_start, &t_wave_end, &t_up_end, &t_down_start, &t_io}) {
       for (auto e : *v) cudaEventDestroy(e);
       v->clear();
     }
@@ -859,6 +862,24 @@ int coe_runtime_wave_phases(coe_runtime *rt, float *phase_iv, double *wave_flops
   return COE_CUDA_OK;
 }
 
+int coe_runtime_io_intervals(coe_runtime *rt, float *iv, int32_t *n_in, int32_t *n_out) {
+  if (!rt->cfg.profile) {
+    coe_set_error("runtime created without profile events");
+    return COE_CUDA_ERR_CONFIG;
+  }
+  *n_in = *n_out = 0;
+  for (uint8_t k : rt->io_kind) (k ? *n_out : *n_in) += 1;
+  if (iv) {  // input pairs first, then output pairs
+    int32_t wi = 0, wo = 2 * *n_in;
+    for (size_t p = 0; p < rt->io_kind.size(); ++p) {
+      int32_t &w = rt->io_kind[p] ? wo : wi;
+      iv[w++] = elapsed(rt->t_step_start, rt->t_io[2 * p]);
+      iv[w++] = elapsed(rt->t_step_start, rt->t_io[2 * p + 1]);
+    }
+  }
+  return COE_CUDA_OK;
+}
+
 int coe_runtime_counts(coe_runtime *rt, int32_t *copies, int32_t *waves) {
   *copies = rt->last_copies;
   *waves = rt->last_waves;
@@ -891,7 +912,7 @@ struct BatchInfo {
   double done = 0.0;               // estimated completion
   std::vector<int32_t> inputs;     // e2e: stage-0 requests whose inputs this batch uploads
   std::vector<int32_t> finals;     // e2e: requests whose final output this batch produces
-  int32_t input_event = -1;
+  int32_t input_event = -1;        // e2e: the input chunk this batch needs last (its event)
 };
 
 struct CopyInfo {
@@ -901,6 +922,7 @@ struct CopyInfo {
   bool first_write;                // slot not written earlier this step
   double up_end = 0.0, end = 0.0;  // estimated
   bool issued = false;
+  int64_t op_pos = 0;              // op-log position of the LOAD (restores: of the first batch)
 };
 
 }  // namespace
@@ -1007,7 +1029,7 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     for (int64_t i = 0; i < in->num_admissions; ++i)
       final_stage[adm[i].request] = std::max(final_stage[adm[i].request], adm[i].stage);
   }
-  auto issue_copy = [&](int32_t e, bool restore) -> bool {
+  auto issue_copy = [&](int32_t e, bool restore, int64_t op_pos) -> bool {
     if (rt->store_off[e] < 0) {
       coe_set_error("swap-in of an expert that is not in the host store");
       return false;
@@ -1024,6 +1046,7 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
       return false;
     }
     CopyInfo ci{e, best, restore, slot_readers[best], !slot_written[best]};
+    ci.op_pos = op_pos;
     copies.push_back(ci);
     slot_readers[best].clear();
     slot_written[best] = 1;
@@ -1053,7 +1076,7 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
         rt->slot_expert[s] = -1;
         rt->expert_slot[op.expert] = -1;
       }
-      if (!issue_copy(op.expert, false)) return COE_CUDA_ERR_CHECK;
+      if (!issue_copy(op.expert, false, my_ops[k])) return COE_CUDA_ERR_CHECK;
       continue;
     }
     const int32_t e = op.expert;
@@ -1063,7 +1086,7 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
         return COE_CUDA_ERR_CHECK;
       }
       pending_restore[e] = 0;
-      if (!issue_copy(e, true)) return COE_CUDA_ERR_CHECK;
+      if (!issue_copy(e, true, my_ops[k])) return COE_CUDA_ERR_CHECK;
     }
     BatchInfo b;
     b.op_index = (int32_t)my_ops[k];
@@ -1137,7 +1160,30 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
       ++send_ptr;
     return send_ptr >= send_slots.size() || all_hops[my_hops[send_slots[send_ptr]]].index > hop_index;
   };
+  // e2e: stage-0 inputs move in request-ordered chunks of >= 32 MB (full-rate DMA); batch b
+  // needs chunks 0..b.input_event.  chunk_end < 0: not issued yet.
+  std::vector<int32_t> in_reqs;
+  for (const BatchInfo &b : batches) in_reqs.insert(in_reqs.end(), b.inputs.begin(), b.inputs.end());
+  std::sort(in_reqs.begin(), in_reqs.end());
+  const int64_t in_chunk = std::max<int64_t>(1, (32ll << 20) / std::max<int64_t>(1, rt->row_elems * 2));
+  const int32_t n_chunks = (int32_t)((in_reqs.size() + in_chunk - 1) / in_chunk);
+  std::vector<double> chunk_end(n_chunks, -1.0);
+  std::vector<int64_t> chunk_pos(n_chunks, INT64_MAX);  // op position of the first batch needing it
+  {
+    std::unordered_map<int32_t, int32_t> chunk_of;
+    for (size_t i = 0; i < in_reqs.size(); ++i) chunk_of[in_reqs[i]] = (int32_t)(i / in_chunk);
+    for (BatchInfo &b : batches) {
+      b.input_event = -1;
+      for (int32_t r : b.inputs) {
+        const int32_t k = chunk_of[r];
+        b.input_event = std::max(b.input_event, k);
+        chunk_pos[k] = std::min<int64_t>(chunk_pos[k], b.op_index);
+      }
+    }
+    for (int32_t k = n_chunks - 2; k >= 0; --k) chunk_pos[k] = std::min(chunk_pos[k], chunk_pos[k + 1]);
+  }
   auto issuable = [&](const BatchInfo &b) {
+    if (b.input_event >= 0 && chunk_end[b.input_event] < 0) return false;  // inputs not uploaded yet
     for (int32_t p : b.producers)
       if (!issued[p]) return false;
     if (b.copy >= 0 && !copies[b.copy].issued) return false;
@@ -1145,7 +1191,7 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     return true;
   };
   auto ready_time = [&](const BatchInfo &b) {
-    double t = 0.0;
+    double t = b.input_event >= 0 ? chunk_end[b.input_event] : 0.0;
     for (int32_t p : b.producers) t = std::max(t, batches[p].done);
     if (b.copy >= 0) t = std::max(t, copies[b.copy].up_end);
     return t;
@@ -1222,7 +1268,13 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
   // two copies into the same slot keep their order.
   const size_t kCopyWindow = 8;
   size_t copy_pick = 0;
-  while (next_copy < copies.size() || next_rel < rel_order.size() || !main_pending.empty()) {
+  // e2e: the stage-0 input uploads ride the same copy engine (one H2D queue): in op order with
+  // the swap-ins, and ahead of a swap-in whose victim slot is still being read -- the PCIe
+  // link, which both share, never idles while either has work
+  int32_t next_in = 0;
+  const double row_bytes = (double)rt->row_elems * 2;
+  while (next_copy < copies.size() || next_in < n_chunks || next_rel < rel_order.size() ||
+         !main_pending.empty()) {
     const double INF = 1e30;
     while (next_copy < copies.size() && copies[next_copy].issued) ++next_copy;
     // candidate: the earliest-startable swap-in in the window
@@ -1240,6 +1292,12 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
         copy_pick = k;
       }
     }
+    // candidate: the next input upload (always startable; op order against the swap-in)
+    bool take_input = false;
+    if (next_in < n_chunks) {
+      take_input = c_start == INF || t_copy < c_start || chunk_pos[next_in] < copies[copy_pick].op_pos;
+      if (take_input) c_start = t_copy;
+    }
     // candidate: next release wave (singleton, in order)
     double r_start = INF;
     if (next_rel < rel_order.size() && issuable(batches[rel_order[next_rel]]))
@@ -1255,7 +1313,13 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
       coe_set_error("internal: runtime list scheduler found no issuable action");
       return COE_CUDA_ERR_CHECK;
     }
-    if (c_start <= r_start && c_start <= m_start) {
+    if (take_input && c_start <= r_start && c_start <= m_start) {
+      const int64_t nreq_k = std::min<int64_t>(in_chunk, (int64_t)in_reqs.size() - (int64_t)next_in * in_chunk);
+      chunk_end[next_in] = c_start + (double)nreq_k * row_bytes / 55.0e9;
+      t_copy = chunk_end[next_in];
+      actions.push_back(Action{false, next_in, true});
+      ++next_in;
+    } else if (c_start <= r_start && c_start <= m_start) {
       CopyInfo &ci = copies[copy_pick];
       ci.issued = true;
       ci.up_end = c_start + copy_half_s(ci.expert);
@@ -1332,6 +1396,7 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     std::vector<int32_t> last_reader_wave(NS * NCLS, -1);
     std::vector<uint8_t> written(NS, 0);
     for (const Action &a : actions) {
+      if (a.is_input) continue;
       if (a.is_copy) {
         const CopyInfo &ci = copies[a.index];
         CopyAct &ca = copy_acts[a.index];
@@ -1362,7 +1427,8 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     if (FILE *f = fopen(dump, "w")) {
       fprintf(f, "{\"actions\": [");
       for (size_t i = 0; i < actions.size(); ++i)
-        fprintf(f, "%s[%d, %d]", i ? ", " : "", actions[i].is_copy ? 1 : 0, actions[i].index);
+        fprintf(f, "%s[%d, %d]", i ? ", " : "", actions[i].is_copy ? 1 : (actions[i].is_input ? 2 : 0),
+                actions[i].index);
       fprintf(f, "], \"copies\": [");
       for (size_t i = 0; i < copy_acts.size(); ++i) {
         fprintf(f, "%s{\"expert\": %d, \"slot\": %d, \"est_start\": %.6f, \"wait_waves\": [", i ? ", " : "",
@@ -1495,35 +1561,41 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     for (int k = 0; k < NCLS; ++k)
       if (!ok(cudaStreamWaitEvent(rt->cls_stream[k], rt->out_drained, 0), "P reuse waits downloads"))
         return fail_cuda();
-  if (e2e_in) {
-    int32_t n_in = 0;
-    for (const BatchInfo &b : batches) n_in += b.inputs.empty() ? 0 : 1;
-    if (!rt->ensure_events(rt->in_ev, (size_t)n_in, false)) return fail_cuda();
-    if (rt->have_step_end && !ok(cudaStreamWaitEvent(rt->in_stream, rt->step_end, 0), "X reuse waits step"))
-      return fail_cuda();
+  bool x_reuse_waited = false;
+  if (e2e_in && !rt->ensure_events(rt->in_ev, (size_t)n_chunks, false)) return fail_cuda();
+  // stage-0 rows of batch b, pinned host -> X, coalescing consecutive request rows
+  int32_t io_n = 0;  // profile events recorded this step
+  rt->io_kind.clear();
+  auto io_mark = [&](cudaStream_t s_) -> bool {
+    if (!c.profile) return true;
+    if (!rt->ensure_events(rt->t_io, (size_t)io_n + 1, true)) return false;
+    return ok(cudaEventRecord(rt->t_io[io_n++], s_), "record");
+  };
+  auto upload_inputs = [&](int32_t k) -> bool {
+    if (!x_reuse_waited) {  // X rows are free once last step's readers are done
+      x_reuse_waited = true;
+      if (rt->have_step_end && !ok(cudaStreamWaitEvent(ks, rt->step_end, 0), "X reuse waits step")) return false;
+    }
+    if (c.profile) rt->io_kind.push_back(0);
+    if (!io_mark(ks)) return false;
     const size_t rb = (size_t)rt->row_elems * 2;
     const char *hin = static_cast<const char *>(in->host_inputs);
-    int32_t ev = 0;
-    for (BatchInfo &b : batches) {
-      if (b.inputs.empty()) continue;
-      std::vector<int32_t> rq = b.inputs;
-      std::sort(rq.begin(), rq.end());
-      std::vector<void *> dsts, srcs;
-      std::vector<size_t> sizes;
-      for (size_t i = 0; i < rq.size();) {  // coalesce consecutive request rows
-        size_t j = i + 1;
-        while (j < rq.size() && rq[j] == rq[j - 1] + 1) ++j;
-        dsts.push_back(reinterpret_cast<char *>(rt->x) + rq[i] * rb);
-        srcs.push_back(const_cast<char *>(hin) + rq[i] * rb);
-        sizes.push_back((j - i) * rb);
-        st.h2d_input_bytes += (int64_t)((j - i) * rb);
-        i = j;
-      }
-      if (!batched_copy(dsts, srcs, sizes, rt->in_stream, "input H2D")) return fail_cuda();
-      if (!ok(cudaEventRecord(rt->in_ev[ev], rt->in_stream), "record")) return fail_cuda();
-      b.input_event = ev++;
+    const size_t lo = (size_t)k * in_chunk, hi = std::min(in_reqs.size(), lo + (size_t)in_chunk);
+    std::vector<int32_t> rq(in_reqs.begin() + lo, in_reqs.begin() + hi);
+    std::vector<void *> dsts, srcs;
+    std::vector<size_t> sizes;
+    for (size_t i = 0; i < rq.size();) {
+      size_t j = i + 1;
+      while (j < rq.size() && rq[j] == rq[j - 1] + 1) ++j;
+      dsts.push_back(reinterpret_cast<char *>(rt->x) + rq[i] * rb);
+      srcs.push_back(const_cast<char *>(hin) + rq[i] * rb);
+      sizes.push_back((j - i) * rb);
+      st.h2d_input_bytes += (int64_t)((j - i) * rb);
+      i = j;
     }
-  }
+    return batched_copy(dsts, srcs, sizes, ks, "input H2D") && io_mark(ks) &&
+           ok(cudaEventRecord(rt->in_ev[k], ks), "record");
+  };
   size_t hop_cursor = 0;
   const size_t row_elems = (size_t)rt->row_elems;
   auto issue_hops_until = [&](int64_t limit) -> bool {
@@ -1553,6 +1625,10 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
 
   const coe_mlp_group *dg_up = sb.groups, *dg_down = sb.groups + n_batches;
   for (const Action &a : actions) {
+    if (a.is_input) {
+      if (!upload_inputs(a.index)) return fail_cuda();
+      continue;
+    }
     if (a.is_copy) {
       const CopyAct &cp = copy_acts[a.index];
       char *dst = rt->slot_ptr(cp.slot);
@@ -1655,7 +1731,10 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
           sizes.push_back(rb);
           st.d2h_output_bytes += (int64_t)rb;
         }
-        if (!batched_copy(dsts, srcs, sizes, rt->out_stream, "output D2H")) return fail_cuda();
+        if (c.profile) rt->io_kind.push_back(1);
+        if (!io_mark(rt->out_stream) || !batched_copy(dsts, srcs, sizes, rt->out_stream, "output D2H") ||
+            !io_mark(rt->out_stream))
+          return fail_cuda();
       }
     }
   }
@@ -1701,6 +1780,7 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     rt->last_wave_flops.push_back(4.0 * (double)w.rows * rt->sd[w.shape] * rt->sh[w.shape]);
   }
   rt->last_copies = (int32_t)nc;
+
   rt->last_adm = n_adm;
   rt->last_batches = n_batches;
   rt->last_set = set_idx;

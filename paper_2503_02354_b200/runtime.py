@@ -123,6 +123,8 @@ def _lib():
         lib.coe_runtime_counts.restype = ctypes.c_int
         lib.coe_runtime_intervals.argtypes = [V, V, V, V]
         lib.coe_runtime_intervals.restype = ctypes.c_int
+        lib.coe_runtime_io_intervals.argtypes = [V, V, P(I32), P(I32)]
+        lib.coe_runtime_io_intervals.restype = ctypes.c_int
         lib.coe_runtime_wave_phases.argtypes = [V, V, V]
         lib.coe_runtime_wave_phases.restype = ctypes.c_int
         lib.coe_runtime_read_buffer.argtypes = [V, ctypes.c_int, V, I64]
@@ -410,6 +412,16 @@ class B200Runtime:
         fl = np.zeros(max(1, nw.value), np.float64)
         _check(self.lib, self.lib.coe_runtime_wave_phases(self.handle, iv.ctypes.data, fl.ctypes.data), "wave_phases")
         return {"phases": iv[:4 * nw.value].reshape(-1, 4).tolist(), "flops": fl[:nw.value].tolist()}
+
+    def io_intervals(self) -> dict:
+        """e2e steps (profile mode): input-upload and output-download [start, end] ms."""
+        ni, no = ctypes.c_int32(), ctypes.c_int32()
+        _check(self.lib, self.lib.coe_runtime_io_intervals(self.handle, None, ctypes.byref(ni), ctypes.byref(no)), "io")
+        iv = np.zeros(2 * (ni.value + no.value) + 1, np.float32)
+        _check(self.lib, self.lib.coe_runtime_io_intervals(self.handle, iv.ctypes.data, ctypes.byref(ni),
+                                                           ctypes.byref(no)), "io")
+        pairs = iv[:2 * (ni.value + no.value)].reshape(-1, 2)
+        return {"inputs": pairs[:ni.value].tolist(), "outputs": pairs[ni.value:].tolist()}
 
     def bench_mlp(self, groups: int, requests_per_group: int, iters: int = 10) -> tuple:
         up, down = ctypes.c_float(), ctypes.c_float()

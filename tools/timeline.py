@@ -35,6 +35,7 @@ def main():
     name = sys.argv[1] if len(sys.argv) > 1 else "c3"
     nreq = int(sys.argv[2]) if len(sys.argv) > 2 else 10000
     out = sys.argv[3] if len(sys.argv) > 3 else f"gpurun_out/timeline_{name}_{nreq}.json"
+    e2e = len(sys.argv) > 4 and sys.argv[4] == "e2e"
     w = configs.load(name, nreq)
     shape = runtime.shape_of(w)
     cfg = configs.run_config(w, trace=False)
@@ -42,9 +43,18 @@ def main():
     rt = runtime.B200Runtime.for_plan(plan, shape, profile=True)
     rt.fill_inputs(len(plan.resolved.request_ids))
     keep = []
+    kw = {}
+    if e2e:
+        import torch
+
+        n = len(plan.resolved.request_ids)
+        row = rt.shapes[0].T * rt.act_ld
+        hin = torch.empty(n * row, dtype=torch.bfloat16).pin_memory()
+        hout = torch.empty(n * row, dtype=torch.bfloat16).pin_memory()
+        kw = dict(host_inputs=hin.data_ptr(), host_outputs=hout.data_ptr())
     for _ in range(4):
         p = engine.plan(cfg)
-        st = rt.step(p)
+        st = rt.step(p, **kw)
         keep.append(p)
         rt.synchronize()
     timing = rt.timing()
@@ -82,7 +92,17 @@ def main():
                "idle_ms_in_step": timing["total_ms"] - busy, "by_rows": buckets, "by_stream_class": cls},
         "copies": {"n": len(iv["copies"]), "busy_ms": union([tuple(c) for c in iv["copies"]])},
     }
-    print(json.dumps(summary))
+    if e2e:
+        io = rt.io_intervals()
+        h2d = [tuple(c) for c in iv["copies"]] + [tuple(c) for c in io["inputs"]]
+        summary["e2e"] = {"h2d_busy_ms": union(h2d), "input_busy_ms": union([tuple(c) for c in io["inputs"]]),
+                          "d2h_busy_ms": union([tuple(c) for c in io["outputs"]]),
+                          "first_h2d_ms": min(a for a, _ in h2d) if h2d else None,
+                          "last_h2d_end_ms": max(b for _, b in h2d) if h2d else None,
+                          "last_d2h_end_ms": max((b for _, b in io["outputs"]), default=None),
+                          "inputs": len(io["inputs"]), "outputs": len(io["outputs"])}
+        summary["io"] = io
+    print(json.dumps({k: v for k, v in summary.items() if k != "io"}))
     json.dump({"summary": summary, "phases": ph["phases"], "flops": ph["flops"], "wave_info": iv["wave_info"],
                "copies": iv["copies"]}, open(out, "w"))
     rt.close()
