@@ -22,6 +22,7 @@ reference's own rule (engine.py:720-727).
 from __future__ import annotations
 
 import ctypes
+import itertools
 import json
 from dataclasses import dataclass, field, replace
 
@@ -294,13 +295,20 @@ def resolve(config: RunConfig) -> ResolvedRun:
     by_id: dict = {}
     for req in config.stream:
         by_id[req.request_id] = req
+    # per component type: the two concrete chains routing.resolve_chain can return (shared,
+    # read-only lists), then one comparison per request (engine.py:721-725)
+    forms = {}
+    for comp, plan in plans.items():
+        short = [index[eid] for eid in routing.resolve_chain(plan, float("inf"))]
+        full = [index[eid] for eid in plan.experts] if len(plan.experts) > 1 else short
+        forms[comp] = (full, short, plan.branch_prob, len(plan.experts) > 1)
     chains, arrivals = [], []
     for req in by_id.values():
         try:
-            plan = plans[req.component_type]
+            full, short, prob, branches = forms[req.component_type]
         except KeyError:
             raise KeyError(req.component_type) from None
-        chains.append([index[eid] for eid in routing.resolve_chain(plan, req.detect_u)])
+        chains.append(full if (branches and req.detect_u < prob) else short)
         arrivals.append(req.arrival_time_s)
     return ResolvedRun(
         config=config, policy=policy, cost=cost, perf=perf, alloc=alloc, window_results=window_results,
@@ -360,8 +368,9 @@ class Plan:
         keep["ex_ks"] = np.array([float(e[3]) for e in ex], np.float64)
         keep["req"] = np.array(resolved.request_ids, np.int64)
         keep["arr"] = np.array(resolved.arrivals, np.float64)
-        keep["ch_off"] = np.cumsum([0] + [len(c) for c in resolved.chains]).astype(np.int32)
-        keep["ch_exp"] = np.array([e for c in resolved.chains for e in c], np.int32)
+        lens = np.fromiter(map(len, resolved.chains), np.int32, len(resolved.chains))
+        keep["ch_off"] = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+        keep["ch_exp"] = np.fromiter(itertools.chain.from_iterable(resolved.chains), np.int32, int(lens.sum()))
 
         device = cfg.device
         numa = device.architecture == "numa"
