@@ -90,7 +90,10 @@ int coe_mlp_create(const coe_mlp_config *cfg, coe_mlp **out);
 void coe_mlp_destroy(coe_mlp *m);
 int coe_mlp_max_groups(void);
 /* which: bit0 = up projection (gelu(X W1^T) -> H), bit1 = down (H W2^T -> Y).
- * max_ctas: persistent grid cap (0 = one CTA per SM). */
+ * max_ctas: persistent grid cap (0 = one CTA per SM).  tiles_up / tiles_down and each
+ * group's tile_start count 128-row x 256-column tiles (m fastest inside (group, n-block));
+ * the default CTA-pair kernel (COE_K3_CG=2) walks 256-row pair tiles and derives them from
+ * the groups' row counts itself, so callers always pass the 128-row figures. */
 int coe_grouped_mlp(coe_mlp *m, const coe_mlp_group *groups_up, const coe_mlp_group *groups_down, int num_groups,
                     int tiles_up, int tiles_down, const int32_t *batch_off, const int32_t *member_req,
                     const int32_t *member_stage, int which, int max_ctas, cudaStream_t stream);
