@@ -42,8 +42,9 @@ constexpr int BM = 128;  // rows per CTA tile (TMEM lanes)
 constexpr int BN = 256;  // output columns per tile (one 256-column TMEM accumulator)
 constexpr int BK = 64;   // K per stage (one 128-byte swizzle row of bf16)
 constexpr int TMEM_COLS = 512;  // 2 accumulator buffers x BN fp32 columns
-constexpr int NUM_THREADS = 256;
+constexpr int NUM_THREADS = 384;
 constexpr int EPI_WARP0 = 4;
+constexpr int EPI_WARPS = 8;  // two warps per TMEM lane quarter, each drains half the columns
 constexpr int MAX_GROUPS = 1024;
 
 // CG = CTAs per MMA: 1 -- one CTA computes a 128 x 256 tile and loads A (128 x 64) and B
@@ -179,7 +180,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     for (int s = 0; s < 2; ++s) {
       sm100::mbar_init(&tfull_bar[s], 1);
       // CG 1: every epilogue thread arrives; CG 2: one lane per epilogue warp of both CTAs
-      sm100::mbar_init(&tempty_bar[s], CG == 1 ? 128 : 8);
+      sm100::mbar_init(&tempty_bar[s], CG == 1 ? 32 * EPI_WARPS : 2 * EPI_WARPS);
     }
     sm100::fence_mbar_init();
   }
@@ -297,8 +298,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else if (warp >= EPI_WARP0) {
-    // ===== epilogue (each CTA drains its own 128 TMEM lanes) =====
+    // ===== epilogue (each CTA drains its own 128 TMEM lanes; warps w and w+4 share a lane
+    // quarter and split its 256 columns; TMEM loads run one 32-column chunk ahead) =====
     const uint32_t quarter = warp & 3;
+    const int chunk0 = (int)((warp - EPI_WARP0) >> 2) * (BN / 32 / 2);
+    constexpr int CHUNKS = BN / 32 / 2;
     const uint32_t tempty_leader = CG == 2 ? sm100::mapa_shared(sm100::smem_u32(&tempty_bar[0]), 0) : 0;
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -328,28 +332,31 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       sm100::mbar_wait(&tfull_bar[acc], acc_phase);
       sm100::tc_fence_after();
       const uint32_t taddr = tmem_base + ((quarter * 32) << 16) + acc * BN;
-#pragma unroll 1
-      for (int chunk = 0; chunk < BN / 32; ++chunk) {
-        uint32_t v[32];
-        sm100::tmem_ld_32x32b_x32(taddr + chunk * 32, v);
-        sm100::tmem_ld_wait();
+      uint32_t v[2][32];
+      sm100::tmem_ld_32x32b_x32(taddr + chunk0 * 32, v[0]);
+      sm100::tmem_ld_wait_regs(v[0]);
+#pragma unroll
+      for (int k = 0; k < CHUNKS; ++k) {
+        uint32_t(&cur)[32] = v[k & 1];
+        if (k + 1 < CHUNKS) sm100::tmem_ld_32x32b_x32(taddr + (chunk0 + k + 1) * 32, v[(k + 1) & 1]);
         if (valid) {
           uint32_t packed[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
-            float lo = __uint_as_float(v[2 * i]);
-            float hi = __uint_as_float(v[2 * i + 1]);
+            float lo = __uint_as_float(cur[2 * i]);
+            float hi = __uint_as_float(cur[2 * i + 1]);
             if (args.mode == 0) {
               lo = gelu_tanh(lo);
               hi = gelu_tanh(hi);
             }
             packed[i] = pack_bf16(lo, hi);
           }
-          uint4 *dst = reinterpret_cast<uint4 *>(out_row + chunk * 32);
+          uint4 *dst = reinterpret_cast<uint4 *>(out_row + (chunk0 + k) * 32);
 #pragma unroll
           for (int i = 0; i < 4; ++i)
             dst[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
         }
+        if (k + 1 < CHUNKS) sm100::tmem_ld_wait_regs(v[(k + 1) & 1]);
       }
       sm100::tc_fence_before();
       if constexpr (CG == 1) {
