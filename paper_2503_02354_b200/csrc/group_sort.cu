@@ -12,9 +12,11 @@
 // finds their offsets, gathers (request, stage) members for the grouped MLP,
 // counts runs and flags any batch that would straddle two runs.
 //
-// Layout: SoA int32 arrays; 2048-element tiles (256 threads x 8 rounds);
-// per-tile digit histograms -> one-block exclusive scan -> stable scatter with
-// warp match_any ranks.  Everything is HBM/latency-bound integer work.
+// Layout: SoA int32 arrays; 4096-key tiles (256 threads x 16).  Per 8-bit pass:
+// per-tile digit counts -> per-digit row scans (one block per digit) -> a stable
+// in-shared-memory ranking of each tile (warp match_any) written out digit-segment by
+// digit-segment, so the global stores are coalesced.  HBM-bound integer work at scale
+// (20 B moved per key per pass); launch-latency-bound at serving size.
 
 #include <cstdint>
 #include <string>
@@ -27,9 +29,12 @@
 namespace {
 
 constexpr int SORT_THREADS = 256;
-constexpr int ROUNDS = 8;
-constexpr int TILE = SORT_THREADS * ROUNDS;
+// keys per thread per tile: 16 (4096-key tiles) at scale, 4 (1024-key tiles) for serving-size
+// steps, where the per-tile ranking rounds are the serial chain and more CTAs help
+constexpr int ITEMS_LARGE = 16, ITEMS_SMALL = 4;
+constexpr int64_t SMALL_SORT_MAX = 1 << 20;
 constexpr int RADIX = 256;
+constexpr int SORT_WARPS = SORT_THREADS / 32;
 
 __global__ void make_keys(const int32_t *exec, const int32_t *rank, int64_t n, int rank_bits, uint32_t *keys,
                           int32_t *vals) {
@@ -40,75 +45,168 @@ __global__ void make_keys(const int32_t *exec, const int32_t *rank, int64_t n, i
   }
 }
 
-__global__ void radix_hist(const uint32_t *keys, int64_t n, int shift, int num_tiles, uint32_t *hist) {
-  __shared__ uint32_t h[RADIX];
-  h[threadIdx.x] = 0;
+// Pass step 1: per-tile digit counts (coalesced key reads, warp-private smem histograms),
+// stored digit-major: hist[digit * num_tiles + tile].
+template <int ITEMS>
+__global__ void __launch_bounds__(SORT_THREADS) radix_hist(const uint32_t *keys, int64_t n, int shift, int num_tiles,
+                                                           uint32_t *hist) {
+  constexpr int TILE = SORT_THREADS * ITEMS;
+  __shared__ uint32_t h[SORT_WARPS][RADIX];
+  for (int j = threadIdx.x; j < SORT_WARPS * RADIX; j += SORT_THREADS) (&h[0][0])[j] = 0;
   __syncthreads();
-  int64_t base = (int64_t)blockIdx.x * TILE;
-  for (int r = 0; r < ROUNDS; ++r) {
-    int64_t i = base + r * SORT_THREADS + threadIdx.x;
-    if (i < n) atomicAdd(&h[(keys[i] >> shift) & 255], 1u);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t base = (int64_t)blockIdx.x * TILE;
+  uint32_t kreg[ITEMS];  // all loads first: ITEMS independent requests in flight per thread
+#pragma unroll
+  for (int r = 0; r < ITEMS; ++r) {
+    const int64_t i = base + r * SORT_THREADS + threadIdx.x;
+    kreg[r] = i < n ? keys[i] : 0u;
+  }
+#pragma unroll
+  for (int r = 0; r < ITEMS; ++r) {
+    // warp-aggregated: one shared atomic per distinct digit in the warp (serving keys are
+    // nearly sorted, so most of a warp shares a digit in the high passes)
+    const int64_t i = base + r * SORT_THREADS + threadIdx.x;
+    const uint32_t digit = i < n ? (kreg[r] >> shift) & 255u : 256u;
+    const uint32_t same = __match_any_sync(0xffffffffu, digit);
+    if (digit < 256u && (same & ((1u << lane) - 1u)) == 0) atomicAdd(&h[warp][digit], __popc(same));
   }
   __syncthreads();
-  hist[threadIdx.x * num_tiles + blockIdx.x] = h[threadIdx.x];
+  uint32_t c = 0;
+#pragma unroll
+  for (int w = 0; w < SORT_WARPS; ++w) c += h[w][threadIdx.x];
+  hist[(int64_t)threadIdx.x * num_tiles + blockIdx.x] = c;
 }
 
-// single-block exclusive scan of m uint32 values in place
-__global__ void exclusive_scan_1block(uint32_t *data, int64_t m) {
-  __shared__ uint32_t partial[1024];
-  const int t = threadIdx.x;
-  const int64_t per = (m + blockDim.x - 1) / blockDim.x;
-  const int64_t lo = t * per;
-  const int64_t hi = lo + per < m ? lo + per : m;
-  uint32_t sum = 0;
-  for (int64_t i = lo; i < hi; ++i) sum += data[i];
-  partial[t] = sum;
+// Pass step 2: one block per digit scans that digit's row of tile counts in place (exclusive)
+// and writes the row total.
+__global__ void __launch_bounds__(1024) scan_rows(uint32_t *hist, int num_tiles, uint32_t *row_total) {
+  __shared__ uint32_t warp_sums[32];
+  __shared__ uint32_t carry;
+  uint32_t *row = hist + (int64_t)blockIdx.x * num_tiles;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  if (t == 0) carry = 0;
   __syncthreads();
-  for (int off = 1; off < (int)blockDim.x; off <<= 1) {  // Hillis-Steele over thread totals
-    uint32_t v = t >= off ? partial[t - off] : 0;
+  for (int base = 0; base < num_tiles; base += 1024) {
+    const int i = base + t;
+    const uint32_t v = i < num_tiles ? row[i] : 0u;
+    uint32_t x = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, off);
+      if (lane >= off) x += y;
+    }
+    if (lane == 31) warp_sums[warp] = x;
     __syncthreads();
-    partial[t] += v;
-    __syncthreads();
-  }
-  uint32_t run = partial[t] - sum;
-  for (int64_t i = lo; i < hi; ++i) {
-    uint32_t v = data[i];
-    data[i] = run;
-    run += v;
-  }
-}
-
-__global__ void radix_scatter(const uint32_t *keys_in, const int32_t *vals_in, uint32_t *keys_out, int32_t *vals_out,
-                              const uint32_t *offsets, int64_t n, int shift, int num_tiles) {
-  __shared__ uint32_t run_base[RADIX];
-  __shared__ uint32_t warp_cnt[SORT_THREADS / 32][RADIX];
-  const int tid = threadIdx.x;
-  const int warp = tid >> 5, lane = tid & 31;
-  run_base[tid] = offsets[tid * num_tiles + blockIdx.x];
-  const uint32_t lt_mask = (1u << lane) - 1u;
-  int64_t base = (int64_t)blockIdx.x * TILE;
-  for (int r = 0; r < ROUNDS; ++r) {
-    for (int j = tid; j < (SORT_THREADS / 32) * RADIX; j += SORT_THREADS) (&warp_cnt[0][0])[j] = 0;
-    __syncthreads();
-    int64_t i = base + r * SORT_THREADS + tid;
-    bool valid = i < n;
-    uint32_t key = valid ? keys_in[i] : 0u;
-    uint32_t digit = valid ? ((key >> shift) & 255u) : 256u;
-    uint32_t same = __match_any_sync(0xffffffffu, digit);
-    uint32_t rank = __popc(same & lt_mask);
-    if (valid && rank == 0) warp_cnt[warp][digit] = __popc(same);
-    __syncthreads();
-    if (valid) {
-      uint32_t pos = run_base[digit] + rank;
-      for (int w = 0; w < warp; ++w) pos += warp_cnt[w][digit];
-      keys_out[pos] = key;
-      vals_out[pos] = vals_in[i];
+    if (warp == 0) {
+      uint32_t w = warp_sums[lane];
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, w, off);
+        if (lane >= off) w += y;
+      }
+      warp_sums[lane] = w;
     }
     __syncthreads();
-    uint32_t add = 0;
-    for (int w = 0; w < SORT_THREADS / 32; ++w) add += warp_cnt[w][tid];
-    run_base[tid] += add;
+    const uint32_t incl = x + (warp ? warp_sums[warp - 1] : 0u) + carry;
+    if (i < num_tiles) row[i] = incl - v;
     __syncthreads();
+    if (t == 1023) carry = incl;
+    __syncthreads();
+  }
+  if (t == 0) row_total[blockIdx.x] = carry;
+}
+
+// Pass step 3: each CTA ranks its tile stably by digit in shared memory -- every warp walks
+// its own contiguous chunk of the tile 32 keys at a time (match_any ranks + warp-private digit
+// counters, no block barrier inside the walk), one block-wide prefix over (warp, digit) turns
+// warp-local ranks into tile positions -- then writes the locally sorted tile out so that
+// consecutive threads store consecutive addresses of a digit's output segment (coalesced).
+template <int ITEMS>
+__global__ void __launch_bounds__(SORT_THREADS) radix_scatter(const uint32_t *keys_in, const int32_t *vals_in,
+                                                              uint32_t *keys_out, int32_t *vals_out,
+                                                              const uint32_t *offsets, const uint32_t *row_total,
+                                                              int64_t n, int shift, int num_tiles) {
+  constexpr int TILE = SORT_THREADS * ITEMS;
+  constexpr int CHUNK = 32 * ITEMS;  // keys per warp
+  __shared__ uint32_t sk[TILE];
+  __shared__ int32_t sv[TILE];
+  __shared__ uint32_t wcnt[SORT_WARPS][RADIX];  // per-warp digit counts, then per-warp tile offsets
+  __shared__ uint32_t local_off[RADIX], global_off[RADIX], scan_tmp[RADIX];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t base = (int64_t)blockIdx.x * TILE;
+  const int tile_n = (int)((n - base) < TILE ? (n - base) : TILE);
+  // digit base = exclusive scan of the 256 row totals (every CTA redoes this tiny scan)
+  scan_tmp[tid] = row_total[tid];
+  for (int j = tid; j < SORT_WARPS * RADIX; j += SORT_THREADS) (&wcnt[0][0])[j] = 0;
+  __syncthreads();
+  for (int off = 1; off < RADIX; off <<= 1) {
+    const uint32_t y = tid >= off ? scan_tmp[tid - off] : 0u;
+    __syncthreads();
+    scan_tmp[tid] += y;
+    __syncthreads();
+  }
+  global_off[tid] = scan_tmp[tid] - row_total[tid] + offsets[(int64_t)tid * num_tiles + blockIdx.x];
+  // warp walk: warp-local stable ranks
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  uint32_t key[ITEMS], rnk[ITEMS];
+  int32_t val[ITEMS];
+#pragma unroll
+  for (int r = 0; r < ITEMS; ++r) {  // all loads first: 2 x ITEMS requests in flight per thread
+    const int i = warp * CHUNK + r * 32 + lane;
+    key[r] = i < tile_n ? keys_in[base + i] : 0u;
+    val[r] = i < tile_n ? vals_in[base + i] : 0;
+  }
+#pragma unroll
+  for (int r = 0; r < ITEMS; ++r) {
+    const int i = warp * CHUNK + r * 32 + lane;
+    const bool valid = i < tile_n;
+    const uint32_t digit = valid ? ((key[r] >> shift) & 255u) : 256u;
+    const uint32_t same = __match_any_sync(0xffffffffu, digit);
+    const uint32_t before = __popc(same & lt_mask);
+    rnk[r] = valid ? wcnt[warp][digit] + before : 0u;
+    __syncwarp();
+    if (valid && before == 0) wcnt[warp][digit] += __popc(same);
+    __syncwarp();
+  }
+  __syncthreads();
+  // (warp, digit) prefix: thread = digit; tile-local digit starts from the digit totals
+  uint32_t total = 0;
+#pragma unroll
+  for (int w = 0; w < SORT_WARPS; ++w) total += wcnt[w][tid];
+  scan_tmp[tid] = total;
+  __syncthreads();
+  for (int off = 1; off < RADIX; off <<= 1) {
+    const uint32_t y = tid >= off ? scan_tmp[tid - off] : 0u;
+    __syncthreads();
+    scan_tmp[tid] += y;
+    __syncthreads();
+  }
+  uint32_t run = scan_tmp[tid] - total;
+  local_off[tid] = run;
+#pragma unroll
+  for (int w = 0; w < SORT_WARPS; ++w) {
+    const uint32_t c = wcnt[w][tid];
+    wcnt[w][tid] = run;
+    run += c;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < ITEMS; ++r) {
+    const int i = warp * CHUNK + r * 32 + lane;
+    if (i < tile_n) {
+      const uint32_t pos = wcnt[warp][(key[r] >> shift) & 255u] + rnk[r];
+      sk[pos] = key[r];
+      sv[pos] = val[r];
+    }
+  }
+  __syncthreads();
+  for (int k = tid; k < tile_n; k += SORT_THREADS) {
+    const uint32_t kk = sk[k];
+    const uint32_t d = (kk >> shift) & 255u;
+    const uint32_t g = global_off[d] + (uint32_t)k - local_off[d];
+    keys_out[g] = kk;
+    vals_out[g] = sv[k];
   }
 }
 
@@ -139,39 +237,90 @@ __global__ void compact_gather(const int32_t *perm, const uint32_t *keys, const 
   }
 }
 
-// K2 part 2: per-executor exclusive scan of batch sizes in op order (one block),
-// then batch offsets = segment start + prefix; check single-run batches.
-__global__ void compact_batches(const int32_t *batch_exec, const int32_t *batch_size, int num_batches,
-                                int num_executors, const int32_t *seg_start, const uint32_t *keys, int64_t n,
-                                int rank_bits, int32_t *batch_off, int32_t *violations) {
-  __shared__ int32_t scan[1024];
-  __shared__ int32_t carry;
-  const int t = threadIdx.x;
-  for (int x = 0; x < num_executors; ++x) {
-    if (t == 0) carry = 0;
+// K2 part 2: batch offsets = executor segment start + exclusive scan of that executor's
+// batch sizes in op order; three kernels so it scales with the batch count: per-block sums
+// per executor, a scan of those sums, then per-block scans + offsets + the one-run check.
+constexpr int BATCH_THREADS = 1024;
+
+__device__ __forceinline__ int block_exclusive_scan(int v, int *warp_sums, int &total) {
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  int x = v;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, off);
+    if (lane >= off) x += y;
+  }
+  if (lane == 31) warp_sums[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int w = warp_sums[lane];
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, w, off);
+      if (lane >= off) w += y;
+    }
+    warp_sums[lane] = w;
+  }
+  __syncthreads();
+  const int incl = x + (warp ? warp_sums[warp - 1] : 0);
+  total = warp_sums[31];
+  __syncthreads();
+  return incl - v;
+}
+
+__global__ void __launch_bounds__(BATCH_THREADS) batch_block_sums(const int32_t *batch_exec, const int32_t *batch_size,
+                                                                  int num_batches, int num_executors,
+                                                                  int32_t *block_sums) {
+  __shared__ int warp_sums[32];
+  const int b = blockIdx.x * BATCH_THREADS + threadIdx.x;
+  const int x = b < num_batches ? batch_exec[b] : -1;
+  const int v = b < num_batches ? batch_size[b] : 0;
+  for (int e = 0; e < num_executors; ++e) {
+    int total;
+    block_exclusive_scan(x == e ? v : 0, warp_sums, total);
+    if (threadIdx.x == 0) block_sums[(int64_t)blockIdx.x * num_executors + e] = total;
+  }
+}
+
+__global__ void __launch_bounds__(BATCH_THREADS) scan_block_sums(int32_t *block_sums, int num_blocks,
+                                                                 int num_executors) {
+  __shared__ int warp_sums[32];
+  __shared__ int carry;
+  for (int e = 0; e < num_executors; ++e) {
+    if (threadIdx.x == 0) carry = 0;
     __syncthreads();
-    for (int base = 0; base < num_batches; base += blockDim.x) {
-      int b = base + t;
-      int v = (b < num_batches && batch_exec[b] == x) ? batch_size[b] : 0;
-      scan[t] = v;
+    for (int base = 0; base < num_blocks; base += BATCH_THREADS) {
+      const int i = base + threadIdx.x;
+      const int v = i < num_blocks ? block_sums[(int64_t)i * num_executors + e] : 0;
+      int total;
+      const int ex = block_exclusive_scan(v, warp_sums, total);
+      if (i < num_blocks) block_sums[(int64_t)i * num_executors + e] = carry + ex;
       __syncthreads();
-      for (int off = 1; off < (int)blockDim.x; off <<= 1) {
-        int add = t >= off ? scan[t - off] : 0;
-        __syncthreads();
-        scan[t] += add;
-        __syncthreads();
-      }
-      if (b < num_batches && batch_exec[b] == x) batch_off[b] = seg_start[x] + carry + scan[t] - v;
-      __syncthreads();
-      if (t == blockDim.x - 1) carry += scan[t];
+      if (threadIdx.x == 0) carry += total;
       __syncthreads();
     }
   }
-  for (int b = t; b < num_batches; b += blockDim.x) {
-    int lo = batch_off[b];
-    int hi = lo + batch_size[b] - 1;
-    bool bad = batch_size[b] <= 0 || lo < 0 || hi >= n || keys[lo] != keys[hi] ||
-               (int)(keys[lo] >> rank_bits) != batch_exec[b];
+}
+
+__global__ void __launch_bounds__(BATCH_THREADS) compact_batches(const int32_t *batch_exec, const int32_t *batch_size,
+                                                                 int num_batches, int num_executors,
+                                                                 const int32_t *seg_start, const int32_t *block_sums,
+                                                                 const uint32_t *keys, int64_t n, int rank_bits,
+                                                                 int32_t *batch_off, int32_t *violations) {
+  __shared__ int warp_sums[32];
+  const int b = blockIdx.x * BATCH_THREADS + threadIdx.x;
+  const int x = b < num_batches ? batch_exec[b] : -1;
+  const int v = b < num_batches ? batch_size[b] : 0;
+  int mine = 0;
+  for (int e = 0; e < num_executors; ++e) {
+    int total;
+    const int ex = block_exclusive_scan(x == e ? v : 0, warp_sums, total);
+    if (x == e) mine = seg_start[e] + block_sums[(int64_t)blockIdx.x * num_executors + e] + ex;
+  }
+  if (b < num_batches) {
+    batch_off[b] = mine;
+    const int64_t lo = mine, hi = lo + v - 1;
+    const bool bad = v <= 0 || lo < 0 || hi >= n || keys[lo] != keys[hi] || (int)(keys[lo] >> rank_bits) != x;
     if (bad) atomicAdd(violations, 1);
   }
 }
@@ -203,9 +352,10 @@ bool check(cudaError_t e, const char *what) { return coe_cuda_ok(e, what); }
 extern "C" {
 
 int64_t coe_group_sort_scratch_bytes(int64_t n) {
-  int64_t tiles = (n + TILE - 1) / TILE;
+  const int64_t tile = SORT_THREADS * (int64_t)(n <= SMALL_SORT_MAX ? ITEMS_SMALL : ITEMS_LARGE);
+  int64_t tiles = (n + tile - 1) / tile;
   if (tiles < 1) tiles = 1;
-  return 4 * 4 * (n + 64) + 4 * RADIX * tiles + 1024;
+  return 4 * 4 * (n + 64) + 4 * RADIX * (tiles + 1) + 1024;
 }
 
 int coe_group_sort(const int32_t *executor, const int32_t *run_rank, int64_t n, int rank_bits, int num_passes,
@@ -215,31 +365,43 @@ int coe_group_sort(const int32_t *executor, const int32_t *run_rank, int64_t n, 
     coe_set_error("coe_group_sort: bad pass count / rank bits");
     return COE_CUDA_ERR_CONFIG;
   }
-  const int num_tiles = (int)((n + TILE - 1) / TILE);
+  const bool small = n <= SMALL_SORT_MAX;
+  const int64_t tile = SORT_THREADS * (int64_t)(small ? ITEMS_SMALL : ITEMS_LARGE);
+  const int num_tiles = (int)((n + tile - 1) / tile);
   char *s = static_cast<char *>(scratch);
   uint32_t *ka = reinterpret_cast<uint32_t *>(s);
   uint32_t *kb = ka + n + 16;
   int32_t *va = reinterpret_cast<int32_t *>(kb + n + 16);
   int32_t *vb = va + n + 16;
   uint32_t *hist = reinterpret_cast<uint32_t *>(vb + n + 16);
+  uint32_t *row_total = hist + (int64_t)RADIX * num_tiles;
   const int blocks = (int)((n + 255) / 256);
   make_keys<<<blocks, 256, 0, stream>>>(executor, run_rank, n, rank_bits, ka, va);
   for (int p = 0; p < num_passes; ++p) {
-    radix_hist<<<num_tiles, SORT_THREADS, 0, stream>>>(ka, n, 8 * p, num_tiles, hist);
-    exclusive_scan_1block<<<1, 1024, 0, stream>>>(hist, (int64_t)RADIX * num_tiles);
-    radix_scatter<<<num_tiles, SORT_THREADS, 0, stream>>>(ka, va, kb, vb, hist, n, 8 * p, num_tiles);
+    // the last pass scatters straight into the caller's arrays
+    uint32_t *ko = p == num_passes - 1 ? reinterpret_cast<uint32_t *>(out_keys) : kb;
+    int32_t *vo = p == num_passes - 1 ? out_perm : vb;
+    if (small) {
+      radix_hist<ITEMS_SMALL><<<num_tiles, SORT_THREADS, 0, stream>>>(ka, n, 8 * p, num_tiles, hist);
+      scan_rows<<<RADIX, 1024, 0, stream>>>(hist, num_tiles, row_total);
+      radix_scatter<ITEMS_SMALL><<<num_tiles, SORT_THREADS, 0, stream>>>(ka, va, ko, vo, hist, row_total, n, 8 * p,
+                                                                          num_tiles);
+    } else {
+      radix_hist<ITEMS_LARGE><<<num_tiles, SORT_THREADS, 0, stream>>>(ka, n, 8 * p, num_tiles, hist);
+      scan_rows<<<RADIX, 1024, 0, stream>>>(hist, num_tiles, row_total);
+      radix_scatter<ITEMS_LARGE><<<num_tiles, SORT_THREADS, 0, stream>>>(ka, va, ko, vo, hist, row_total, n, 8 * p,
+                                                                          num_tiles);
+    }
     std::swap(ka, kb);
     std::swap(va, vb);
   }
-  if (!check(cudaMemcpyAsync(out_perm, va, n * 4, cudaMemcpyDeviceToDevice, stream), "sort perm copy")) return COE_CUDA_ERR_CUDA;
-  if (!check(cudaMemcpyAsync(out_keys, ka, n * 4, cudaMemcpyDeviceToDevice, stream), "sort key copy")) return COE_CUDA_ERR_CUDA;
   return check(cudaGetLastError(), "coe_group_sort") ? COE_CUDA_OK : COE_CUDA_ERR_CUDA;
 }
 
 int64_t coe_run_compact_scratch_bytes(int64_t n, int num_batches, int num_executors) {
   (void)n;
-  (void)num_batches;
-  return 4 * (int64_t)(num_executors + 16);
+  const int64_t blocks = (num_batches + BATCH_THREADS - 1) / BATCH_THREADS;
+  return 4 * ((int64_t)num_executors + 16) + 4 * (blocks + 1) * num_executors;
 }
 
 int coe_run_compact(const int32_t *perm, const int32_t *sorted_keys, const int32_t *adm_request,
@@ -248,6 +410,7 @@ int coe_run_compact(const int32_t *perm, const int32_t *sorted_keys, const int32
                     int32_t *out_member_req, int32_t *out_member_stage, int32_t *out_run_count,
                     int32_t *out_violations, void *scratch, cudaStream_t stream) {
   int32_t *seg_start = static_cast<int32_t *>(scratch);
+  int32_t *block_sums = seg_start + num_executors + 16;
   if (!check(cudaMemsetAsync(seg_start, 0, 4 * (size_t)num_executors, stream), "compact memset") ||
       !check(cudaMemsetAsync(out_run_count, 0, 4, stream), "compact memset") ||
       !check(cudaMemsetAsync(out_violations, 0, 4, stream), "compact memset"))
@@ -258,10 +421,20 @@ int coe_run_compact(const int32_t *perm, const int32_t *sorted_keys, const int32
                                                adm_stage, n, rank_bits, out_member_req, out_member_stage, seg_start,
                                                out_run_count);
   }
-  if (num_batches > 0)
-    compact_batches<<<1, 1024, 0, stream>>>(batch_exec, batch_size, num_batches, num_executors, seg_start,
-                                            reinterpret_cast<const uint32_t *>(sorted_keys), n, rank_bits,
-                                            out_batch_off, out_violations);
+  if (num_batches > 0) {
+    const int blocks = (num_batches + BATCH_THREADS - 1) / BATCH_THREADS;
+    if (blocks > 1) {
+      batch_block_sums<<<blocks, BATCH_THREADS, 0, stream>>>(batch_exec, batch_size, num_batches, num_executors,
+                                                             block_sums);
+      scan_block_sums<<<1, BATCH_THREADS, 0, stream>>>(block_sums, blocks, num_executors);
+    } else if (!check(cudaMemsetAsync(block_sums, 0, 4 * (size_t)num_executors, stream), "compact memset")) {
+      return COE_CUDA_ERR_CUDA;
+    }
+    compact_batches<<<blocks, BATCH_THREADS, 0, stream>>>(batch_exec, batch_size, num_batches, num_executors,
+                                                          seg_start, block_sums,
+                                                          reinterpret_cast<const uint32_t *>(sorted_keys), n,
+                                                          rank_bits, out_batch_off, out_violations);
+  }
   return check(cudaGetLastError(), "coe_run_compact") ? COE_CUDA_OK : COE_CUDA_ERR_CUDA;
 }
 

@@ -51,7 +51,8 @@ def _run_ranks(rng, n, executors):
     return ex, rank
 
 
-@pytest.mark.parametrize("n, executors", [(1, 1), (7, 1), (2048, 2), (2049, 3), (50000, 8), (120000, 4)])
+@pytest.mark.parametrize("n, executors", [(1, 1), (7, 1), (2048, 2), (2049, 3), (4097, 1), (50000, 8), (120000, 4),
+                                          (1 << 20, 2)])
 def test_group_sort_matches_stable_lexsort(lib, n, executors):
     import torch
 
@@ -73,11 +74,11 @@ def test_group_sort_matches_stable_lexsort(lib, n, executors):
     assert np.array_equal(k, (ex[ref].astype(np.int64) << bits) | rank[ref])
 
 
-def test_run_compact_offsets_members_and_violations(lib):
+@pytest.mark.parametrize("n, X", [(5000, 2), (200000, 3)])
+def test_run_compact_offsets_members_and_violations(lib, n, X):
     import torch
 
     rng = np.random.default_rng(5)
-    n, X = 5000, 2
     ex, rank = _run_ranks(rng, n, X)
     bits = max(1, int(rank.max()).bit_length())
     dev = torch.device("cuda")
