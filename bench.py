@@ -303,6 +303,7 @@ def main() -> None:
             p = engine.plan(cfg)  # the public call: plan + serve with pinned host buffers
             io = rt.step(p, rank, host_inputs=host_in.data_ptr(), host_outputs=host_out.data_ptr())
             keep.append(p)
+        rt.join()  # the end event covers the last step's output downloads
         e1.record(stream)
         rt.synchronize()
         barrier()
@@ -314,8 +315,9 @@ def main() -> None:
         e2e = {"value": n_req * args.e2e_steps / (e2e_ms / 1e3), "unit": "requests/s",
                "h2d_bytes_per_step": io["h2d_input_bytes"], "d2h_bytes_per_step": io["d2h_output_bytes"],
                "ms_per_step": e2e_ms / args.e2e_steps,
-               "note": "planner + stage-0 inputs streamed H2D just in time + final outputs streamed D2H per wave, "
-                       "all inside the timed region; swap-ins share the same PCIe H2D link"}
+               "note": "planner + stage-0 inputs streamed H2D just in time (32 MB chunks on the swap-in copy "
+                       "engine) + final outputs gathered per wave and streamed D2H in completion order, all "
+                       "inside the timed region; swap-ins and inputs share the PCIe H2D link"}
 
     # ---- CPU baseline (rank 0, N=1) ----
     cpu = None
@@ -350,6 +352,9 @@ def main() -> None:
         traffic = ncu.get("dram_bytes_per_launch")  # the profiled wave's average up/down launch
         traffic_algo = ncu.get("algorithmic_bytes_per_launch")
     load_bytes = stats["load_bytes"] + stats["restore_bytes"]
+    registry = plan_last.resolved.config.registry
+    expert_gb = sum(spec.param_bytes for spec in registry.experts.values()) / 1e9
+    act_gb = 3 * n_req * rt.shapes[0].T * rt.act_ld * 2 / 1e9  # X read, P0 / P1 written and read
     copy_s = timing["copy_busy_ms"] / 1e3
     short = min(timing["copy_busy_ms"], timing["compute_busy_ms"])
     line = {
@@ -364,7 +369,8 @@ def main() -> None:
                    "expert_budget_bytes": plan0.resolved.alloc["gpu"]["expert_budget_bytes"],
                    "hbm_slots": rt.num_slots, "policy": w.run["policy"], "parallelism": f"executor-per-gpu x{world}",
                    "hop_transport": (transport if world > 1 else None),
-                   "l2": "no flush needed: 60 GB of experts and >2 GB of activations per step exceed the 126 MB L2"},
+                   "l2": (f"no flush needed: {expert_gb:.1f} GB of experts and {act_gb:.1f} GB of activations "
+                          "touched per step exceed the 126 MB L2")},
         "swaps_per_1k_requests": 1000.0 * metrics.expert_switches / n_req,
         "gb_moved_per_1k_requests": 1000.0 * ps["bytes_moved"] / 1e9 / n_req,
         "planner": {"makespan_virtual_s": metrics.makespan_s, "switches": metrics.expert_switches,

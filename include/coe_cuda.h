@@ -103,6 +103,9 @@ int coe_grouped_mlp(coe_mlp *m, const coe_mlp_group *groups_up, const coe_mlp_gr
  * local buffer.  hop_dst == NULL turns it off.  world <= COE_MAX_PEERS. */
 #define COE_MAX_PEERS 8
 int coe_mlp_set_hops(coe_mlp *m, const int8_t *hop_dst, int hop_stride, void *const *peer_act, int world);
+/* Stage-0 inputs of later launches from `x` (same shape / stride as cfg.x; NULL or cfg.x:
+ * back to cfg.x) -- lets e2e steps double-buffer their input uploads. */
+int coe_mlp_set_input(coe_mlp *m, void *x);
 
 /* ---------------- GPU serving runtime (one executor per GPU) --------------- */
 
@@ -148,9 +151,10 @@ typedef struct coe_step_input {
   const int32_t *op_args;
   int32_t num_initial;                      /* initial residency of this executor          */
   const int32_t *initial;
-  /* end-to-end serving (optional, pinned host memory, [requests][T][d] bf16 by request
-   * index): stage-0 inputs are uploaded just in time on an input stream, each final
-   * stage output is downloaded as soon as its wave completes */
+  /* end-to-end serving (optional, pinned host memory, [requests][T][ld] bf16): inputs are
+   * indexed by request and uploaded just in time on the copy engine; outputs are streamed
+   * back in COMPLETION order -- each wave's final rows are gathered on the GPU and leave in
+   * one D2H copy -- and coe_runtime_output_order names the request of every output row */
   const void *host_inputs;
   void *host_outputs;
 } coe_step_input;
@@ -191,12 +195,18 @@ int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_step_stats *
 int coe_runtime_download_outputs(coe_runtime *rt, const int32_t *last_stage_host, int32_t num_requests, void *host);
 int coe_runtime_synchronize(coe_runtime *rt);
 /* after synchronize: K2 run count / violations, and the grouped members */
+/* make the compute stream (coe_runtime_stream(rt, 0)) wait for the last step's output
+ * downloads -- e2e steps do not join them, so an event recorded after this covers them */
+int coe_runtime_join(coe_runtime *rt);
 int coe_runtime_check(coe_runtime *rt, int32_t *runs, int32_t *violations);
 int coe_runtime_members(coe_runtime *rt, int32_t *member_req, int32_t *member_stage, int32_t *batch_off);
 int coe_runtime_timing(coe_runtime *rt, coe_step_timing *out);
 /* profile mode: per-copy [start,end) and per-wave [start,end) ms since step start,
  * wave_info = (stream class, rows, groups) per wave; sizes from coe_runtime_counts */
 int coe_runtime_counts(coe_runtime *rt, int32_t *copies, int32_t *waves);
+/* e2e: request id of each row of host_outputs after the last step (completion order);
+ * returns the row count, copies at most `capacity` ids (requests may be NULL) */
+int32_t coe_runtime_output_order(coe_runtime *rt, int32_t *requests, int32_t capacity);
 /* K3 in isolation on the runtime's buffers: one wave of `groups` batches x
  * `requests_per_group` requests; average up / down projection launch times */
 int coe_runtime_bench_mlp(coe_runtime *rt, int32_t groups, int32_t requests_per_group, int32_t iters,

@@ -435,6 +435,9 @@ struct coe_mlp {
   int num_sms;
   int a_box_rows;
   int cg = 2;                        // CTAs per MMA (COE_K3_CG=1 selects the single-CTA kernel)
+  CUtensorMap xmap_alt;              // stage-0 inputs from a second X buffer (coe_mlp_set_input)
+  const void *x_alt = nullptr;
+  bool use_alt = false;
   const int8_t *hop_dst = nullptr;   // fused hops (coe_mlp_set_hops)
   int hop_stride = 0;
   __nv_bfloat16 *peer_act[COE_MAX_PEERS][2] = {};
@@ -494,6 +497,23 @@ int coe_mlp_create(const coe_mlp_config *cfg, coe_mlp **out) {
 
 void coe_mlp_destroy(coe_mlp *m) { delete m; }
 
+int coe_mlp_set_input(coe_mlp *m, void *x) {
+  if (!x || x == m->cfg.x) {
+    m->use_alt = false;
+    return COE_CUDA_OK;
+  }
+  if (x != m->x_alt) {
+    const uint64_t ld = m->cfg.act_ld > 0 ? (uint64_t)m->cfg.act_ld : (uint64_t)m->cfg.d;
+    if (!make_map_2d(&m->xmap_alt, x, (uint64_t)m->cfg.act_rows, m->cfg.d, m->a_box_rows, ld)) {
+      coe_set_error("coe_mlp_set_input: cuTensorMapEncodeTiled failed");
+      return COE_CUDA_ERR_CUDA;
+    }
+    m->x_alt = x;
+  }
+  m->use_alt = true;
+  return COE_CUDA_OK;
+}
+
 int coe_mlp_max_groups(void) { return MAX_GROUPS; }
 
 int coe_mlp_set_hops(coe_mlp *m, const int8_t *hop_dst, int hop_stride, void *const *peer_act, int world) {
@@ -542,7 +562,7 @@ int coe_grouped_mlp(coe_mlp *m, const coe_mlp_group *groups_up, const coe_mlp_gr
     std::memcpy(a.peer_act, m->peer_act, sizeof(a.peer_act));
     if (a.total_tiles <= 0) continue;
     int cap = (max_ctas > 0 && max_ctas < m->num_sms) ? max_ctas : m->num_sms;
-    const CUtensorMap &ta0 = pass == 0 ? m->xmap : m->hmap, &ta1 = pass == 0 ? m->act0 : m->hmap,
+    const CUtensorMap &ta0 = pass == 0 ? (m->use_alt ? m->xmap_alt : m->xmap) : m->hmap, &ta1 = pass == 0 ? m->act0 : m->hmap,
                       &ta2 = pass == 0 ? m->act1 : m->hmap, &tb = pass == 0 ? m->w1 : m->w2;
     cudaError_t e;
     if (m->cg == 1) {

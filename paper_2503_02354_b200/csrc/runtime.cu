@@ -62,6 +62,17 @@ uint64_t splitmix64_host(uint64_t z) {
   return z ^ (z >> 31);
 }
 
+// e2e: one wave's final rows, packed (request << 1 | P parity), gathered contiguously (one
+// block per row, 16-byte vectors) so the wave's results leave in a single D2H copy
+__global__ void gather_rows(const __nv_bfloat16 *p0, const __nv_bfloat16 *p1, const int32_t *req_par, int64_t row_elems,
+                            __nv_bfloat16 *out) {
+  const int32_t rp = req_par[blockIdx.x];
+  const __nv_bfloat16 *src = ((rp & 1) ? p1 : p0) + (int64_t)(rp >> 1) * row_elems;
+  const uint4 *sv = reinterpret_cast<const uint4 *>(src);
+  uint4 *dv = reinterpret_cast<uint4 *>(out + (int64_t)blockIdx.x * row_elems);
+  for (int64_t i = threadIdx.x; i < row_elems / 8; i += blockDim.x) dv[i] = sv[i];
+}
+
 __global__ void gather_outputs(const __nv_bfloat16 *p0, const __nv_bfloat16 *p1, const int32_t *last_stage,
                                int32_t num_requests, int64_t row_elems, __nv_bfloat16 *out) {
   int32_t r = blockIdx.x;  // one block per request, 16-byte vectors
@@ -175,6 +186,7 @@ struct StepBuffers {  // device arrays one step uses; two sets alternate
   int32_t *boff = nullptr;
   int32_t *mreq = nullptr, *mstage = nullptr;
   coe_mlp_group *groups = nullptr;  // [2][max_batches]
+  int32_t *fin = nullptr;           // e2e: final rows in completion order, request << 1 | parity
   cudaEvent_t free_ev = nullptr;    // recorded on compute when the step using this set ends
   bool used = false;
 };
@@ -223,7 +235,8 @@ struct coe_runtime {
   std::vector<cudaEvent_t> slot_free_up, slot_free_down;
   std::vector<uint8_t> slot_free_valid;
   // events
-  std::vector<cudaEvent_t> wave_up_ev, wave_down_ev, copy_up_ev, copy_down_ev;
+  std::vector<cudaEvent_t> wave_up_ev, wave_down_ev, copy_up_ev, copy_down_ev, out_ev;
+  std::vector<int32_t> out_order;  // e2e: request of each host output row (completion order)
   std::vector<cudaEvent_t> t_copy_start, t_copy_end, t_wave_start, t_wave_end, t_up_end, t_down_start;
   std::vector<cudaEvent_t> t_io;    // profile, e2e: [start, end] event pairs of uploads / downloads
   std::vector<uint8_t> io_kind;      // per pair: 0 input upload, 1 output download
@@ -239,6 +252,12 @@ struct coe_runtime {
   std::vector<cudaEvent_t> in_ev;
   cudaEvent_t out_drained = nullptr;
   bool have_out = false;
+  // e2e input double buffer: step k uploads into X[k & 1] (x, then x_alt) while step k-1 may
+  // still read the other; x_free[p] marks the end of the last step that read X[p]
+  __nv_bfloat16 *x_alt = nullptr;
+  int64_t e2e_steps = 0;
+  cudaEvent_t x_free[2] = {nullptr, nullptr};
+  bool x_free_valid[2] = {false, false};
   coe_comm *comm = nullptr;            // hop transport (N > 1)
   cudaStream_t hop = nullptr;
   std::vector<cudaEvent_t> recv_ev;
@@ -270,12 +289,12 @@ struct coe_runtime {
     for (auto &per : mlps)
       for (auto m : per)
         if (m) coe_mlp_destroy(m);
-    std::vector<void *> dev = {x, p0, p1, hbuf[0], hbuf[1], hbuf[2], outbuf, d_perm, d_keys, d_flags, d_last, d_sort_scratch,
+    std::vector<void *> dev = {x, x_alt, p0, p1, hbuf[0], hbuf[1], hbuf[2], outbuf, d_perm, d_keys, d_flags, d_last, d_sort_scratch,
                                d_compact_scratch};
     for (char *sl : slabs) dev.push_back(sl);
     for (auto &s : sets) {
       for (void *p : {(void *)s.adm, (void *)s.batch, (void *)s.boff, (void *)s.mreq, (void *)s.mstage,
-                      (void *)s.groups})
+                      (void *)s.groups, (void *)s.fin})
         dev.push_back(p);
       if (s.free_ev) cudaEventDestroy(s.free_ev);
     }
@@ -292,12 +311,12 @@ struct coe_runtime {
     } else if (host_store) {
       cudaFreeHost(host_store);
     }
-    for (auto *v : {&in_ev, &recv_ev, &slot_free_up, &slot_free_down, &wave_up_ev, &wave_down_ev, &copy_up_ev, &copy_down_ev,
+    for (auto *v : {&in_ev, &recv_ev, &slot_free_up, &slot_free_down, &wave_up_ev, &wave_down_ev, &copy_up_ev, &copy_down_ev, &out_ev,
                     &t_copy_start, &t_copy_end, &t_wave_start, &t_wave_end, &t_up_end, &t_down_start, &t_io}) {
       for (auto e : *v) cudaEventDestroy(e);
       v->clear();
     }
-    for (cudaEvent_t e : {out_drained, hop_drained, step_end, staged, copy_drained, grouped, cls_drained[0], cls_drained[1], cls_drained[2], t_step_start, t_group_end, t_step_end, staging_done[0],
+    for (cudaEvent_t e : {x_free[0], x_free[1], out_drained, hop_drained, step_end, staged, copy_drained, grouped, cls_drained[0], cls_drained[1], cls_drained[2], t_step_start, t_group_end, t_step_end, staging_done[0],
                           staging_done[1]})
       if (e) cudaEventDestroy(e);
     for (auto st : cls_stream)
@@ -472,10 +491,11 @@ int coe_runtime_create(const coe_runtime_config *cfg, coe_runtime **out) {
     good = good && dmalloc(&s.adm, 16 * A, "adm alloc") && dmalloc(&s.batch, 8 * B, "batch alloc") &&
            dmalloc(&s.boff, 4 * B, "boff alloc") && dmalloc(&s.mreq, 4 * A, "member alloc") &&
            dmalloc(&s.mstage, 4 * A, "member alloc") && dmalloc(&s.groups, 2 * sizeof(coe_mlp_group) * B, "groups") &&
+           dmalloc(&s.fin, 4 * (size_t)c.max_requests + 16, "final list") &&
            ok(cudaEventCreateWithFlags(&s.free_ev, cudaEventDisableTiming), "event");
   rt->compute = rt->cls_stream[0];
   if (good) {
-    rt->staging_bytes = 16 * A + 8 * B + 2 * sizeof(coe_mlp_group) * B + 256;
+    rt->staging_bytes = 16 * A + 8 * B + 2 * sizeof(coe_mlp_group) * B + 4 * (size_t)c.max_requests + 512;
     good = ok(cudaHostAlloc(reinterpret_cast<void **>(&rt->staging[0]), rt->staging_bytes, cudaHostAllocDefault), "staging") &&
            ok(cudaHostAlloc(reinterpret_cast<void **>(&rt->staging[1]), rt->staging_bytes, cudaHostAllocDefault), "staging") &&
            ok(cudaHostAlloc(reinterpret_cast<void **>(&rt->h_last), 4 * (size_t)c.max_requests, cudaHostAllocDefault), "last") &&
@@ -648,6 +668,11 @@ int coe_runtime_synchronize(coe_runtime *rt) {
               ok(cudaStreamSynchronize(rt->in_stream), "sync in") && ok(cudaStreamSynchronize(rt->out_stream), "sync out");
   for (int k = coe_runtime::NCLS - 1; k >= 0; --k) good = ok(cudaStreamSynchronize(rt->cls_stream[k]), "sync") && good;
   return good ? COE_CUDA_OK : fail_cuda();
+}
+
+int coe_runtime_join(coe_runtime *rt) {
+  if (rt->have_out && !ok(cudaStreamWaitEvent(rt->compute, rt->out_drained, 0), "join downloads")) return fail_cuda();
+  return COE_CUDA_OK;
 }
 
 int coe_runtime_check(coe_runtime *rt, int32_t *runs, int32_t *violations) {
@@ -878,6 +903,13 @@ int coe_runtime_io_intervals(coe_runtime *rt, float *iv, int32_t *n_in, int32_t 
     }
   }
   return COE_CUDA_OK;
+}
+
+int32_t coe_runtime_output_order(coe_runtime *rt, int32_t *requests, int32_t capacity) {
+  const int32_t n = (int32_t)rt->out_order.size();
+  if (requests)
+    for (int32_t i = 0; i < n && i < capacity; ++i) requests[i] = rt->out_order[i];
+  return n;
 }
 
 int coe_runtime_counts(coe_runtime *rt, int32_t *copies, int32_t *waves) {
@@ -1514,6 +1546,29 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     std::memcpy(s_groups + n_batches, g_down.data(), sizeof(coe_mlp_group) * n_batches);
   }
 
+  // e2e: final rows leave in completion order -- per wave, its finals by request id
+  std::vector<int32_t> fin_begin(nw, 0), fin_end(nw, 0);  // per wave: slice of the output order
+  int32_t *s_fin = reinterpret_cast<int32_t *>((reinterpret_cast<uintptr_t>(s_groups + 2 * n_batches) + 31) &
+                                               ~uintptr_t(31));
+  if (e2e_out) {
+    rt->out_order.clear();
+    for (size_t a = 0; a < actions.size(); ++a) {
+      if (actions[a].is_copy || actions[a].is_input) continue;
+      const WaveAct &w = waves[actions[a].index];
+      std::vector<int32_t> fin;
+      for (int32_t gi = w.first_group; gi < w.first_group + w.num_groups; ++gi)
+        for (int32_t r : batches[g_up[gi].batch].finals) fin.push_back(r);
+      std::sort(fin.begin(), fin.end());
+      fin_begin[actions[a].index] = (int32_t)rt->out_order.size();
+      for (int32_t r : fin) {
+        s_fin[rt->out_order.size()] = (r << 1) | (final_stage[r] & 1);
+        rt->out_order.push_back(r);
+      }
+      fin_end[actions[a].index] = (int32_t)rt->out_order.size();
+    }
+    if (!rt->ensure_events(rt->out_ev, nw, false)) return fail_cuda();
+  }
+
   cudaStream_t cs = rt->compute, ks = rt->copy;
   if (c.profile && !ok(cudaEventRecord(rt->t_step_start, cs), "record")) return fail_cuda();
   if (sb.used && !ok(cudaStreamWaitEvent(ks, sb.free_ev, 0), "set reuse")) return fail_cuda();
@@ -1524,6 +1579,9 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
        !ok(cudaMemcpyAsync(sb.groups, s_groups, 2 * sizeof(coe_mlp_group) * (size_t)n_batches,
                            cudaMemcpyHostToDevice, ks),
            "group H2D")))
+    return fail_cuda();
+  if (e2e_out && !rt->out_order.empty() &&
+      !ok(cudaMemcpyAsync(sb.fin, s_fin, 4 * rt->out_order.size(), cudaMemcpyHostToDevice, ks), "final list H2D"))
     return fail_cuda();
   if (peer_mode && !ok(cudaMemcpyAsync(rt->d_hopdst[set_idx], rt->h_hopdst[set_idx],
                                        (size_t)c.max_requests * HOP_STRIDE, cudaMemcpyHostToDevice, ks),
@@ -1555,12 +1613,23 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
 
   if (!my_hops.empty() && rt->have_step_end && !ok(cudaStreamWaitEvent(rt->hop, rt->step_end, 0), "hop waits step"))
     return fail_cuda();
-  // e2e: this step's P writes follow last step's output downloads; its X uploads follow last
-  // step's readers of X; uploads are issued in op order (just in time), one event per batch
-  if (rt->have_out)
-    for (int k = 0; k < NCLS; ++k)
-      if (!ok(cudaStreamWaitEvent(rt->cls_stream[k], rt->out_drained, 0), "P reuse waits downloads"))
-        return fail_cuda();
+  // e2e: inputs double-buffered across steps; this step's first output gather on each stream
+  // waits for last step's downloads (the gathers reuse the staging buffer they read)
+  bool out_waited[NCLS] = {false, false, false};
+  const int xp = (int)(rt->e2e_steps & 1);
+  __nv_bfloat16 *x_step = rt->x;
+  if (e2e_in) {
+    if (!rt->x_alt) {  // at the first e2e step (cudaMalloc synchronises: keep it out of later steps)
+      if (!ok(cudaMalloc(&rt->x_alt, (size_t)c.max_requests * rt->row_elems * 2), "X alt alloc")) return fail_cuda();
+    }
+    if (!rt->x_free[0] && (!ok(cudaEventCreateWithFlags(&rt->x_free[0], cudaEventDisableTiming), "event") ||
+                           !ok(cudaEventCreateWithFlags(&rt->x_free[1], cudaEventDisableTiming), "event")))
+      return fail_cuda();
+    x_step = xp ? rt->x_alt : rt->x;
+  }
+  for (auto &per : rt->mlps)
+    for (coe_mlp *m : per)
+      if (m && coe_mlp_set_input(m, x_step)) return COE_CUDA_ERR_CUDA;
   bool x_reuse_waited = false;
   if (e2e_in && !rt->ensure_events(rt->in_ev, (size_t)n_chunks, false)) return fail_cuda();
   // stage-0 rows of batch b, pinned host -> X, coalescing consecutive request rows
@@ -1572,9 +1641,10 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     return ok(cudaEventRecord(rt->t_io[io_n++], s_), "record");
   };
   auto upload_inputs = [&](int32_t k) -> bool {
-    if (!x_reuse_waited) {  // X rows are free once last step's readers are done
+    if (!x_reuse_waited) {  // X[xp] is free once the step before last (its last reader) ended
       x_reuse_waited = true;
-      if (rt->have_step_end && !ok(cudaStreamWaitEvent(ks, rt->step_end, 0), "X reuse waits step")) return false;
+      if (rt->x_free_valid[xp] && !ok(cudaStreamWaitEvent(ks, rt->x_free[xp], 0), "X reuse waits step"))
+        return false;
     }
     if (c.profile) rt->io_kind.push_back(0);
     if (!io_mark(ks)) return false;
@@ -1587,7 +1657,7 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     for (size_t i = 0; i < rq.size();) {
       size_t j = i + 1;
       while (j < rq.size() && rq[j] == rq[j - 1] + 1) ++j;
-      dsts.push_back(reinterpret_cast<char *>(rt->x) + rq[i] * rb);
+      dsts.push_back(reinterpret_cast<char *>(x_step) + rq[i] * rb);
       srcs.push_back(const_cast<char *>(hin) + rq[i] * rb);
       sizes.push_back((j - i) * rb);
       st.h2d_input_bytes += (int64_t)((j - i) * rb);
@@ -1713,35 +1783,36 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     }
     for (int32_t gi = w.first_group; gi < w.first_group + w.num_groups; ++gi) issued[g_up[gi].batch] = 1;
     if (c.profile && !ok(cudaEventRecord(rt->t_wave_end[a.index], ws), "record")) return fail_cuda();
-    if (e2e_out) {  // final outputs of this wave stream back while later waves run
-      std::vector<int32_t> fin;
-      for (int32_t gi = w.first_group; gi < w.first_group + w.num_groups; ++gi)
-        for (int32_t r : batches[g_up[gi].batch].finals) fin.push_back(r);
-      if (!fin.empty()) {
-        if (!ok(cudaStreamWaitEvent(rt->out_stream, rt->wave_down_ev[a.index], 0), "download waits wave"))
-          return fail_cuda();
-        const size_t rb = (size_t)rt->row_elems * 2;
-        char *hout = static_cast<char *>(in->host_outputs);
-        std::vector<void *> dsts, srcs;
-        std::vector<size_t> sizes;
-        for (int32_t r : fin) {
-          const int32_t fs = final_stage[r];
-          dsts.push_back(hout + (size_t)r * rb);
-          srcs.push_back(reinterpret_cast<char *>((fs & 1) ? rt->p1 : rt->p0) + (size_t)r * rb);
-          sizes.push_back(rb);
-          st.d2h_output_bytes += (int64_t)rb;
+    if (e2e_out) {  // final outputs of this wave: gathered on its stream, one D2H copy
+      const int32_t b0 = fin_begin[a.index], b1 = fin_end[a.index];
+      if (b1 > b0) {
+        const int64_t re = rt->row_elems;
+        if (rt->have_out && !out_waited[w.cls]) {
+          out_waited[w.cls] = true;
+          if (!ok(cudaStreamWaitEvent(ws, rt->out_drained, 0), "gather waits last downloads")) return fail_cuda();
         }
+        gather_rows<<<b1 - b0, 256, 0, ws>>>(rt->p0, rt->p1, sb.fin + b0, re, rt->outbuf + (int64_t)b0 * re);
+        st.launches += 1;
+        if (!ok(cudaGetLastError(), "gather rows") || !ok(cudaEventRecord(rt->out_ev[a.index], ws), "record") ||
+            !ok(cudaStreamWaitEvent(rt->out_stream, rt->out_ev[a.index], 0), "download waits gather"))
+          return fail_cuda();
+        const size_t rb = (size_t)re * 2;
+        char *hout = static_cast<char *>(in->host_outputs);
         if (c.profile) rt->io_kind.push_back(1);
-        if (!io_mark(rt->out_stream) || !batched_copy(dsts, srcs, sizes, rt->out_stream, "output D2H") ||
+        if (!io_mark(rt->out_stream) ||
+            !ok(cudaMemcpyAsync(hout + (size_t)b0 * rb, reinterpret_cast<char *>(rt->outbuf) + (size_t)b0 * rb,
+                                (size_t)(b1 - b0) * rb, cudaMemcpyDeviceToHost, rt->out_stream),
+                "output D2H") ||
             !io_mark(rt->out_stream))
           return fail_cuda();
+        st.d2h_output_bytes += (int64_t)(b1 - b0) * (int64_t)rb;
       }
     }
   }
   if (e2e_out) {
-    if (!ok(cudaEventRecord(rt->out_drained, rt->out_stream), "record") ||
-        !ok(cudaStreamWaitEvent(cs, rt->out_drained, 0), "join downloads"))
-      return fail_cuda();
+    // not joined into the compute stream: the next step's waves need not wait for this step's
+    // downloads (only its gathers do); coe_runtime_join / synchronize cover them
+    if (!ok(cudaEventRecord(rt->out_drained, rt->out_stream), "record")) return fail_cuda();
     rt->have_out = true;
   }
   if (!peer_mode && !issue_hops_until(INT64_MAX)) return COE_CUDA_ERR_CUDA;
@@ -1767,6 +1838,11 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
   if (!ok(cudaEventRecord(sb.free_ev, cs), "record") || !ok(cudaEventRecord(rt->step_end, cs), "record"))
     return fail_cuda();
   rt->have_step_end = true;
+  if (e2e_in) {  // X[xp] is read by nothing after this step's end
+    if (!ok(cudaEventRecord(rt->x_free[xp], cs), "record")) return fail_cuda();
+    rt->x_free_valid[xp] = true;
+    rt->e2e_steps += 1;
+  }
   sb.used = true;
   rt->last_waves = (int32_t)nw;
   rt->last_wave_cls.clear();

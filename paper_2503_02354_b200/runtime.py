@@ -123,6 +123,10 @@ def _lib():
         lib.coe_runtime_counts.restype = ctypes.c_int
         lib.coe_runtime_intervals.argtypes = [V, V, V, V]
         lib.coe_runtime_intervals.restype = ctypes.c_int
+        lib.coe_runtime_join.argtypes = [V]
+        lib.coe_runtime_join.restype = ctypes.c_int
+        lib.coe_runtime_output_order.argtypes = [V, V, I32]
+        lib.coe_runtime_output_order.restype = I32
         lib.coe_runtime_io_intervals.argtypes = [V, V, P(I32), P(I32)]
         lib.coe_runtime_io_intervals.restype = ctypes.c_int
         lib.coe_runtime_wave_phases.argtypes = [V, V, V]
@@ -357,7 +361,8 @@ class B200Runtime:
     # -- execution ---------------------------------------------------------
     def step(self, plan, executor: int = 0, host_inputs: int | None = None, host_outputs: int | None = None) -> dict:
         """Execute ``plan``'s op log for ``executor``.  With pinned host buffers the step is
-        end to end: inputs stream in just in time, final outputs stream out per wave."""
+        end to end: inputs (row r = request r) stream in just in time, final outputs stream
+        out per wave in completion order (``output_order()`` names each row's request)."""
         lib = plan.lib
         h = plan.handle
         init = np.ascontiguousarray(plan.initial_residency()[executor], dtype=np.int32)
@@ -372,6 +377,10 @@ class B200Runtime:
         stats = StepStats()
         _check(self.lib, self.lib.coe_runtime_step(self.handle, ctypes.byref(inp), ctypes.byref(stats)), "step")
         return stats.as_dict()
+
+    def join(self) -> None:
+        """Order the compute stream after the last e2e step's output downloads."""
+        _check(self.lib, self.lib.coe_runtime_join(self.handle), "join")
 
     def synchronize(self) -> None:
         _check(self.lib, self.lib.coe_runtime_synchronize(self.handle), "synchronize")
@@ -412,6 +421,13 @@ class B200Runtime:
         fl = np.zeros(max(1, nw.value), np.float64)
         _check(self.lib, self.lib.coe_runtime_wave_phases(self.handle, iv.ctypes.data, fl.ctypes.data), "wave_phases")
         return {"phases": iv[:4 * nw.value].reshape(-1, 4).tolist(), "flops": fl[:nw.value].tolist()}
+
+    def output_order(self) -> np.ndarray:
+        """After an e2e step: the request id of each host_outputs row (completion order)."""
+        n = self.lib.coe_runtime_output_order(self.handle, None, 0)
+        out = np.zeros(max(1, n), np.int32)
+        self.lib.coe_runtime_output_order(self.handle, out.ctypes.data, n)
+        return out[:n]
 
     def io_intervals(self) -> dict:
         """e2e steps (profile mode): input-upload and output-download [start, end] ms."""

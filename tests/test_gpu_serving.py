@@ -153,8 +153,10 @@ def test_streamed_end_to_end_io_matches_device_path():
     st = rt.step(p2, host_inputs=host_in.data_ptr(), host_outputs=host_out.data_ptr())
     rt.synchronize()
     assert st["h2d_input_bytes"] == n * row * 2 and st["d2h_output_bytes"] == n * row * 2
+    order = rt.output_order()  # rows arrive in completion order
+    assert sorted(order.tolist()) == list(range(n))
     got = host_out.view(n, shape.T, shape.d).float().numpy()
-    assert np.array_equal(got, outs[0])
+    assert np.array_equal(got, outs[0][order])
 
 
 def test_c5_heterogeneous_expert_shapes():
