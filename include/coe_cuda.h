@@ -126,8 +126,7 @@ typedef struct coe_runtime_config {
   uint64_t weight_seed;     /* synthetic expert weights, see coe_expert_seed         */
   int32_t profile;          /* record per-copy / per-wave events for overlap stats   */
   int32_t reserve_sms;      /* SMs kept for the swap-in-gating waves (0: no split)   */
-  int32_t swapped_stream;   /* experiments: waves on experts swapped in this step on
-                               their own stream (default 0: main stream)             */
+  int32_t swapped_stream;   /* reserved (ignored)                                    */
   const char *store_path;   /* NULL: private pinned store; else a shared file mapping
                                (one copy per node for N ranks; host-registered)     */
   int64_t wave_rows_cap;    /* main-stream wave size cap (0: max_wave_rows)          */

@@ -248,7 +248,7 @@ struct coe_runtime {
   std::vector<int32_t> last_wave_cls, last_wave_rows, last_wave_groups;
   int64_t last_adm = 0, last_batches = 0;
   int last_set = 0;
-  cudaStream_t in_stream = nullptr, out_stream = nullptr;  // e2e input uploads / output downloads
+  cudaStream_t out_stream = nullptr;  // e2e output downloads (inputs ride the copy engine)
   std::vector<cudaEvent_t> in_ev;
   cudaEvent_t out_drained = nullptr;
   bool have_out = false;
@@ -284,7 +284,6 @@ struct coe_runtime {
       if (st) cudaStreamSynchronize(st);
     if (copy) cudaStreamSynchronize(copy);
     if (hop) cudaStreamSynchronize(hop);
-    if (in_stream) cudaStreamSynchronize(in_stream);
     if (out_stream) cudaStreamSynchronize(out_stream);
     for (auto &per : mlps)
       for (auto m : per)
@@ -323,7 +322,6 @@ struct coe_runtime {
       if (st) cudaStreamDestroy(st);
     if (copy) cudaStreamDestroy(copy);
     if (hop) cudaStreamDestroy(hop);
-    if (in_stream) cudaStreamDestroy(in_stream);
     if (out_stream) cudaStreamDestroy(out_stream);
   }
 
@@ -469,7 +467,6 @@ int coe_runtime_create(const coe_runtime_config *cfg, coe_runtime **out) {
               ok(cudaStreamCreateWithPriority(&rt->cls_stream[2], cudaStreamNonBlocking, prio_low), "stream") &&
               ok(cudaStreamCreateWithFlags(&rt->copy, cudaStreamNonBlocking), "stream") &&
               ok(cudaStreamCreateWithFlags(&rt->hop, cudaStreamNonBlocking), "stream") &&
-              ok(cudaStreamCreateWithFlags(&rt->in_stream, cudaStreamNonBlocking), "stream") &&
               ok(cudaStreamCreateWithFlags(&rt->out_stream, cudaStreamNonBlocking), "stream") &&
               dmalloc(&rt->x, act_bytes, "X alloc") && dmalloc(&rt->p0, act_bytes, "P0 alloc") &&
               dmalloc(&rt->p1, act_bytes, "P1 alloc") && dmalloc(&rt->outbuf, act_bytes, "out alloc") &&
@@ -665,7 +662,7 @@ int coe_runtime_download_outputs(coe_runtime *rt, const int32_t *last_stage_host
 
 int coe_runtime_synchronize(coe_runtime *rt) {
   bool good = ok(cudaStreamSynchronize(rt->copy), "sync copy") && ok(cudaStreamSynchronize(rt->hop), "sync hop") &&
-              ok(cudaStreamSynchronize(rt->in_stream), "sync in") && ok(cudaStreamSynchronize(rt->out_stream), "sync out");
+              ok(cudaStreamSynchronize(rt->out_stream), "sync out");
   for (int k = coe_runtime::NCLS - 1; k >= 0; --k) good = ok(cudaStreamSynchronize(rt->cls_stream[k]), "sync") && good;
   return good ? COE_CUDA_OK : fail_cuda();
 }
