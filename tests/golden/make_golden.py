@@ -102,6 +102,10 @@ def cases():
     out["c5_1k_g8"] = config_case("c5", 1000, gpu_executors=8)
     out["c2_10k"] = config_case("c2", 10000)
     out["c3_10k"] = config_case("c3", 10000)
+    out["c1_10k"] = config_case("c1", 10000)
+    out["c4_10k_g2"] = config_case("c4", 10000, gpu_executors=2)
+    out["c4_10k_g8"] = config_case("c4", 10000, gpu_executors=8)
+    out["c5_10k_g8"] = config_case("c5", 10000, gpu_executors=8)
     for policy in ("coserve", "coserve_em_ra", "coserve_em", "coserve_none", "samba_lru", "samba_fifo",
                    "samba_parallel"):
         out[f"numa_a80_{policy}"] = inline_case("numa-3080ti", 80, 300, 0.004, 3, policy=policy, seed=3,
