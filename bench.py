@@ -113,6 +113,58 @@ class ClockSampler:
                 "power_w_median": statistics.median(pw) if pw else None, "power_w_max": max(pw) if pw else None}
 
 
+class PcieSampler:
+    """NVML PCIe throughput counters (nvmlDeviceGetPcieThroughput: bytes over a ~20 ms window)
+    sampled on a thread during the timed region: hardware evidence for the swap-in link rate."""
+
+    def __init__(self, enabled: bool, gpu_index: int):
+        self.enabled, self.gpu = enabled, gpu_index
+        self.rx, self.tx = [], []
+        self._stop = None
+
+    def __enter__(self):
+        if not self.enabled:
+            return self
+        try:
+            import threading
+
+            import pynvml
+
+            pynvml.nvmlInit()
+            handle = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            self._stop = threading.Event()
+
+            def run():
+                while not self._stop.is_set():
+                    try:  # KB/s
+                        self.rx.append(pynvml.nvmlDeviceGetPcieThroughput(handle, pynvml.NVML_PCIE_UTIL_RX_BYTES))
+                        self.tx.append(pynvml.nvmlDeviceGetPcieThroughput(handle, pynvml.NVML_PCIE_UTIL_TX_BYTES))
+                    except Exception:
+                        return
+                    self._stop.wait(0.05)
+
+            self._thread = threading.Thread(target=run, daemon=True)
+            self._thread.start()
+        except Exception:
+            self._stop = None
+        return self
+
+    def __exit__(self, *exc):
+        if self._stop is not None:
+            self._stop.set()
+            self._thread.join(timeout=2)
+
+    def summary(self) -> dict | None:
+        if not self.rx:
+            return None
+        med = lambda v: statistics.median(v) * 1e3 / 1e9  # noqa: E731  (KB/s -> GB/s)
+        return {"h2d_rx_gbs_median": med(self.rx), "h2d_rx_gbs_max": max(self.rx) * 1e3 / 1e9,
+                "d2h_tx_gbs_median": med(self.tx), "samples": len(self.rx),
+                "source": "NVML nvmlDeviceGetPcieThroughput (GPU RX = host->device; raw link bytes incl. "
+                          "protocol overhead, sampled every ~50 ms; medians are the evidence, maxima are "
+                          "window artefacts)"}
+
+
 def plan_stats(plan) -> dict:
     """Swaps and bytes moved from the planner's op log (the reference's decisions)."""
     from paper_2503_02354_b200 import _native
@@ -264,7 +316,7 @@ def main() -> None:
     end = torch.cuda.Event(enable_timing=True)
     launches = 0
     stats = None
-    with ClockSampler(not args.no_clocks, local) as clocks:
+    with ClockSampler(not args.no_clocks, local) as clocks, PcieSampler(not args.no_clocks, local) as pcie:
         start.record(stream)
         for _ in range(args.steps):
             p = engine.plan(cfg)
@@ -400,7 +452,8 @@ def main() -> None:
                     "achieved_gbs": load_bytes / copy_s / 1e9 if copy_s > 0 else None, "peak_gbs": PCIE_H2D_GBS,
                     "copy_busy_ms": timing["copy_busy_ms"], "compute_busy_ms": timing["compute_busy_ms"],
                     "overlap_ms": timing["overlap_ms"],
-                    "overlap_frac_of_shorter": timing["overlap_ms"] / short if short > 0 else None},
+                    "overlap_frac_of_shorter": timing["overlap_ms"] / short if short > 0 else None,
+                    "pcie_counters": pcie.summary()},
         "grouping": {"admissions": stats["admissions"], "group_ms": timing["group_ms"], "runs": runs,
                      "violations": violations, "waves": stats["waves"]},
         "gpu_launches": launches,
