@@ -122,6 +122,13 @@ def load(name: str, requests: int = 1000, gpu_executors: int | None = None) -> W
     run = dict(cfg["run"])
     if gpu_executors is not None:
         run["gpu_executors"] = gpu_executors
+        # The reference's alloc_override counts experts for ALL gpu lanes of one device (its
+        # lanes share that device's memory: budget = bytes of the top-k experts / lanes,
+        # engine.py:436).  Here each executor is its own B200, so "12 GB per GPU" at N GPUs
+        # is an override of N x the single-GPU count.
+        ov = run.get("alloc_override")
+        if ov and "gpu" in ov and gpu_executors > 1:
+            run["alloc_override"] = dict(ov, gpu=int(ov["gpu"]) * gpu_executors)
     if run.get("alloc_override") is None:
         run.pop("alloc_override", None)
     return Workload(

@@ -105,6 +105,10 @@ def cases():
     out["c1_10k"] = config_case("c1", 10000)
     out["c4_10k_g2"] = config_case("c4", 10000, gpu_executors=2)
     out["c4_10k_g8"] = config_case("c4", 10000, gpu_executors=8)
+    # the multi-GPU configurations as benched: 12 GB per GPU (override scales with the GPU count)
+    for n in (2, 4, 8):
+        out[f"c4_10k_g{n}_pergpu"] = config_case("c4", 10000, gpu_executors=n, alloc_override={"gpu": 59 * n})
+        out[f"c3_10k_g{n}_pergpu"] = config_case("c3", 10000, gpu_executors=n, alloc_override={"gpu": 59 * n})
     out["c5_10k_g8"] = config_case("c5", 10000, gpu_executors=8)
     for policy in ("coserve", "coserve_em_ra", "coserve_em", "coserve_none", "samba_lru", "samba_fifo",
                    "samba_parallel"):
