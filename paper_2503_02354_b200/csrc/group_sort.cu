@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(1024) scan_rows(uint32_t *hist, int num_tiles,
 // warp-local ranks into tile positions -- then writes the locally sorted tile out so that
 // consecutive threads store consecutive addresses of a digit's output segment (coalesced).
 template <int ITEMS>
-__global__ void __launch_bounds__(SORT_THREADS) radix_scatter(const uint32_t *keys_in, const int32_t *vals_in,
+__global__ void __launch_bounds__(SORT_THREADS, 3) radix_scatter(const uint32_t *keys_in, const int32_t *vals_in,
                                                               uint32_t *keys_out, int32_t *vals_out,
                                                               const uint32_t *offsets, const uint32_t *row_total,
                                                               int64_t n, int shift, int num_tiles) {
