@@ -342,9 +342,10 @@ def main() -> None:
     e2e = None
     if not args.no_e2e and args.e2e_steps > 0:
         row = rt.shapes[0].T * rt.act_ld
-        host_in = torch.empty(n_req * row, dtype=torch.bfloat16).pin_memory()
-        host_out = torch.empty(n_req * row, dtype=torch.bfloat16).pin_memory()
-        rt.read_buffer(0, host_in.data_ptr(), n_req * row * 2)  # the seeded inputs, copied once (untimed)
+        n_in, n_out = runtime.io_rows(plan0, rank)  # this executor's inputs / outputs only
+        host_in = torch.empty(max(1, n_in) * row, dtype=torch.bfloat16).pin_memory()
+        host_out = torch.empty(max(1, n_out) * row, dtype=torch.bfloat16).pin_memory()
+        rt.read_buffer(0, host_in.data_ptr(), n_in * row * 2)  # synthetic input rows, copied once (untimed)
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         io = None

@@ -150,8 +150,9 @@ typedef struct coe_step_input {
   const int32_t *op_args;
   int32_t num_initial;                      /* initial residency of this executor          */
   const int32_t *initial;
-  /* end-to-end serving (optional, pinned host memory, [requests][T][ld] bf16): inputs are
-   * indexed by request and uploaded just in time on the copy engine; outputs are streamed
+  /* end-to-end serving (optional, pinned host memory, [rows][T][ld] bf16): input row i holds
+   * the i-th smallest request whose stage 0 runs on this executor (with one executor: row r =
+   * request r), uploaded just in time on the copy engine; outputs are streamed
    * back in COMPLETION order -- each wave's final rows are gathered on the GPU and leave in
    * one D2H copy -- and coe_runtime_output_order names the request of every output row */
   const void *host_inputs;

@@ -1651,11 +1651,11 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     std::vector<int32_t> rq(in_reqs.begin() + lo, in_reqs.begin() + hi);
     std::vector<void *> dsts, srcs;
     std::vector<size_t> sizes;
-    for (size_t i = 0; i < rq.size();) {
+    for (size_t i = 0; i < rq.size();) {  // host row lo + i holds request rq[i] (this executor's order)
       size_t j = i + 1;
       while (j < rq.size() && rq[j] == rq[j - 1] + 1) ++j;
       dsts.push_back(reinterpret_cast<char *>(x_step) + rq[i] * rb);
-      srcs.push_back(const_cast<char *>(hin) + rq[i] * rb);
+      srcs.push_back(const_cast<char *>(hin) + (lo + i) * rb);
       sizes.push_back((j - i) * rb);
       st.h2d_input_bytes += (int64_t)((j - i) * rb);
       i = j;

@@ -531,6 +531,19 @@ def hops_from_plan(plan) -> list:
     return [(int(idx[i]), int(cols[0][i]), int(cols[1][i]), int(cols[2][i]), int(cols[3][i])) for i in range(n)]
 
 
+def io_rows(plan, executor: int = 0) -> tuple:
+    """e2e host buffer rows for one executor: (stage-0 requests it uploads, final outputs it
+    returns).  host_inputs row i is the i-th smallest such request; outputs come back in
+    completion order (``B200Runtime.output_order``)."""
+    chains = plan.resolved.chains
+    n_in = n_out = 0
+    for _e, members in batches_from_plan(plan, executor):
+        for r, s in members:
+            n_in += s == 0
+            n_out += s == len(chains[r]) - 1
+    return n_in, n_out
+
+
 def batches_from_plan(plan, executor: int = 0) -> list:
     """(expert, [(request, stage), ...]) per planned batch of ``executor``, in op order."""
     ops = plan.ops()
