@@ -388,3 +388,38 @@ def test_c3_full_shape_swapped_experts():
         worst = max(worst, mlp.rel_l2(out[r], mlp.chain_forward(x, chains[r], weights)))
     rt.close()
     assert worst <= TOL, worst
+
+
+def test_consecutive_different_plans_share_one_runtime():
+    """A serving runtime steps through DIFFERENT plans (two disjoint slices of the config-3
+    stream, at the mini shape) back to back: slot state left by the first plan (swapped-in
+    experts, evicted initial ones) is reconciled with the second plan's initial placement,
+    the second plan's loads move exactly its bytes, and both match the oracle."""
+    import torch
+
+    shape = runtime.RuntimeShape(1024, 2048, 64)
+    plans, ws = [], []
+    for lo, hi in ((0, 300), (300, 600)):
+        w = configs.load("c3", 1000)
+        w.stream = w.stream[lo:hi]
+        w.docs = dict(w.docs, stream={"schema_version": 1, "requests": w.docs["stream"]["requests"][lo:hi]})
+        plans.append(engine.plan(configs.run_config(w, trace=False)))
+        ws.append(w)
+    assert [int(o["expert"]) for o in plans[0].ops()] != [int(o["expert"]) for o in plans[1].ops()]
+    # a long-lived serving runtime: every expert in the host store, slots = the 12 GB budget
+    n = len(plans[0].resolved.request_ids)
+    adm = max(sum(len(c) for c in p.resolved.chains) for p in plans)
+    rt = runtime.B200Runtime(shape, num_experts=len(plans[0].resolved.expert_ids), num_slots=59, max_requests=n,
+                             max_admissions=adm)
+    rt.fill_inputs(n)
+    for w, plan in zip(ws + ws[::-1], plans + plans[::-1]):  # A, B, B, A
+        _check_against_oracle_batches(w, plan)
+        st = rt.step(plan)
+        rt.synchronize()
+        _check_grouping(plan, rt, st)
+        assert st["loads"] == sum(1 for o in plan.ops() if o["kind"] == 0)
+        host = torch.empty(n * shape.T * shape.d, dtype=torch.bfloat16).pin_memory()
+        rt.download_outputs(runtime.last_stages(plan), host.data_ptr())
+        rt.synchronize()
+        _check_outputs(plan, [host.view(n, shape.T, shape.d).float().numpy()], shape, sample=8)
+    rt.close()
