@@ -283,10 +283,21 @@ def main() -> None:
     transport = os.environ.get("COE_HOP_TRANSPORT", "peer")
     if dist is not None:
         dist.barrier()  # local rank 0 has filled the shared store
+        if transport != "nccl":
+            try:
+                rt.attach_peers_ipc(rank, world)  # hops fused into K3's down pass (NVLink peer stores)
+            except RuntimeError as exc:  # no IPC / peer access on this box: keep serving over NCCL
+                print(f"rank {rank}: fused peer hops unavailable ({exc}); using NCCL send/recv", file=sys.stderr)
+                transport = "nccl"
+            ok = torch.tensor([1 if transport != "nccl" else 0], device=red_dev)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)  # every rank must use the same transport
+            if int(ok.item()) == 0 and transport != "nccl":
+                transport = "nccl"
+                rt.close()  # drop this rank's peer mappings; a fresh runtime serves over NCCL
+                rt = runtime.B200Runtime.for_plan(plan0, shape, executor=rank, profile=True, store_path=store_path,
+                                                  init_experts=(store_path is None or local == 0))
         if transport == "nccl":
             rt.attach_comm(rank, world)  # NCCL send/recv pairs on a hop stream
-        else:
-            rt.attach_peers_ipc(rank, world)  # hops fused into K3's down pass (NVLink peer stores)
     rt.fill_inputs(n_req)
     stream = torch.cuda.ExternalStream(rt.stream_handle(0))
 
