@@ -91,3 +91,20 @@ def test_single_request_and_duplicate_ids():
     dup = [w.stream[0], w.stream[1], w.stream[0]]
     m2, _ = engine.run(configs.run_config(w, stream=dup))
     assert m2.completed_requests == 2  # reference dict semantics: ids are unique keys
+
+
+def test_multi_gpu_configs_give_each_gpu_its_own_budget():
+    """configs.load(..., gpu_executors=N): one executor per B200, so the reference's
+    alloc_override (an expert count for all lanes of ONE device) scales with N and every
+    executor gets the single-GPU 12 GB regime (59 x 201 MB), capped by the registry."""
+    from paper_2503_02354_b200 import configs, engine
+
+    one = engine.resolve(configs.run_config(configs.load("c3", 1000)))
+    b1 = one.alloc["gpu"]["expert_budget_bytes"]
+    for n in (2, 4):
+        r = engine.resolve(configs.run_config(configs.load("c3", 1000, gpu_executors=n)))
+        assert len(r.executors) == n
+        assert r.alloc["gpu"]["expert_budget_bytes"] == b1
+    r8 = engine.resolve(configs.run_config(configs.load("c3", 1000, gpu_executors=8)))
+    total = sum(s.param_bytes for s in r8.config.registry.experts.values())
+    assert r8.alloc["gpu"]["expert_budget_bytes"] == total / 8  # all 300 experts fit: full residency
