@@ -423,3 +423,34 @@ def test_consecutive_different_plans_share_one_runtime():
         rt.synchronize()
         _check_outputs(plan, [host.view(n, shape.T, shape.d).float().numpy()], shape, sample=8)
     rt.close()
+
+
+@pytest.mark.parametrize("pick", ["one_request", "one_component", "first_stage_only"])
+def test_degenerate_streams(pick):
+    """Edge cases through the whole GPU path: a single request; every request of one
+    component (one long run, batches capped by the profiled max batch); only requests whose
+    chain stops at the first stage.  Grouping exact, outputs match the numpy fp32 chain."""
+    import torch
+
+    w = configs.load("c1", 1000)
+    reqs = w.docs["stream"]["requests"]
+    if pick == "one_request":
+        keep = [0]
+    elif pick == "one_component":
+        comp = reqs[0]["component_type"]
+        keep = [i for i, r in enumerate(reqs) if r["component_type"] == comp][:120]
+    else:
+        plan_all = engine.plan(configs.run_config(w, trace=False))
+        keep = [i for i, c in enumerate(plan_all.resolved.chains) if len(c) == 1][:150]
+    assert keep
+    w.stream = [w.stream[i] for i in keep]
+    w.docs = dict(w.docs, stream={"schema_version": 1, "requests": [reqs[i] for i in keep]})
+    shape = runtime.shape_of(w)
+    plan, rt, stats, outs = _serve(w, shape, steps=2)
+    _check_against_oracle_batches(w, plan)
+    _check_grouping(plan, rt, stats[-1])
+    _check_outputs(plan, outs, shape, sample=min(8, len(keep)))
+    if pick == "one_component":  # one long run split into max-batch slices
+        sizes = [len(m) for _e, m in runtime.batches_from_plan(plan)]
+        assert len(sizes) > 1 and max(sizes) == max(e.max_batch for e in plan.resolved.perf.entries.values())
+    rt.close()
