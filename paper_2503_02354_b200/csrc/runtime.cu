@@ -1289,13 +1289,13 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
   const int64_t wave_rows_cap = c.wave_rows_cap > 0 ? std::min<int64_t>(c.wave_rows_cap, c.max_wave_rows)
                                                     : c.max_wave_rows;
   const int64_t urgent_rows_cap = c.urgent_rows_cap > 0 ? c.urgent_rows_cap : wave_rows_cap;
-  const int urgent_horizon = 2;
+  const int urgent_horizon = getenv("COE_URGENT_HORIZON") ? atoi(getenv("COE_URGENT_HORIZON")) : 2;
   // Swap-ins may leave op order within a small window: a copy whose victim slot is still
   // being read (e.g. the expert the previous copy brought in, evicted right after its
   // batches) must not idle the copy engine while a later copy's slot is already free.  The
   // planner's decisions are unaffected -- only the physical order of slot writes changes;
   // two copies into the same slot keep their order.
-  const size_t kCopyWindow = 8;
+  const size_t kCopyWindow = getenv("COE_COPY_WINDOW") ? (size_t)atoi(getenv("COE_COPY_WINDOW")) : 8;
   size_t copy_pick = 0;
   // e2e: the stage-0 input uploads ride the same copy engine (one H2D queue): in op order with
   // the swap-ins, and ahead of a swap-in whose victim slot is still being read -- the PCIe
