@@ -454,3 +454,62 @@ def test_degenerate_streams(pick):
         sizes = [len(m) for _e, m in runtime.batches_from_plan(plan)]
         assert len(sizes) > 1 and max(sizes) == max(e.max_batch for e in plan.resolved.perf.entries.values())
     rt.close()
+
+
+def test_c4_full_shape_two_executors_fused_hops():
+    """Config 4 at its real expert shape (4096 x 12288, T = 256) with two executors sharing
+    the GPU, 12 GB each, fused hops between them: exact grouping per executor, the planner's
+    loads, and hopped requests' final outputs match the numpy fp32 chain."""
+    import torch
+
+    w = _trim(configs.load("c4", 1000, gpu_executors=2), 160)
+    plan = engine.plan(configs.run_config(w, trace=False))
+    _check_against_oracle_batches(w, plan)
+    hops = runtime.hops_from_plan(plan)
+    assert hops
+    shape = runtime.shape_of(w)
+    assert (shape.d, shape.h, shape.T) == (4096, 12288, 256)
+    rts = [runtime.B200Runtime.for_plan(plan, shape, executor=x) for x in range(2)]
+    n = len(plan.resolved.request_ids)
+    for rt in rts:
+        rt.fill_inputs(n)
+    hub = runtime.attach_peers_local(rts)
+    stats = runtime.step_executors(plan, rts, hub)
+    chains = plan.resolved.chains
+    final_exec = {}
+    outs = []
+    for x, rt in enumerate(rts):
+        _, violations = rt.check()
+        assert violations == 0
+        assert stats[x]["loads"] == sum(1 for o in plan.ops() if o["kind"] == 0 and o["executor"] == x)
+        for _e, members in runtime.batches_from_plan(plan, executor=x):
+            for r, s in members:
+                if s == len(chains[r]) - 1:
+                    final_exec[r] = x
+        host = torch.empty(n * shape.T * shape.d, dtype=torch.bfloat16).pin_memory()
+        rt.download_outputs(runtime.last_stages(plan), host.data_ptr())
+        rt.synchronize()
+        outs.append(host.view(n, shape.T, shape.d).float().numpy().copy())
+    hopped = sorted({h[3] for h in hops})
+    picks, experts = [], set()
+    for r in hopped:  # hopped requests, few distinct weights to regenerate
+        if len(experts | set(chains[r])) <= 5:
+            picks.append(r)
+            experts |= set(chains[r])
+        if len(picks) == 3:
+            break
+    assert picks
+    cache = {}
+
+    def weights(e):
+        if e not in cache:
+            cache[e] = synth.expert_weights(runtime.DEFAULT_WEIGHT_SEED, e, shape.d, shape.h)
+        return cache[e]
+
+    worst = 0.0
+    for r in picks:
+        x = synth.request_inputs(runtime.DEFAULT_INPUT_SEED, r, shape.T, shape.d)
+        worst = max(worst, mlp.rel_l2(outs[final_exec[r]][r], mlp.chain_forward(x, chains[r], weights)))
+    for rt in rts:
+        rt.close()
+    assert worst <= TOL, worst
