@@ -8,21 +8,29 @@
 //   mode 0 (up):   H[g]   = gelu(X[g] . W1[slot_g]^T)   X rows gathered per request
 //   mode 1 (down): Y[g]   = H[g] . W2[slot_g]^T          Y rows scattered per request
 //
-// Activations are [requests*T, d] row blocks: stage 0 reads the request
-// inputs X, stage s > 0 reads ping-pong buffer P[(s-1)&1]; the output of stage
-// s is written to P[s&1] (so X stays pristine across steps).  Which requests form a group comes from the GPU grouping
-// (coe_group_sort / coe_run_compact): member_req/member_stage are the sorted
-// admissions and batch_off the start of each planned batch inside them.
+// Activations are [requests*T, ld] row blocks: stage 0 reads the request inputs X,
+// stage s > 0 reads ping-pong buffer P[(s-1)&1]; the output of stage s is written to
+// P[s&1] (so X stays pristine across steps) -- or, for a request whose next stage runs
+// on another executor, straight into that executor's P (fused hop, coe_mlp_set_hops).
+// Which requests form a group comes from the GPU grouping (coe_group_sort /
+// coe_run_compact): member_req/member_stage are the sorted admissions and batch_off the
+// start of each planned batch inside them.
 //
-// Kernel shape: persistent, one CTA per SM, warp-specialised --
-//   warp 0: TMA producer (A: per-request row boxes, B: one 3-D box of the
-//           expert-slot weight tensor), 4-stage smem ring, mbarrier handshake;
-//   warp 1: single-thread tcgen05.mma issuer, 128x256x16 bf16 -> f32 into a
-//           double-buffered TMEM accumulator (2 x 256 columns);
-//   warp 2: TMEM allocator;
-//   warps 4-7: epilogue, tcgen05.ld 32x32b -> gelu/convert -> bf16 stores.
-// Tiles are walked m-fastest inside (group, n-block) so concurrently running
-// CTAs share the same weight tile through L2.
+// Kernel shape (default CG = 2): persistent, warp-specialised, CTA PAIRS -- a cluster of
+// 2 CTAs on one TPC computes a 256 x 256 tile with tcgen05.mma.cta_group::2:
+//   warp 0: TMA producer in each CTA: its own 128 A rows (per-request row boxes) and HALF
+//           of B (128 rows of the expert-slot weight tensor), 6-stage 32 KB smem ring;
+//           the .cta_group::2 loads complete on the LEADER CTA's mbarrier;
+//   warp 1: leader only: single-thread issuer of 256x256x16 bf16 -> f32 MMAs into a
+//           double-buffered TMEM accumulator (2 x 256 columns per CTA); multicast
+//           commits free the stage / publish the accumulator in both CTAs;
+//   warp 2: TMEM allocator (cta_group::2 in both CTAs); warp 3: tile-table scan;
+//   warps 4-11: epilogue, two warps per TMEM lane quarter (half the columns each),
+//           tcgen05.ld one 32-column chunk ahead -> gelu / bf16 -> stores; one lane per
+//           warp signals the leader's TMEM-empty barrier.
+// CG = 1 (COE_K3_CG=1) is the single-CTA 128 x 256 variant (4-stage 48 KB ring).
+// Tiles are walked m-fastest inside (group, n-block) so concurrently running pairs share
+// the same weight tile through L2.
 
 #include <cuda_bf16.h>
 
