@@ -5,27 +5,28 @@
 // /root/reference/pkg/src/coesim/engine.py:643-758); here the same op log is
 // *executed*:
 //
-//   copy stream:    the step's plan upload, then K4 swap-ins (pinned host
-//                   expert store -> HBM slot), each half of an expert (W1 |
-//                   W2) issued as soon as the slot's last reader of that half
-//                   has finished -- dependency-aware prefetch
-//   compute stream: K1 group sort -> K2 run compaction -> waves of K3 grouped
-//                   expert MLPs; a wave's up-projection waits only for the W1
-//                   halves it needs, its down-projection for the W2 halves
+//   copy stream:     the step's plan upload, then K4 swap-ins (pinned host expert
+//                    store -> HBM slot), each half of an expert (W1 | W2) issued as soon
+//                    as the slot's last reader of that half has finished -- dependency-
+//                    aware prefetch -- and, end to end, the stage-0 input chunks
+//   compute streams: K1 group sort -> K2 run compaction, then waves of K3 grouped expert
+//                    MLPs on two alternating main streams plus a high-priority release
+//                    stream; a wave's up projection waits only for the W1 halves it needs,
+//                    its down projection for the W2 halves; the down pass stores hopping
+//                    rows into the destination executor (fused hops, peer mode)
+//   output stream:   end to end, each wave's gathered final rows, one D2H copy
 //
-// Physical layout (HBM): `num_slots` fixed expert slots ([W1 h*d | W2 d*h]
-// bf16; the planner's ModelPool budget / expert bytes), the request inputs X,
-// ping-pong activations P0/P1, the H scratch of a wave, double-buffered step
-// arrays.  Host: one pinned store of every expert (the host tier, types.py:17).
+// Physical layout (HBM): fixed expert slots per shape ([W1 h*d | W2 d*h] bf16; the
+// planner's ModelPool budget / expert bytes), the request inputs X (two buffers end to
+// end), ping-pong activations P0/P1, the H scratch of a wave per stream, double-buffered
+// step arrays.  Host: one pinned store of the experts this executor touches (the host
+// tier, types.py:17).
 //
-// Host pass 1 turns the op log into actions (COPY / WAVE): slot assignment
-// (victim slots are reused; initial-residency experts missing after the
-// previous step are restored lazily, at first use, so a step always starts
-// from initialize_pools' placement), wave cuts (a wave closes before a batch
-// that must wait for a copy, that touches a request already in the wave, or
-// that overflows the H scratch; a batch that is the last reader of a slot
-// some later LOAD overwrites runs as its own wave, so that swap-in waits for
-// nothing else).  Pass 2 issues them.  Timing never feeds back into decisions.
+// Phase A walks the op log (slot assignment: victim slots are reused; initial-residency
+// experts missing after the previous step are restored lazily at first use, so a step
+// always starts from initialize_pools' placement; data dependencies; hops).  Phase B
+// list-schedules copies, input chunks and waves on estimated clocks.
+// Phase C issues them with explicit events.  Timing never feeds back into decisions.
 
 #include <cuda.h>
 #include <cuda_bf16.h>
