@@ -11,6 +11,15 @@ if TESTS not in sys.path:
     sys.path.insert(0, TESTS)
 
 
+def pytest_sessionstart(session):
+    """Build the in-tree native libraries if they are missing or older than their sources
+    (build.py is incremental: a no-op when they are current)."""
+    import build
+
+    build.build_planner()
+    build.build_cuda()
+
+
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (sm_100a) and the built CUDA library")
     config.addinivalue_line("markers", "slow: long-running CPU test")
