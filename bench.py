@@ -414,8 +414,11 @@ def main() -> None:
     if os.path.exists(ncu_path):
         with open(ncu_path) as fh:
             ncu = json.load(fh)
-        traffic = ncu.get("dram_bytes_per_launch")  # the profiled wave's average up/down launch
-        traffic_algo = ncu.get("algorithmic_bytes_per_launch")
+        # the capture of this config's expert shape (the same isolated wave), else no traffic figure
+        cap = ncu.get("shapes", {}).get(f"{k3_shape.d}x{k3_shape.h}x{k3_shape.T}")
+        if cap is not None:
+            traffic = cap.get("dram_bytes_per_launch")  # the profiled wave's average up/down launch
+            traffic_algo = cap.get("algorithmic_bytes_per_launch")
     load_bytes = stats["load_bytes"] + stats["restore_bytes"]
     registry = plan_last.resolved.config.registry
     expert_gb = sum(spec.param_bytes for spec in registry.experts.values()) / 1e9
@@ -446,7 +449,7 @@ def main() -> None:
                      "peak_source": f"{peak_src} bf16_tflops_sustained (K3 timed inside the serving step)",
                      "traffic": traffic,
                      "traffic_note": "dram__bytes_read+write per launch from profiles/k3_ncu_summary.json (ncu --set "
-                                     "full of the isolated wave below); algorithmic bytes per launch "
+                                     "full of the isolated wave below, this expert shape; null if not captured); algorithmic bytes per launch "
                                      f"{traffic_algo}",
                      "measured_over": {"k3_launches_per_step": timing["k3_launches"],
                                        "algorithmic_flops_per_step": flops,

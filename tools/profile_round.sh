@@ -13,8 +13,13 @@ timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/$
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 4000 --csv \
   --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline --no-clocks \
   > gpurun_out/${TAG}_ncu_launches.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:grouped_gemm -c 2 -f \
-  -o gpurun_out/k3_full python tools/k3_profile.py 16 6 1 > gpurun_out/${TAG}_ncu_k3.log 2>&1
+# K3: the bench's isolated wave for each config's expert shape (groups x max batch), C3 / C2 / C1
+for w in "16 6 4096 12288 256" "11 22 2048 8192 128" "11 44 1024 4096 64"; do
+  set -- $w
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:grouped_gemm -c 2 -f \
+    -o gpurun_out/k3_full_$1_$2_$3x$4x$5 python tools/k3_profile.py $1 $2 1 $3 $4 $5 \
+    > gpurun_out/${TAG}_ncu_k3_$3.log 2>&1
+done
 timeout 900 ncu --set full --clock-control none -k regex:"make_keys|radix|scan|compact" -c 12 -f \
   -o gpurun_out/k12_full python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline --no-clocks \
   > gpurun_out/${TAG}_ncu_k12.log 2>&1

@@ -2,9 +2,9 @@
 
     python tools/summarize_profiles.py <round-tag>
 Reads gpurun_out/launches.csv (gpu__time_duration.sum launch list) and
-gpurun_out/k3_full.ncu-rep (--set full capture of grouped_gemm_kernel).
+gpurun_out/k3_full_*.ncu-rep (--set full captures of grouped_gemm_kernel, one per config shape).
 """
-import collections, csv, io, json, os, subprocess, sys
+import collections, csv, io, json, os, re, subprocess, sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "gpurun_out")
@@ -38,8 +38,7 @@ def launches():
     return "\n".join(lines) + "\n", {k: {"launches": cnt[k], "ms": tot[k], "share": tot[k] / total} for k in tot}
 
 
-def full():
-    path = os.path.join(OUT, "k3_full.ncu-rep")
+def full(path):
     if not os.path.exists(path):
         return None
     raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
@@ -101,22 +100,34 @@ if res:
     text, table = res
     open(os.path.join(PROF, f"{tag}_launches_summary.txt"), "w").write(text)
     print(text)
-kf = full()
-if kf:
-    G, R, T, d, h = 16, 6, 256, 4096, 12288  # tools/profile_round.sh: k3_profile.py 16 6 (the bench's wave)
+# K3 captures: gpurun_out/k3_full_<G>_<R>_<d>x<h>x<T>.ncu-rep (tools/profile_round.sh: one isolated wave per
+# config shape, the bench's own wave), merged into profiles/k3_ncu_summary.json keyed by "<d>x<h>x<T>"
+ncu_json = os.path.join(PROF, "k3_ncu_summary.json")
+summary = json.load(open(ncu_json)) if os.path.exists(ncu_json) else {}
+summary = summary if "shapes" in summary else {"shapes": {}}
+for fn in sorted(os.listdir(OUT)) if os.path.isdir(OUT) else []:
+    m = re.fullmatch(r"k3_full_(\d+)_(\d+)_(\d+)x(\d+)x(\d+)\.ncu-rep", fn)
+    if not m:
+        continue
+    G, R, d, h, T = (int(v) for v in m.groups())
+    kf = full(os.path.join(OUT, fn))
+    if not kf:
+        continue
     rows = G * R * T
-    k3 = {"launches": kf, "note": f"ncu --set full --clock-control none, tools/k3_profile.py {G} {R}: one wave of "
-                                  f"{G} batches x {R} requests x T={T} ({rows} rows), d={d} h={h} (the bench's "
-                                  "isolated wave); launch 0 = up projection (gelu), launch 1 = down projection; "
-                                  "CTA-pair kernel (tcgen05.mma.cta_group::2)",
+    k3 = {"launches": kf, "note": f"{tag}: ncu --set full --clock-control none, tools/k3_profile.py {G} {R} 1 {d} {h} "
+                                  f"{T}: one wave of {G} batches x {R} requests x T={T} ({rows} rows), d={d} h={h} (the "
+                                  "bench's isolated wave for this shape); launch 0 = up projection (gelu), launch 1 = "
+                                  "down projection; CTA-pair kernel (tcgen05.mma.cta_group::2)",
           "flops_per_launch": 2.0 * rows * d * h}
     k3["dram_bytes_per_wave"] = sum(l["dram_read"] + l["dram_write"] for l in kf)
     k3["dram_bytes_per_launch"] = k3["dram_bytes_per_wave"] / len(kf)
     # weights once + activations in/out, per projection: up reads X (rows x d) writes H (rows x h)
     k3["algorithmic_bytes_per_wave"] = 2 * (G * d * h * 2) + 2 * (rows * d * 2) + 2 * (rows * h * 2)
     k3["algorithmic_bytes_per_launch"] = k3["algorithmic_bytes_per_wave"] / 2
-    json.dump(k3, open(os.path.join(PROF, f"k3_ncu_summary.json"), "w"), indent=1)
-    print(json.dumps(k3, indent=1))
+    summary["shapes"][f"{d}x{h}x{T}"] = k3
+    print(fn, json.dumps(k3, indent=1))
+if summary["shapes"]:
+    json.dump(summary, open(ncu_json, "w"), indent=1)
 
 kg = grouping()
 if kg:
