@@ -12,12 +12,15 @@
 // finds their offsets, gathers (request, stage) members for the grouped MLP,
 // counts runs and flags any batch that would straddle two runs.
 //
-// Layout: SoA int32 arrays; 4096-key tiles (256 threads x 16).  Per 8-bit pass:
-// per-tile digit counts -> per-digit row scans (one block per digit) -> a stable
-// in-shared-memory ranking of each tile (warp match_any) written out digit-segment by
-// digit-segment, so the global stores are coalesced.  HBM-bound integer work at scale
-// (20 B moved per key per pass); launch-latency-bound at serving size.
+// Layout: SoA int32 arrays; 4096-key tiles (256 threads x 16; 1024-key tiles up to 1M keys).
+// One read of (executor, run_rank) counts every pass's digits; then ONE kernel per 8-bit
+// pass: a stable in-shared-memory ranking of each tile (warp match_any), the tile's
+// per-digit offsets by decoupled look-back over its predecessors, and a coalesced
+// digit-segment write-out.  The first pass builds the keys on the fly.  HBM-bound integer
+// work at scale (8 B for the counting read + 16 B moved per key per pass); launch-latency-
+// bound at serving size (a memset + 1 + passes launches).
 
+#include <algorithm>
 #include <cstdint>
 #include <string>
 
@@ -29,134 +32,111 @@
 namespace {
 
 constexpr int SORT_THREADS = 256;
-// keys per thread per tile: 16 (4096-key tiles) at scale, 4 (1024-key tiles) for serving-size
-// steps, where the per-tile ranking rounds are the serial chain and more CTAs help
+// keys per thread per tile: 16 (4096-key tiles) at scale -- fewer, larger tiles shorten the
+// look-back chains (measured at 16.8M keys: 2048-key tiles 16 % slower, 1024-key tiles 74 %) --
+// and 4 (1024-key tiles) for serving-size steps, where more CTAs help
 constexpr int ITEMS_LARGE = 16, ITEMS_SMALL = 4;
 constexpr int64_t SMALL_SORT_MAX = 1 << 20;
 constexpr int RADIX = 256;
 constexpr int SORT_WARPS = SORT_THREADS / 32;
 
-__global__ void make_keys(const int32_t *exec, const int32_t *rank, int64_t n, int rank_bits, uint32_t *keys,
-                          int32_t *vals) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < n) {
-    keys[i] = ((uint32_t)exec[i] << rank_bits) | (uint32_t)rank[i];
-    vals[i] = (int32_t)i;
-  }
+constexpr int MAX_PASSES = 4;
+// decoupled look-back words: bits 31:30 = status (0 not ready, 1 tile aggregate, 2 inclusive
+// prefix), bits 29:0 = count (n < 2^30)
+constexpr uint32_t LB_AGG = 1u << 30, LB_INC = 2u << 30, LB_VAL = LB_AGG - 1u;
+
+__device__ __forceinline__ uint32_t sort_key(const int32_t *exec, const int32_t *rank, int64_t i, int rank_bits) {
+  return ((uint32_t)exec[i] << rank_bits) | (uint32_t)rank[i];
 }
 
-// Pass step 1: per-tile digit counts (coalesced key reads, warp-private smem histograms),
-// stored digit-major: hist[digit * num_tiles + tile].
+// Step 0: the global digit counts of EVERY pass in one read of (executor, run_rank) -- a
+// digit's total does not depend on the order the keys are in (block-private shared
+// histograms, warp-aggregated: nearly sorted serving keys share digits within a warp).
 template <int ITEMS>
-__global__ void __launch_bounds__(SORT_THREADS) radix_hist(const uint32_t *keys, int64_t n, int shift, int num_tiles,
-                                                           uint32_t *hist) {
+__global__ void __launch_bounds__(SORT_THREADS) radix_global_hist(const int32_t *exec, const int32_t *rank, int64_t n,
+                                                                  int rank_bits, int num_passes, uint32_t *ghist) {
   constexpr int TILE = SORT_THREADS * ITEMS;
-  __shared__ uint32_t h[SORT_WARPS][RADIX];
-  for (int j = threadIdx.x; j < SORT_WARPS * RADIX; j += SORT_THREADS) (&h[0][0])[j] = 0;
+  __shared__ uint32_t h[MAX_PASSES][RADIX];
+  for (int j = threadIdx.x; j < MAX_PASSES * RADIX; j += SORT_THREADS) (&h[0][0])[j] = 0;
   __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t base = (int64_t)blockIdx.x * TILE;
-  uint32_t kreg[ITEMS];  // all loads first: ITEMS independent requests in flight per thread
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = (int64_t)blockIdx.x * TILE; base < n; base += (int64_t)gridDim.x * TILE) {
+    uint32_t kreg[ITEMS];
 #pragma unroll
-  for (int r = 0; r < ITEMS; ++r) {
-    const int64_t i = base + r * SORT_THREADS + threadIdx.x;
-    kreg[r] = i < n ? keys[i] : 0u;
-  }
-#pragma unroll
-  for (int r = 0; r < ITEMS; ++r) {
-    // warp-aggregated: one shared atomic per distinct digit in the warp (serving keys are
-    // nearly sorted, so most of a warp shares a digit in the high passes)
-    const int64_t i = base + r * SORT_THREADS + threadIdx.x;
-    const uint32_t digit = i < n ? (kreg[r] >> shift) & 255u : 256u;
-    const uint32_t same = __match_any_sync(0xffffffffu, digit);
-    if (digit < 256u && (same & ((1u << lane) - 1u)) == 0) atomicAdd(&h[warp][digit], __popc(same));
-  }
-  __syncthreads();
-  uint32_t c = 0;
-#pragma unroll
-  for (int w = 0; w < SORT_WARPS; ++w) c += h[w][threadIdx.x];
-  hist[(int64_t)threadIdx.x * num_tiles + blockIdx.x] = c;
-}
-
-// Pass step 2: one block per digit scans that digit's row of tile counts in place (exclusive)
-// and writes the row total.
-__global__ void __launch_bounds__(1024) scan_rows(uint32_t *hist, int num_tiles, uint32_t *row_total) {
-  __shared__ uint32_t warp_sums[32];
-  __shared__ uint32_t carry;
-  uint32_t *row = hist + (int64_t)blockIdx.x * num_tiles;
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  if (t == 0) carry = 0;
-  __syncthreads();
-  for (int base = 0; base < num_tiles; base += 1024) {
-    const int i = base + t;
-    const uint32_t v = i < num_tiles ? row[i] : 0u;
-    uint32_t x = v;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, x, off);
-      if (lane >= off) x += y;
+    for (int r = 0; r < ITEMS; ++r) {  // all loads first
+      const int64_t i = base + r * SORT_THREADS + threadIdx.x;
+      kreg[r] = i < n ? sort_key(exec, rank, i, rank_bits) : 0u;
     }
-    if (lane == 31) warp_sums[warp] = x;
-    __syncthreads();
-    if (warp == 0) {
-      uint32_t w = warp_sums[lane];
 #pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, w, off);
-        if (lane >= off) w += y;
+    for (int r = 0; r < ITEMS; ++r) {
+      const bool valid = base + r * SORT_THREADS + threadIdx.x < n;
+      for (int p = 0; p < num_passes; ++p) {
+        const uint32_t digit = valid ? (kreg[r] >> (8 * p)) & 255u : 256u;
+        const uint32_t same = __match_any_sync(0xffffffffu, digit);
+        if (digit < 256u && (same & ((1u << lane) - 1u)) == 0) atomicAdd(&h[p][digit], __popc(same));
       }
-      warp_sums[lane] = w;
     }
-    __syncthreads();
-    const uint32_t incl = x + (warp ? warp_sums[warp - 1] : 0u) + carry;
-    if (i < num_tiles) row[i] = incl - v;
-    __syncthreads();
-    if (t == 1023) carry = incl;
-    __syncthreads();
   }
-  if (t == 0) row_total[blockIdx.x] = carry;
+  __syncthreads();
+  for (int j = threadIdx.x; j < num_passes * RADIX; j += SORT_THREADS) {
+    const uint32_t c = (&h[0][0])[j];
+    if (c) atomicAdd(&ghist[j], c);
+  }
 }
 
-// Pass step 3: each CTA ranks its tile stably by digit in shared memory -- every warp walks
-// its own contiguous chunk of the tile 32 keys at a time (match_any ranks + warp-private digit
-// counters, no block barrier inside the walk), one block-wide prefix over (warp, digit) turns
-// warp-local ranks into tile positions -- then writes the locally sorted tile out so that
-// consecutive threads store consecutive addresses of a digit's output segment (coalesced).
-template <int ITEMS>
-__global__ void __launch_bounds__(SORT_THREADS, 3) radix_scatter(const uint32_t *keys_in, const int32_t *vals_in,
-                                                              uint32_t *keys_out, int32_t *vals_out,
-                                                              const uint32_t *offsets, const uint32_t *row_total,
-                                                              int64_t n, int shift, int num_tiles) {
+// One 8-bit pass, one kernel (single-pass "onesweep" scheme): tiles are numbered in the
+// order their CTAs start (atomic counter), so a tile only ever waits on tiles that are
+// already running.  Each CTA ranks its tile stably by digit in shared memory -- every warp
+// walks its own contiguous chunk 32 keys at a time (match_any ranks + warp-private digit
+// counters) -- publishes its per-digit counts, resolves its exclusive per-digit prefix by
+// decoupled look-back over the preceding tiles' published aggregates / inclusive prefixes,
+// then writes the locally sorted tile out so consecutive threads store consecutive
+// addresses of a digit's output segment (coalesced).  The first pass builds the keys from
+// (executor, run_rank) on the fly and its values are the admission indices.
+template <int ITEMS, bool FIRST>
+__global__ void __launch_bounds__(SORT_THREADS, ITEMS >= 16 ? 3 : 6)
+    onesweep_pass(const uint32_t *keys_in, const int32_t *vals_in, const int32_t *exec, const int32_t *rank,
+                  int rank_bits, uint32_t *keys_out, int32_t *vals_out, const uint32_t *ghist, uint32_t *lookback,
+                  uint32_t *tile_counter, int64_t n, int shift) {
   constexpr int TILE = SORT_THREADS * ITEMS;
   constexpr int CHUNK = 32 * ITEMS;  // keys per warp
   __shared__ uint32_t sk[TILE];
   __shared__ int32_t sv[TILE];
   __shared__ uint32_t wcnt[SORT_WARPS][RADIX];  // per-warp digit counts, then per-warp tile offsets
   __shared__ uint32_t local_off[RADIX], global_off[RADIX], scan_tmp[RADIX];
+  __shared__ int tile_sh;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t base = (int64_t)blockIdx.x * TILE;
-  const int tile_n = (int)((n - base) < TILE ? (n - base) : TILE);
-  // digit base = exclusive scan of the 256 row totals (every CTA redoes this tiny scan)
-  scan_tmp[tid] = row_total[tid];
+  if (tid == 0) tile_sh = (int)atomicAdd(tile_counter, 1u);
+  const uint32_t digit_total = ghist[tid];
+  scan_tmp[tid] = digit_total;
   for (int j = tid; j < SORT_WARPS * RADIX; j += SORT_THREADS) (&wcnt[0][0])[j] = 0;
   __syncthreads();
-  for (int off = 1; off < RADIX; off <<= 1) {
+  const int tile = tile_sh;
+  const int64_t base = (int64_t)tile * TILE;
+  const int tile_n = (int)((n - base) < TILE ? (n - base) : TILE);
+  // keys first (independent requests in flight), then the digit-base scan while they land
+  uint32_t key[ITEMS], rnk[ITEMS];
+  int32_t val[ITEMS];
+#pragma unroll
+  for (int r = 0; r < ITEMS; ++r) {
+    const int i = warp * CHUNK + r * 32 + lane;
+    if constexpr (FIRST) {
+      key[r] = i < tile_n ? sort_key(exec, rank, base + i, rank_bits) : 0u;
+      val[r] = (int32_t)(base + i);
+    } else {
+      key[r] = i < tile_n ? keys_in[base + i] : 0u;
+      val[r] = i < tile_n ? vals_in[base + i] : 0;
+    }
+  }
+  for (int off = 1; off < RADIX; off <<= 1) {  // digit base = exclusive scan of the global counts
     const uint32_t y = tid >= off ? scan_tmp[tid - off] : 0u;
     __syncthreads();
     scan_tmp[tid] += y;
     __syncthreads();
   }
-  global_off[tid] = scan_tmp[tid] - row_total[tid] + offsets[(int64_t)tid * num_tiles + blockIdx.x];
+  const uint32_t digit_base = scan_tmp[tid] - digit_total;
   // warp walk: warp-local stable ranks
   const uint32_t lt_mask = (1u << lane) - 1u;
-  uint32_t key[ITEMS], rnk[ITEMS];
-  int32_t val[ITEMS];
-#pragma unroll
-  for (int r = 0; r < ITEMS; ++r) {  // all loads first: 2 x ITEMS requests in flight per thread
-    const int i = warp * CHUNK + r * 32 + lane;
-    key[r] = i < tile_n ? keys_in[base + i] : 0u;
-    val[r] = i < tile_n ? vals_in[base + i] : 0;
-  }
 #pragma unroll
   for (int r = 0; r < ITEMS; ++r) {
     const int i = warp * CHUNK + r * 32 + lane;
@@ -170,10 +150,27 @@ __global__ void __launch_bounds__(SORT_THREADS, 3) radix_scatter(const uint32_t 
     __syncwarp();
   }
   __syncthreads();
-  // (warp, digit) prefix: thread = digit; tile-local digit starts from the digit totals
+  // thread = digit: this tile's count, published at once; then the look-back
   uint32_t total = 0;
 #pragma unroll
   for (int w = 0; w < SORT_WARPS; ++w) total += wcnt[w][tid];
+  volatile uint32_t *lb = lookback;
+  uint32_t prefix = 0;
+  if (tile == 0) {
+    lb[tid] = LB_INC | total;
+  } else {
+    lb[(int64_t)tile * RADIX + tid] = LB_AGG | total;
+    for (int j = tile - 1;;) {
+      const uint32_t v = lb[(int64_t)j * RADIX + tid];
+      if ((v & (LB_AGG | LB_INC)) == 0) continue;  // predecessor still ranking: spin
+      prefix += v & LB_VAL;
+      if (v & LB_INC) break;
+      --j;
+    }
+    lb[(int64_t)tile * RADIX + tid] = LB_INC | (prefix + total);
+  }
+  global_off[tid] = digit_base + prefix;
+  // (warp, digit) prefix: tile-local digit starts from the digit totals
   scan_tmp[tid] = total;
   __syncthreads();
   for (int off = 1; off < RADIX; off <<= 1) {
@@ -352,17 +349,18 @@ bool check(cudaError_t e, const char *what) { return coe_cuda_ok(e, what); }
 extern "C" {
 
 int64_t coe_group_sort_scratch_bytes(int64_t n) {
-  const int64_t tile = SORT_THREADS * (int64_t)(n <= SMALL_SORT_MAX ? ITEMS_SMALL : ITEMS_LARGE);
+  const int64_t tile = SORT_THREADS * (int64_t)ITEMS_SMALL;  // the smallest tile bounds the tile count
   int64_t tiles = (n + tile - 1) / tile;
   if (tiles < 1) tiles = 1;
-  return 4 * 4 * (n + 64) + 4 * RADIX * (tiles + 1) + 1024;
+  // ping-pong keys / values + per-pass look-back words + global digit counts + tile counters
+  return 4 * 4 * (n + 16) + 4 * (int64_t)MAX_PASSES * RADIX * tiles + 4 * MAX_PASSES * RADIX + 64 + 1024;
 }
 
 int coe_group_sort(const int32_t *executor, const int32_t *run_rank, int64_t n, int rank_bits, int num_passes,
                    int32_t *out_perm, int32_t *out_keys, void *scratch, cudaStream_t stream) {
   if (n <= 0) return COE_CUDA_OK;
-  if (num_passes < 1 || num_passes > 4 || rank_bits < 1 || rank_bits > 31) {
-    coe_set_error("coe_group_sort: bad pass count / rank bits");
+  if (num_passes < 1 || num_passes > MAX_PASSES || rank_bits < 1 || rank_bits > 31 || n >= (int64_t)LB_AGG) {
+    coe_set_error("coe_group_sort: bad pass count / rank bits / size");
     return COE_CUDA_ERR_CONFIG;
   }
   const bool small = n <= SMALL_SORT_MAX;
@@ -373,27 +371,37 @@ int coe_group_sort(const int32_t *executor, const int32_t *run_rank, int64_t n, 
   uint32_t *kb = ka + n + 16;
   int32_t *va = reinterpret_cast<int32_t *>(kb + n + 16);
   int32_t *vb = va + n + 16;
-  uint32_t *hist = reinterpret_cast<uint32_t *>(vb + n + 16);
-  uint32_t *row_total = hist + (int64_t)RADIX * num_tiles;
-  const int blocks = (int)((n + 255) / 256);
-  make_keys<<<blocks, 256, 0, stream>>>(executor, run_rank, n, rank_bits, ka, va);
+  // zeroed together: look-back words of every pass, global digit counts, tile counters
+  uint32_t *lookback = reinterpret_cast<uint32_t *>(vb + n + 16);
+  uint32_t *ghist = lookback + (int64_t)num_passes * RADIX * num_tiles;
+  uint32_t *counters = ghist + MAX_PASSES * RADIX;
+  const size_t zero_bytes = 4 * ((size_t)num_passes * RADIX * num_tiles + MAX_PASSES * RADIX + 16);
+  if (!check(cudaMemsetAsync(lookback, 0, zero_bytes, stream), "coe_group_sort memset")) return COE_CUDA_ERR_CUDA;
+  const int hist_grid = std::min(num_tiles, 148 * 8);
+  if (small)
+    radix_global_hist<ITEMS_SMALL><<<hist_grid, SORT_THREADS, 0, stream>>>(executor, run_rank, n, rank_bits,
+                                                                            num_passes, ghist);
+  else
+    radix_global_hist<ITEMS_LARGE><<<hist_grid, SORT_THREADS, 0, stream>>>(executor, run_rank, n, rank_bits,
+                                                                            num_passes, ghist);
+  const uint32_t *ki = nullptr;
+  const int32_t *vi = nullptr;
   for (int p = 0; p < num_passes; ++p) {
     // the last pass scatters straight into the caller's arrays
-    uint32_t *ko = p == num_passes - 1 ? reinterpret_cast<uint32_t *>(out_keys) : kb;
-    int32_t *vo = p == num_passes - 1 ? out_perm : vb;
-    if (small) {
-      radix_hist<ITEMS_SMALL><<<num_tiles, SORT_THREADS, 0, stream>>>(ka, n, 8 * p, num_tiles, hist);
-      scan_rows<<<RADIX, 1024, 0, stream>>>(hist, num_tiles, row_total);
-      radix_scatter<ITEMS_SMALL><<<num_tiles, SORT_THREADS, 0, stream>>>(ka, va, ko, vo, hist, row_total, n, 8 * p,
-                                                                          num_tiles);
-    } else {
-      radix_hist<ITEMS_LARGE><<<num_tiles, SORT_THREADS, 0, stream>>>(ka, n, 8 * p, num_tiles, hist);
-      scan_rows<<<RADIX, 1024, 0, stream>>>(hist, num_tiles, row_total);
-      radix_scatter<ITEMS_LARGE><<<num_tiles, SORT_THREADS, 0, stream>>>(ka, va, ko, vo, hist, row_total, n, 8 * p,
-                                                                          num_tiles);
-    }
-    std::swap(ka, kb);
-    std::swap(va, vb);
+    uint32_t *ko = p == num_passes - 1 ? reinterpret_cast<uint32_t *>(out_keys) : (p & 1 ? ka : kb);
+    int32_t *vo = p == num_passes - 1 ? out_perm : (p & 1 ? va : vb);
+    uint32_t *lb = lookback + (int64_t)p * RADIX * num_tiles;
+    const uint32_t *gh = ghist + p * RADIX;
+    auto launch = [&](auto kernel) {
+      // a max shared-memory carve-out so the register limit, not shared memory, bounds occupancy
+      cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+      kernel<<<num_tiles, SORT_THREADS, 0, stream>>>(ki, vi, executor, run_rank, rank_bits, ko, vo, gh, lb,
+                                                     counters + p, n, 8 * p);
+    };
+    if (small) p == 0 ? launch(onesweep_pass<ITEMS_SMALL, true>) : launch(onesweep_pass<ITEMS_SMALL, false>);
+    else p == 0 ? launch(onesweep_pass<ITEMS_LARGE, true>) : launch(onesweep_pass<ITEMS_LARGE, false>);
+    ki = ko;
+    vi = vo;
   }
   return check(cudaGetLastError(), "coe_group_sort") ? COE_CUDA_OK : COE_CUDA_ERR_CUDA;
 }

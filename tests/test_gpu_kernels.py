@@ -74,6 +74,30 @@ def test_group_sort_matches_stable_lexsort(lib, n, executors):
     assert np.array_equal(k, (ex[ref].astype(np.int64) << bits) | rank[ref])
 
 
+@pytest.mark.parametrize("n, executors, rank_bits", [((1 << 20) + 1, 3, 18), (3_000_000, 8, 22)])
+def test_group_sort_large_tiles_and_four_passes(lib, n, executors, rank_bits):
+    """Past 1M admissions K1 switches to 4096-key tiles; 8 executors x 22 rank bits = 4 passes."""
+    import torch
+
+    rng = np.random.default_rng(n)
+    ex = rng.integers(0, executors, n).astype(np.int32)
+    rank = rng.integers(0, 1 << rank_bits, n).astype(np.int32)
+    rank[rng.random(n) < 0.5] = 7  # long equal-key runs: stability across many tiles
+    passes = (rank_bits + (executors - 1).bit_length() + 7) // 8
+    dev = torch.device("cuda")
+    t_ex, t_rk = torch.from_numpy(ex).to(dev), torch.from_numpy(rank).to(dev)
+    perm = torch.empty(n, dtype=torch.int32, device=dev)
+    keys = torch.empty(n, dtype=torch.int32, device=dev)
+    scratch = torch.empty(lib.coe_group_sort_scratch_bytes(n), dtype=torch.uint8, device=dev)
+    _ck(lib, lib.coe_group_sort(t_ex.data_ptr(), t_rk.data_ptr(), n, rank_bits, passes, perm.data_ptr(),
+                                keys.data_ptr(), scratch.data_ptr(), _stream()), "sort")
+    torch.cuda.synchronize()
+    ref = np.lexsort((np.arange(n), rank, ex))
+    assert np.array_equal(perm.cpu().numpy(), ref)
+    k = keys.cpu().numpy().astype(np.int64) & 0xFFFFFFFF
+    assert np.array_equal(k, (ex[ref].astype(np.int64) << rank_bits) | rank[ref])
+
+
 @pytest.mark.parametrize("n, X", [(5000, 2), (200000, 3)])
 def test_run_compact_offsets_members_and_violations(lib, n, X):
     import torch

@@ -20,7 +20,7 @@ for w in "16 6 4096 12288 256" "11 22 2048 8192 128" "11 44 1024 4096 64"; do
     -o gpurun_out/k3_full_$1_$2_$3x$4x$5 python tools/k3_profile.py $1 $2 1 $3 $4 $5 \
     > gpurun_out/${TAG}_ncu_k3_$3.log 2>&1
 done
-timeout 900 ncu --set full --clock-control none -k regex:"make_keys|radix|scan|compact" -c 12 -f \
+timeout 900 ncu --set full --clock-control none -k regex:"radix|onesweep|compact|batch" -c 12 -f \
   -o gpurun_out/k12_full python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline --no-clocks \
   > gpurun_out/${TAG}_ncu_k12.log 2>&1
 tail -c 400 gpurun_out/${TAG}_bench_c3.log

@@ -69,7 +69,7 @@ def full(path):
 
 
 def grouping():
-    """K1/K2 (make_keys, radix passes, scan, compaction) from gpurun_out/k12_full.ncu-rep."""
+    """K1/K2 (counting read, one-kernel radix passes, compaction) from gpurun_out/k12_full.ncu-rep."""
     path = os.path.join(OUT, "k12_full.ncu-rep")
     if not os.path.exists(path):
         return None
@@ -131,8 +131,8 @@ if summary["shapes"]:
 
 kg = grouping()
 if kg:
-    summ = {"launches": kg, "note": "ncu --set full, one bench step of C3 (13,642 admissions): K1 make_keys + "
-                                    "8-bit LSD radix passes (hist / scan / scatter), K2 compaction. Latency-bound: "
+    summ = {"launches": kg, "note": "ncu --set full, one bench step of C3 (13,642 admissions): K1 counting read + "
+                                    "one-kernel 8-bit LSD passes (decoupled look-back), K2 compaction. Latency-bound: "
                                     "~218 KB of algorithmic traffic per step (16 B per admission)",
             "total_us": sum(k["duration_us"] for k in kg), "total_dram_bytes": sum(k["dram_bytes"] for k in kg)}
     json.dump(summ, open(os.path.join(PROF, f"{tag}_k12_ncu_summary.json"), "w"), indent=1)
