@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(SORT_THREADS, ITEMS >= 16 ? 3 : 6)
   __shared__ uint32_t sk[TILE];
   __shared__ int32_t sv[TILE];
   __shared__ uint32_t wcnt[SORT_WARPS][RADIX];  // per-warp digit counts, then per-warp tile offsets
-  __shared__ uint32_t local_off[RADIX], global_off[RADIX], scan_tmp[RADIX];
+  __shared__ uint32_t out_shift[RADIX], scan_tmp[RADIX];  // out_shift[d]: global start - tile-local start
   __shared__ int tile_sh;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) tile_sh = (int)atomicAdd(tile_counter, 1u);
@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(SORT_THREADS, ITEMS >= 16 ? 3 : 6)
     }
     lb[(int64_t)tile * RADIX + tid] = LB_INC | (prefix + total);
   }
-  global_off[tid] = digit_base + prefix;
+  const uint32_t global_start = digit_base + prefix;
   // (warp, digit) prefix: tile-local digit starts from the digit totals
   scan_tmp[tid] = total;
   __syncthreads();
@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(SORT_THREADS, ITEMS >= 16 ? 3 : 6)
     __syncthreads();
   }
   uint32_t run = scan_tmp[tid] - total;
-  local_off[tid] = run;
+  out_shift[tid] = global_start - run;  // mod 2^32
 #pragma unroll
   for (int w = 0; w < SORT_WARPS; ++w) {
     const uint32_t c = wcnt[w][tid];
@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(SORT_THREADS, ITEMS >= 16 ? 3 : 6)
   for (int k = tid; k < tile_n; k += SORT_THREADS) {
     const uint32_t kk = sk[k];
     const uint32_t d = (kk >> shift) & 255u;
-    const uint32_t g = global_off[d] + (uint32_t)k - local_off[d];
+    const uint32_t g = out_shift[d] + (uint32_t)k;
     keys_out[g] = kk;
     vals_out[g] = sv[k];
   }
