@@ -93,117 +93,130 @@ __global__ void __launch_bounds__(SORT_THREADS) radix_global_hist(const int32_t 
 // then writes the locally sorted tile out so consecutive threads store consecutive
 // addresses of a digit's output segment (coalesced).  The first pass builds the keys from
 // (executor, run_rank) on the fly and its values are the admission indices.
+// Exclusive scan of one value per thread over the 256-thread block: warp shuffles, then the
+// eight warp totals (two barriers instead of a 16-barrier Hillis-Steele scan).
+__device__ __forceinline__ uint32_t block_exclusive_scan256(uint32_t v, uint32_t *warp_tot) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, off);
+    if (lane >= off) x += y;
+  }
+  if (lane == 31) warp_tot[warp] = x;
+  __syncthreads();
+  uint32_t base = 0;
+#pragma unroll
+  for (int w = 0; w < SORT_WARPS; ++w) base += w < warp ? warp_tot[w] : 0u;
+  return base + x - v;
+}
+
+// One 8-bit pass, one persistent kernel (single-pass "onesweep" scheme): each CTA claims
+// tiles in order from an atomic counter, so a tile only ever waits on tiles that running
+// CTAs already hold.  Each CTA ranks its tile stably by digit in shared memory -- every warp
+// walks its own contiguous chunk 32 keys at a time (match_any ranks + warp-private digit
+// counters) -- publishes its per-digit counts, resolves its exclusive per-digit prefix by
+// decoupled look-back over the preceding tiles' published aggregates / inclusive prefixes,
+// then writes the locally sorted tile out so consecutive threads store consecutive
+// addresses of a digit's output segment (coalesced).  The digit bases (scan of the global
+// counts) are computed once per CTA.  The first pass builds the keys from
+// (executor, run_rank) on the fly and its values are the admission indices.
 template <int ITEMS, bool FIRST>
 __global__ void __launch_bounds__(SORT_THREADS, ITEMS >= 16 ? 3 : 6)
     onesweep_pass(const uint32_t *keys_in, const int32_t *vals_in, const int32_t *exec, const int32_t *rank,
                   int rank_bits, uint32_t *keys_out, int32_t *vals_out, const uint32_t *ghist, uint32_t *lookback,
-                  uint32_t *tile_counter, int64_t n, int shift) {
+                  uint32_t *tile_counter, int64_t n, int num_tiles, int shift) {
   constexpr int TILE = SORT_THREADS * ITEMS;
   constexpr int CHUNK = 32 * ITEMS;  // keys per warp
   __shared__ uint32_t sk[TILE];
   __shared__ int32_t sv[TILE];
   __shared__ uint32_t wcnt[SORT_WARPS][RADIX];  // per-warp digit counts, then per-warp tile offsets
-  __shared__ uint32_t out_shift[RADIX], scan_tmp[RADIX];  // out_shift[d]: global start - tile-local start
+  __shared__ uint32_t out_shift[RADIX];         // global start - tile-local start, per digit
+  __shared__ uint32_t warp_tot[2][SORT_WARPS];
   __shared__ int tile_sh;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (tid == 0) tile_sh = (int)atomicAdd(tile_counter, 1u);
-  const uint32_t digit_total = ghist[tid];
-  scan_tmp[tid] = digit_total;
-  for (int j = tid; j < SORT_WARPS * RADIX; j += SORT_THREADS) (&wcnt[0][0])[j] = 0;
-  __syncthreads();
-  const int tile = tile_sh;
-  const int64_t base = (int64_t)tile * TILE;
-  const int tile_n = (int)((n - base) < TILE ? (n - base) : TILE);
-  // keys first (independent requests in flight), then the digit-base scan while they land
-  uint32_t key[ITEMS], rnk[ITEMS];
-  int32_t val[ITEMS];
-#pragma unroll
-  for (int r = 0; r < ITEMS; ++r) {
-    const int i = warp * CHUNK + r * 32 + lane;
-    if constexpr (FIRST) {
-      key[r] = i < tile_n ? sort_key(exec, rank, base + i, rank_bits) : 0u;
-      val[r] = (int32_t)(base + i);
-    } else {
-      key[r] = i < tile_n ? keys_in[base + i] : 0u;
-      val[r] = i < tile_n ? vals_in[base + i] : 0;
-    }
-  }
-  for (int off = 1; off < RADIX; off <<= 1) {  // digit base = exclusive scan of the global counts
-    const uint32_t y = tid >= off ? scan_tmp[tid - off] : 0u;
-    __syncthreads();
-    scan_tmp[tid] += y;
-    __syncthreads();
-  }
-  const uint32_t digit_base = scan_tmp[tid] - digit_total;
-  // warp walk: warp-local stable ranks
+  const uint32_t digit_base = block_exclusive_scan256(ghist[tid], warp_tot[0]);  // thread = digit
   const uint32_t lt_mask = (1u << lane) - 1u;
-#pragma unroll
-  for (int r = 0; r < ITEMS; ++r) {
-    const int i = warp * CHUNK + r * 32 + lane;
-    const bool valid = i < tile_n;
-    const uint32_t digit = valid ? ((key[r] >> shift) & 255u) : 256u;
-    const uint32_t same = __match_any_sync(0xffffffffu, digit);
-    const uint32_t before = __popc(same & lt_mask);
-    rnk[r] = valid ? wcnt[warp][digit] + before : 0u;
-    __syncwarp();
-    if (valid && before == 0) wcnt[warp][digit] += __popc(same);
-    __syncwarp();
-  }
-  __syncthreads();
-  // thread = digit: this tile's count, published at once; then the look-back
-  uint32_t total = 0;
-#pragma unroll
-  for (int w = 0; w < SORT_WARPS; ++w) total += wcnt[w][tid];
   volatile uint32_t *lb = lookback;
-  uint32_t prefix = 0;
-  if (tile == 0) {
-    lb[tid] = LB_INC | total;
-  } else {
-    lb[(int64_t)tile * RADIX + tid] = LB_AGG | total;
-    for (int j = tile - 1;;) {
-      const uint32_t v = lb[(int64_t)j * RADIX + tid];
-      if ((v & (LB_AGG | LB_INC)) == 0) continue;  // predecessor still ranking: spin
-      prefix += v & LB_VAL;
-      if (v & LB_INC) break;
-      --j;
-    }
-    lb[(int64_t)tile * RADIX + tid] = LB_INC | (prefix + total);
-  }
-  const uint32_t global_start = digit_base + prefix;
-  // (warp, digit) prefix: tile-local digit starts from the digit totals
-  scan_tmp[tid] = total;
-  __syncthreads();
-  for (int off = 1; off < RADIX; off <<= 1) {
-    const uint32_t y = tid >= off ? scan_tmp[tid - off] : 0u;
-    __syncthreads();
-    scan_tmp[tid] += y;
-    __syncthreads();
-  }
-  uint32_t run = scan_tmp[tid] - total;
-  out_shift[tid] = global_start - run;  // mod 2^32
+  for (;;) {
+    if (tid == 0) tile_sh = (int)atomicAdd(tile_counter, 1u);
+    for (int j = tid; j < SORT_WARPS * RADIX; j += SORT_THREADS) (&wcnt[0][0])[j] = 0;
+    __syncthreads();  // also: the previous tile's write-out is done with sk / sv / out_shift
+    const int tile = tile_sh;
+    if (tile >= num_tiles) break;
+    const int64_t base = (int64_t)tile * TILE;
+    const int tile_n = (int)((n - base) < TILE ? (n - base) : TILE);
+    uint32_t key[ITEMS], rnk[ITEMS];
+    int32_t val[ITEMS];
 #pragma unroll
-  for (int w = 0; w < SORT_WARPS; ++w) {
-    const uint32_t c = wcnt[w][tid];
-    wcnt[w][tid] = run;
-    run += c;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int r = 0; r < ITEMS; ++r) {
-    const int i = warp * CHUNK + r * 32 + lane;
-    if (i < tile_n) {
-      const uint32_t pos = wcnt[warp][(key[r] >> shift) & 255u] + rnk[r];
-      sk[pos] = key[r];
-      sv[pos] = val[r];
+    for (int r = 0; r < ITEMS; ++r) {  // all loads first: independent requests in flight
+      const int i = warp * CHUNK + r * 32 + lane;
+      if constexpr (FIRST) {
+        key[r] = i < tile_n ? sort_key(exec, rank, base + i, rank_bits) : 0u;
+        val[r] = (int32_t)(base + i);
+      } else {
+        key[r] = i < tile_n ? keys_in[base + i] : 0u;
+        val[r] = i < tile_n ? vals_in[base + i] : 0;
+      }
     }
-  }
-  __syncthreads();
-  for (int k = tid; k < tile_n; k += SORT_THREADS) {
-    const uint32_t kk = sk[k];
-    const uint32_t d = (kk >> shift) & 255u;
-    const uint32_t g = out_shift[d] + (uint32_t)k;
-    keys_out[g] = kk;
-    vals_out[g] = sv[k];
+    // warp walk: warp-local stable ranks
+#pragma unroll
+    for (int r = 0; r < ITEMS; ++r) {
+      const int i = warp * CHUNK + r * 32 + lane;
+      const bool valid = i < tile_n;
+      const uint32_t digit = valid ? ((key[r] >> shift) & 255u) : 256u;
+      const uint32_t same = __match_any_sync(0xffffffffu, digit);
+      const uint32_t before = __popc(same & lt_mask);
+      rnk[r] = valid ? wcnt[warp][digit] + before : 0u;
+      __syncwarp();
+      if (valid && before == 0) wcnt[warp][digit] += __popc(same);
+      __syncwarp();
+    }
+    __syncthreads();
+    // thread = digit: this tile's count, published at once; then the look-back
+    uint32_t total = 0;
+#pragma unroll
+    for (int w = 0; w < SORT_WARPS; ++w) total += wcnt[w][tid];
+    uint32_t prefix = 0;
+    if (tile == 0) {
+      lb[tid] = LB_INC | total;
+    } else {
+      lb[(int64_t)tile * RADIX + tid] = LB_AGG | total;
+      for (int j = tile - 1;;) {
+        const uint32_t v = lb[(int64_t)j * RADIX + tid];
+        if ((v & (LB_AGG | LB_INC)) == 0) continue;  // predecessor still ranking: spin
+        prefix += v & LB_VAL;
+        if (v & LB_INC) break;
+        --j;
+      }
+      lb[(int64_t)tile * RADIX + tid] = LB_INC | (prefix + total);
+    }
+    // tile-local digit starts, then per-(warp, digit) offsets
+    uint32_t run = block_exclusive_scan256(total, warp_tot[1]);
+    out_shift[tid] = digit_base + prefix - run;  // mod 2^32
+#pragma unroll
+    for (int w = 0; w < SORT_WARPS; ++w) {
+      const uint32_t c = wcnt[w][tid];
+      wcnt[w][tid] = run;
+      run += c;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < ITEMS; ++r) {
+      const int i = warp * CHUNK + r * 32 + lane;
+      if (i < tile_n) {
+        const uint32_t pos = wcnt[warp][(key[r] >> shift) & 255u] + rnk[r];
+        sk[pos] = key[r];
+        sv[pos] = val[r];
+      }
+    }
+    __syncthreads();
+    for (int k = tid; k < tile_n; k += SORT_THREADS) {
+      const uint32_t kk = sk[k];
+      const uint32_t g = out_shift[(kk >> shift) & 255u] + (uint32_t)k;
+      keys_out[g] = kk;
+      vals_out[g] = sv[k];
+    }
   }
 }
 
@@ -395,8 +408,16 @@ int coe_group_sort(const int32_t *executor, const int32_t *run_rank, int64_t n, 
     auto launch = [&](auto kernel) {
       // a max shared-memory carve-out so the register limit, not shared memory, bounds occupancy
       cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
-      kernel<<<num_tiles, SORT_THREADS, 0, stream>>>(ki, vi, executor, run_rank, rank_bits, ko, vo, gh, lb,
-                                                     counters + p, n, 8 * p);
+      static const int resident = [&] {  // persistent CTAs: every SM slot, once per kernel
+        int per_sm = 0, sms = 0, dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, SORT_THREADS, 0);
+        return std::max(1, sms * std::max(per_sm, 1));
+      }();
+      const int grid = std::min(num_tiles, resident);
+      kernel<<<grid, SORT_THREADS, 0, stream>>>(ki, vi, executor, run_rank, rank_bits, ko, vo, gh, lb, counters + p,
+                                                n, num_tiles, 8 * p);
     };
     if (small) p == 0 ? launch(onesweep_pass<ITEMS_SMALL, true>) : launch(onesweep_pass<ITEMS_SMALL, false>);
     else p == 0 ? launch(onesweep_pass<ITEMS_LARGE, true>) : launch(onesweep_pass<ITEMS_LARGE, false>);
