@@ -357,6 +357,25 @@ __global__ void fill_uniform_bf16(__nv_bfloat16_raw *dst, int64_t n, uint64_t se
 
 bool check(cudaError_t e, const char *what) { return coe_cuda_ok(e, what); }
 
+// Persistent grid of one pass kernel: every SM slot it can occupy (queried once per
+// instantiation), with a max shared-memory carve-out so registers bound occupancy.
+template <int ITEMS, bool FIRST>
+void launch_pass(const uint32_t *ki, const int32_t *vi, const int32_t *executor, const int32_t *run_rank,
+                 int rank_bits, uint32_t *ko, int32_t *vo, const uint32_t *gh, uint32_t *lb, uint32_t *counter,
+                 int64_t n, int num_tiles, int shift, cudaStream_t stream) {
+  static const int resident = [] {
+    auto kernel = onesweep_pass<ITEMS, FIRST>;
+    cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    int per_sm = 0, sms = 0, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, SORT_THREADS, 0);
+    return std::max(1, sms * std::max(per_sm, 1));
+  }();
+  onesweep_pass<ITEMS, FIRST><<<std::min(num_tiles, resident), SORT_THREADS, 0, stream>>>(
+      ki, vi, executor, run_rank, rank_bits, ko, vo, gh, lb, counter, n, num_tiles, shift);
+}
+
 }  // namespace
 
 extern "C" {
@@ -405,22 +424,14 @@ int coe_group_sort(const int32_t *executor, const int32_t *run_rank, int64_t n, 
     int32_t *vo = p == num_passes - 1 ? out_perm : (p & 1 ? va : vb);
     uint32_t *lb = lookback + (int64_t)p * RADIX * num_tiles;
     const uint32_t *gh = ghist + p * RADIX;
-    auto launch = [&](auto kernel) {
-      // a max shared-memory carve-out so the register limit, not shared memory, bounds occupancy
-      cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
-      static const int resident = [&] {  // persistent CTAs: every SM slot, once per kernel
-        int per_sm = 0, sms = 0, dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, SORT_THREADS, 0);
-        return std::max(1, sms * std::max(per_sm, 1));
-      }();
-      const int grid = std::min(num_tiles, resident);
-      kernel<<<grid, SORT_THREADS, 0, stream>>>(ki, vi, executor, run_rank, rank_bits, ko, vo, gh, lb, counters + p,
-                                                n, num_tiles, 8 * p);
-    };
-    if (small) p == 0 ? launch(onesweep_pass<ITEMS_SMALL, true>) : launch(onesweep_pass<ITEMS_SMALL, false>);
-    else p == 0 ? launch(onesweep_pass<ITEMS_LARGE, true>) : launch(onesweep_pass<ITEMS_LARGE, false>);
+    if (small) p == 0 ? launch_pass<ITEMS_SMALL, true>(ki, vi, executor, run_rank, rank_bits, ko, vo, gh, lb,
+                                                        counters + p, n, num_tiles, 8 * p, stream)
+                      : launch_pass<ITEMS_SMALL, false>(ki, vi, executor, run_rank, rank_bits, ko, vo, gh, lb,
+                                                         counters + p, n, num_tiles, 8 * p, stream);
+    else p == 0 ? launch_pass<ITEMS_LARGE, true>(ki, vi, executor, run_rank, rank_bits, ko, vo, gh, lb, counters + p,
+                                                 n, num_tiles, 8 * p, stream)
+                : launch_pass<ITEMS_LARGE, false>(ki, vi, executor, run_rank, rank_bits, ko, vo, gh, lb, counters + p,
+                                                  n, num_tiles, 8 * p, stream);
     ki = ko;
     vi = vo;
   }
