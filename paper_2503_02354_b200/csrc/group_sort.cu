@@ -60,22 +60,30 @@ __global__ void __launch_bounds__(SORT_THREADS) radix_global_hist(const int32_t 
   for (int j = threadIdx.x; j < MAX_PASSES * RADIX; j += SORT_THREADS) (&h[0][0])[j] = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  for (int64_t base = (int64_t)blockIdx.x * TILE; base < n; base += (int64_t)gridDim.x * TILE) {
-    uint32_t kreg[ITEMS];
+  const int64_t stride = (int64_t)gridDim.x * TILE;
+  uint32_t cur[ITEMS], nxt[ITEMS];
+  auto load = [&](uint32_t *k, int64_t base) {
 #pragma unroll
-    for (int r = 0; r < ITEMS; ++r) {  // all loads first
+    for (int r = 0; r < ITEMS; ++r) {
       const int64_t i = base + r * SORT_THREADS + threadIdx.x;
-      kreg[r] = i < n ? sort_key(exec, rank, i, rank_bits) : 0u;
+      k[r] = i < n ? sort_key(exec, rank, i, rank_bits) : 0u;
     }
+  };
+  int64_t base = (int64_t)blockIdx.x * TILE;
+  if (base < n) load(cur, base);
+  for (; base < n; base += stride) {
+    if (base + stride < n) load(nxt, base + stride);  // next tile in flight while this one counts
 #pragma unroll
     for (int r = 0; r < ITEMS; ++r) {
       const bool valid = base + r * SORT_THREADS + threadIdx.x < n;
       for (int p = 0; p < num_passes; ++p) {
-        const uint32_t digit = valid ? (kreg[r] >> (8 * p)) & 255u : 256u;
+        const uint32_t digit = valid ? (cur[r] >> (8 * p)) & 255u : 256u;
         const uint32_t same = __match_any_sync(0xffffffffu, digit);
         if (digit < 256u && (same & ((1u << lane) - 1u)) == 0) atomicAdd(&h[p][digit], __popc(same));
       }
     }
+#pragma unroll
+    for (int r = 0; r < ITEMS; ++r) cur[r] = nxt[r];
   }
   __syncthreads();
   for (int j = threadIdx.x; j < num_passes * RADIX; j += SORT_THREADS) {
@@ -414,8 +422,8 @@ int coe_group_sort(const int32_t *executor, const int32_t *run_rank, int64_t n, 
     radix_global_hist<ITEMS_SMALL><<<hist_grid, SORT_THREADS, 0, stream>>>(executor, run_rank, n, rank_bits,
                                                                             num_passes, ghist);
   else
-    radix_global_hist<ITEMS_LARGE><<<hist_grid, SORT_THREADS, 0, stream>>>(executor, run_rank, n, rank_bits,
-                                                                            num_passes, ghist);
+    radix_global_hist<ITEMS_LARGE / 2><<<hist_grid, SORT_THREADS, 0, stream>>>(executor, run_rank, n, rank_bits,
+                                                                                num_passes, ghist);
   const uint32_t *ki = nullptr;
   const int32_t *vi = nullptr;
   for (int p = 0; p < num_passes; ++p) {
