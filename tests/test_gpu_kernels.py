@@ -74,9 +74,12 @@ def test_group_sort_matches_stable_lexsort(lib, n, executors):
     assert np.array_equal(k, (ex[ref].astype(np.int64) << bits) | rank[ref])
 
 
-@pytest.mark.parametrize("n, executors, rank_bits", [((1 << 20) + 1, 3, 18), (3_000_000, 8, 22)])
+@pytest.mark.parametrize("n, executors, rank_bits",
+                         [(1_000_000, 2, 20), ((1 << 20) + 1, 3, 18), (3_000_000, 8, 22)])
 def test_group_sort_large_tiles_and_four_passes(lib, n, executors, rank_bits):
-    """Past 1M admissions K1 switches to 4096-key tiles; 8 executors x 22 rank bits = 4 passes."""
+    """Past 1M admissions K1 switches to 4096-key tiles; 8 executors x 22 rank bits = 4 passes.
+    1M and 3M keys have more tiles than the persistent grid has CTAs (977 x 1,024-key tiles vs
+    6 per SM; 733 x 4,096-key tiles vs 3 per SM), so CTAs claim several tiles each."""
     import torch
 
     rng = np.random.default_rng(n)
