@@ -159,6 +159,34 @@ def test_streamed_end_to_end_io_matches_device_path():
     assert np.array_equal(got, outs[0][order])
 
 
+def test_back_to_back_end_to_end_steps():
+    """Three e2e steps issued back to back (no host sync between them): inputs alternate
+    between two device buffers across steps and each step's gathers wait for the previous
+    step's downloads; every step's host output buffer holds the same bytes as the
+    device-resident path."""
+    import torch
+
+    w = _trim(configs.load("c2", 1000), 200)
+    shape = runtime.shape_of(w)
+    plan, rt, stats, outs = _serve(w, shape, steps=1)
+    n = len(plan.resolved.request_ids)
+    row = shape.T * shape.d
+    host_in = torch.empty(n * row, dtype=torch.bfloat16).pin_memory()
+    rt.read_buffer(0, host_in.data_ptr(), n * row * 2)
+    host_outs = [torch.zeros(n * row, dtype=torch.bfloat16).pin_memory() for _ in range(3)]
+    keep = []
+    for h in host_outs:
+        p = engine.plan(configs.run_config(w, trace=False))
+        keep.append(p)
+        rt.step(p, host_inputs=host_in.data_ptr(), host_outputs=h.data_ptr())
+    rt.synchronize()
+    order = rt.output_order()
+    assert sorted(order.tolist()) == list(range(n))
+    for h in host_outs:
+        got = h.view(n, shape.T, shape.d).float().numpy()
+        assert np.array_equal(got, outs[0][order])
+
+
 def test_c5_heterogeneous_expert_shapes():
     """Config 5: 11 expert shapes (d in 1k..8k, h up to 61k), 5-stage chains.  Per-shape HBM
     slabs and K3 tensor maps; activations are [T][max d] rows, a chain of width d uses the
