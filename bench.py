@@ -345,7 +345,10 @@ def main() -> None:
         for _ in range(args.steps):
             p = take_plan()
             stats = rt.step(p, rank)
-            launches += stats["launches"] + 3 + 3 * ((stats["rank_bits"] + 7) // 8)
+            # + K1 (counting read + one kernel per 8-bit pass) + K2 (gather, two batch-scan
+            # kernels past 1,024 batches, batch offsets)
+            launches += (stats["launches"] + 1 + (stats["rank_bits"] + 7) // 8
+                         + 2 + (2 if stats["batches"] > 1024 else 0))
             keep.append(p)
         end.record(stream)
         rt.synchronize()
