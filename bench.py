@@ -44,7 +44,8 @@ def parse_args():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", default="c3")
     ap.add_argument("--requests", type=int, default=10000)
-    ap.add_argument("--cpu-sample", type=int, default=48, help="requests in the CPU-baseline sample")
+    ap.add_argument("--cpu-budget", type=float, default=12.0,
+                    help="seconds of sampled CPU expert work per CPU-baseline / reference-arm step")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -199,40 +200,48 @@ def algorithmic_flops(plan, shape, executor: int = 0) -> float:
     return total
 
 
-def cpu_sample(workload, n: int) -> dict:
+def cpu_sample(workload, budget_s: float, sample_index: int = 0, plan=None) -> dict:
+    """The CPU restatement over the whole workload (oracle/cpu_serve.py): the full DES plus a
+    uniform sample of the plan's batches / swap-ins, scaled by total over sampled work."""
     from oracle import cpu_serve
 
-    run = dict(workload.run)
     shapes = {a: list(s) for a, s in workload.shapes.items()}
-    res = cpu_serve.serve_sample(workload.docs, run, shapes, n)
-    return res
+    if plan is None:
+        return cpu_serve.serve_plan_sample(workload.docs, dict(workload.run), shapes, budget_s, sample_index)
+    return cpu_serve.serve_plan_sample(workload.docs, dict(workload.run), shapes, budget_s, sample_index,
+                                       plan=plan[0], plan_seconds=plan[1])
 
 
 def reference_arm(args) -> None:
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    from oracle import cpu_serve
     from paper_2503_02354_b200 import configs
 
     w = configs.load(args.config, args.requests, gpu_executors=args.gpus)
     times = []
     res = None
     for i in range(args.warmup + args.steps):
-        res = cpu_sample(w, args.cpu_sample)
+        # every step re-runs the full DES and executes a different uniform sample of its work
+        res = cpu_sample(w, args.cpu_budget, sample_index=i)
         if i >= args.warmup:
             times.append(res["seconds"])
+    n_req = res["requests"]
     total = sum(times)
-    value = args.cpu_sample * len(times) / total
+    value = n_req * len(times) / total
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "requests/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (committed registry/stream documents; random weights)",
-        "config": {"workload": w.name + ": " + w.description, "requests": args.requests,
-                   "sample_requests": args.cpu_sample},
+        "config": {"workload": w.name + ": " + w.description, "requests": n_req,
+                   "same_plan_as_gpu_arm": True},
         "cpu_baseline": {"value": value, "unit": "requests/s", "cores": res["threads"], "kind": "port",
-                         "sample": f"first {args.cpu_sample} requests of the {args.requests}-request stream, served "
-                                   f"end to end: oracle DES (1 thread) + numpy fp32 expert MLPs + host swap-in memcpy"},
+                         "sample": cpu_serve.describe(res),
+                         "detail": {k: res[k] for k in ("plan_seconds", "exec_seconds", "load_seconds",
+                                                        "sampled_batches", "batches", "sampled_loads", "loads",
+                                                        "cpu_tflops", "memcpy_gbs", "sample_wall_seconds")}},
         "e2e": {"value": value, "unit": "requests/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -405,12 +414,14 @@ def main() -> None:
     # ---- CPU baseline (rank 0, N=1) ----
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        res = cpu_sample(w, args.cpu_sample)
-        cpu = {"value": args.cpu_sample / res["seconds"], "unit": "requests/s", "cores": res["threads"],
-               "kind": "port",
-               "sample": f"first {args.cpu_sample} requests, served end to end on the host: oracle DES "
-                         f"(1 thread, {res['plan_seconds']:.2f}s) + numpy fp32 expert MLPs ({res['threads']} threads) "
-                         f"+ {res['loads']} swap-in memcpys"}
+        from oracle import cpu_serve
+
+        res = cpu_sample(w, args.cpu_budget)
+        cpu = {"value": res["requests"] / res["seconds"], "unit": "requests/s", "cores": res["threads"],
+               "kind": "port", "sample": cpu_serve.describe(res),
+               "detail": {k: res[k] for k in ("plan_seconds", "exec_seconds", "load_seconds", "sampled_batches",
+                                              "batches", "sampled_loads", "loads", "cpu_tflops", "memcpy_gbs",
+                                              "sample_wall_seconds")}}
 
     if rank != 0:
         if dist is not None:

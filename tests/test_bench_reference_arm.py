@@ -12,7 +12,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def _run(env_extra):
     env = dict(os.environ, **env_extra)
     proc = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--config", "c1", "--requests", "1000",
-                           "--cpu-sample", "4", "--steps", "1", "--warmup", "0"],
+                           "--cpu-budget", "0.5", "--requests", "1000", "--steps", "1", "--warmup", "0"],
                           cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert proc.returncode == 0, proc.stderr[-2000:]
     return proc.stdout.strip().splitlines()
