@@ -200,6 +200,45 @@ def algorithmic_flops(plan, shape, executor: int = 0) -> float:
     return total
 
 
+def self_check(rt, plan, stats, executor: int, shape) -> dict:
+    """After the timed loop (untimed): K2 reported no straddling batch, every GPU-grouped batch
+    of the last step equals the planner's members (which equal the oracle DES's -- pinned by
+    the golden tests), and a spread of this executor's finished requests matches the fp32
+    chain on the GPU.  Fails loudly: a mis-grouped or corrupted step prints no bench line."""
+    import numpy as np
+
+    from paper_2503_02354_b200 import runtime, selfcheck
+
+    runs, violations = rt.check()
+    if violations != 0:
+        raise RuntimeError(f"K2 found {violations} batches straddling two runs")
+    batches = runtime.batches_from_plan(plan, executor)
+    req, stage, boff = rt.members(stats["admissions"], stats["batches"])
+    if len(batches) != stats["batches"]:
+        raise RuntimeError("GPU batch count differs from the plan")
+    for b, (_e, members) in enumerate(batches):
+        o = int(boff[b])
+        got = list(zip(req[o:o + len(members)].tolist(), stage[o:o + len(members)].tolist()))
+        if got != members:
+            raise RuntimeError(f"GPU grouping differs from the plan at batch {b}")
+    chains = plan.resolved.chains
+    finals = sorted(r for _e, m in batches for r, s in m if s == len(chains[r]) - 1)
+    picks = [finals[int(i)] for i in np.linspace(0, len(finals) - 1, min(8, len(finals)))] if finals else []
+    registry, ids = plan.resolved.config.registry, plan.resolved.expert_ids
+    if isinstance(shape, runtime.RuntimeShape):
+        shape_of = lambda e: (shape.d, shape.h)  # noqa: E731
+    else:
+        shape_of = lambda e: tuple(shape[registry.experts[ids[e]].arch][:2])  # noqa: E731
+    errs = selfcheck.check_requests(rt, plan, picks, shape_of, rt.shapes[0].T) if picks else {}
+    worst = max(errs.values()) if errs else None
+    if worst is not None and worst > 1e-2:
+        raise RuntimeError(f"expert outputs off: worst rel-L2 {worst:.3e} over requests {picks}")
+    return {"violations": violations, "runs": runs, "batches_equal_plan": len(batches),
+            "requests_checked": len(picks), "worst_rel_l2_vs_fp32_chain": worst,
+            "note": "untimed, after the timed loop: GPU members of every batch == planner batches; sampled "
+                    "final outputs vs an fp32 chain on the GPU (paper_2503_02354_b200/selfcheck.py), tol 1e-2"}
+
+
 def cpu_sample(workload, budget_s: float, sample_index: int = 0, plan=None) -> dict:
     """The CPU restatement over the whole workload (oracle/cpu_serve.py): the full DES plus a
     uniform sample of the plan's batches / swap-ins, scaled by total over sampled work."""
@@ -370,6 +409,7 @@ def main() -> None:
         elapsed_ms = float(t.item())
     plan_last = keep[-1]
     runs, violations = rt.check()
+    verified = self_check(rt, plan_last, stats, rank, shape)  # untimed: grouping + sampled outputs
     metrics = engine.metrics_from_plan(plan_last)
     ps = plan_stats(plan_last)
     value = n_req * args.steps / (elapsed_ms / 1e3)
@@ -501,6 +541,7 @@ def main() -> None:
                     "pcie_counters": pcie.summary()},
         "grouping": {"admissions": stats["admissions"], "group_ms": timing["group_ms"], "runs": runs,
                      "violations": violations, "waves": stats["waves"]},
+        "self_check": verified,
         "gpu_launches": launches,
         "clocks": clocks.summary(),
         "e2e": e2e,

@@ -193,6 +193,10 @@ int coe_runtime_upload_inputs(coe_runtime *rt, const void *host, int32_t num_req
 int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_step_stats *stats);
 /* gather each request's final activation (stage last_stage[r]) and copy to host */
 int coe_runtime_download_outputs(coe_runtime *rt, const int32_t *last_stage_host, int32_t num_requests, void *host);
+/* the activation rows of (requests[i], stage stages[i]) -- normally each request's final
+ * stage -- gathered on the GPU into host[i] ([n][T][ld] bf16, pageable or pinned); synchronous */
+int coe_runtime_download_requests(coe_runtime *rt, const int32_t *requests, const int32_t *stages, int32_t n,
+                                  void *host);
 int coe_runtime_synchronize(coe_runtime *rt);
 /* after synchronize: K2 run count / violations, and the grouped members */
 /* make the compute stream (coe_runtime_stream(rt, 0)) wait for the last step's output
@@ -278,6 +282,8 @@ int coe_runtime_set_knobs(coe_runtime *rt, int64_t wave_rows_cap, int64_t urgent
 /* Fill n bf16 values with the counter-based uniform generator shared with the
  * oracle (oracle/synth.py): value(i) = scale * (u(seed, i) - 0.5) * 2. */
 int coe_fill_uniform_bf16(void *dst, int64_t n, uint64_t seed, float scale, cudaStream_t stream);
+/* elements [start, start + n) of the same stream (e.g. one request's rows of the X buffer) */
+int coe_fill_uniform_bf16_at(void *dst, int64_t start, int64_t n, uint64_t seed, float scale, cudaStream_t stream);
 
 #ifdef __cplusplus
 }

@@ -43,6 +43,8 @@ def declare(lib: ctypes.CDLL) -> None:
     lib.coe_grouped_mlp.restype = c_int
     lib.coe_fill_uniform_bf16.argtypes = [c_void_p, c_int64, c_uint64, c_float, c_void_p]
     lib.coe_fill_uniform_bf16.restype = c_int
+    lib.coe_fill_uniform_bf16_at.argtypes = [c_void_p, c_int64, c_int64, c_uint64, c_float, c_void_p]
+    lib.coe_fill_uniform_bf16_at.restype = c_int
 
 
 def check(lib: ctypes.CDLL, code: int, what: str = "") -> None:

@@ -350,9 +350,9 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
   return z ^ (z >> 31);
 }
 
-__global__ void fill_uniform_bf16(__nv_bfloat16_raw *dst, int64_t n, uint64_t seed, float two_scale) {
+__global__ void fill_uniform_bf16(__nv_bfloat16_raw *dst, int64_t start, int64_t n, uint64_t seed, float two_scale) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    uint64_t z = splitmix64(seed + (uint64_t)(i + 1) * 0x9E3779B97F4A7C15ull);
+    uint64_t z = splitmix64(seed + (uint64_t)(start + i + 1) * 0x9E3779B97F4A7C15ull);
     float u = __uint2float_rn((uint32_t)(z >> 40)) * (1.0f / 16777216.0f);
     float v = __fmul_rn(__fsub_rn(u, 0.5f), two_scale);
     uint32_t bits = __float_as_uint(v);
@@ -486,12 +486,21 @@ int coe_run_compact(const int32_t *perm, const int32_t *sorted_keys, const int32
   return check(cudaGetLastError(), "coe_run_compact") ? COE_CUDA_OK : COE_CUDA_ERR_CUDA;
 }
 
-int coe_fill_uniform_bf16(void *dst, int64_t n, uint64_t seed, float scale, cudaStream_t stream) {
+int coe_fill_uniform_bf16_at(void *dst, int64_t start, int64_t n, uint64_t seed, float scale, cudaStream_t stream) {
   if (n <= 0) return COE_CUDA_OK;
+  if (start < 0) {
+    coe_set_error("coe_fill_uniform_bf16_at: negative start");
+    return COE_CUDA_ERR_CONFIG;
+  }
   int blocks = (int)((n + 255) / 256);
   if (blocks > 148 * 16) blocks = 148 * 16;
-  fill_uniform_bf16<<<blocks, 256, 0, stream>>>(static_cast<__nv_bfloat16_raw *>(dst), n, seed, 2.0f * scale);
+  fill_uniform_bf16<<<blocks, 256, 0, stream>>>(static_cast<__nv_bfloat16_raw *>(dst), start, n, seed,
+                                                2.0f * scale);
   return check(cudaGetLastError(), "coe_fill_uniform_bf16") ? COE_CUDA_OK : COE_CUDA_ERR_CUDA;
+}
+
+int coe_fill_uniform_bf16(void *dst, int64_t n, uint64_t seed, float scale, cudaStream_t stream) {
+  return coe_fill_uniform_bf16_at(dst, 0, n, seed, scale, stream);
 }
 
 }  // extern "C"

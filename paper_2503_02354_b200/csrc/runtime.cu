@@ -136,11 +136,48 @@ const StreamMemops *stream_memops() {
   }
   return ops.wait ? &ops : nullptr;
 }
-bool wait_flag(cudaStream_t s, const int32_t *addr, uint32_t value) {
+// A flag satisfied by a REMOTE write (a peer GPU's cuStreamWriteValue32 after its NVLink row
+// stores) does not by itself make those stores visible to later work on this device: the
+// device may reorder remote writes internally.  Where the device can flush remote writes
+// (CU_DEVICE_ATTRIBUTE_CAN_FLUSH_REMOTE_WRITES) the wait carries CU_STREAM_WAIT_VALUE_FLUSH;
+// elsewhere a one-thread kernel re-reads the flag with a system-scope acquire, which orders
+// every later kernel on the stream after the peer's release.
+__global__ void acquire_flag(const int32_t *addr, uint32_t value) {
+  uint32_t v;
+  do {
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(addr) : "memory");
+  } while ((int32_t)(v - value) < 0);
+}
+int can_flush_remote_writes() {
+  static int cached = -1;
+  if (cached < 0) {
+    using AttrFn = CUresult (*)(int *, CUdevice_attribute, CUdevice);
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    if (cudaGetDriverEntryPoint("cuDeviceGetAttribute", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess &&
+        reinterpret_cast<AttrFn>(p)(&v, CU_DEVICE_ATTRIBUTE_CAN_FLUSH_REMOTE_WRITES, dev) == CUDA_SUCCESS)
+      cached = v ? 1 : 0;
+    else
+      cached = 0;
+  }
+  return cached;
+}
+bool wait_flag(cudaStream_t s, const int32_t *addr, uint32_t value, bool remote = true) {
+  const bool flush = remote && can_flush_remote_writes();
   CUresult r = stream_memops()->wait(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(addr), value,
-                                     CU_STREAM_WAIT_VALUE_GEQ);
-  if (r != CUDA_SUCCESS) coe_set_error("cuStreamWaitValue32 failed (" + std::to_string((int)r) + ")");
-  return r == CUDA_SUCCESS;
+                                     CU_STREAM_WAIT_VALUE_GEQ | (flush ? CU_STREAM_WAIT_VALUE_FLUSH : 0));
+  if (r != CUDA_SUCCESS) {
+    coe_set_error("cuStreamWaitValue32 failed (" + std::to_string((int)r) + ")");
+    return false;
+  }
+  if (remote && !flush) {
+    acquire_flag<<<1, 1, 0, s>>>(addr, value);
+    return coe_cuda_ok(cudaGetLastError(), "acquire flag");
+  }
+  return true;
 }
 // default flags: the write follows a memory barrier, so the producer kernel's stores (peer
 // stores included) are visible before the flag is
@@ -657,6 +694,31 @@ int coe_runtime_download_outputs(coe_runtime *rt, const int32_t *last_stage_host
   return ok(cudaMemcpyAsync(host, rt->outbuf, (size_t)num_requests * rt->row_elems * 2, cudaMemcpyDeviceToHost,
                             rt->compute),
             "output D2H")
+             ? COE_CUDA_OK
+             : fail_cuda();
+}
+
+int coe_runtime_download_requests(coe_runtime *rt, const int32_t *requests, const int32_t *stages, int32_t n,
+                                  void *host) {
+  if (n <= 0) return COE_CUDA_OK;
+  if (n > rt->cfg.max_requests) {
+    coe_set_error("download_requests: more rows than the runtime was sized for");
+    return COE_CUDA_ERR_CONFIG;
+  }
+  for (int32_t i = 0; i < n; ++i)
+    if (requests[i] < 0 || requests[i] >= rt->cfg.max_requests || stages[i] < 0) {
+      coe_set_error("download_requests: request or stage out of range");
+      return COE_CUDA_ERR_CONFIG;
+    }
+  if (!ok(cudaStreamSynchronize(rt->compute), "download sync")) return fail_cuda();  // h_last reuse
+  for (int32_t i = 0; i < n; ++i) rt->h_last[i] = (requests[i] << 1) | (stages[i] & 1);
+  if (!ok(cudaMemcpyAsync(rt->d_last, rt->h_last, 4 * (size_t)n, cudaMemcpyHostToDevice, rt->compute),
+          "rows H2D"))
+    return fail_cuda();
+  gather_rows<<<n, 256, 0, rt->compute>>>(rt->p0, rt->p1, rt->d_last, rt->row_elems, rt->outbuf);
+  if (!ok(cudaGetLastError(), "gather rows")) return fail_cuda();
+  return ok(cudaMemcpyAsync(host, rt->outbuf, (size_t)n * rt->row_elems * 2, cudaMemcpyDeviceToHost, rt->compute),
+            "rows D2H") && ok(cudaStreamSynchronize(rt->compute), "rows sync")
              ? COE_CUDA_OK
              : fail_cuda();
 }

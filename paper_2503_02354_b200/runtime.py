@@ -93,6 +93,7 @@ def _lib():
         lib.coe_runtime_step.argtypes = [V, P(StepInput), P(StepStats)]
         lib.coe_runtime_download_outputs.argtypes = [V, V, I32, V]
         lib.coe_runtime_synchronize.argtypes = [V]
+        lib.coe_runtime_download_requests.argtypes = [V, V, V, I32, V]
         lib.coe_runtime_check.argtypes = [V, P(I32), P(I32)]
         lib.coe_runtime_members.argtypes = [V, V, V, V]
         lib.coe_runtime_timing.argtypes = [V, P(StepTiming)]
@@ -147,6 +148,7 @@ def _lib():
         lib.coe_expert_seed.restype = ctypes.c_uint64
         for name in ("coe_runtime_create", "coe_runtime_init_experts", "coe_runtime_fill_inputs",
                      "coe_runtime_upload_inputs", "coe_runtime_step", "coe_runtime_download_outputs",
+                     "coe_runtime_download_requests",
                      "coe_runtime_synchronize", "coe_runtime_check", "coe_runtime_members", "coe_runtime_timing",
                      "coe_runtime_slot_of"):
             getattr(lib, name).restype = ctypes.c_int
@@ -256,6 +258,13 @@ class B200Runtime:
                 kw.setdefault("store_mask", touched)
             return cls(shape, len(ids), slots, len(resolved.request_ids), adm, **kw)
         arch_shapes = shape
+        width = {e: arch_shapes[registry.experts[eid].arch][0] for e, eid in enumerate(ids)}
+        for r, chain in enumerate(resolved.chains):
+            # activations are [T][max d] rows and an expert of width d reads the first d columns,
+            # so a chain must keep one width (coe_runtime_config.num_shapes)
+            if len({width[e] for e in chain}) > 1:
+                raise ValueError(f"request {resolved.request_ids[r]}: its chain changes the expert width "
+                                 f"({[width[e] for e in chain]}); every stage of a chain must share d")
         shapes = sorted({RuntimeShape(*arch_shapes[registry.experts[e].arch]) for e in ids},
                         key=lambda s: (s.d, s.h))
         index = {s: i for i, s in enumerate(shapes)}
@@ -348,6 +357,18 @@ class B200Runtime:
         last = np.ascontiguousarray(last_stage, dtype=np.int32)
         _check(self.lib, self.lib.coe_runtime_download_outputs(self.handle, last.ctypes.data, len(last), host_ptr),
                "download")
+
+    def download_requests(self, requests, stages) -> np.ndarray:
+        """Final activations of selected requests: float32 [n, T, act_ld] (synchronous)."""
+        req = np.ascontiguousarray(requests, dtype=np.int32)
+        st = np.ascontiguousarray(stages, dtype=np.int32)
+        if req.shape != st.shape:
+            raise ValueError("one stage per request")
+        T = self.shapes[0].T
+        out = np.zeros((max(1, len(req)), T, self.act_ld), np.uint16)
+        _check(self.lib, self.lib.coe_runtime_download_requests(self.handle, req.ctypes.data, st.ctypes.data,
+                                                                len(req), out.ctypes.data), "download requests")
+        return (out[:len(req)].astype(np.uint32) << 16).view(np.float32)
 
     def buffer(self, which: int) -> int:
         return int(self.lib.coe_runtime_buffer(self.handle, which) or 0)

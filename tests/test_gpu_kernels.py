@@ -4,7 +4,7 @@ K1 coe_group_sort: stable segmented radix sort by (executor, run_rank) equals
 numpy's stable lexsort, bit-exact, across sizes incl. empty / ragged tiles.
 K2 coe_run_compact: batch offsets, members and violation detection.
 K3 coe_grouped_mlp: grouped gelu-MLP over gathered request rows vs a plain
-PyTorch fp32 reference of the same op (rel-L2 <= 1e-2; bf16 operands / fp32
+PyTorch fp32 reference of the same op (rel-L2 <= 5e-3; bf16 operands / fp32
 accumulate), for T in {64, 128, 256}, partial M tiles, mixed stages (X vs
 ping-pong buffers), several expert slots per launch.
 """
@@ -224,17 +224,22 @@ def _mlp_case(lib, d, h, T, spec, slots=3):
         xs = torch.cat([src[0 if s == 0 else 1 + ((s - 1) & 1)][r * T:(r + 1) * T] for r, s in mem]).float()
         h_ref = torch.nn.functional.gelu(xs @ w1.T, approximate="tanh")
         h_got = hs[hrow: hrow + len(mem) * T].float()
-        y_ref = h_got @ w2.T  # isolate the down projection from H's bf16 rounding
+        y_iso = h_got @ w2.T  # the down projection alone (from the kernel's own bf16 H)
+        y_ref = h_ref @ w2.T  # the whole expert in fp32 (fp32 hidden activations)
         y_got = torch.cat([(p1 if s & 1 else p0)[r * T:(r + 1) * T] for r, s in mem]).float()
-        for name, got, ref in (("H", h_got, h_ref), ("Y", y_got, y_ref)):
+        for name, got, ref in (("H", h_got, h_ref), ("Y_down", y_got, y_iso), ("Y", y_got, y_ref)):
             err = ((got - ref).norm() / ref.norm()).item()
-            if err > 1e-2 and os.environ.get("COE_DEBUG"):
+            if err > K3_TOL and os.environ.get("COE_DEBUG"):
                 print(f"group slot={slot} members={mem} {name} err={err:.3g}")
             worst = max(worst, err)
         hrow += len(mem) * T
     lib.coe_mlp_destroy(handle)
     return worst
 
+
+# bf16 operands, fp32 accumulation, bf16 H and Y storage: each rounding contributes ~1.1e-3
+# rel-L2 (2^-9 / sqrt(3)); H, the down pass alone and the whole expert against fp32 (fp32 H)
+K3_TOL = 5e-3
 
 SPEC = [([(0, 0)], 0), ([(1, 0), (2, 1), (3, 2)], 1), ([(4, 1), (5, 3)], 2), ([(6, 0)], 1),
         ([(7 + i, i % 4) for i in range(9)], 0)]
@@ -245,11 +250,11 @@ SPEC = [([(0, 0)], 0), ([(1, 0), (2, 1), (3, 2)], 1), ([(4, 1), (5, 3)], 2), ([(
 def test_grouped_mlp_matches_torch_fp32(lib, d, h, T, cg, monkeypatch):
     """cg 2: the CTA-pair kernel (tcgen05.mma.cta_group::2, 256 x 256 tiles); cg 1: one CTA."""
     monkeypatch.setenv("COE_K3_CG", str(cg))
-    assert _mlp_case(lib, d, h, T, SPEC) <= 1e-2
+    assert _mlp_case(lib, d, h, T, SPEC) <= K3_TOL
 
 
 @pytest.mark.parametrize("cg", [2, 1])
 def test_grouped_mlp_single_row_block_and_many_groups(lib, cg, monkeypatch):
     monkeypatch.setenv("COE_K3_CG", str(cg))
     spec = [([(i, i % 2)], i % 3) for i in range(40)]
-    assert _mlp_case(lib, 1024, 1024, 64, spec) <= 1e-2
+    assert _mlp_case(lib, 1024, 1024, 64, spec) <= K3_TOL
