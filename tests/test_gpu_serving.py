@@ -307,6 +307,23 @@ def test_window_search_with_measured_b200_throughput():
     assert res.throughput_samples and all(t > 0 for _, t in res.throughput_samples)
     counts = [c for c, _ in res.throughput_samples]
     assert counts == sorted(counts) and res.lower <= res.chosen <= res.upper
+    # the same decision as the window rule replayed over the measured samples (the rule itself is
+    # pinned to the reference on CPU: tests/test_window_search_golden.py, which also replays every
+    # measured curve committed under profiles/ through the reference)
+    table = dict(res.throughput_samples)
+    max_count = counts[-1]  # the last probe is either the stop point or the clamp at max_count
+    replay = profiler.decay_window_search(lambda c: table[c], max_count=max_count, choose="midpoint")
+    assert (replay.lower, replay.upper, replay.chosen) == (res.lower, res.upper, res.chosen)
+    import json
+    import os
+
+    os.makedirs("gpurun_out", exist_ok=True)
+    with open("gpurun_out/window_search_measured_test.json", "w") as fh:
+        json.dump({"config": "c3 (1024x2048x64 physical stand-in)", "sample_requests": 120,
+                   "measured": res.to_doc(),
+                   "search": {"max_count": max_count, "initial_window": profiler.DEFAULT_INITIAL_WINDOW,
+                              "error_margin": profiler.DEFAULT_ERROR_MARGIN,
+                              "fit_points": profiler.DEFAULT_FIT_POINTS, "choose": "midpoint", "seed": 0}}, fh)
 
 
 def test_fused_hops_across_processes_ipc():

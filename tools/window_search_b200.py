@@ -16,7 +16,14 @@ measured = profiler.search_memory_allocation_measured(cfg, runtime.shape_of(w), 
                                                       seed=subseed(0, "alloc", "gpu"))
 virtual = profiler.search_memory_allocation(w.registry, w.device, "gpu", cfg.stream[:n], seed=subseed(0, "alloc", "gpu"),
                                             policy=cfg.policy, gpu_executors=1, cpu_executors=0)
-out = {"config": name, "sample_requests": n, "measured": measured.to_doc(), "virtual": virtual.to_doc()}
+from dataclasses import replace
+base = replace(cfg, stream=cfg.stream[:n], search_enabled=False, trace=False)
+gx, cx = engine._executor_counts(base, engine.resolve(base).policy)
+out = {"config": name, "sample_requests": n, "measured": measured.to_doc(), "virtual": virtual.to_doc(),
+       "search": {"max_count": engine.max_useful_expert_count(base.registry, base.device, "gpu", gx, cx,
+                                                              base.cpu_mem_fraction),
+                  "initial_window": profiler.DEFAULT_INITIAL_WINDOW, "error_margin": profiler.DEFAULT_ERROR_MARGIN,
+                  "fit_points": profiler.DEFAULT_FIT_POINTS, "choose": "random", "seed": subseed(0, "alloc", "gpu")}}
 os.makedirs("gpurun_out", exist_ok=True)
 json.dump(out, open(f"gpurun_out/window_search_{name}.json", "w"), indent=1)
 print(json.dumps({k: (v["lower"], v["upper"], v["chosen"]) for k, v in out.items() if isinstance(v, dict)}))
