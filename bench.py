@@ -496,7 +496,8 @@ def main() -> None:
     load_bytes = stats["load_bytes"] + stats["restore_bytes"]
     registry = plan_last.resolved.config.registry
     expert_gb = sum(spec.param_bytes for spec in registry.experts.values()) / 1e9
-    act_gb = 3 * n_req * rt.shapes[0].T * rt.act_ld * 2 / 1e9  # X read, P0 / P1 written and read
+    act_gb = 3 * n_req * rt.shapes[0].T * rt.act_ld * 2 / 1e9  # X read, ring rows written and read
+    mem = rt.memory()
     copy_s = timing["copy_busy_ms"] / 1e3
     short = min(timing["copy_busy_ms"], timing["compute_busy_ms"])
     line = {
@@ -511,6 +512,7 @@ def main() -> None:
                    "expert_budget_bytes": plan0.resolved.alloc["gpu"]["expert_budget_bytes"],
                    "hbm_slots": rt.num_slots, "policy": w.run["policy"], "parallelism": f"executor-per-gpu x{world}",
                    "hop_transport": (transport if world > 1 else None),
+                   "device_memory": dict(mem, note="activations: the request-slot ring (peak occupancy of this plan, stages in place) + hop-in landing rows + H scratch + e2e output staging; device_io_xy: the device-resident request inputs X and outputs Y of the `value` run (the e2e run streams both through the ring / staging instead)"),
                    "l2": (f"no flush needed: {expert_gb:.1f} GB of experts and {act_gb:.1f} GB of activations "
                           "touched per step exceed the 126 MB L2")},
         "swaps_per_1k_requests": 1000.0 * metrics.expert_switches / n_req,

@@ -57,6 +57,14 @@ int coe_run_compact(const int32_t *perm, const int32_t *sorted_keys, const int32
                     int32_t *out_member_stage, int32_t *out_run_count, int32_t *out_violations, void *scratch,
                     cudaStream_t stream);
 int64_t coe_run_compact_scratch_bytes(int64_t n, int num_batches, int num_executors);
+/* coe_run_compact that also gathers each admission's activation-row routes (adm_in /
+ * adm_out -> out_member_in / out_member_out, same permutation; see coe_grouped_mlp_routed) */
+int coe_run_compact_routes(const int32_t *perm, const int32_t *sorted_keys, const int32_t *adm_request,
+                           const int32_t *adm_stage, const int32_t *adm_in, const int32_t *adm_out, int64_t n,
+                           int rank_bits, const int32_t *batch_exec, const int32_t *batch_size, int num_batches,
+                           int num_executors, int32_t *out_batch_off, int32_t *out_member_req,
+                           int32_t *out_member_stage, int32_t *out_member_in, int32_t *out_member_out,
+                           int32_t *out_run_count, int32_t *out_violations, void *scratch, cudaStream_t stream);
 
 /* ---------------- K3: grouped expert MLP (tcgen05) ------------------------ */
 
@@ -72,6 +80,7 @@ typedef struct coe_mlp_config {
   int64_t slot_stride_bytes;
   int32_t act_ld;               /* row stride of X / P0 / P1 in elements (0: d);
                                    > d when experts of several widths share them */
+  int64_t x_rows;               /* rows of x (0: act_rows)                       */
 } coe_mlp_config;
 
 /* One planned batch inside a wave.  tile_start is the wave-relative prefix of
@@ -103,6 +112,18 @@ int coe_grouped_mlp(coe_mlp *m, const coe_mlp_group *groups_up, const coe_mlp_gr
  * local buffer.  hop_dst == NULL turns it off.  world <= COE_MAX_PEERS. */
 #define COE_MAX_PEERS 8
 int coe_mlp_set_hops(coe_mlp *m, const int8_t *hop_dst, int hop_stride, void *const *peer_act, int world);
+/* Routed mode: each member (sorted admission) names its own activation rows instead of
+ * (request, stage) ping-pong addressing.  member_in[i] = (row << 1) | from_x: the A operand
+ * is request-row block `row` of cfg.x (from_x = 1) or of cfg.act0 (the activation ring A);
+ * member_out[i] = (row << 4) | kind: the down pass stores the member's rows into block `row`
+ * of kind 0 = cfg.act0 (in place: the up pass has consumed the input), 1 = the device output
+ * buffer y, 2 = the output staging ring, 3 + r = executor r's act0 (peer_act of
+ * coe_mlp_set_hops; a fused hop).  Up passes only read member_in, down passes member_out. */
+int coe_mlp_set_outputs(coe_mlp *m, void *y, void *out_stage);
+int coe_grouped_mlp_routed(coe_mlp *m, const coe_mlp_group *groups_up, const coe_mlp_group *groups_down,
+                           int num_groups, int tiles_up, int tiles_down, const int32_t *batch_off,
+                           const int32_t *member_in, const int32_t *member_out, int which, int max_ctas,
+                           cudaStream_t stream);
 /* Stage-0 inputs of later launches from `x` (same shape / stride as cfg.x; NULL or cfg.x:
  * back to cfg.x) -- lets e2e steps double-buffer their input uploads. */
 int coe_mlp_set_input(coe_mlp *m, void *x);
@@ -138,7 +159,15 @@ typedef struct coe_runtime_config {
   const int32_t *shape_d, *shape_h, *shape_slots;   /* [num_shapes]                  */
   const int32_t *expert_shape;                       /* [num_experts] shape index     */
   const uint8_t *store_mask; /* [num_experts] experts held in the host store (NULL: all) */
+  /* activation memory (act_rows.h): A = [landing_slots | ring_slots] request-row blocks of
+   * T x max-d bf16 -- a request's activation occupies one ring slot from its first batch
+   * here until its output leaves (stages run in place), hop-ins land in landing rows;
+   * size both with coe_runtime_plan_rows.  out_slots: e2e output staging rows (0: auto). */
+  int32_t ring_slots, landing_slots, out_slots;
+  int32_t device_io;        /* 1: X / Y of max_requests rows for device-resident steps
+                               (fill_inputs, value-mode steps, download_*); 0: e2e only */
 } coe_runtime_config;
+
 
 typedef struct coe_step_input {
   int32_t executor;                         /* ops / admissions of other executors ignored */
@@ -159,6 +188,12 @@ typedef struct coe_step_input {
   void *host_outputs;
 } coe_step_input;
 
+/* Activation rows one step of `in` needs on executor in->executor (host only, no GPU):
+ * the ring's peak occupancy and the landing rows for hop-ins.  e2e: stage-0 inputs also
+ * occupy slots; nccl: hop-outs keep their slots until the step ends (the NCCL transport). */
+int coe_runtime_plan_rows(const coe_step_input *in, int32_t max_requests, int e2e, int nccl,
+                          int32_t *ring_slots, int32_t *landing_slots);
+
 typedef struct coe_step_stats {
   int64_t admissions, batches, waves, launches;
   int64_t h2d_input_bytes, d2h_output_bytes;
@@ -166,6 +201,8 @@ typedef struct coe_step_stats {
   int64_t max_wave_rows;
   int32_t max_wave_groups;
   int32_t rank_bits;
+  int32_t ring_peak;        /* activation ring slots occupied at most during the step  */
+  int32_t landing_rows;     /* landing rows the step's hop-ins used                     */
 } coe_step_stats;
 
 typedef struct coe_step_timing {

@@ -12,6 +12,7 @@ class MlpConfig(ctypes.Structure):
         ("x", c_void_p), ("act0", c_void_p), ("act1", c_void_p), ("act_rows", c_int64),
         ("h_scratch", c_void_p), ("h_rows", c_int64),
         ("slab", c_void_p), ("num_slots", c_int32), ("slot_stride_bytes", c_int64), ("act_ld", c_int32),
+        ("x_rows", c_int64),
     ]
 
 

@@ -230,14 +230,19 @@ __global__ void __launch_bounds__(SORT_THREADS, ITEMS >= 16 ? 3 : 6)
 
 // K2 part 1: gather members, mark run starts / executor segment starts.
 __global__ void compact_gather(const int32_t *perm, const uint32_t *keys, const int32_t *adm_req,
-                               const int32_t *adm_stage, int64_t n, int rank_bits, int32_t *member_req,
-                               int32_t *member_stage, int32_t *seg_start, int32_t *run_count) {
+                               const int32_t *adm_stage, const int32_t *adm_in, const int32_t *adm_out, int64_t n,
+                               int rank_bits, int32_t *member_req, int32_t *member_stage, int32_t *member_in,
+                               int32_t *member_out, int32_t *seg_start, int32_t *run_count) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   int starts = 0;
   if (i < n) {
     int32_t p = perm[i];
     member_req[i] = adm_req[p];
     member_stage[i] = adm_stage[p];
+    if (adm_in) {  // activation-row routes (coe_run_compact_routes)
+      member_in[i] = adm_in[p];
+      member_out[i] = adm_out[p];
+    }
     uint32_t k = keys[i];
     bool new_run = i == 0 || keys[i - 1] != k;
     starts = new_run ? 1 : 0;
@@ -457,6 +462,21 @@ int coe_run_compact(const int32_t *perm, const int32_t *sorted_keys, const int32
                     const int32_t *batch_size, int num_batches, int num_executors, int32_t *out_batch_off,
                     int32_t *out_member_req, int32_t *out_member_stage, int32_t *out_run_count,
                     int32_t *out_violations, void *scratch, cudaStream_t stream) {
+  return coe_run_compact_routes(perm, sorted_keys, adm_request, adm_stage, nullptr, nullptr, n, rank_bits, batch_exec,
+                                batch_size, num_batches, num_executors, out_batch_off, out_member_req,
+                                out_member_stage, nullptr, nullptr, out_run_count, out_violations, scratch, stream);
+}
+
+int coe_run_compact_routes(const int32_t *perm, const int32_t *sorted_keys, const int32_t *adm_request,
+                           const int32_t *adm_stage, const int32_t *adm_in, const int32_t *adm_out, int64_t n,
+                           int rank_bits, const int32_t *batch_exec, const int32_t *batch_size, int num_batches,
+                           int num_executors, int32_t *out_batch_off, int32_t *out_member_req,
+                           int32_t *out_member_stage, int32_t *out_member_in, int32_t *out_member_out,
+                           int32_t *out_run_count, int32_t *out_violations, void *scratch, cudaStream_t stream) {
+  if ((adm_in == nullptr) != (adm_out == nullptr) || (adm_in && (!out_member_in || !out_member_out))) {
+    coe_set_error("coe_run_compact_routes: route arrays must be given in / out together");
+    return COE_CUDA_ERR_CONFIG;
+  }
   int32_t *seg_start = static_cast<int32_t *>(scratch);
   int32_t *block_sums = seg_start + num_executors + 16;
   if (!check(cudaMemsetAsync(seg_start, 0, 4 * (size_t)num_executors, stream), "compact memset") ||
@@ -466,7 +486,8 @@ int coe_run_compact(const int32_t *perm, const int32_t *sorted_keys, const int32
   if (n > 0) {
     const int blocks = (int)((n + 255) / 256);
     compact_gather<<<blocks, 256, 0, stream>>>(perm, reinterpret_cast<const uint32_t *>(sorted_keys), adm_request,
-                                               adm_stage, n, rank_bits, out_member_req, out_member_stage, seg_start,
+                                               adm_stage, adm_in, adm_out, n, rank_bits, out_member_req,
+                                               out_member_stage, out_member_in, out_member_out, seg_start,
                                                out_run_count);
   }
   if (num_batches > 0) {

@@ -93,6 +93,14 @@ struct GemmArgs {
   const int8_t *hop_dst;
   int hop_stride;
   __nv_bfloat16 *peer_act[COE_MAX_PEERS][2];
+  // routed mode (coe_grouped_mlp_routed; member_in != nullptr): every member carries its own
+  // activation rows -- in = (row << 1) | from_X, out = (row << 4) | kind with kind 0 the local
+  // activation ring A, 1 the device output buffer Y, 2 the e2e output staging ring, 3 + r
+  // executor r's A (a fused hop into its landing rows); rows count requests (T rows each)
+  const int32_t *member_in;
+  const int32_t *member_out;
+  __nv_bfloat16 *out_y;
+  __nv_bfloat16 *out_stage;
 };
 
 // A-operand source of a member at chain stage s: 0 = X, 1 = P0, 2 = P1.
@@ -233,8 +241,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             int j = r / args.T;
             const int within = r - j * args.T;
             j = min(j, members - 1);  // rows past the group (pair tail): any valid member, discarded
-            box_row[b] = args.member_req[boff + j] * args.T + within;
-            box_par[b] = a_source(args.member_stage[boff + j]);
+            if (args.member_in) {
+              const int code = args.member_in[boff + j];
+              box_row[b] = (code >> 1) * args.T + within;
+              box_par[b] = (code & 1) ? 0 : 1;
+            } else {
+              box_row[b] = args.member_req[boff + j] * args.T + within;
+              box_par[b] = a_source(args.member_stage[boff + j]);
+            }
           }
           a_bytes = (uint32_t)(nboxes * args.a_box_rows * BK * 2);
         } else {
@@ -331,14 +345,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         } else {
           const int boff = args.batch_off[grp.batch];
           const int j = row / args.T;
-          const int req = args.member_req[boff + j];
-          const int st = args.member_stage[boff + j];
-          __nv_bfloat16 *dst = (st & 1) ? args.out_act1 : args.out_act0;
-          if (args.hop_dst) {
-            const int hd = args.hop_dst[(size_t)req * args.hop_stride + st];
-            if (hd >= 0) dst = args.peer_act[hd][st & 1];
+          if (args.member_out) {
+            const int code = args.member_out[boff + j];
+            const int kind = code & 15;
+            __nv_bfloat16 *dst = kind == 0   ? args.out_act0
+                                 : kind == 1 ? args.out_y
+                                 : kind == 2 ? args.out_stage
+                                             : args.peer_act[kind - 3][0];
+            out_row = dst + ((size_t)(code >> 4) * args.T + (row - j * args.T)) * args.ld;
+          } else {
+            const int req = args.member_req[boff + j];
+            const int st = args.member_stage[boff + j];
+            __nv_bfloat16 *dst = (st & 1) ? args.out_act1 : args.out_act0;
+            if (args.hop_dst) {
+              const int hd = args.hop_dst[(size_t)req * args.hop_stride + st];
+              if (hd >= 0) dst = args.peer_act[hd][st & 1];
+            }
+            out_row = dst + ((size_t)req * args.T + (row - j * args.T)) * args.ld;
           }
-          out_row = dst + ((size_t)req * args.T + (row - j * args.T)) * args.ld;
         }
         out_row += c.n_blk * BN;
       }
@@ -454,6 +478,7 @@ struct coe_mlp {
   const int8_t *hop_dst = nullptr;   // fused hops (coe_mlp_set_hops)
   int hop_stride = 0;
   __nv_bfloat16 *peer_act[COE_MAX_PEERS][2] = {};
+  __nv_bfloat16 *out_y = nullptr, *out_stage = nullptr;  // routed mode (coe_mlp_set_outputs)
 };
 
 extern "C" {
@@ -477,7 +502,8 @@ int coe_mlp_create(const coe_mlp_config *cfg, coe_mlp **out) {
   m->a_box_rows = cfg->T < BM ? cfg->T : BM;
   bool ok = true;
   const uint64_t ld = cfg->act_ld > 0 ? (uint64_t)cfg->act_ld : (uint64_t)cfg->d;
-  ok &= make_map_2d(&m->xmap, cfg->x, (uint64_t)cfg->act_rows, cfg->d, m->a_box_rows, ld);
+  const uint64_t x_rows = cfg->x_rows > 0 ? (uint64_t)cfg->x_rows : (uint64_t)cfg->act_rows;
+  ok &= make_map_2d(&m->xmap, cfg->x, x_rows, cfg->d, m->a_box_rows, ld);
   ok &= make_map_2d(&m->act0, cfg->act0, (uint64_t)cfg->act_rows, cfg->d, m->a_box_rows, ld);
   ok &= make_map_2d(&m->act1, cfg->act1, (uint64_t)cfg->act_rows, cfg->d, m->a_box_rows, ld);
   ok &= make_map_2d(&m->hmap, cfg->h_scratch, (uint64_t)cfg->h_rows, cfg->h, BM);
@@ -517,7 +543,8 @@ int coe_mlp_set_input(coe_mlp *m, void *x) {
   }
   if (x != m->x_alt) {
     const uint64_t ld = m->cfg.act_ld > 0 ? (uint64_t)m->cfg.act_ld : (uint64_t)m->cfg.d;
-    if (!make_map_2d(&m->xmap_alt, x, (uint64_t)m->cfg.act_rows, m->cfg.d, m->a_box_rows, ld)) {
+    const uint64_t x_rows = m->cfg.x_rows > 0 ? (uint64_t)m->cfg.x_rows : (uint64_t)m->cfg.act_rows;
+    if (!make_map_2d(&m->xmap_alt, x, x_rows, m->cfg.d, m->a_box_rows, ld)) {
       coe_set_error("coe_mlp_set_input: cuTensorMapEncodeTiled failed");
       return COE_CUDA_ERR_CUDA;
     }
@@ -538,13 +565,44 @@ int coe_mlp_set_hops(coe_mlp *m, const int8_t *hop_dst, int hop_stride, void *co
   m->hop_stride = hop_stride;
   for (int r = 0; r < COE_MAX_PEERS; ++r)
     for (int b = 0; b < 2; ++b)
-      m->peer_act[r][b] = (hop_dst && r < world) ? static_cast<__nv_bfloat16 *>(peer_act[2 * r + b]) : nullptr;
+      m->peer_act[r][b] = (peer_act && r < world) ? static_cast<__nv_bfloat16 *>(peer_act[2 * r + b]) : nullptr;
   return COE_CUDA_OK;
 }
+
+int coe_mlp_set_outputs(coe_mlp *m, void *y, void *out_stage) {
+  m->out_y = static_cast<__nv_bfloat16 *>(y);
+  m->out_stage = static_cast<__nv_bfloat16 *>(out_stage);
+  return COE_CUDA_OK;
+}
+
+static int launch_grouped(coe_mlp *m, const coe_mlp_group *groups_up, const coe_mlp_group *groups_down, int num_groups,
+                          int tiles_up, int tiles_down, const int32_t *batch_off, const int32_t *member_req,
+                          const int32_t *member_stage, const int32_t *member_in, const int32_t *member_out,
+                          int which, int max_ctas, cudaStream_t stream);
 
 int coe_grouped_mlp(coe_mlp *m, const coe_mlp_group *groups_up, const coe_mlp_group *groups_down, int num_groups,
                     int tiles_up, int tiles_down, const int32_t *batch_off, const int32_t *member_req,
                     const int32_t *member_stage, int which, int max_ctas, cudaStream_t stream) {
+  return launch_grouped(m, groups_up, groups_down, num_groups, tiles_up, tiles_down, batch_off, member_req,
+                        member_stage, nullptr, nullptr, which, max_ctas, stream);
+}
+
+int coe_grouped_mlp_routed(coe_mlp *m, const coe_mlp_group *groups_up, const coe_mlp_group *groups_down,
+                           int num_groups, int tiles_up, int tiles_down, const int32_t *batch_off,
+                           const int32_t *member_in, const int32_t *member_out, int which, int max_ctas,
+                           cudaStream_t stream) {
+  if (!member_in || !member_out) {
+    coe_set_error("coe_grouped_mlp_routed: member routes required");
+    return COE_CUDA_ERR_CONFIG;
+  }
+  return launch_grouped(m, groups_up, groups_down, num_groups, tiles_up, tiles_down, batch_off, nullptr, nullptr,
+                        member_in, member_out, which, max_ctas, stream);
+}
+
+static int launch_grouped(coe_mlp *m, const coe_mlp_group *groups_up, const coe_mlp_group *groups_down, int num_groups,
+                          int tiles_up, int tiles_down, const int32_t *batch_off, const int32_t *member_req,
+                          const int32_t *member_stage, const int32_t *member_in, const int32_t *member_out,
+                          int which, int max_ctas, cudaStream_t stream) {
   if (num_groups <= 0) return COE_CUDA_OK;
   if (num_groups > MAX_GROUPS) {
     coe_set_error("too many groups in one wave");
@@ -570,13 +628,17 @@ int coe_grouped_mlp(coe_mlp *m, const coe_mlp_group *groups_up, const coe_mlp_gr
     a.out_h = reinterpret_cast<__nv_bfloat16 *>(c.h_scratch);
     a.out_act0 = reinterpret_cast<__nv_bfloat16 *>(c.act0);
     a.out_act1 = reinterpret_cast<__nv_bfloat16 *>(c.act1);
-    a.hop_dst = pass == 1 ? m->hop_dst : nullptr;
+    a.hop_dst = (pass == 1 && !member_in) ? m->hop_dst : nullptr;
     a.hop_stride = m->hop_stride;
     std::memcpy(a.peer_act, m->peer_act, sizeof(a.peer_act));
+    a.member_in = member_in;
+    a.member_out = member_out;
+    a.out_y = m->out_y;
+    a.out_stage = m->out_stage;
     if (a.total_tiles <= 0) continue;
     int cap = (max_ctas > 0 && max_ctas < m->num_sms) ? max_ctas : m->num_sms;
     const CUtensorMap &ta0 = pass == 0 ? (m->use_alt ? m->xmap_alt : m->xmap) : m->hmap, &ta1 = pass == 0 ? m->act0 : m->hmap,
-                      &ta2 = pass == 0 ? m->act1 : m->hmap, &tb = pass == 0 ? m->w1 : m->w2;
+                      &ta2 = pass == 0 ? (member_in ? m->act0 : m->act1) : m->hmap, &tb = pass == 0 ? m->w1 : m->w2;
     cudaError_t e;
     if (m->cg == 1) {
       const int grid = a.total_tiles < cap ? a.total_tiles : cap;

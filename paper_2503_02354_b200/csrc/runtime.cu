@@ -38,6 +38,7 @@
 #include <array>
 #include <cstring>
 #include <climits>
+#include <deque>
 #include <cstdlib>
 #include <string>
 #include <unordered_map>
@@ -48,6 +49,7 @@
 #include "coe_planner.h"
 #include "comm.h"
 #include "common.cuh"
+#include "act_rows.h"
 #include "hops.h"
 
 namespace {
@@ -72,16 +74,6 @@ __global__ void gather_rows(const __nv_bfloat16 *p0, const __nv_bfloat16 *p1, co
   const uint4 *sv = reinterpret_cast<const uint4 *>(src);
   uint4 *dv = reinterpret_cast<uint4 *>(out + (int64_t)blockIdx.x * row_elems);
   for (int64_t i = threadIdx.x; i < row_elems / 8; i += blockDim.x) dv[i] = sv[i];
-}
-
-__global__ void gather_outputs(const __nv_bfloat16 *p0, const __nv_bfloat16 *p1, const int32_t *last_stage,
-                               int32_t num_requests, int64_t row_elems, __nv_bfloat16 *out) {
-  int32_t r = blockIdx.x;  // one block per request, 16-byte vectors
-  if (r >= num_requests) return;
-  const __nv_bfloat16 *src = (last_stage[r] & 1) ? p1 : p0;
-  const uint4 *s = reinterpret_cast<const uint4 *>(src + r * row_elems);
-  uint4 *d = reinterpret_cast<uint4 *>(out + r * row_elems);
-  for (int64_t i = threadIdx.x; i < row_elems / 8; i += blockDim.x) d[i] = s[i];
 }
 
 struct CopyAct {
@@ -187,7 +179,6 @@ bool write_flag(cudaStream_t s, int32_t *addr, uint32_t value) {
   if (r != CUDA_SUCCESS) coe_set_error("cuStreamWriteValue32 failed (" + std::to_string((int)r) + ")");
   return r == CUDA_SUCCESS;
 }
-constexpr int HOP_STRIDE = 8;  // hop_dst row per request: one entry per chain stage (<= 8 stages)
 
 // Release-wave grid: the reserved SMs (COE_RELEASE_CTAS overrides, for experiments).
 int release_grid(int reserved, int /*sms*/) {
@@ -219,12 +210,11 @@ bool batched_copy(std::vector<void *> &dsts, std::vector<void *> &srcs, std::vec
 void coe_set_error(const std::string &msg) { g_last_error = msg; }
 
 struct StepBuffers {  // device arrays one step uses; two sets alternate
-  int32_t *adm = nullptr;   // [4][max_adm]: exec, rank, req, stage
+  int32_t *adm = nullptr;   // [6][max_adm]: exec, rank, req, stage, in route, out route
   int32_t *batch = nullptr; // [2][max_batches]: exec, size
   int32_t *boff = nullptr;
-  int32_t *mreq = nullptr, *mstage = nullptr;
+  int32_t *mreq = nullptr, *mstage = nullptr, *min = nullptr, *mout = nullptr;
   coe_mlp_group *groups = nullptr;  // [2][max_batches]
-  int32_t *fin = nullptr;           // e2e: final rows in completion order, request << 1 | parity
   cudaEvent_t free_ev = nullptr;    // recorded on compute when the step using this set ends
   bool used = false;
 };
@@ -251,8 +241,22 @@ struct coe_runtime {
   static constexpr int NCLS = 3;
   cudaStream_t cls_stream[NCLS] = {nullptr, nullptr, nullptr};
   cudaStream_t compute = nullptr, copy = nullptr;  // compute == cls_stream[0]
-  // device memory
-  __nv_bfloat16 *x = nullptr, *p0 = nullptr, *p1 = nullptr, *outbuf = nullptr;
+  // device memory: X / Y device-resident request inputs / final outputs ([requests][T][ld],
+  // device_io only); A the activation rows [landing | ring] (act_rows.h); the output staging
+  // ring (e2e finals, download staging)
+  __nv_bfloat16 *x = nullptr, *y = nullptr, *act = nullptr, *outbuf = nullptr;
+  int32_t ring_slots = 0, landing_slots = 0, out_slots = 0;
+  std::vector<int32_t> ring_order;     // free list of ring slots (absolute A rows), FIFO across steps
+  std::vector<int32_t> act_prev_wave;  // per A row: wave of the previous step that freed it (-1: none)
+  bool prev_nccl_hold = false;         // the previous step kept NCCL hop-out rows until its end
+  int64_t out_pos = 0;                 // e2e: global position of the next staging row
+  struct OutUse {
+    int64_t begin, end;
+    cudaEvent_t ev;
+  };
+  std::deque<OutUse> out_hist;         // e2e: staging rows still being downloaded
+  std::vector<cudaEvent_t> out_ev_pool;
+  int step_parity = 0;                 // wave events alternate by step (the next step refers back)
   __nv_bfloat16 *hbuf[NCLS] = {nullptr, nullptr, nullptr};
   StepBuffers sets[2];
   int cur_set = 0;
@@ -272,8 +276,8 @@ struct coe_runtime {
   // last reader of each slot half in the previous step, per compute stream ([slot * NCLS + cls])
   std::vector<cudaEvent_t> slot_free_up, slot_free_down;
   std::vector<uint8_t> slot_free_valid;
-  // events
-  std::vector<cudaEvent_t> wave_up_ev, wave_down_ev, copy_up_ev, copy_down_ev, out_ev;
+  // events (wave events per step parity: e2e uploads of step k+1 wait on step k's waves)
+  std::vector<cudaEvent_t> wave_up_evs[2], wave_down_evs[2], copy_up_ev, copy_down_ev, out_ev;
   std::vector<int32_t> out_order;  // e2e: request of each host output row (completion order)
   std::vector<cudaEvent_t> t_copy_start, t_copy_end, t_wave_start, t_wave_end, t_up_end, t_down_start;
   std::vector<cudaEvent_t> t_io;    // profile, e2e: [start, end] event pairs of uploads / downloads
@@ -290,12 +294,6 @@ struct coe_runtime {
   std::vector<cudaEvent_t> in_ev;
   cudaEvent_t out_drained = nullptr;
   bool have_out = false;
-  // e2e input double buffer: step k uploads into X[k & 1] (x, then x_alt) while step k-1 may
-  // still read the other; x_free[p] marks the end of the last step that read X[p]
-  __nv_bfloat16 *x_alt = nullptr;
-  int64_t e2e_steps = 0;
-  cudaEvent_t x_free[2] = {nullptr, nullptr};
-  bool x_free_valid[2] = {false, false};
   coe_comm *comm = nullptr;            // hop transport (N > 1)
   cudaStream_t hop = nullptr;
   std::vector<cudaEvent_t> recv_ev;
@@ -312,8 +310,6 @@ struct coe_runtime {
   int32_t peer_rank = -1, peer_world = 0;
   coe_local_hub *peer_hub = nullptr;  // same-process peers: host-side event handoff, no flags
   uint32_t step_seq = 0;
-  int8_t *d_hopdst[2] = {nullptr, nullptr};  // per step set: [max_requests][HOP_STRIDE]
-  int8_t *h_hopdst[2] = {nullptr, nullptr};
   int m_ctas = 148, r_ctas = 16;  // SM split: main waves vs the swap-in-gating waves
   int rel_launch_ctas = 148;      // grid of a release wave (all SMs; see phase C)
 
@@ -326,21 +322,20 @@ struct coe_runtime {
     for (auto &per : mlps)
       for (auto m : per)
         if (m) coe_mlp_destroy(m);
-    std::vector<void *> dev = {x, x_alt, p0, p1, hbuf[0], hbuf[1], hbuf[2], outbuf, d_perm, d_keys, d_flags, d_last, d_sort_scratch,
-                               d_compact_scratch};
+    std::vector<void *> dev = {x, y, act, hbuf[0], hbuf[1], hbuf[2], outbuf, d_perm, d_keys, d_flags, d_last,
+                               d_sort_scratch, d_compact_scratch};
     for (char *sl : slabs) dev.push_back(sl);
     for (auto &s : sets) {
       for (void *p : {(void *)s.adm, (void *)s.batch, (void *)s.boff, (void *)s.mreq, (void *)s.mstage,
-                      (void *)s.groups, (void *)s.fin})
+                      (void *)s.min, (void *)s.mout, (void *)s.groups})
         dev.push_back(p);
       if (s.free_ev) cudaEventDestroy(s.free_ev);
     }
     for (void *p : dev)
       if (p) cudaFree(p);
     for (void *p : ipc_opened) cudaIpcCloseMemHandle(p);
-    for (void *p : {(void *)d_hflags, (void *)d_hopdst[0], (void *)d_hopdst[1]})
-      if (p) cudaFree(p);
-    for (void *p : {(void *)staging[0], (void *)staging[1], (void *)h_last, (void *)h_hopdst[0], (void *)h_hopdst[1]})
+    if (d_hflags) cudaFree(d_hflags);
+    for (void *p : {(void *)staging[0], (void *)staging[1], (void *)h_last})
       if (p) cudaFreeHost(p);
     if (host_store && store_mapped) {
       cudaHostUnregister(host_store);
@@ -348,12 +343,14 @@ struct coe_runtime {
     } else if (host_store) {
       cudaFreeHost(host_store);
     }
-    for (auto *v : {&in_ev, &recv_ev, &slot_free_up, &slot_free_down, &wave_up_ev, &wave_down_ev, &copy_up_ev, &copy_down_ev, &out_ev,
+    for (auto *v : {&in_ev, &recv_ev, &slot_free_up, &slot_free_down, &wave_up_evs[0], &wave_down_evs[0],
+                    &wave_up_evs[1], &wave_down_evs[1], &copy_up_ev, &copy_down_ev, &out_ev, &out_ev_pool,
                     &t_copy_start, &t_copy_end, &t_wave_start, &t_wave_end, &t_up_end, &t_down_start, &t_io}) {
       for (auto e : *v) cudaEventDestroy(e);
       v->clear();
     }
-    for (cudaEvent_t e : {x_free[0], x_free[1], out_drained, hop_drained, step_end, staged, copy_drained, grouped, cls_drained[0], cls_drained[1], cls_drained[2], t_step_start, t_group_end, t_step_end, staging_done[0],
+    for (auto &u : out_hist) cudaEventDestroy(u.ev);
+    for (cudaEvent_t e : {out_drained, hop_drained, step_end, staged, copy_drained, grouped, cls_drained[0], cls_drained[1], cls_drained[2], t_step_start, t_group_end, t_step_end, staging_done[0],
                           staging_done[1]})
       if (e) cudaEventDestroy(e);
     for (auto st : cls_stream)
@@ -496,7 +493,12 @@ int coe_runtime_create(const coe_runtime_config *cfg, coe_runtime **out) {
       }
   }
   rt->row_elems = (int64_t)c.T * rt->act_ld;
-  const int64_t act_bytes = (int64_t)c.max_requests * rt->row_elems * 2;
+  const int64_t io_bytes = c.device_io ? (int64_t)c.max_requests * rt->row_elems * 2 : 0;
+  rt->ring_slots = std::max(1, c.ring_slots);
+  rt->landing_slots = std::max(0, c.landing_slots);
+  // staging for e2e finals: several waves' worth (a wave holds at most max_wave_rows / T requests)
+  rt->out_slots = c.out_slots > 0 ? c.out_slots : (int32_t)std::max<int64_t>(64, 2 * c.max_wave_rows / c.T);
+  const int64_t a_rows = (int64_t)rt->landing_slots + rt->ring_slots;
   const size_t A = (size_t)c.max_admissions, B = (size_t)c.max_batches;
   int prio_low = 0, prio_high = 0;
   cudaDeviceGetStreamPriorityRange(&prio_low, &prio_high);
@@ -506,8 +508,9 @@ int coe_runtime_create(const coe_runtime_config *cfg, coe_runtime **out) {
               ok(cudaStreamCreateWithFlags(&rt->copy, cudaStreamNonBlocking), "stream") &&
               ok(cudaStreamCreateWithFlags(&rt->hop, cudaStreamNonBlocking), "stream") &&
               ok(cudaStreamCreateWithFlags(&rt->out_stream, cudaStreamNonBlocking), "stream") &&
-              dmalloc(&rt->x, act_bytes, "X alloc") && dmalloc(&rt->p0, act_bytes, "P0 alloc") &&
-              dmalloc(&rt->p1, act_bytes, "P1 alloc") && dmalloc(&rt->outbuf, act_bytes, "out alloc") &&
+              (!c.device_io || (dmalloc(&rt->x, io_bytes, "X alloc") && dmalloc(&rt->y, io_bytes, "Y alloc"))) &&
+              dmalloc(&rt->act, a_rows * rt->row_elems * 2, "activation ring alloc") &&
+              dmalloc(&rt->outbuf, (int64_t)rt->out_slots * rt->row_elems * 2, "output staging alloc") &&
               dmalloc(&rt->hbuf[0], (size_t)c.max_wave_rows * rt->h_max * 2, "H alloc") &&
               dmalloc(&rt->hbuf[1], (size_t)c.max_wave_rows * rt->h_max * 2, "H alloc") &&
               dmalloc(&rt->hbuf[2], (size_t)c.max_wave_rows * rt->h_max * 2, "H alloc") &&
@@ -523,14 +526,14 @@ int coe_runtime_create(const coe_runtime_config *cfg, coe_runtime **out) {
   for (int k = 0; k < rt->S; ++k)
     good = good && dmalloc(&rt->slabs[k], (size_t)rt->sbytes[k] * std::max(1, rt->slot_count[k]), "slab alloc");
   for (auto &s : rt->sets)
-    good = good && dmalloc(&s.adm, 16 * A, "adm alloc") && dmalloc(&s.batch, 8 * B, "batch alloc") &&
+    good = good && dmalloc(&s.adm, 24 * A, "adm alloc") && dmalloc(&s.batch, 8 * B, "batch alloc") &&
            dmalloc(&s.boff, 4 * B, "boff alloc") && dmalloc(&s.mreq, 4 * A, "member alloc") &&
-           dmalloc(&s.mstage, 4 * A, "member alloc") && dmalloc(&s.groups, 2 * sizeof(coe_mlp_group) * B, "groups") &&
-           dmalloc(&s.fin, 4 * (size_t)c.max_requests + 16, "final list") &&
+           dmalloc(&s.mstage, 4 * A, "member alloc") && dmalloc(&s.min, 4 * A, "member alloc") &&
+           dmalloc(&s.mout, 4 * A, "member alloc") && dmalloc(&s.groups, 2 * sizeof(coe_mlp_group) * B, "groups") &&
            ok(cudaEventCreateWithFlags(&s.free_ev, cudaEventDisableTiming), "event");
   rt->compute = rt->cls_stream[0];
   if (good) {
-    rt->staging_bytes = 16 * A + 8 * B + 2 * sizeof(coe_mlp_group) * B + 4 * (size_t)c.max_requests + 512;
+    rt->staging_bytes = 24 * A + 8 * B + 2 * sizeof(coe_mlp_group) * B + 512;
     good = ok(cudaHostAlloc(reinterpret_cast<void **>(&rt->staging[0]), rt->staging_bytes, cudaHostAllocDefault), "staging") &&
            ok(cudaHostAlloc(reinterpret_cast<void **>(&rt->staging[1]), rt->staging_bytes, cudaHostAllocDefault), "staging") &&
            ok(cudaHostAlloc(reinterpret_cast<void **>(&rt->h_last), 4 * (size_t)c.max_requests, cudaHostAllocDefault), "last") &&
@@ -558,10 +561,11 @@ int coe_runtime_create(const coe_runtime_config *cfg, coe_runtime **out) {
       mc.d = rt->sd[sk];
       mc.h = rt->sh[sk];
       mc.T = c.T;
-      mc.x = rt->x;
-      mc.act0 = rt->p0;
-      mc.act1 = rt->p1;
-      mc.act_rows = (int64_t)c.max_requests * c.T;
+      mc.x = c.device_io ? rt->x : rt->act;  // e2e-only runtimes read stage-0 inputs from A
+      mc.act0 = rt->act;
+      mc.act1 = rt->act;
+      mc.act_rows = a_rows * c.T;
+      mc.x_rows = c.device_io ? (int64_t)c.max_requests * c.T : a_rows * c.T;
       mc.act_ld = rt->act_ld;
       mc.h_rows = c.max_wave_rows;
       mc.slab = rt->slabs[sk];
@@ -569,7 +573,9 @@ int coe_runtime_create(const coe_runtime_config *cfg, coe_runtime **out) {
       mc.slot_stride_bytes = rt->sbytes[sk];
       for (int k = 0; k < coe_runtime::NCLS && good; ++k) {
         mc.h_scratch = rt->hbuf[k];
-        if (coe_mlp_create(&mc, &rt->mlps[sk][k]) != COE_CUDA_OK) good = false;
+        if (coe_mlp_create(&mc, &rt->mlps[sk][k]) != COE_CUDA_OK ||
+            coe_mlp_set_outputs(rt->mlps[sk][k], rt->y, rt->outbuf) != COE_CUDA_OK)
+          good = false;
       }
     }
   }
@@ -591,6 +597,8 @@ int coe_runtime_create(const coe_runtime_config *cfg, coe_runtime **out) {
   rt->slot_expert.assign(rt->total_slots, -1);
   rt->expert_slot.assign(c.num_experts, -1);
   rt->slot_free_valid.assign((size_t)rt->total_slots * coe_runtime::NCLS, 0);
+  for (int32_t q = 0; q < rt->ring_slots; ++q) rt->ring_order.push_back(rt->landing_slots + q);
+  rt->act_prev_wave.assign((size_t)a_rows, -1);
   *out = rt;
   return COE_CUDA_OK;
 }
@@ -600,8 +608,8 @@ void coe_runtime_destroy(coe_runtime *rt) { delete rt; }
 void *coe_runtime_buffer(coe_runtime *rt, int which) {
   switch (which) {
     case 0: return rt->x;
-    case 1: return rt->p0;
-    case 2: return rt->p1;
+    case 1: return rt->act;
+    case 2: return rt->y;
     case 3: return rt->hbuf[0];
     case 4: return rt->slabs[0];
     case 5: return rt->host_store;
@@ -660,6 +668,10 @@ int coe_runtime_init_experts(coe_runtime *rt) {
 }
 
 int coe_runtime_fill_inputs(coe_runtime *rt, uint64_t seed, int32_t num_requests) {
+  if (!rt->x) {
+    coe_set_error("fill_inputs: runtime created without device_io (no X buffer)");
+    return COE_CUDA_ERR_CONFIG;
+  }
   if (num_requests > rt->cfg.max_requests) {
     coe_set_error("fill_inputs: more requests than the runtime was sized for");
     return COE_CUDA_ERR_CONFIG;
@@ -670,6 +682,10 @@ int coe_runtime_fill_inputs(coe_runtime *rt, uint64_t seed, int32_t num_requests
 }
 
 int coe_runtime_upload_inputs(coe_runtime *rt, const void *host, int32_t num_requests) {
+  if (!rt->x) {
+    coe_set_error("upload_inputs: runtime created without device_io (no X buffer)");
+    return COE_CUDA_ERR_CONFIG;
+  }
   if (num_requests > rt->cfg.max_requests) {
     coe_set_error("upload_inputs: more requests than the runtime was sized for");
     return COE_CUDA_ERR_CONFIG;
@@ -682,16 +698,13 @@ int coe_runtime_upload_inputs(coe_runtime *rt, const void *host, int32_t num_req
 }
 
 int coe_runtime_download_outputs(coe_runtime *rt, const int32_t *last_stage_host, int32_t num_requests, void *host) {
+  (void)last_stage_host;  // device-resident steps store every request's final rows in Y[request]
   if (num_requests <= 0) return COE_CUDA_OK;
-  if (!ok(cudaStreamSynchronize(rt->compute), "download sync")) return fail_cuda();  // h_last reuse
-  std::memcpy(rt->h_last, last_stage_host, 4 * (size_t)num_requests);
-  if (!ok(cudaMemcpyAsync(rt->d_last, rt->h_last, 4 * (size_t)num_requests, cudaMemcpyHostToDevice, rt->compute),
-          "last stage H2D"))
-    return fail_cuda();
-  gather_outputs<<<num_requests, 256, 0, rt->compute>>>(rt->p0, rt->p1, rt->d_last, num_requests, rt->row_elems,
-                                                        rt->outbuf);
-  if (!ok(cudaGetLastError(), "gather outputs")) return fail_cuda();
-  return ok(cudaMemcpyAsync(host, rt->outbuf, (size_t)num_requests * rt->row_elems * 2, cudaMemcpyDeviceToHost,
+  if (!rt->y || num_requests > rt->cfg.max_requests) {
+    coe_set_error("download_outputs: no device output buffer (device_io) or too many requests");
+    return COE_CUDA_ERR_CONFIG;
+  }
+  return ok(cudaMemcpyAsync(host, rt->y, (size_t)num_requests * rt->row_elems * 2, cudaMemcpyDeviceToHost,
                             rt->compute),
             "output D2H")
              ? COE_CUDA_OK
@@ -710,17 +723,28 @@ int coe_runtime_download_requests(coe_runtime *rt, const int32_t *requests, cons
       coe_set_error("download_requests: request or stage out of range");
       return COE_CUDA_ERR_CONFIG;
     }
-  if (!ok(cudaStreamSynchronize(rt->compute), "download sync")) return fail_cuda();  // h_last reuse
-  for (int32_t i = 0; i < n; ++i) rt->h_last[i] = (requests[i] << 1) | (stages[i] & 1);
-  if (!ok(cudaMemcpyAsync(rt->d_last, rt->h_last, 4 * (size_t)n, cudaMemcpyHostToDevice, rt->compute),
-          "rows H2D"))
-    return fail_cuda();
-  gather_rows<<<n, 256, 0, rt->compute>>>(rt->p0, rt->p1, rt->d_last, rt->row_elems, rt->outbuf);
-  if (!ok(cudaGetLastError(), "gather rows")) return fail_cuda();
-  return ok(cudaMemcpyAsync(host, rt->outbuf, (size_t)n * rt->row_elems * 2, cudaMemcpyDeviceToHost, rt->compute),
-            "rows D2H") && ok(cudaStreamSynchronize(rt->compute), "rows sync")
-             ? COE_CUDA_OK
-             : fail_cuda();
+  if (!rt->y) {
+    coe_set_error("download_requests: runtime created without device_io (no Y buffer)");
+    return COE_CUDA_ERR_CONFIG;
+  }
+  // final rows live in Y[request] (stages: the caller's view of the chain; kept for the ABI)
+  if (!ok(cudaStreamSynchronize(rt->out_stream), "download sync")) return fail_cuda();  // e2e staging use
+  const size_t rb = (size_t)rt->row_elems * 2;
+  for (int32_t i0 = 0; i0 < n; i0 += rt->out_slots) {  // staging holds out_slots rows at a time
+    const int32_t k = std::min(rt->out_slots, n - i0);
+    if (!ok(cudaStreamSynchronize(rt->compute), "download sync")) return fail_cuda();  // h_last / staging reuse
+    for (int32_t i = 0; i < k; ++i) rt->h_last[i] = requests[i0 + i] << 1;
+    if (!ok(cudaMemcpyAsync(rt->d_last, rt->h_last, 4 * (size_t)k, cudaMemcpyHostToDevice, rt->compute), "rows H2D"))
+      return fail_cuda();
+    gather_rows<<<k, 256, 0, rt->compute>>>(rt->y, rt->y, rt->d_last, rt->row_elems, rt->outbuf);
+    if (!ok(cudaGetLastError(), "gather rows") ||
+        !ok(cudaMemcpyAsync(static_cast<char *>(host) + (size_t)i0 * rb, rt->outbuf, (size_t)k * rb,
+                            cudaMemcpyDeviceToHost, rt->compute),
+            "rows D2H") ||
+        !ok(cudaStreamSynchronize(rt->compute), "rows sync"))
+      return fail_cuda();
+  }
+  return COE_CUDA_OK;
 }
 
 int coe_runtime_synchronize(coe_runtime *rt) {
@@ -803,29 +827,29 @@ int coe_runtime_attach_comm(coe_runtime *rt, coe_comm *comm) {
 }
 
 int coe_runtime_peer_buffers(coe_runtime *rt, coe_peer_buffers *out) {
-  out->p0 = rt->p0;
-  out->p1 = rt->p1;
+  out->p0 = rt->act;  // fused hops store into a peer's landing rows of A
+  out->p1 = rt->act;
   out->flags = rt->d_hflags;
   return COE_CUDA_OK;
 }
 
 int coe_runtime_ipc_export(coe_runtime *rt, void *handles) {
   auto *h = static_cast<cudaIpcMemHandle_t *>(handles);
-  bool good = ok(cudaIpcGetMemHandle(&h[0], rt->p0), "ipc export P0") &&
-              ok(cudaIpcGetMemHandle(&h[1], rt->p1), "ipc export P1") &&
+  bool good = ok(cudaIpcGetMemHandle(&h[0], rt->act), "ipc export A") &&
               ok(cudaIpcGetMemHandle(&h[2], rt->d_hflags), "ipc export flags");
+  if (good) h[1] = h[0];  // slot kept for the ABI (one activation buffer)
   return good ? COE_CUDA_OK : fail_cuda();
 }
 
 int coe_runtime_ipc_open(coe_runtime *rt, const void *handles, coe_peer_buffers *out) {
   const auto *h = static_cast<const cudaIpcMemHandle_t *>(handles);
   void *p[3] = {nullptr, nullptr, nullptr};
-  for (int i = 0; i < 3; ++i) {
+  for (int i : {0, 2}) {
     if (!ok(cudaIpcOpenMemHandle(&p[i], h[i], cudaIpcMemLazyEnablePeerAccess), "ipc open")) return fail_cuda();
     rt->ipc_opened.push_back(p[i]);
   }
   out->p0 = p[0];
-  out->p1 = p[1];
+  out->p1 = p[0];
   out->flags = p[2];
   return COE_CUDA_OK;
 }
@@ -839,13 +863,6 @@ int coe_runtime_attach_peers(coe_runtime *rt, int32_t rank, int32_t world, const
   if (!hub && !stream_memops()) {
     coe_set_error("attach_peers: cuStreamWaitValue32 / cuStreamWriteValue32 unavailable");
     return COE_CUDA_ERR_CUDA;
-  }
-  const size_t bytes = (size_t)rt->cfg.max_requests * HOP_STRIDE;
-  for (int k = 0; k < 2; ++k) {
-    if (!rt->d_hopdst[k] && !dmalloc(&rt->d_hopdst[k], bytes, "hop dst")) return fail_cuda();
-    if (!rt->h_hopdst[k] &&
-        !ok(cudaHostAlloc(reinterpret_cast<void **>(&rt->h_hopdst[k]), bytes, cudaHostAllocDefault), "hop dst"))
-      return fail_cuda();
   }
   rt->peers.assign(peers, peers + world);
   rt->peer_hub = hub;
@@ -876,7 +893,12 @@ int coe_runtime_bench_mlp(coe_runtime *rt, int32_t groups, int32_t requests_per_
     td += mt * (rt->sd[0] / BN);
     boff[g] = g * requests_per_group;
   }
-  for (int32_t r = 0; r < nreq; ++r) mreq[r] = r;
+  // routed rows: inputs from X (or A without device_io), outputs into Y (or A), one block per request
+  const int32_t a_rows = rt->landing_slots + rt->ring_slots;
+  for (int32_t r = 0; r < nreq; ++r) {
+    mreq[r] = rt->x ? ((r << 1) | 1) : ((r % a_rows) << 1);
+    mst[r] = rt->y ? ((r << 4) | coe::OUT_Y) : (((r % a_rows) << 4) | coe::OUT_RING);
+  }
   coe_mlp_group *d_g = nullptr;
   int32_t *d_i = nullptr;
   cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr;
@@ -892,11 +914,11 @@ int coe_runtime_bench_mlp(coe_runtime *rt, int32_t groups, int32_t requests_per_
   float tot_up = 0.f, tot_down = 0.f;
   for (int it = -2; good && it < iters; ++it) {  // two untimed warm-up launches
     good = ok(cudaEventRecord(e0, cs), "record") &&
-           coe_grouped_mlp(rt->mlps[0][0], d_g, d_g + groups, groups, tu, td, d_i, d_i + groups, d_i + groups + nreq, 1, 0,
-                           cs) == COE_CUDA_OK &&
+           coe_grouped_mlp_routed(rt->mlps[0][0], d_g, d_g + groups, groups, tu, td, d_i, d_i + groups,
+                                  d_i + groups + nreq, 1, 0, cs) == COE_CUDA_OK &&
            ok(cudaEventRecord(e1, cs), "record") &&
-           coe_grouped_mlp(rt->mlps[0][0], d_g, d_g + groups, groups, tu, td, d_i, d_i + groups, d_i + groups + nreq, 2, 0,
-                           cs) == COE_CUDA_OK &&
+           coe_grouped_mlp_routed(rt->mlps[0][0], d_g, d_g + groups, groups, tu, td, d_i, d_i + groups,
+                                  d_i + groups + nreq, 2, 0, cs) == COE_CUDA_OK &&
            ok(cudaEventRecord(e2, cs), "record") && ok(cudaEventSynchronize(e2), "sync");
     if (good && it >= 0) {
       tot_up += elapsed(e0, e1);
@@ -1019,6 +1041,42 @@ struct CopyInfo {
 
 }  // namespace
 
+extern "C" int coe_runtime_plan_rows(const coe_step_input *in, int32_t max_requests, int e2e, int nccl,
+                                     int32_t *ring_slots, int32_t *landing_slots) {
+  const coe_op *ops = static_cast<const coe_op *>(in->ops);
+  const coe_admission *adm = static_cast<const coe_admission *>(in->admissions);
+  const int32_t x = in->executor;
+  std::unordered_map<int64_t, int32_t> adm_index;
+  std::vector<int32_t> final_stage(max_requests, -1);
+  int64_t n_adm = 0;
+  for (int64_t i = 0; i < in->num_admissions; ++i) {
+    const coe_admission &a = adm[i];
+    if (a.request < 0 || a.request >= max_requests || a.stage < 0 || a.stage >= coe::ROW_STAGES) {
+      coe_set_error("plan_rows: request beyond max_requests or chain longer than 8 stages");
+      return COE_CUDA_ERR_CONFIG;
+    }
+    final_stage[a.request] = std::max(final_stage[a.request], a.stage);
+    if (a.executor == x) adm_index[(int64_t)a.request * coe::ROW_STAGES + a.stage] = (int32_t)n_adm++;
+  }
+  std::vector<int64_t> batch_ops;
+  for (int64_t i = 0; i < in->num_ops; ++i)
+    if (ops[i].executor == x && ops[i].kind == COE_OP_BATCH) batch_ops.push_back(i);
+  const std::vector<coe::Hop> all_hops = coe::hop_schedule(adm, in->num_admissions, max_requests);
+  std::vector<int32_t> my_hops;
+  for (size_t i = 0; i < all_hops.size(); ++i)
+    if (all_hops[i].src == x || all_hops[i].dst == x) my_hops.push_back((int32_t)i);
+  coe::RowPlan rows;
+  std::string err;
+  if (!coe::plan_rows(ops, in->op_args, batch_ops, adm_index, all_hops, my_hops, final_stage, x, e2e != 0, e2e != 0,
+                      nccl == 0, 0, -1, {}, max_requests, n_adm, rows, err)) {
+    coe_set_error(err);
+    return COE_CUDA_ERR_CONFIG;
+  }
+  *ring_slots = rows.peak_ring;
+  *landing_slots = rows.landing;
+  return COE_CUDA_OK;
+}
+
 extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_step_stats *stats) {
   const auto &c = rt->cfg;
   const coe_op *ops = static_cast<const coe_op *>(in->ops);
@@ -1029,9 +1087,15 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
 
   // ---- admissions of this executor (admission order) ----
   std::vector<int32_t> a_rank, a_req, a_stage;
+  std::unordered_map<int64_t, int32_t> adm_index;  // (request, stage) -> admission of this executor
   int32_t max_rank = 0;
   for (int64_t i = 0; i < in->num_admissions; ++i) {
     if (adm[i].executor != x) continue;
+    if (adm[i].stage < 0 || adm[i].stage >= coe::ROW_STAGES) {
+      coe_set_error("chains longer than 8 stages are not supported");
+      return COE_CUDA_ERR_CONFIG;
+    }
+    adm_index[(int64_t)adm[i].request * coe::ROW_STAGES + adm[i].stage] = (int32_t)a_rank.size();
     a_rank.push_back(adm[i].run_rank);
     a_req.push_back(adm[i].request);
     a_stage.push_back(adm[i].stage);
@@ -1115,12 +1179,14 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
   std::vector<BatchInfo> batches;
   std::vector<int32_t> req_last(c.max_requests, -1);  // latest batch of each request on this executor
   const bool e2e_in = in->host_inputs != nullptr, e2e_out = in->host_outputs != nullptr;
-  std::vector<int32_t> final_stage;
-  if (e2e_out) {
-    final_stage.assign(c.max_requests, -1);
-    for (int64_t i = 0; i < in->num_admissions; ++i)
-      final_stage[adm[i].request] = std::max(final_stage[adm[i].request], adm[i].stage);
+  if ((!e2e_in && !rt->x) || (!e2e_out && !rt->y)) {
+    coe_set_error("device-resident inputs / outputs need a runtime created with device_io");
+    return COE_CUDA_ERR_CONFIG;
   }
+  std::vector<int32_t> final_stage(c.max_requests, -1);
+  for (int64_t i = 0; i < in->num_admissions; ++i)
+    if (adm[i].request >= 0 && adm[i].request < c.max_requests)
+      final_stage[adm[i].request] = std::max(final_stage[adm[i].request], adm[i].stage);
   auto issue_copy = [&](int32_t e, bool restore, int64_t op_pos) -> bool {
     if (rt->store_off[e] < 0) {
       coe_set_error("swap-in of an expert that is not in the host store");
@@ -1221,6 +1287,23 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     coe_set_error("more batches than the runtime was sized for");
     return COE_CUDA_ERR_CONFIG;
   }
+  // ---- activation rows: ring slots / landing rows per member, slot-reuse order ----
+  coe::RowPlan rows;
+  {
+    std::vector<int64_t> batch_ops;
+    for (const BatchInfo &b : batches) batch_ops.push_back(b.op_index);
+    std::string err;
+    if (!coe::plan_rows(ops, in->op_args, batch_ops, adm_index, all_hops, my_hops, final_stage, x, e2e_in, e2e_out,
+                        peer_mode, rt->landing_slots, rt->ring_slots, rt->ring_order, c.max_requests, n_adm, rows,
+                        err)) {
+      coe_set_error(err);
+      return COE_CUDA_ERR_CONFIG;
+    }
+    for (size_t b = 0; b < batches.size(); ++b)  // write-after-read on a reused slot
+      for (int32_t p : rows.preds[b])
+        if (std::find(batches[b].producers.begin(), batches[b].producers.end(), p) == batches[b].producers.end())
+          batches[b].producers.push_back(p);
+  }
   // sends ordered by global index: a batch needing recv h may only be issued once every
   // send of this executor with a smaller index has its producer issued
   std::vector<int32_t> send_slots;
@@ -1252,18 +1335,50 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
       ++send_ptr;
     return send_ptr >= send_slots.size() || all_hops[my_hops[send_slots[send_ptr]]].index > hop_index;
   };
-  // e2e: stage-0 inputs move in request-ordered chunks of >= 32 MB (full-rate DMA); batch b
-  // needs chunks 0..b.input_event.  chunk_end < 0: not issued yet.
-  std::vector<int32_t> in_reqs;
-  for (const BatchInfo &b : batches) in_reqs.insert(in_reqs.end(), b.inputs.begin(), b.inputs.end());
-  std::sort(in_reqs.begin(), in_reqs.end());
+  // e2e: stage-0 inputs move in chunks of >= 32 MB (full-rate DMA) in the order batches need
+  // them, each request straight into its ring slot; batch b needs chunks 0..b.input_event.  A
+  // chunk waits for the batches that freed its slots (their up passes read the old rows), so a
+  // chunk never holds a request whose slot predecessor shares the chunk.  chunk_end < 0: not
+  // issued yet.
+  std::vector<int32_t> in_reqs, in_batch(e2e_in ? c.max_requests : 0, -1);
+  for (size_t bi = 0; bi < batches.size(); ++bi)
+    for (int32_t r : batches[bi].inputs) {
+      in_reqs.push_back(r);
+      in_batch[r] = (int32_t)bi;
+    }
+  std::vector<int32_t> host_row;  // host_inputs row of a request: rank among this executor's stage-0 requests
+  if (e2e_in) {
+    host_row.assign(c.max_requests, -1);
+    std::vector<int32_t> sorted(in_reqs);
+    std::sort(sorted.begin(), sorted.end());
+    for (size_t i = 0; i < sorted.size(); ++i) host_row[sorted[i]] = (int32_t)i;
+  }
   const int64_t in_chunk = std::max<int64_t>(1, (32ll << 20) / std::max<int64_t>(1, rt->row_elems * 2));
-  const int32_t n_chunks = (int32_t)((in_reqs.size() + in_chunk - 1) / in_chunk);
+  std::vector<int32_t> chunk_start;  // first in_reqs index of each chunk
+  {
+    int32_t first_b = -1;
+    for (size_t i = 0; i < in_reqs.size(); ++i) {
+      const int32_t r = in_reqs[i], p = rows.in_pred[r];
+      if (chunk_start.empty() || (int64_t)i - chunk_start.back() >= in_chunk || (p >= 0 && p >= first_b)) {
+        chunk_start.push_back((int32_t)i);
+        first_b = in_batch[r];
+      }
+    }
+  }
+  const int32_t n_chunks = (int32_t)chunk_start.size();
+  chunk_start.push_back((int32_t)in_reqs.size());
   std::vector<double> chunk_end(n_chunks, -1.0);
   std::vector<int64_t> chunk_pos(n_chunks, INT64_MAX);  // op position of the first batch needing it
+  std::vector<std::vector<int32_t>> chunk_preds(n_chunks);
   {
     std::unordered_map<int32_t, int32_t> chunk_of;
-    for (size_t i = 0; i < in_reqs.size(); ++i) chunk_of[in_reqs[i]] = (int32_t)(i / in_chunk);
+    for (int32_t k = 0; k < n_chunks; ++k)
+      for (int32_t i = chunk_start[k]; i < chunk_start[k + 1]; ++i) {
+        const int32_t r = in_reqs[i], p = rows.in_pred[r];
+        chunk_of[r] = k;
+        if (p >= 0 && std::find(chunk_preds[k].begin(), chunk_preds[k].end(), p) == chunk_preds[k].end())
+          chunk_preds[k].push_back(p);
+      }
     for (BatchInfo &b : batches) {
       b.input_event = -1;
       for (int32_t r : b.inputs) {
@@ -1274,6 +1389,11 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     }
     for (int32_t k = n_chunks - 2; k >= 0; --k) chunk_pos[k] = std::min(chunk_pos[k], chunk_pos[k + 1]);
   }
+  auto chunk_ready = [&](int32_t k) {
+    for (int32_t p : chunk_preds[k])
+      if (!issued[p]) return false;
+    return true;
+  };
   auto issuable = [&](const BatchInfo &b) {
     if (b.input_event >= 0 && chunk_end[b.input_event] < 0) return false;  // inputs not uploaded yet
     for (int32_t p : b.producers)
@@ -1386,9 +1506,11 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     }
     // candidate: the next input upload (always startable; op order against the swap-in)
     bool take_input = false;
-    if (next_in < n_chunks) {
-      take_input = c_start == INF || t_copy < c_start || chunk_pos[next_in] < copies[copy_pick].op_pos;
-      if (take_input) c_start = t_copy;
+    if (next_in < n_chunks && chunk_ready(next_in)) {
+      double t_in = t_copy;
+      for (int32_t p : chunk_preds[next_in]) t_in = std::max(t_in, batches[p].done);
+      take_input = c_start == INF || t_in < c_start || chunk_pos[next_in] < copies[copy_pick].op_pos;
+      if (take_input) c_start = t_in;
     }
     // candidate: next release wave (singleton, in order)
     double r_start = INF;
@@ -1406,7 +1528,7 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
       return COE_CUDA_ERR_CHECK;
     }
     if (take_input && c_start <= r_start && c_start <= m_start) {
-      const int64_t nreq_k = std::min<int64_t>(in_chunk, (int64_t)in_reqs.size() - (int64_t)next_in * in_chunk);
+      const int64_t nreq_k = chunk_start[next_in + 1] - chunk_start[next_in];
       chunk_end[next_in] = c_start + (double)nreq_k * row_bytes / 55.0e9;
       t_copy = chunk_end[next_in];
       actions.push_back(Action{false, next_in, true});
@@ -1549,7 +1671,9 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
 
   // ---- phase C: issue ----
   const size_t nw = waves.size(), nc = copies.size();
-  if (!rt->ensure_events(rt->wave_up_ev, nw, false) || !rt->ensure_events(rt->wave_down_ev, nw, false) ||
+  const int par = rt->step_parity;  // this step's wave events; par ^ 1 holds the previous step's
+  std::vector<cudaEvent_t> &wave_up_ev = rt->wave_up_evs[par], &wave_down_ev = rt->wave_down_evs[par];
+  if (!rt->ensure_events(wave_up_ev, nw, false) || !rt->ensure_events(wave_down_ev, nw, false) ||
       !rt->ensure_events(rt->copy_up_ev, nc, false) || !rt->ensure_events(rt->copy_down_ev, nc, false) ||
       !rt->ensure_events(rt->recv_ev, my_hops.size(), false))
     return fail_cuda();
@@ -1564,28 +1688,46 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
   if (!ok(cudaEventSynchronize(rt->staging_done[set_idx]), "staging reuse")) return fail_cuda();
   char *stg = rt->staging[set_idx];
   uint32_t seq = 0;
-  if (peer_mode) {  // fused hops: where each of this executor's hopping rows goes
+  if (peer_mode) {  // fused hops: K3's down pass stores hopping rows into the peers' landing rows
     seq = ++rt->step_seq;
-    int8_t *hd = rt->h_hopdst[set_idx];
-    std::memset(hd, 0xFF, (size_t)c.max_requests * HOP_STRIDE);
-    for (int32_t hs : my_hops) {
-      const coe::Hop &h = all_hops[hs];
-      if (h.src != x) continue;
-      if (h.stage >= HOP_STRIDE || h.dst >= rt->peer_world) {
-        coe_set_error("peer hops: chain longer than 8 stages or destination outside the peer group");
-        return COE_CUDA_ERR_CONFIG;
-      }
-      hd[(size_t)h.request * HOP_STRIDE + h.stage] = (int8_t)h.dst;
-    }
     std::vector<void *> pa(2 * rt->peer_world);
     for (int r = 0; r < rt->peer_world; ++r) {
       pa[2 * r] = rt->peers[r].p0;
-      pa[2 * r + 1] = rt->peers[r].p1;
+      pa[2 * r + 1] = rt->peers[r].p0;
     }
     for (auto &per : rt->mlps)
       for (coe_mlp *m : per)
-        if (m && coe_mlp_set_hops(m, rt->d_hopdst[set_idx], HOP_STRIDE, pa.data(), rt->peer_world))
-          return COE_CUDA_ERR_CONFIG;
+        if (m && coe_mlp_set_hops(m, nullptr, 0, pa.data(), rt->peer_world)) return COE_CUDA_ERR_CONFIG;
+  }
+
+  // e2e: final rows leave in completion order -- per wave, its finals by request id, each
+  // stored by the down pass straight into the output staging ring at its global position
+  std::vector<int32_t> fin_begin(nw, 0), fin_end(nw, 0);  // per wave: slice of the output order
+  const int64_t out_base = rt->out_pos;
+  if (e2e_out) {
+    rt->out_order.clear();
+    for (size_t a = 0; a < actions.size(); ++a) {
+      if (actions[a].is_copy || actions[a].is_input) continue;
+      const WaveAct &w = waves[actions[a].index];
+      std::vector<int32_t> fin;
+      for (int32_t gi = w.first_group; gi < w.first_group + w.num_groups; ++gi)
+        for (int32_t r : batches[g_up[gi].batch].finals) fin.push_back(r);
+      std::sort(fin.begin(), fin.end());
+      if ((int64_t)fin.size() > rt->out_slots) {
+        coe_set_error("output staging ring smaller than one wave's final rows");
+        return COE_CUDA_ERR_CONFIG;
+      }
+      fin_begin[actions[a].index] = (int32_t)rt->out_order.size();
+      for (int32_t r : fin) {
+        const int64_t pos = out_base + (int64_t)rt->out_order.size();
+        const int32_t ai = adm_index[(int64_t)r * coe::ROW_STAGES + final_stage[r]];
+        rows.out_code[ai] = (int32_t)((pos % rt->out_slots) << 4) | coe::OUT_STAGE;
+        rt->out_order.push_back(r);
+      }
+      fin_end[actions[a].index] = (int32_t)rt->out_order.size();
+    }
+    rt->out_pos += (int64_t)rt->out_order.size();
+    if (!rt->ensure_events(rt->out_ev, nw, false)) return fail_cuda();
   }
   int32_t *s_adm = reinterpret_cast<int32_t *>(stg);
   for (int64_t i = 0; i < n_adm; ++i) {
@@ -1593,8 +1735,10 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     s_adm[n_adm + i] = a_rank[i];
     s_adm[2 * n_adm + i] = a_req[i];
     s_adm[3 * n_adm + i] = a_stage[i];
+    s_adm[4 * n_adm + i] = rows.in_code[i];
+    s_adm[5 * n_adm + i] = rows.out_code[i];
   }
-  int32_t *s_batch = s_adm + 4 * n_adm;
+  int32_t *s_batch = s_adm + 6 * n_adm;
   for (int64_t b = 0; b < n_batches; ++b) {
     s_batch[b] = 0;
     s_batch[n_batches + b] = batches[b].count;
@@ -1606,33 +1750,10 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     std::memcpy(s_groups + n_batches, g_down.data(), sizeof(coe_mlp_group) * n_batches);
   }
 
-  // e2e: final rows leave in completion order -- per wave, its finals by request id
-  std::vector<int32_t> fin_begin(nw, 0), fin_end(nw, 0);  // per wave: slice of the output order
-  int32_t *s_fin = reinterpret_cast<int32_t *>((reinterpret_cast<uintptr_t>(s_groups + 2 * n_batches) + 31) &
-                                               ~uintptr_t(31));
-  if (e2e_out) {
-    rt->out_order.clear();
-    for (size_t a = 0; a < actions.size(); ++a) {
-      if (actions[a].is_copy || actions[a].is_input) continue;
-      const WaveAct &w = waves[actions[a].index];
-      std::vector<int32_t> fin;
-      for (int32_t gi = w.first_group; gi < w.first_group + w.num_groups; ++gi)
-        for (int32_t r : batches[g_up[gi].batch].finals) fin.push_back(r);
-      std::sort(fin.begin(), fin.end());
-      fin_begin[actions[a].index] = (int32_t)rt->out_order.size();
-      for (int32_t r : fin) {
-        s_fin[rt->out_order.size()] = (r << 1) | (final_stage[r] & 1);
-        rt->out_order.push_back(r);
-      }
-      fin_end[actions[a].index] = (int32_t)rt->out_order.size();
-    }
-    if (!rt->ensure_events(rt->out_ev, nw, false)) return fail_cuda();
-  }
-
   cudaStream_t cs = rt->compute, ks = rt->copy;
   if (c.profile && !ok(cudaEventRecord(rt->t_step_start, cs), "record")) return fail_cuda();
   if (sb.used && !ok(cudaStreamWaitEvent(ks, sb.free_ev, 0), "set reuse")) return fail_cuda();
-  if (n_adm && !ok(cudaMemcpyAsync(sb.adm, s_adm, 16 * (size_t)n_adm, cudaMemcpyHostToDevice, ks), "adm H2D"))
+  if (n_adm && !ok(cudaMemcpyAsync(sb.adm, s_adm, 24 * (size_t)n_adm, cudaMemcpyHostToDevice, ks), "adm H2D"))
     return fail_cuda();
   if (n_batches &&
       (!ok(cudaMemcpyAsync(sb.batch, s_batch, 8 * (size_t)n_batches, cudaMemcpyHostToDevice, ks), "batch H2D") ||
@@ -1640,15 +1761,8 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
                            cudaMemcpyHostToDevice, ks),
            "group H2D")))
     return fail_cuda();
-  if (e2e_out && !rt->out_order.empty() &&
-      !ok(cudaMemcpyAsync(sb.fin, s_fin, 4 * rt->out_order.size(), cudaMemcpyHostToDevice, ks), "final list H2D"))
-    return fail_cuda();
-  if (peer_mode && !ok(cudaMemcpyAsync(rt->d_hopdst[set_idx], rt->h_hopdst[set_idx],
-                                       (size_t)c.max_requests * HOP_STRIDE, cudaMemcpyHostToDevice, ks),
-                       "hop dst H2D"))
-    return fail_cuda();
-  // step fence: every peer has finished the previous step (its P rows are free).  Same-process
-  // peers (hub) are stepped and synchronised together (runtime.step_executors): no fence.
+  // step fence: every peer has finished the previous step (its landing rows are free).
+  // Same-process peers (hub) are stepped and synchronised together (runtime.step_executors).
   if (peer_mode && !rt->peer_hub)
     for (int r = 0; r < rt->peer_world; ++r)
       if (r != x && !wait_flag(cs, rt->d_hflags + rt->hflag_step_base + r, seq - 1)) return COE_CUDA_ERR_CUDA;
@@ -1661,9 +1775,10 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     if (rc) return rc;
   }
   {
-    int rc = coe_run_compact(rt->d_perm, rt->d_keys, d_req, d_stage, n_adm, rank_bits, sb.batch, sb.batch + n_batches,
-                             (int)n_batches, 1, sb.boff, sb.mreq, sb.mstage, rt->d_flags, rt->d_flags + 1,
-                             rt->d_compact_scratch, cs);
+    int rc = coe_run_compact_routes(rt->d_perm, rt->d_keys, d_req, d_stage, sb.adm + 4 * n_adm, sb.adm + 5 * n_adm,
+                                    n_adm, rank_bits, sb.batch, sb.batch + n_batches, (int)n_batches, 1, sb.boff,
+                                    sb.mreq, sb.mstage, sb.min, sb.mout, rt->d_flags, rt->d_flags + 1,
+                                    rt->d_compact_scratch, cs);
     if (rc) return rc;
   }
   if (c.profile && !ok(cudaEventRecord(rt->t_group_end, cs), "record")) return fail_cuda();
@@ -1673,26 +1788,9 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
 
   if (!my_hops.empty() && rt->have_step_end && !ok(cudaStreamWaitEvent(rt->hop, rt->step_end, 0), "hop waits step"))
     return fail_cuda();
-  // e2e: inputs double-buffered across steps; this step's first output gather on each stream
-  // waits for last step's downloads (the gathers reuse the staging buffer they read)
-  bool out_waited[NCLS] = {false, false, false};
-  const int xp = (int)(rt->e2e_steps & 1);
-  __nv_bfloat16 *x_step = rt->x;
-  if (e2e_in) {
-    if (!rt->x_alt) {  // at the first e2e step (cudaMalloc synchronises: keep it out of later steps)
-      if (!ok(cudaMalloc(&rt->x_alt, (size_t)c.max_requests * rt->row_elems * 2), "X alt alloc")) return fail_cuda();
-    }
-    if (!rt->x_free[0] && (!ok(cudaEventCreateWithFlags(&rt->x_free[0], cudaEventDisableTiming), "event") ||
-                           !ok(cudaEventCreateWithFlags(&rt->x_free[1], cudaEventDisableTiming), "event")))
-      return fail_cuda();
-    x_step = xp ? rt->x_alt : rt->x;
-  }
-  for (auto &per : rt->mlps)
-    for (coe_mlp *m : per)
-      if (m && coe_mlp_set_input(m, x_step)) return COE_CUDA_ERR_CUDA;
-  bool x_reuse_waited = false;
   if (e2e_in && !rt->ensure_events(rt->in_ev, (size_t)n_chunks, false)) return fail_cuda();
-  // stage-0 rows of batch b, pinned host -> X, coalescing consecutive request rows
+  bool in_prev_waited = false;
+  // stage-0 rows of a chunk, pinned host -> their ring slots, coalescing consecutive rows
   int32_t io_n = 0;  // profile events recorded this step
   rt->io_kind.clear();
   auto io_mark = [&](cudaStream_t s_) -> bool {
@@ -1700,26 +1798,36 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     if (!rt->ensure_events(rt->t_io, (size_t)io_n + 1, true)) return false;
     return ok(cudaEventRecord(rt->t_io[io_n++], s_), "record");
   };
+  const size_t rb = (size_t)rt->row_elems * 2;
   auto upload_inputs = [&](int32_t k) -> bool {
-    if (!x_reuse_waited) {  // X[xp] is free once the step before last (its last reader) ended
-      x_reuse_waited = true;
-      if (rt->x_free_valid[xp] && !ok(cudaStreamWaitEvent(ks, rt->x_free[xp], 0), "X reuse waits step"))
-        return false;
+    if (!in_prev_waited && rt->prev_nccl_hold && rt->have_step_end) {  // slots held for NCCL sends
+      in_prev_waited = true;
+      if (!ok(cudaStreamWaitEvent(ks, rt->step_end, 0), "inputs wait last step")) return false;
     }
+    // write-after-read: the batches that last read these slots (this step, or the previous one)
+    std::vector<cudaEvent_t> waits;
+    for (int32_t i = chunk_start[k]; i < chunk_start[k + 1]; ++i) {
+      const int32_t r = in_reqs[i], p = rows.in_pred[r], q = rows.in_slot[r];
+      cudaEvent_t ev = nullptr;
+      if (p >= 0) ev = wave_up_ev[batches[p].wave];
+      else if (rt->act_prev_wave[q] >= 0) ev = rt->wave_up_evs[par ^ 1][rt->act_prev_wave[q]];
+      if (ev && std::find(waits.begin(), waits.end(), ev) == waits.end()) waits.push_back(ev);
+    }
+    for (cudaEvent_t ev : waits)
+      if (!ok(cudaStreamWaitEvent(ks, ev, 0), "inputs wait slot readers")) return false;
     if (c.profile) rt->io_kind.push_back(0);
     if (!io_mark(ks)) return false;
-    const size_t rb = (size_t)rt->row_elems * 2;
     const char *hin = static_cast<const char *>(in->host_inputs);
-    const size_t lo = (size_t)k * in_chunk, hi = std::min(in_reqs.size(), lo + (size_t)in_chunk);
-    std::vector<int32_t> rq(in_reqs.begin() + lo, in_reqs.begin() + hi);
     std::vector<void *> dsts, srcs;
     std::vector<size_t> sizes;
-    for (size_t i = 0; i < rq.size();) {  // host row lo + i holds request rq[i] (this executor's order)
-      size_t j = i + 1;
-      while (j < rq.size() && rq[j] == rq[j - 1] + 1) ++j;
-      dsts.push_back(reinterpret_cast<char *>(x_step) + rq[i] * rb);
-      srcs.push_back(const_cast<char *>(hin) + (lo + i) * rb);
-      sizes.push_back((j - i) * rb);
+    for (int32_t i = chunk_start[k]; i < chunk_start[k + 1];) {
+      int32_t j = i + 1;
+      while (j < chunk_start[k + 1] && rows.in_slot[in_reqs[j]] == rows.in_slot[in_reqs[j - 1]] + 1 &&
+             host_row[in_reqs[j]] == host_row[in_reqs[j - 1]] + 1)
+        ++j;
+      dsts.push_back(reinterpret_cast<char *>(rt->act) + (size_t)rows.in_slot[in_reqs[i]] * rb);
+      srcs.push_back(const_cast<char *>(hin) + (size_t)host_row[in_reqs[i]] * rb);
+      sizes.push_back((size_t)(j - i) * rb);
       st.h2d_input_bytes += (int64_t)((j - i) * rb);
       i = j;
     }
@@ -1731,14 +1839,14 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
   auto issue_hops_until = [&](int64_t limit) -> bool {
     while (hop_cursor < my_hops.size() && all_hops[my_hops[hop_cursor]].index <= limit) {
       const coe::Hop &h = all_hops[my_hops[hop_cursor]];
-      __nv_bfloat16 *row = ((h.stage & 1) ? rt->p1 : rt->p0) + (size_t)h.request * row_elems;
+      __nv_bfloat16 *row = rt->act + (size_t)rows.hop_row[hop_cursor] * row_elems;
       if (h.src == x) {
         const int32_t pb = hop_batch[hop_cursor];
         if (pb < 0 || !issued[pb] || batches[pb].wave < 0) {
           coe_set_error("internal: hop send issued before its producer wave");
           return false;
         }
-        if (!ok(cudaStreamWaitEvent(rt->hop, rt->wave_down_ev[batches[pb].wave], 0), "send waits producer") ||
+        if (!ok(cudaStreamWaitEvent(rt->hop, wave_down_ev[batches[pb].wave], 0), "send waits producer") ||
             !coe_comm_send_bf16(rt->comm, row, row_elems, h.dst, rt->hop))
           return false;
       } else {
@@ -1747,6 +1855,18 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
           return false;
       }
       ++hop_cursor;
+    }
+    return true;
+  };
+  // output staging ring: before a wave's down pass stores rows [p0, p1) (global positions), the
+  // downloads of the rows' previous occupants [p0 - R, p1 - R) must have finished
+  auto out_wait = [&](cudaStream_t ws, int64_t p0, int64_t p1) -> bool {
+    const int64_t R = rt->out_slots;
+    for (const auto &u : rt->out_hist)
+      if (u.end > p0 - R && u.begin < p1 - R && !ok(cudaStreamWaitEvent(ws, u.ev, 0), "staging reuse")) return false;
+    while (!rt->out_hist.empty() && rt->out_hist.front().end <= p1 - R) {
+      rt->out_ev_pool.push_back(rt->out_hist.front().ev);
+      rt->out_hist.pop_front();
     }
     return true;
   };
@@ -1765,7 +1885,7 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
       const char *src = rt->host_store + rt->store_off[cp.expert];
       const int64_t half_bytes = rt->sbytes[rt->slot_shape[cp.slot]] / 2;
       for (int32_t wv : cp.wait_waves)
-        if (!ok(cudaStreamWaitEvent(ks, rt->wave_up_ev[wv], 0), "copy waits W1 readers")) return fail_cuda();
+        if (!ok(cudaStreamWaitEvent(ks, wave_up_ev[wv], 0), "copy waits W1 readers")) return fail_cuda();
       for (int k = 0; k < NCLS; ++k)
         if (cp.wait_prev[k] &&
             !ok(cudaStreamWaitEvent(ks, rt->slot_free_up[(size_t)cp.slot * NCLS + k], 0), "copy waits last step"))
@@ -1775,7 +1895,7 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
           !ok(cudaEventRecord(rt->copy_up_ev[a.index], ks), "record"))
         return fail_cuda();
       for (int32_t wv : cp.wait_waves)
-        if (!ok(cudaStreamWaitEvent(ks, rt->wave_down_ev[wv], 0), "copy waits W2 readers")) return fail_cuda();
+        if (!ok(cudaStreamWaitEvent(ks, wave_down_ev[wv], 0), "copy waits W2 readers")) return fail_cuda();
       for (int k = 0; k < NCLS; ++k)
         if (cp.wait_prev[k] &&
             !ok(cudaStreamWaitEvent(ks, rt->slot_free_down[(size_t)cp.slot * NCLS + k], 0), "copy waits last step"))
@@ -1804,7 +1924,7 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
         if (!ok(cudaStreamWaitEvent(ws, rt->recv_ev[hslot], 0), "wave waits hop")) return fail_cuda();
     }
     for (int32_t wid : w.wait_waves)
-      if (!ok(cudaStreamWaitEvent(ws, rt->wave_down_ev[wid], 0), "wave waits producer")) return fail_cuda();
+      if (!ok(cudaStreamWaitEvent(ws, wave_down_ev[wid], 0), "wave waits producer")) return fail_cuda();
     for (int32_t cid : w.wait_copies)
       if (!ok(cudaStreamWaitEvent(ws, rt->copy_up_ev[cid], 0), "wave waits W1")) return fail_cuda();
     for (int32_t gi = w.first_group; gi < w.first_group + w.num_groups; ++gi) {
@@ -1814,21 +1934,23 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     if (c.profile && !ok(cudaEventRecord(rt->t_wave_start[a.index], ws), "record")) return fail_cuda();
     // release waves gate the copy engine: they start on the reserved SMs at once
     const int ctas = w.cls == 1 ? rt->rel_launch_ctas : rt->m_ctas;
-    int rc = coe_grouped_mlp(m, dg_up + w.first_group, dg_down + w.first_group, w.num_groups, w.tiles_up, w.tiles_down,
-                             sb.boff, sb.mreq, sb.mstage, 1, ctas, ws);
+    int rc = coe_grouped_mlp_routed(m, dg_up + w.first_group, dg_down + w.first_group, w.num_groups, w.tiles_up,
+                                    w.tiles_down, sb.boff, sb.min, sb.mout, 1, ctas, ws);
     if (rc) return rc;
-    if (!ok(cudaEventRecord(rt->wave_up_ev[a.index], ws), "record")) return fail_cuda();
+    if (!ok(cudaEventRecord(wave_up_ev[a.index], ws), "record")) return fail_cuda();
     if (c.profile && !ok(cudaEventRecord(rt->t_up_end[a.index], ws), "record")) return fail_cuda();
     for (int32_t sk : w.frees_slots)
       if (!ok(cudaEventRecord(rt->slot_free_up[sk], ws), "record")) return fail_cuda();
     for (int32_t cid : w.wait_copies)
       if (!ok(cudaStreamWaitEvent(ws, rt->copy_down_ev[cid], 0), "wave waits W2")) return fail_cuda();
+    const int32_t b0 = fin_begin[a.index], b1 = fin_end[a.index];
+    if (e2e_out && b1 > b0 && !out_wait(ws, out_base + b0, out_base + b1)) return fail_cuda();
     if (c.profile && !ok(cudaEventRecord(rt->t_down_start[a.index], ws), "record")) return fail_cuda();
-    rc = coe_grouped_mlp(m, dg_up + w.first_group, dg_down + w.first_group, w.num_groups, w.tiles_up, w.tiles_down,
-                         sb.boff, sb.mreq, sb.mstage, 2, ctas, ws);
+    rc = coe_grouped_mlp_routed(m, dg_up + w.first_group, dg_down + w.first_group, w.num_groups, w.tiles_up,
+                                w.tiles_down, sb.boff, sb.min, sb.mout, 2, ctas, ws);
     if (rc) return rc;
     st.launches += 2;
-    if (!ok(cudaEventRecord(rt->wave_down_ev[a.index], ws), "record")) return fail_cuda();
+    if (!ok(cudaEventRecord(wave_down_ev[a.index], ws), "record")) return fail_cuda();
     if (peer_mode)  // publish the hops this wave's down pass just stored into the peers
       for (int32_t gi = w.first_group; gi < w.first_group + w.num_groups; ++gi)
         for (int32_t hslot : batches[g_up[gi].batch].sends) {
@@ -1843,35 +1965,38 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     }
     for (int32_t gi = w.first_group; gi < w.first_group + w.num_groups; ++gi) issued[g_up[gi].batch] = 1;
     if (c.profile && !ok(cudaEventRecord(rt->t_wave_end[a.index], ws), "record")) return fail_cuda();
-    if (e2e_out) {  // final outputs of this wave: gathered on its stream, one D2H copy
-      const int32_t b0 = fin_begin[a.index], b1 = fin_end[a.index];
-      if (b1 > b0) {
-        const int64_t re = rt->row_elems;
-        if (rt->have_out && !out_waited[w.cls]) {
-          out_waited[w.cls] = true;
-          if (!ok(cudaStreamWaitEvent(ws, rt->out_drained, 0), "gather waits last downloads")) return fail_cuda();
-        }
-        gather_rows<<<b1 - b0, 256, 0, ws>>>(rt->p0, rt->p1, sb.fin + b0, re, rt->outbuf + (int64_t)b0 * re);
-        st.launches += 1;
-        if (!ok(cudaGetLastError(), "gather rows") || !ok(cudaEventRecord(rt->out_ev[a.index], ws), "record") ||
-            !ok(cudaStreamWaitEvent(rt->out_stream, rt->out_ev[a.index], 0), "download waits gather"))
+    if (e2e_out && b1 > b0) {  // this wave's final rows are in the staging ring: download them
+      if (!ok(cudaEventRecord(rt->out_ev[a.index], ws), "record") ||
+          !ok(cudaStreamWaitEvent(rt->out_stream, rt->out_ev[a.index], 0), "download waits wave"))
+        return fail_cuda();
+      char *hout = static_cast<char *>(in->host_outputs);
+      const int64_t R = rt->out_slots;
+      if (c.profile) rt->io_kind.push_back(1);
+      if (!io_mark(rt->out_stream)) return fail_cuda();
+      for (int64_t p = out_base + b0; p < out_base + b1;) {  // at most two pieces (ring wrap)
+        const int64_t q = p % R, n = std::min<int64_t>(out_base + b1 - p, R - q);
+        if (!ok(cudaMemcpyAsync(hout + (size_t)(p - out_base) * rb, reinterpret_cast<char *>(rt->outbuf) + (size_t)q * rb,
+                                (size_t)n * rb, cudaMemcpyDeviceToHost, rt->out_stream),
+                "output D2H"))
           return fail_cuda();
-        const size_t rb = (size_t)re * 2;
-        char *hout = static_cast<char *>(in->host_outputs);
-        if (c.profile) rt->io_kind.push_back(1);
-        if (!io_mark(rt->out_stream) ||
-            !ok(cudaMemcpyAsync(hout + (size_t)b0 * rb, reinterpret_cast<char *>(rt->outbuf) + (size_t)b0 * rb,
-                                (size_t)(b1 - b0) * rb, cudaMemcpyDeviceToHost, rt->out_stream),
-                "output D2H") ||
-            !io_mark(rt->out_stream))
-          return fail_cuda();
-        st.d2h_output_bytes += (int64_t)(b1 - b0) * (int64_t)rb;
+        p += n;
       }
+      if (!io_mark(rt->out_stream)) return fail_cuda();
+      cudaEvent_t done = nullptr;
+      if (!rt->out_ev_pool.empty()) {
+        done = rt->out_ev_pool.back();
+        rt->out_ev_pool.pop_back();
+      } else if (!ok(cudaEventCreateWithFlags(&done, cudaEventDisableTiming), "event")) {
+        return fail_cuda();
+      }
+      if (!ok(cudaEventRecord(done, rt->out_stream), "record")) return fail_cuda();
+      rt->out_hist.push_back(coe_runtime::OutUse{out_base + b0, out_base + b1, done});
+      st.d2h_output_bytes += (int64_t)(b1 - b0) * (int64_t)rb;
     }
   }
   if (e2e_out) {
     // not joined into the compute stream: the next step's waves need not wait for this step's
-    // downloads (only its gathers do); coe_runtime_join / synchronize cover them
+    // downloads (only the staging rows they overwrite do); coe_runtime_join / synchronize cover them
     if (!ok(cudaEventRecord(rt->out_drained, rt->out_stream), "record")) return fail_cuda();
     rt->have_out = true;
   }
@@ -1898,11 +2023,16 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
   if (!ok(cudaEventRecord(sb.free_ev, cs), "record") || !ok(cudaEventRecord(rt->step_end, cs), "record"))
     return fail_cuda();
   rt->have_step_end = true;
-  if (e2e_in) {  // X[xp] is read by nothing after this step's end
-    if (!ok(cudaEventRecord(rt->x_free[xp], cs), "record")) return fail_cuda();
-    rt->x_free_valid[xp] = true;
-    rt->e2e_steps += 1;
-  }
+  // the ring carries over: the free list in release order, and for the next step's input
+  // uploads the wave (this parity) whose up pass last read each slot freed in this step
+  std::fill(rt->act_prev_wave.begin(), rt->act_prev_wave.end(), -1);
+  for (size_t i = 0; i < rows.freed_slot.size(); ++i)
+    rt->act_prev_wave[rows.freed_slot[i]] = batches[rows.freed_by[i]].wave;
+  rt->ring_order = rows.free_after;
+  rt->prev_nccl_hold = rows.nccl_hold;
+  rt->step_parity ^= 1;
+  st.ring_peak = rows.peak_ring;
+  st.landing_rows = rows.landing;
   sb.used = true;
   rt->last_waves = (int32_t)nw;
   rt->last_wave_cls.clear();

@@ -43,7 +43,8 @@ class StepStats(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int64) for n in ("admissions", "batches", "waves", "launches", "h2d_input_bytes",
                                                "d2h_output_bytes", "loads", "load_bytes",
                                                "restores", "restore_bytes", "max_wave_rows")] + \
-               [("max_wave_groups", ctypes.c_int32), ("rank_bits", ctypes.c_int32)]
+               [("max_wave_groups", ctypes.c_int32), ("rank_bits", ctypes.c_int32), ("ring_peak", ctypes.c_int32),
+                ("landing_rows", ctypes.c_int32)]
 
     def as_dict(self) -> dict:
         return {name: getattr(self, name) for name, _ in self._fields_}
@@ -73,7 +74,9 @@ class RuntimeConfig(ctypes.Structure):
                 ("reserve_sms", ctypes.c_int32), ("swapped_stream", ctypes.c_int32), ("store_path", ctypes.c_char_p),
                 ("wave_rows_cap", ctypes.c_int64), ("urgent_rows_cap", ctypes.c_int64),
                 ("num_shapes", ctypes.c_int32), ("shape_d", ctypes.c_void_p), ("shape_h", ctypes.c_void_p),
-                ("shape_slots", ctypes.c_void_p), ("expert_shape", ctypes.c_void_p), ("store_mask", ctypes.c_void_p)]
+                ("shape_slots", ctypes.c_void_p), ("expert_shape", ctypes.c_void_p), ("store_mask", ctypes.c_void_p),
+                ("ring_slots", ctypes.c_int32), ("landing_slots", ctypes.c_int32), ("out_slots", ctypes.c_int32),
+                ("device_io", ctypes.c_int32)]
 
 
 _declared = False
@@ -144,6 +147,8 @@ def _lib():
         lib.coe_runtime_ipc_open.restype = ctypes.c_int
         lib.coe_runtime_attach_peers.argtypes = [V, I32, I32, V, V]
         lib.coe_runtime_attach_peers.restype = ctypes.c_int
+        lib.coe_runtime_plan_rows.argtypes = [P(StepInput), I32, ctypes.c_int, ctypes.c_int, P(I32), P(I32)]
+        lib.coe_runtime_plan_rows.restype = ctypes.c_int
         lib.coe_expert_seed.argtypes = [ctypes.c_uint64, I32, I32]
         lib.coe_expert_seed.restype = ctypes.c_uint64
         for name in ("coe_runtime_create", "coe_runtime_init_experts", "coe_runtime_fill_inputs",
@@ -188,9 +193,13 @@ class B200Runtime:
                  max_admissions: int, max_wave_rows: int | None = None, weight_seed: int = DEFAULT_WEIGHT_SEED,
                  profile: bool = False, init_experts: bool = True, reserve_sms: int = 0,
                  store_path: str | None = None, wave_rows_cap: int | None = None,
-                 urgent_rows_cap: int | None = 8192, expert_shape=None, store_mask=None):
+                 urgent_rows_cap: int | None = 8192, expert_shape=None, store_mask=None,
+                 ring_slots: int | None = None, landing_slots: int = 0, out_slots: int = 0,
+                 device_io: bool = True):
         """``shape``: one ``RuntimeShape`` or a list (heterogeneous experts, ``expert_shape``
-        maps each expert to its index); ``num_slots``: HBM slots (per shape for a list)."""
+        maps each expert to its index); ``num_slots``: HBM slots (per shape for a list).
+        ``ring_slots`` / ``landing_slots``: activation rows (``plan_rows``; default: one ring
+        slot per request); ``device_io``: allocate the device-resident X / Y buffers."""
         import torch
 
         if not torch.cuda.is_available():
@@ -224,7 +233,27 @@ class B200Runtime:
                             int(os.environ.get("COE_WAVE_ROWS", wave_rows_cap or 0)),
                             int(os.environ.get("COE_URGENT_ROWS", urgent_rows_cap or 0)),
                             len(shapes), k["d"].ctypes.data, k["h"].ctypes.data, k["slots"].ctypes.data,
-                            k["es"].ctypes.data, None if k["mask"] is None else k["mask"].ctypes.data)
+                            k["es"].ctypes.data, None if k["mask"] is None else k["mask"].ctypes.data,
+                            int(ring_slots if ring_slots is not None else max_requests), int(landing_slots),
+                            int(out_slots), 1 if device_io else 0)
+        self.ring_slots = cfg.ring_slots
+        self.landing_slots = cfg.landing_slots
+        self.device_io = device_io
+        self.max_wave_rows = rows
+        self.out_slots = out_slots or max(64, 2 * rows // T)
+
+    def memory(self) -> dict:
+        """Device bytes by role: expert slots (the budget), activations (ring + landing rows,
+        the H scratch of the three wave streams, the e2e output staging ring) and the
+        device-resident request inputs / outputs X, Y (device_io only)."""
+        row = self.shapes[0].T * self.act_ld * 2
+        act = {"ring": self.ring_slots * row, "landing": self.landing_slots * row,
+               "h_scratch": 3 * self.max_wave_rows * max(s.h for s in self.shapes) * 2,
+               "out_staging": self.out_slots * row}
+        slots = sum(n * s.expert_bytes for n, s in zip(self._keep["slots"].tolist(), self.shapes))
+        return {"expert_slots": int(slots), "activations": act, "activations_total": int(sum(act.values())),
+                "device_io_xy": (2 * self.max_requests * row) if self.device_io else 0,
+                "ring_slots": self.ring_slots, "landing_rows": self.landing_slots}
         self.profile = profile
         self.handle = ctypes.c_void_p()
         _check(self.lib, self.lib.coe_runtime_create(ctypes.byref(cfg), ctypes.byref(self.handle)), "runtime create")
@@ -251,6 +280,13 @@ class B200Runtime:
             if op["executor"] == executor:
                 touched[int(op["expert"])] = 1
         adm = sum(len(c) for c in resolved.chains)
+        # activation rows: the ring's peak for this executor's op log, e2e included (stage-0
+        # inputs occupy slots too); with several executors also the NCCL transport's needs
+        ring, landing = plan_rows(plan, executor, e2e=True)
+        if len(resolved.executors) > 1:
+            ring = max(ring, plan_rows(plan, executor, e2e=True, nccl=True)[0])
+        kw.setdefault("ring_slots", max(1, ring))
+        kw.setdefault("landing_slots", landing)
         if isinstance(shape, RuntimeShape):
             largest = max(spec.param_bytes for spec in registry.experts.values())
             slots = max(1, min(int(budget // largest), int(touched.sum()) or 1))
@@ -538,6 +574,27 @@ def nccl_library() -> str:
     except Exception:
         pass
     return "libnccl.so.2"
+
+
+def _step_input(plan, executor: int) -> StepInput:
+    lib, h = plan.lib, plan.handle
+    return StepInput(executor,
+                     lib.coe_plan_num_admissions(h), ctypes.cast(lib.coe_plan_admissions(h), ctypes.c_void_p),
+                     lib.coe_plan_num_ops(h), ctypes.cast(lib.coe_plan_ops(h), ctypes.c_void_p),
+                     lib.coe_plan_num_op_args(h), ctypes.cast(lib.coe_plan_op_args(h), ctypes.c_void_p),
+                     0, None, None, None)
+
+
+def plan_rows(plan, executor: int = 0, e2e: bool = True, nccl: bool = False) -> tuple:
+    """(ring slots, landing rows) one step of ``plan`` needs on ``executor``: the activation
+    ring's peak occupancy and the hop-in landing rows (act_rows.h; the runtime's own pass,
+    host only).  ``e2e``: stage-0 inputs stream into ring slots too."""
+    lib = _lib()
+    ring, landing = ctypes.c_int32(), ctypes.c_int32()
+    inp = _step_input(plan, executor)
+    _check(lib, lib.coe_runtime_plan_rows(ctypes.byref(inp), len(plan.resolved.request_ids), 1 if e2e else 0,
+                                          1 if nccl else 0, ctypes.byref(ring), ctypes.byref(landing)), "plan rows")
+    return ring.value, landing.value
 
 
 def hops_from_plan(plan) -> list:

@@ -12,7 +12,7 @@ throughput curves through its ``sample_throughput`` callback:
   the recorded samples (a count the B200 search never probed raises, so the window
   schedule itself is pinned too).
 
-Output: ``tests/golden/window_search_cases.json.gz`` -- inputs and the reference's
+Output: ``tests/golden/window/cases.json.gz`` -- inputs and the reference's
 ``WindowSearchResult.to_doc()`` per case.  ``tests/test_window_search_golden.py``
 checks ``paper_2503_02354_b200.profiler.decay_window_search`` against it on CPU.
 """
@@ -94,7 +94,7 @@ def main():
     cases = synthetic_cases() + measured_cases()
     for case in cases:
         case["expected"] = run(case)
-    out = os.path.join(HERE, "window_search_cases.json.gz")
+    out = os.path.join(HERE, "window", "cases.json.gz")
     with gzip.open(out, "wt") as fh:
         json.dump({"generator": "reference coesim.profiler.decay_window_search", "cases": cases}, fh)
     print(len(cases), "cases ->", out)

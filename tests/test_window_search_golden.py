@@ -1,6 +1,6 @@
 """(f1) The decay-window memory-allocation search is pinned to the reference.
 
-``tests/golden/window_search_cases.json.gz`` holds the UNMODIFIED reference's
+``tests/golden/window/cases.json.gz`` holds the UNMODIFIED reference's
 ``decay_window_search`` (profiler.py:281-354) results -- made by
 ``tests/golden/make_window_golden.py`` -- for 525 synthetic throughput curves and for
 every measured B200 curve under ``profiles/`` (``search_memory_allocation_measured``
@@ -17,7 +17,7 @@ import pytest
 from paper_2503_02354_b200 import profiler
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-CASES = json.load(gzip.open(os.path.join(HERE, "golden", "window_search_cases.json.gz"), "rt"))["cases"]
+CASES = json.load(gzip.open(os.path.join(HERE, "golden", "window", "cases.json.gz"), "rt"))["cases"]
 
 
 def _ours(case):
