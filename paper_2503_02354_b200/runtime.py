@@ -242,6 +242,12 @@ class B200Runtime:
         self.max_wave_rows = rows
         self.out_slots = out_slots or max(64, 2 * rows // T)
 
+        self.profile = profile
+        self.handle = ctypes.c_void_p()
+        _check(self.lib, self.lib.coe_runtime_create(ctypes.byref(cfg), ctypes.byref(self.handle)), "runtime create")
+        if init_experts:
+            _check(self.lib, self.lib.coe_runtime_init_experts(self.handle), "init experts")
+
     def memory(self) -> dict:
         """Device bytes by role: expert slots (the budget), activations (ring + landing rows,
         the H scratch of the three wave streams, the e2e output staging ring) and the
@@ -254,11 +260,6 @@ class B200Runtime:
         return {"expert_slots": int(slots), "activations": act, "activations_total": int(sum(act.values())),
                 "device_io_xy": (2 * self.max_requests * row) if self.device_io else 0,
                 "ring_slots": self.ring_slots, "landing_rows": self.landing_slots}
-        self.profile = profile
-        self.handle = ctypes.c_void_p()
-        _check(self.lib, self.lib.coe_runtime_create(ctypes.byref(cfg), ctypes.byref(self.handle)), "runtime create")
-        if init_experts:
-            _check(self.lib, self.lib.coe_runtime_init_experts(self.handle), "init experts")
 
     @classmethod
     def for_plan(cls, plan, shape, executor: int = 0, **kw) -> "B200Runtime":
