@@ -27,6 +27,7 @@ extern "C" {
 #endif
 
 typedef struct CUstream_st *cudaStream_t;
+typedef struct CUevent_st *cudaEvent_t;
 
 enum { COE_CUDA_OK = 0, COE_CUDA_ERR_CONFIG = 2, COE_CUDA_ERR_CHECK = 4, COE_CUDA_ERR_CUDA = 6 };
 
@@ -308,6 +309,21 @@ coe_local_hub *coe_local_hub_create(int world);
 void coe_local_hub_destroy(coe_local_hub *hub);
 void coe_local_hub_reset(coe_local_hub *hub);
 int coe_comm_create_local(coe_local_hub *hub, int rank, coe_comm **out);
+/* K4 on its own: one expert's bytes (or one W1 / W2 half), pinned host -> its HBM slot, on
+ * the caller's copy-engine stream; done_event (may be NULL) is recorded after the copy.
+ * Replaces CostModel.load_latency_from as charged by Simulation._start_load
+ * (costmodel.py:69-73, engine.py:643-677); coe_runtime_step issues these itself. */
+int coe_swap_in(void *dst_slot, const void *src_pinned, int64_t bytes, cudaStream_t copy_stream,
+                cudaEvent_t done_event);
+/* K5 on its own: all-to-all of follow-up activations with exact per-peer counts (bf16
+ * elements): sendbuf / recvbuf hold world contiguous segments in rank order; the self
+ * segment is a device copy, the rest one NCCL group of sends / receives (ring order) on
+ * `stream`.  The follow-ups a batch_done epoch admits on other executors
+ * (engine.py:751-753).  With an in-process hub communicator every rank calls it from its
+ * own host thread.  coe_runtime_step fuses hops into K3 instead (peer mode) or groups its
+ * own sends / receives per wave (NCCL mode). */
+int coe_hop(coe_comm *comm, const void *sendbuf, const int64_t *send_counts, void *recvbuf,
+            const int64_t *recv_counts, cudaStream_t stream);
 /* Attach to a runtime (rank == the executor it serves); steps then exchange
  * hopped activations on a dedicated hop stream. */
 int coe_runtime_attach_comm(coe_runtime *rt, coe_comm *comm);

@@ -7,6 +7,7 @@
 // has no link-time NCCL dependency; one communicator per runtime, all hop
 // traffic on the runtime's hop stream, one ncclSend / ncclRecv per hop in the
 // global hop order (hops.h).
+#include <cuda_bf16.h>
 #include <dlfcn.h>
 
 #include <condition_variable>
@@ -30,6 +31,8 @@ struct NcclApi {
   ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
   ncclResult_t (*send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*group_start)() = nullptr;
+  ncclResult_t (*group_end)() = nullptr;
   const char *(*error_string)(ncclResult_t) = nullptr;
 };
 
@@ -49,7 +52,10 @@ bool load_nccl(const char *path) {
   g_nccl.send = reinterpret_cast<decltype(g_nccl.send)>(dlsym(h, "ncclSend"));
   g_nccl.recv = reinterpret_cast<decltype(g_nccl.recv)>(dlsym(h, "ncclRecv"));
   g_nccl.error_string = reinterpret_cast<decltype(g_nccl.error_string)>(dlsym(h, "ncclGetErrorString"));
-  if (!g_nccl.get_unique_id || !g_nccl.comm_init_rank || !g_nccl.send || !g_nccl.recv) {
+  g_nccl.group_start = reinterpret_cast<decltype(g_nccl.group_start)>(dlsym(h, "ncclGroupStart"));
+  g_nccl.group_end = reinterpret_cast<decltype(g_nccl.group_end)>(dlsym(h, "ncclGroupEnd"));
+  if (!g_nccl.get_unique_id || !g_nccl.comm_init_rank || !g_nccl.send || !g_nccl.recv || !g_nccl.group_start ||
+      !g_nccl.group_end) {
     coe_set_error("NCCL library lacks point-to-point symbols");
     return false;
   }
@@ -135,6 +141,14 @@ bool coe_comm_recv_bf16(coe_comm *c, void *buf, size_t count, int peer, cudaStre
 
 int coe_comm_rank(const coe_comm *c) { return c->rank; }
 
+// One NCCL group around a run of sends / receives: NCCL fuses them into one launch that
+// progresses every transfer concurrently (the all-to-all of a wave's hops).  The in-process
+// hub has nothing to fuse.
+bool coe_comm_group(coe_comm *c, bool start) {
+  if (c->hub) return true;
+  return nccl_ok(start ? g_nccl.group_start() : g_nccl.group_end(), start ? "ncclGroupStart" : "ncclGroupEnd");
+}
+
 // Fused peer hops between runtimes of one process: the producer publishes an event recorded
 // after the down pass that stored the rows; the consumer blocks on the host until it is
 // published and makes its stream wait on it.  (Stream memory-op flags are not used in one
@@ -208,6 +222,59 @@ void coe_local_hub_reset(coe_local_hub *h) {
   h->queues.clear();
   h->published.clear();
   h->next_event = 0;
+}
+
+int coe_swap_in(void *dst_slot, const void *src_pinned, int64_t bytes, cudaStream_t copy_stream,
+                cudaEvent_t done_event) {
+  if (bytes < 0 || (bytes && (!dst_slot || !src_pinned))) {
+    coe_set_error("coe_swap_in: bad buffer or size");
+    return COE_CUDA_ERR_CONFIG;
+  }
+  if (bytes && !coe_cuda_ok(cudaMemcpyAsync(dst_slot, src_pinned, (size_t)bytes, cudaMemcpyHostToDevice, copy_stream),
+                            "coe_swap_in"))
+    return COE_CUDA_ERR_CUDA;
+  if (done_event && !coe_cuda_ok(cudaEventRecord(done_event, copy_stream), "coe_swap_in record"))
+    return COE_CUDA_ERR_CUDA;
+  return COE_CUDA_OK;
+}
+
+int coe_hop(coe_comm *comm, const void *sendbuf, const int64_t *send_counts, void *recvbuf,
+            const int64_t *recv_counts, cudaStream_t stream) {
+  if (!comm || !send_counts || !recv_counts) {
+    coe_set_error("coe_hop: communicator and counts required");
+    return COE_CUDA_ERR_CONFIG;
+  }
+  const int W = comm->world, me = comm->rank;
+  std::vector<int64_t> soff(W + 1, 0), roff(W + 1, 0);
+  for (int r = 0; r < W; ++r) {
+    if (send_counts[r] < 0 || recv_counts[r] < 0) {
+      coe_set_error("coe_hop: negative count");
+      return COE_CUDA_ERR_CONFIG;
+    }
+    soff[r + 1] = soff[r] + send_counts[r];
+    roff[r + 1] = roff[r] + recv_counts[r];
+  }
+  if (send_counts[me] != recv_counts[me]) {
+    coe_set_error("coe_hop: the self segment must send what it receives");
+    return COE_CUDA_ERR_CONFIG;
+  }
+  const auto *sb = static_cast<const __nv_bfloat16 *>(sendbuf);
+  auto *rb = static_cast<__nv_bfloat16 *>(recvbuf);
+  if (send_counts[me] &&
+      !coe_cuda_ok(cudaMemcpyAsync(rb + roff[me], sb + soff[me], 2 * (size_t)send_counts[me], cudaMemcpyDeviceToDevice,
+                                   stream),
+                   "coe_hop self copy"))
+    return COE_CUDA_ERR_CUDA;
+  if (!coe_comm_group(comm, true)) return COE_CUDA_ERR_CUDA;
+  bool good = true;
+  for (int k = 1; k < W && good; ++k) {  // ring order: every rank sends to me+k while receiving from me-k
+    const int to = (me + k) % W, from = (me - k + W) % W;
+    if (send_counts[to]) good = coe_comm_send_bf16(comm, sb + soff[to], (size_t)send_counts[to], to, stream);
+    if (good && recv_counts[from])
+      good = coe_comm_recv_bf16(comm, rb + roff[from], (size_t)recv_counts[from], from, stream);
+  }
+  if (!coe_comm_group(comm, false) || !good) return COE_CUDA_ERR_CUDA;
+  return COE_CUDA_OK;
 }
 
 int coe_comm_create_local(coe_local_hub *hub, int rank, coe_comm **out) {

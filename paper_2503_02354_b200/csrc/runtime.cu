@@ -1836,26 +1836,39 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
   };
   size_t hop_cursor = 0;
   const size_t row_elems = (size_t)rt->row_elems;
+  // NCCL transport: the hops up to `limit` (global order) as ONE NCCL group on the hop stream
+  // -- an all-to-all of this wave's sends / receives with exact counts; the producers of its
+  // sends were issued earlier (phase B), so the stream first waits for their down passes
   auto issue_hops_until = [&](int64_t limit) -> bool {
-    while (hop_cursor < my_hops.size() && all_hops[my_hops[hop_cursor]].index <= limit) {
-      const coe::Hop &h = all_hops[my_hops[hop_cursor]];
-      __nv_bfloat16 *row = rt->act + (size_t)rows.hop_row[hop_cursor] * row_elems;
-      if (h.src == x) {
-        const int32_t pb = hop_batch[hop_cursor];
-        if (pb < 0 || !issued[pb] || batches[pb].wave < 0) {
-          coe_set_error("internal: hop send issued before its producer wave");
-          return false;
-        }
-        if (!ok(cudaStreamWaitEvent(rt->hop, wave_down_ev[batches[pb].wave], 0), "send waits producer") ||
-            !coe_comm_send_bf16(rt->comm, row, row_elems, h.dst, rt->hop))
-          return false;
-      } else {
-        if (!coe_comm_recv_bf16(rt->comm, row, row_elems, h.src, rt->hop) ||
-            !ok(cudaEventRecord(rt->recv_ev[hop_cursor], rt->hop), "record"))
-          return false;
+    size_t end = hop_cursor;
+    while (end < my_hops.size() && all_hops[my_hops[end]].index <= limit) ++end;
+    if (end == hop_cursor) return true;
+    std::vector<int32_t> waited;
+    for (size_t k = hop_cursor; k < end; ++k) {
+      if (all_hops[my_hops[k]].src != x) continue;
+      const int32_t pb = hop_batch[k];
+      if (pb < 0 || !issued[pb] || batches[pb].wave < 0) {
+        coe_set_error("internal: hop send issued before its producer wave");
+        return false;
       }
-      ++hop_cursor;
+      if (std::find(waited.begin(), waited.end(), batches[pb].wave) != waited.end()) continue;
+      waited.push_back(batches[pb].wave);
+      if (!ok(cudaStreamWaitEvent(rt->hop, wave_down_ev[batches[pb].wave], 0), "send waits producer")) return false;
     }
+    if (!coe_comm_group(rt->comm, true)) return false;
+    for (size_t k = hop_cursor; k < end; ++k) {
+      const coe::Hop &h = all_hops[my_hops[k]];
+      __nv_bfloat16 *row = rt->act + (size_t)rows.hop_row[k] * row_elems;
+      if (!(h.src == x ? coe_comm_send_bf16(rt->comm, row, row_elems, h.dst, rt->hop)
+                       : coe_comm_recv_bf16(rt->comm, row, row_elems, h.src, rt->hop))) {
+        coe_comm_group(rt->comm, false);
+        return false;
+      }
+    }
+    if (!coe_comm_group(rt->comm, false)) return false;
+    for (size_t k = hop_cursor; k < end; ++k)
+      if (all_hops[my_hops[k]].dst == x && !ok(cudaEventRecord(rt->recv_ev[k], rt->hop), "record")) return false;
+    hop_cursor = end;
     return true;
   };
   // output staging ring: before a wave's down pass stores rows [p0, p1) (global positions), the

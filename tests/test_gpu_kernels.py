@@ -258,3 +258,75 @@ def test_grouped_mlp_single_row_block_and_many_groups(lib, cg, monkeypatch):
     monkeypatch.setenv("COE_K3_CG", str(cg))
     spec = [([(i, i % 2)], i % 3) for i in range(40)]
     assert _mlp_case(lib, 1024, 1024, 64, spec) <= K3_TOL
+
+
+def test_swap_in_entry_point(lib):
+    """coe_swap_in (K4 alone): pinned host bytes land in the device slot; the event orders them."""
+    import torch
+
+    lib.coe_swap_in.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]
+    lib.coe_swap_in.restype = ctypes.c_int
+    n = 3 << 20
+    src = torch.randint(0, 255, (n,), dtype=torch.uint8).pin_memory()
+    dst = torch.zeros(n, dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.Stream()
+    done = torch.cuda.Event()
+    done.record(stream)  # materialise the event handle
+    _ck(lib, lib.coe_swap_in(dst.data_ptr(), src.data_ptr(), n, stream.cuda_stream, done.cuda_event), "swap_in")
+    done.synchronize()
+    assert torch.equal(dst.cpu(), src)
+    assert lib.coe_swap_in(None, src.data_ptr(), 16, stream.cuda_stream, None) != 0
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_hop_all_to_all_entry_point(lib, world):
+    """coe_hop (K5 alone): exact-count all-to-all of bf16 activations; ragged and empty
+    segments, self copy, one thread per rank over the in-process transport."""
+    import threading
+
+    import torch
+
+    lib.coe_local_hub_create.argtypes = [ctypes.c_int]
+    lib.coe_local_hub_create.restype = ctypes.c_void_p
+    lib.coe_comm_create_local.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]
+    lib.coe_comm_create_local.restype = ctypes.c_int
+    lib.coe_hop.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                            ctypes.c_void_p]
+    lib.coe_hop.restype = ctypes.c_int
+    lib.coe_comm_destroy.argtypes = [ctypes.c_void_p]
+    lib.coe_local_hub_destroy.argtypes = [ctypes.c_void_p]
+    hub = lib.coe_local_hub_create(world)
+    count = lambda s, d: 0 if (s + d) % 4 == 3 else 64 * (1 + s) + 8 * d  # noqa: E731  (some segments empty)
+    send, recv, comms, errs = [], [], [], []
+    for r in range(world):
+        c = ctypes.c_void_p()
+        _ck(lib, lib.coe_comm_create_local(hub, r, ctypes.byref(c)), "comm")
+        comms.append(c)
+        segs = [torch.full((count(r, d),), float(100 * r + d), dtype=torch.bfloat16, device="cuda")
+                for d in range(world)]
+        send.append(torch.cat(segs))
+        recv.append(torch.zeros(sum(count(s, r) for s in range(world)), dtype=torch.bfloat16, device="cuda"))
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream() for _ in range(world)]
+
+    def rank(r):
+        sc = (ctypes.c_int64 * world)(*[count(r, d) for d in range(world)])
+        rc = (ctypes.c_int64 * world)(*[count(s, r) for s in range(world)])
+        code = lib.coe_hop(comms[r], send[r].data_ptr(), sc, recv[r].data_ptr(), rc, streams[r].cuda_stream)
+        if code:
+            errs.append(code)
+
+    threads = [threading.Thread(target=rank, args=(r,)) for r in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    torch.cuda.synchronize()
+    assert not errs
+    for r in range(world):
+        expect = torch.cat([torch.full((count(s, r),), float(100 * s + r), dtype=torch.bfloat16, device="cuda")
+                            for s in range(world)])
+        assert torch.equal(recv[r], expect)
+    for c in comms:
+        lib.coe_comm_destroy(c)
+    lib.coe_local_hub_destroy(hub)
