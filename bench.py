@@ -199,6 +199,24 @@ def algorithmic_flops(plan, shape, executor: int = 0) -> float:
     return total
 
 
+def hop_summary(plan, rank: int, world: int, rt, ms_per_step: float, transport: str) -> dict | None:
+    """Follow-up hops of one step (engine.py:751-753 admits a follow-up on another executor):
+    what this rank sends / receives and the average rate over the step (the fused transport
+    stores rows from K3's epilogue, so the link is busy only inside down passes)."""
+    if world <= 1:
+        return None
+    from paper_2503_02354_b200 import runtime
+
+    hops = runtime.hops_from_plan(plan)
+    row = rt.shapes[0].T * rt.act_ld * 2
+    sent = sum(1 for h in hops if h[1] == rank)
+    got = sum(1 for h in hops if h[2] == rank)
+    return {"transport": transport, "hops_total": len(hops), "sent": sent, "received": got,
+            "hop_bytes_per_step": sent * row, "recv_bytes_per_step": got * row,
+            "all_ranks_hop_bytes_per_step": len(hops) * row,
+            "avg_nvlink_gbs_per_rank": (sent * row) / (ms_per_step / 1e3) / 1e9 if ms_per_step > 0 else None}
+
+
 def self_check(rt, plan, stats, executor: int, shape) -> dict:
     """After the timed loop (untimed): K2 reported no straddling batch, every GPU-grouped batch
     of the last step equals the planner's members (which equal the oracle DES's -- pinned by
@@ -549,6 +567,7 @@ def main() -> None:
                     "overlap_ms": timing["overlap_ms"],
                     "overlap_frac_of_shorter": timing["overlap_ms"] / short if short > 0 else None,
                     "pcie_counters": pcie.summary()},
+        "hops": hop_summary(plan_last, rank, world, rt, elapsed_ms / args.steps, transport),
         "grouping": {"admissions": stats["admissions"], "group_ms": timing["group_ms"], "runs": runs,
                      "violations": violations, "waves": stats["waves"]},
         "self_check": verified,

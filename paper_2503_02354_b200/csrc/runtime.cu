@@ -1548,7 +1548,7 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
       // greedy wave at m_start: ready (by estimate) issuable batches in op order
       std::vector<int32_t> members;
       std::unordered_set<int32_t> reqs;
-      int64_t rows = 0, wave_max_recv = -1, wave_min_send = INT64_MAX;
+      int64_t rows = 0, wave_max_recv = -1, wave_min_send = INT64_MAX, wave_finals = 0;
       std::vector<size_t> taken;
       // candidate order: urgent (slot needed by one of the next swap-ins) first, then op order
       std::vector<size_t> order;
@@ -1586,9 +1586,12 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
         if (clash) continue;
         const int64_t mr = std::max(wave_max_recv, b.max_recv), ms = std::min(wave_min_send, b.min_send);
         if (mr >= 0 && ms < mr) continue;  // a wave may not wait on a hop its own sends precede
+        // e2e: a wave's final rows must fit the output staging ring at once
+        if (!members.empty() && wave_finals + (int64_t)b.finals.size() > rt->out_slots) continue;
         members.push_back(bi);
         taken.push_back(i);
         rows += b.rows;
+        wave_finals += (int64_t)b.finals.size();
         wave_max_recv = mr;
         wave_min_send = ms;
         for (int32_t j = 0; j < b.count; ++j) reqs.insert(in->op_args[ops[b.op_index].offset + 2 * j]);
