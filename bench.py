@@ -43,6 +43,9 @@ def parse_args():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", default="c3")
     ap.add_argument("--requests", type=int, default=10000)
+    ap.add_argument("--alloc-count", type=int, default=None,
+                    help="expert budget as the reference's alloc_override={'gpu': N} (engine.py:436): bytes of "
+                         "the N most-used experts")
     ap.add_argument("--cpu-budget", type=float, default=12.0,
                     help="seconds of sampled CPU expert work per CPU-baseline / reference-arm step")
     ap.add_argument("--e2e-steps", type=int, default=5)
@@ -336,7 +339,8 @@ def main() -> None:
 
     w = configs.load(args.config, args.requests, gpu_executors=world)
     shape = runtime.shape_of(w)
-    cfg = configs.run_config(w, trace=False)
+    cfg = (configs.run_config(w, trace=False) if args.alloc_count is None else
+           configs.run_config(w, trace=False, alloc_override={"gpu": args.alloc_count}, search_enabled=False))
     plan0 = engine.plan(cfg)
     n_req = len(plan0.resolved.request_ids)
     # each rank pins only the experts its executor touches; COE_SHARED_STORE=1 shares one
@@ -426,6 +430,7 @@ def main() -> None:
     barrier()
     elapsed_ms = start.elapsed_time(end)
     timing = rt.timing()
+    k3_shapes = rt.per_shape_k3() if len(rt.shapes) > 1 else None  # the last timed step, per expert shape
     if dist is not None:
         t = torch.tensor([elapsed_ms], device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -537,6 +542,8 @@ def main() -> None:
         "gb_moved_per_1k_requests": 1000.0 * ps["bytes_moved"] / 1e9 / n_req,
         "planner": {"makespan_virtual_s": metrics.makespan_s, "switches": metrics.expert_switches,
                     "evictions": metrics.evictions, "batches": ps["batches"]},
+        "k3_per_shape": ({k: dict(v, frac_of_sustained=(v["tflops"] / sustained if v["tflops"] else None))
+                          for k, v in k3_shapes.items()} if k3_shapes else None),
         "roofline": {"bound": "tensor", "kernel": "grouped_gemm_kernel (K3, tcgen05; up + down launch per wave)",
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak if (peak and achieved) else None,

@@ -282,6 +282,8 @@ int coe_runtime_attach_peers(coe_runtime *rt, int32_t rank, int32_t world, const
 /* profile mode: per wave [up start, up end, down start, down end] ms since step start and
  * the wave's algorithmic FLOPs (4 * rows * d * h) */
 int coe_runtime_wave_phases(coe_runtime *rt, float *phase_iv, double *wave_flops);
+/* after a step: the expert-shape index (coe_runtime_config.shape_d / shape_h order) of each wave */
+int coe_runtime_wave_shapes(coe_runtime *rt, int32_t *shape_index);
 /* profile mode, e2e steps: [start, end] ms of each stage-0 input upload (copy engine) then of
  * each output download (output stream); iv == NULL queries the counts only */
 int coe_runtime_io_intervals(coe_runtime *rt, float *iv, int32_t *n_in, int32_t *n_out);

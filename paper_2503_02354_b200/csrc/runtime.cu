@@ -287,7 +287,7 @@ struct coe_runtime {
   cudaEvent_t cls_drained[NCLS] = {nullptr, nullptr, nullptr};
   cudaEvent_t t_step_start = nullptr, t_group_end = nullptr, t_step_end = nullptr;
   int32_t last_waves = 0, last_copies = 0;
-  std::vector<int32_t> last_wave_cls, last_wave_rows, last_wave_groups;
+  std::vector<int32_t> last_wave_cls, last_wave_rows, last_wave_groups, last_wave_shape;
   int64_t last_adm = 0, last_batches = 0;
   int last_set = 0;
   cudaStream_t out_stream = nullptr;  // e2e output downloads (inputs ride the copy engine)
@@ -951,6 +951,11 @@ int coe_runtime_intervals(coe_runtime *rt, float *copy_iv, float *wave_iv, int32
     wave_info[3 * i + 1] = rt->last_wave_rows[i];
     wave_info[3 * i + 2] = rt->last_wave_groups[i];
   }
+  return COE_CUDA_OK;
+}
+
+int coe_runtime_wave_shapes(coe_runtime *rt, int32_t *shape_index) {
+  for (int i = 0; i < rt->last_waves; ++i) shape_index[i] = rt->last_wave_shape[i];
   return COE_CUDA_OK;
 }
 
@@ -2054,11 +2059,13 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
   rt->last_wave_cls.clear();
   rt->last_wave_rows.clear();
   rt->last_wave_groups.clear();
+  rt->last_wave_shape.clear();
   rt->last_wave_flops.clear();
   for (const WaveAct &w : waves) {
     rt->last_wave_cls.push_back(w.cls);
     rt->last_wave_rows.push_back((int32_t)w.rows);
     rt->last_wave_groups.push_back(w.num_groups);
+    rt->last_wave_shape.push_back(w.shape);
     rt->last_wave_flops.push_back(4.0 * (double)w.rows * rt->sd[w.shape] * rt->sh[w.shape]);
   }
   rt->last_copies = (int32_t)nc;

@@ -480,6 +480,28 @@ class B200Runtime:
         _check(self.lib, self.lib.coe_runtime_wave_phases(self.handle, iv.ctypes.data, fl.ctypes.data), "wave_phases")
         return {"phases": iv[:4 * nw.value].reshape(-1, 4).tolist(), "flops": fl[:nw.value].tolist()}
 
+    def per_shape_k3(self) -> dict:
+        """Profile mode, after a step: per expert shape, the algorithmic FLOPs of its waves and
+        the summed durations of their up + down K3 launches (CUDA events on the launching
+        streams) -> achieved TFLOP/s per shape."""
+        ph = self.wave_phases()
+        nw = len(ph["flops"])
+        idx = np.zeros(max(1, nw), np.int32)
+        self.lib.coe_runtime_wave_shapes.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
+        _check(self.lib, self.lib.coe_runtime_wave_shapes(self.handle, idx.ctypes.data), "wave shapes")
+        out = {}
+        for i in range(nw):
+            s = self.shapes[int(idx[i])]
+            key = f"{s.d}x{s.h}x{s.T}"
+            u0, u1, d0, d1 = ph["phases"][i]
+            e = out.setdefault(key, {"waves": 0, "flops": 0.0, "k3_ms": 0.0})
+            e["waves"] += 1
+            e["flops"] += ph["flops"][i]
+            e["k3_ms"] += (u1 - u0) + (d1 - d0)
+        for e in out.values():
+            e["tflops"] = e["flops"] / (e["k3_ms"] / 1e3) / 1e12 if e["k3_ms"] > 0 else None
+        return out
+
     def output_order(self) -> np.ndarray:
         """After an e2e step: the request id of each host_outputs row (completion order)."""
         n = self.lib.coe_runtime_output_order(self.handle, None, 0)
