@@ -306,10 +306,24 @@ class B200Runtime:
                         key=lambda s: (s.d, s.h))
         index = {s: i for i, s in enumerate(shapes)}
         expert_shape = np.array([index[RuntimeShape(*arch_shapes[registry.experts[e].arch])] for e in ids], np.int32)
-        slots = []
-        for i, s in enumerate(shapes):
-            n_touched = int(touched[expert_shape == i].sum())
-            slots.append(max(1, min(n_touched, int(budget // s.expert_bytes))))
+        # slots per shape = that shape's peak concurrent residency in this executor's op log
+        # (initial placement, then each LOAD's victims out and its expert in): exactly what the
+        # planner's byte-budgeted pool (expert_pool.py:27-59) holds at once, shape by shape
+        cur = np.zeros(len(shapes), np.int64)
+        for e in plan.initial_residency()[executor]:
+            cur[expert_shape[int(e)]] += 1
+        peak = cur.copy()
+        args = plan.op_args()
+        for op in plan.ops():
+            if op["executor"] != executor or op["kind"] != _native.OP_LOAD:
+                continue
+            o = int(op["offset"])
+            for v in args[o:o + int(op["count"])]:
+                cur[expert_shape[int(v)]] -= 1
+            k = expert_shape[int(op["expert"])]
+            cur[k] += 1
+            peak[k] = max(peak[k], cur[k])
+        slots = [max(1, int(p)) for p in peak]
         if not kw.get("store_path"):
             kw.setdefault("store_mask", touched)
         return cls(shapes, len(ids), slots, len(resolved.request_ids), adm, expert_shape=expert_shape, **kw)
