@@ -448,7 +448,10 @@ class B200Runtime:
         )
         stats = StepStats()
         _check(self.lib, self.lib.coe_runtime_step(self.handle, ctypes.byref(inp), ctypes.byref(stats)), "step")
-        return stats.as_dict()
+        out = stats.as_dict()
+        if host_outputs is not None:  # the completion order is fixed at issue time
+            out["output_order"] = self.output_order()
+        return out
 
     def join(self) -> None:
         """Order the compute stream after the last e2e step's output downloads."""

@@ -198,15 +198,15 @@ def test_c1_10k_end_to_end_ring_reuse(out_slots):
     ref = ref.view(n, shape.T, shape.d)
     host_in = torch.empty(n * row, dtype=torch.bfloat16).pin_memory()
     rt.read_buffer(0, host_in.data_ptr(), n * row * 2)
-    outs, keep = [torch.zeros(n * row, dtype=torch.bfloat16).pin_memory() for _ in range(2)], []
+    outs, keep, orders = [torch.zeros(n * row, dtype=torch.bfloat16).pin_memory() for _ in range(2)], [], []
     for h in outs:
         p = engine.plan(configs.run_config(w, trace=False))
         keep.append(p)
         st = rt.step(p, host_inputs=host_in.data_ptr(), host_outputs=h.data_ptr())
         assert st["ring_peak"] <= rt.ring_slots
+        orders.append(st["output_order"])
     rt.synchronize()
-    order = rt.output_order()
-    assert sorted(order.tolist()) == list(range(n))
-    for h in outs:
+    for h, order in zip(outs, orders):
+        assert sorted(order.tolist()) == list(range(n))
         assert torch.equal(h.view(n, shape.T, shape.d), ref[torch.from_numpy(order).long()])
     rt.close()

@@ -29,12 +29,12 @@ def _trim(workload, n):
     return workload
 
 
-def _serve(workload, shape, steps=1, sample=12):
+def _serve(workload, shape, steps=1, sample=12, **kw):
     import torch
 
     cfg = configs.run_config(workload, trace=False)
     plan = engine.plan(cfg)
-    rt = runtime.B200Runtime.for_plan(plan, shape)
+    rt = runtime.B200Runtime.for_plan(plan, shape, **kw)
     n_req = len(plan.resolved.request_ids)
     rt.fill_inputs(n_req)
     stats = []
@@ -159,30 +159,31 @@ def test_streamed_end_to_end_io_matches_device_path():
     assert np.array_equal(got, outs[0][order])
 
 
-def test_back_to_back_end_to_end_steps():
-    """Three e2e steps issued back to back (no host sync between them): inputs alternate
-    between two device buffers across steps and each step's gathers wait for the previous
-    step's downloads; every step's host output buffer holds the same bytes as the
-    device-resident path."""
+@pytest.mark.parametrize("out_slots", [0, 24])
+def test_back_to_back_end_to_end_steps(out_slots):
+    """Three e2e steps issued back to back (no host sync between them): each step's inputs
+    stream into ring slots the previous step's up passes released, final rows leave through
+    the output staging ring (24 rows: smaller waves, many wraps, rows reused before the
+    previous step's downloads would otherwise finish); every step's host output buffer holds
+    the device-resident path's bytes in that step's completion order."""
     import torch
 
     w = _trim(configs.load("c2", 1000), 200)
     shape = runtime.shape_of(w)
-    plan, rt, stats, outs = _serve(w, shape, steps=1)
+    plan, rt, stats, outs = _serve(w, shape, steps=1, out_slots=out_slots)
     n = len(plan.resolved.request_ids)
     row = shape.T * shape.d
     host_in = torch.empty(n * row, dtype=torch.bfloat16).pin_memory()
     rt.read_buffer(0, host_in.data_ptr(), n * row * 2)
     host_outs = [torch.zeros(n * row, dtype=torch.bfloat16).pin_memory() for _ in range(3)]
-    keep = []
+    keep, orders = [], []
     for h in host_outs:
         p = engine.plan(configs.run_config(w, trace=False))
         keep.append(p)
-        rt.step(p, host_inputs=host_in.data_ptr(), host_outputs=h.data_ptr())
+        orders.append(rt.step(p, host_inputs=host_in.data_ptr(), host_outputs=h.data_ptr())["output_order"])
     rt.synchronize()
-    order = rt.output_order()
-    assert sorted(order.tolist()) == list(range(n))
-    for h in host_outs:
+    for h, order in zip(host_outs, orders):
+        assert sorted(order.tolist()) == list(range(n))
         got = h.view(n, shape.T, shape.d).float().numpy()
         assert np.array_equal(got, outs[0][order])
 
