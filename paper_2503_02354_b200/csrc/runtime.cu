@@ -39,6 +39,7 @@
 #include <cstring>
 #include <climits>
 #include <deque>
+#include <memory>
 #include <cstdlib>
 #include <string>
 #include <unordered_map>
@@ -80,8 +81,10 @@ struct CopyAct {
   int32_t expert;
   int32_t slot;
   bool restore;
-  std::vector<int32_t> wait_waves;  // last issued reader wave of the slot, per stream (this step)
-  bool wait_prev[3] = {false, false, false};  // per stream: wait for last step's readers
+  std::vector<int32_t> wait_waves;  // last issued reader wave of the bytes overwritten, per stream (this step)
+  std::vector<int32_t> wait_prev;   // slot * NCLS + stream: last step's readers (slot_free events)
+  std::vector<int32_t> own_waves, own_prev;  // VMM: readers of this slot's stale mapping (unmap safety)
+  std::vector<int32_t> pages;       // VMM: pool pages mapped behind the slot
 };
 
 struct WaveAct {
@@ -209,6 +212,46 @@ bool batched_copy(std::vector<void *> &dsts, std::vector<void *> &srcs, std::vec
 
 void coe_set_error(const std::string &msg) { g_last_error = msg; }
 
+// CUDA VMM driver entry points (resolved once through the runtime, no -lcuda)
+struct VmmApi {
+  CUresult (*create)(CUmemGenericAllocationHandle *, size_t, const CUmemAllocationProp *, unsigned long long) = nullptr;
+  CUresult (*release)(CUmemGenericAllocationHandle) = nullptr;
+  CUresult (*address_reserve)(CUdeviceptr *, size_t, size_t, CUdeviceptr, unsigned long long) = nullptr;
+  CUresult (*address_free)(CUdeviceptr, size_t) = nullptr;
+  CUresult (*map)(CUdeviceptr, size_t, size_t, CUmemGenericAllocationHandle, unsigned long long) = nullptr;
+  CUresult (*unmap)(CUdeviceptr, size_t) = nullptr;
+  CUresult (*set_access)(CUdeviceptr, size_t, const CUmemAccessDesc *, size_t) = nullptr;
+  CUresult (*granularity)(size_t *, const CUmemAllocationProp *, CUmemAllocationGranularity_flags) = nullptr;
+  bool ok = false;
+};
+const VmmApi &vmm_api() {
+  static VmmApi a;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    auto get = [](const char *name, void **fn) {
+      cudaDriverEntryPointQueryResult q;
+      return cudaGetDriverEntryPoint(name, fn, cudaEnableDefault, &q) == cudaSuccess && q == cudaDriverEntryPointSuccess;
+    };
+    a.ok = get("cuMemCreate", reinterpret_cast<void **>(&a.create)) &&
+           get("cuMemRelease", reinterpret_cast<void **>(&a.release)) &&
+           get("cuMemAddressReserve", reinterpret_cast<void **>(&a.address_reserve)) &&
+           get("cuMemAddressFree", reinterpret_cast<void **>(&a.address_free)) &&
+           get("cuMemMap", reinterpret_cast<void **>(&a.map)) && get("cuMemUnmap", reinterpret_cast<void **>(&a.unmap)) &&
+           get("cuMemSetAccess", reinterpret_cast<void **>(&a.set_access)) &&
+           get("cuMemGetAllocationGranularity", reinterpret_cast<void **>(&a.granularity));
+  }
+  return a;
+}
+bool cu_ok(CUresult r, const char *what) {
+  if (r == CUDA_SUCCESS) return true;
+  coe_set_error(std::string(what) + " failed (CUresult " + std::to_string((int)r) + ")");
+  return false;
+}
+
+struct coe_runtime;
+static bool vmm_unmap(coe_runtime *rt, int32_t slot);
+
 struct StepBuffers {  // device arrays one step uses; two sets alternate
   int32_t *adm = nullptr;   // [6][max_adm]: exec, rank, req, stage, in route, out route
   int32_t *batch = nullptr; // [2][max_batches]: exec, size
@@ -225,14 +268,29 @@ struct coe_runtime {
   // its own slab of sbytes[k]-sized slots; act_ld = widest d (activation row stride)
   int S = 1;
   std::vector<int32_t> sd, sh, slot_base, slot_count, slot_shape, expert_shape;
-  std::vector<int64_t> sbytes, store_off;
+  std::vector<int64_t> sbytes, sstride, store_off;
   std::vector<char *> slabs;
   int32_t act_ld = 0, h_max = 0, total_slots = 0;
   int64_t row_elems = 0;  // T * act_ld
+  // Expert memory under ONE byte budget for several shapes (cfg.expert_pool_bytes > 0): every
+  // expert owns a static virtual slot in its shape's reserved range, and a load maps pages of
+  // a shared physical pool into it (CUDA VMM) -- the planner's byte-budgeted pool
+  // (expert_pool.py:27-59) then bounds physical HBM exactly, whatever the shape mix.  Freed
+  // pages remember the slot that last used them: a later copy into them waits for that slot's
+  // readers, and a slot's stale mapping is unmapped only after its own readers have finished.
+  bool vmm = false;
+  int64_t page = 0, pool_pages = 0;
+  CUmemGenericAllocationHandle pool_handle = 0;
+  std::vector<int64_t> va_size;          // per shape: reserved bytes
+  std::deque<int32_t> free_pages;        // FIFO, persists across steps
+  std::vector<int32_t> page_owner;       // slot that last used the page (-1: never)
+  std::vector<std::vector<int32_t>> slot_pages;  // pages mapped (or stale) behind each slot
+  std::vector<uint8_t> slot_mapped;
+  std::vector<int32_t> expert_vslot;     // expert -> its static slot
 
   char *slot_ptr(int32_t s) const {
     const int k = slot_shape[s];
-    return slabs[k] + (int64_t)(s - slot_base[k]) * sbytes[k];
+    return slabs[k] + (int64_t)(s - slot_base[k]) * sstride[k];
   }
   // wave classes, one stream each: 0 main (experts resident since step start; also runs K1/K2
   // and the step join), 1 release (last readers of slots a later swap-in overwrites: high
@@ -324,7 +382,15 @@ struct coe_runtime {
         if (m) coe_mlp_destroy(m);
     std::vector<void *> dev = {x, y, act, hbuf[0], hbuf[1], hbuf[2], outbuf, d_perm, d_keys, d_flags, d_last,
                                d_sort_scratch, d_compact_scratch};
-    for (char *sl : slabs) dev.push_back(sl);
+    if (vmm) {
+      for (int32_t q = 0; q < (int32_t)slot_mapped.size(); ++q)
+        if (slot_mapped[q]) vmm_unmap(this, q);
+      for (int k = 0; k < S; ++k)
+        if (slabs[k]) vmm_api().address_free(reinterpret_cast<CUdeviceptr>(slabs[k]), (size_t)va_size[k]);
+      if (pool_handle) vmm_api().release(pool_handle);
+    } else {
+      for (char *sl : slabs) dev.push_back(sl);
+    }
     for (auto &s : sets) {
       for (void *p : {(void *)s.adm, (void *)s.batch, (void *)s.boff, (void *)s.mreq, (void *)s.mstage,
                       (void *)s.min, (void *)s.mout, (void *)s.groups})
@@ -379,6 +445,92 @@ bool dmalloc(T **p, size_t bytes, const char *what) {
 }
 
 int fail_cuda() { return COE_CUDA_ERR_CUDA; }
+
+constexpr int64_t kVmmPage = 8ll << 20;  // physical page of the expert pool (a multiple of the 2 MB granularity)
+
+// Reserve one virtual range per shape (a static slot per expert of that shape, stride rounded
+// up to whole pages) and one physical pool of pool_bytes; nothing is mapped yet.
+bool vmm_create(coe_runtime *rt, int64_t pool_bytes) {
+  const VmmApi &api = vmm_api();
+  if (!api.ok) {
+    coe_set_error("CUDA VMM entry points unavailable");
+    return false;
+  }
+  int dev = 0;
+  cudaGetDevice(&dev);
+  CUmemAllocationProp prop{};
+  prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  prop.location.id = dev;
+  size_t gran = 0;
+  if (!cu_ok(api.granularity(&gran, &prop, CU_MEM_ALLOC_GRANULARITY_MINIMUM), "cuMemGetAllocationGranularity"))
+    return false;
+  rt->page = ((kVmmPage + (int64_t)gran - 1) / (int64_t)gran) * (int64_t)gran;
+  rt->pool_pages = (pool_bytes + rt->page - 1) / rt->page;
+  if (!cu_ok(api.create(&rt->pool_handle, (size_t)(rt->pool_pages * rt->page), &prop, 0), "cuMemCreate (expert pool)"))
+    return false;
+  rt->va_size.assign(rt->S, 0);
+  for (int k = 0; k < rt->S; ++k) {
+    rt->sstride[k] = (rt->sbytes[k] + rt->page - 1) / rt->page * rt->page;
+    rt->va_size[k] = rt->sstride[k] * std::max(1, rt->slot_count[k]) + rt->page;
+    CUdeviceptr va = 0;
+    if (!cu_ok(api.address_reserve(&va, (size_t)rt->va_size[k], (size_t)rt->page, 0, 0), "cuMemAddressReserve"))
+      return false;
+    rt->slabs[k] = reinterpret_cast<char *>(va);
+  }
+  rt->vmm = true;
+  rt->page_owner.assign(rt->pool_pages, -1);
+  for (int64_t p = 0; p < rt->pool_pages; ++p) rt->free_pages.push_back((int32_t)p);
+  rt->slot_pages.assign(rt->total_slots, {});
+  rt->slot_mapped.assign(rt->total_slots, 0);
+  // static slot of each expert: its rank among the experts of its shape
+  rt->expert_vslot.assign(rt->cfg.num_experts, -1);
+  std::vector<int32_t> next(rt->S, 0);
+  for (int32_t e = 0; e < rt->cfg.num_experts; ++e) {
+    const int k = rt->expert_shape[e];
+    if (next[k] >= rt->slot_count[k]) {
+      coe_set_error("VMM expert memory: more experts of a shape than its slots");
+      return false;
+    }
+    rt->expert_vslot[e] = rt->slot_base[k] + next[k]++;
+  }
+  return true;
+}
+
+// Map the slot's pages (consecutive pages as one mapping) and enable device access.
+bool vmm_map(coe_runtime *rt, int32_t slot) {
+  const VmmApi &api = vmm_api();
+  const auto &pages = rt->slot_pages[slot];
+  const CUdeviceptr base = reinterpret_cast<CUdeviceptr>(rt->slot_ptr(slot));
+  for (size_t i = 0; i < pages.size();) {
+    size_t j = i + 1;
+    while (j < pages.size() && pages[j] == pages[j - 1] + 1) ++j;
+    if (!cu_ok(api.map(base + (CUdeviceptr)(i * rt->page), (size_t)((j - i) * rt->page), (size_t)pages[i] * rt->page,
+                       rt->pool_handle, 0),
+               "cuMemMap"))
+      return false;
+    i = j;
+  }
+  int dev = 0;
+  cudaGetDevice(&dev);
+  CUmemAccessDesc acc{};
+  acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  acc.location.id = dev;
+  acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  if (!cu_ok(api.set_access(base, (size_t)(pages.size() * rt->page), &acc, 1), "cuMemSetAccess")) return false;
+  rt->slot_mapped[slot] = 1;
+  return true;
+}
+
+}  // namespace
+static bool vmm_unmap(coe_runtime *rt, int32_t slot) {
+  const CUdeviceptr base = reinterpret_cast<CUdeviceptr>(rt->slot_ptr(slot));
+  if (!cu_ok(vmm_api().unmap(base, (size_t)(rt->slot_pages[slot].size() * rt->page)), "cuMemUnmap")) return false;
+  rt->slot_mapped[slot] = 0;
+  return true;
+}
+namespace {
+
 
 float elapsed(cudaEvent_t a, cudaEvent_t b) {
   float ms = 0.f;
@@ -523,8 +675,13 @@ int coe_runtime_create(const coe_runtime_config *cfg, coe_runtime **out) {
               ok(cudaMemset(rt->d_hflags, 0, 4 * (A + COE_MAX_PEERS)), "hop flags");
   rt->hflag_step_base = (int64_t)A;
   rt->slabs.assign(rt->S, nullptr);
-  for (int k = 0; k < rt->S; ++k)
-    good = good && dmalloc(&rt->slabs[k], (size_t)rt->sbytes[k] * std::max(1, rt->slot_count[k]), "slab alloc");
+  rt->sstride = rt->sbytes;
+  if (c.expert_pool_bytes > 0) {
+    good = good && vmm_create(rt, c.expert_pool_bytes);
+  } else {
+    for (int k = 0; k < rt->S; ++k)
+      good = good && dmalloc(&rt->slabs[k], (size_t)rt->sbytes[k] * std::max(1, rt->slot_count[k]), "slab alloc");
+  }
   for (auto &s : rt->sets)
     good = good && dmalloc(&s.adm, 24 * A, "adm alloc") && dmalloc(&s.batch, 8 * B, "batch alloc") &&
            dmalloc(&s.boff, 4 * B, "boff alloc") && dmalloc(&s.mreq, 4 * A, "member alloc") &&
@@ -570,7 +727,7 @@ int coe_runtime_create(const coe_runtime_config *cfg, coe_runtime **out) {
       mc.h_rows = c.max_wave_rows;
       mc.slab = rt->slabs[sk];
       mc.num_slots = std::max(1, rt->slot_count[sk]);
-      mc.slot_stride_bytes = rt->sbytes[sk];
+      mc.slot_stride_bytes = rt->sstride[sk];
       for (int k = 0; k < coe_runtime::NCLS && good; ++k) {
         mc.h_scratch = rt->hbuf[k];
         if (coe_mlp_create(&mc, &rt->mlps[sk][k]) != COE_CUDA_OK ||
@@ -642,6 +799,11 @@ int coe_runtime_slot_of(coe_runtime *rt, int32_t expert) {
 int coe_runtime_init_experts(coe_runtime *rt) {
   const auto &c = rt->cfg;
   if (!ok(cudaDeviceSynchronize(), "init experts sync")) return fail_cuda();
+  char *scratch = nullptr;  // VMM: no slot is mapped yet -- generate into a scratch expert
+  if (rt->vmm) {
+    const int64_t big = *std::max_element(rt->sbytes.begin(), rt->sbytes.end());
+    if (!ok(cudaMalloc(&scratch, (size_t)big), "init scratch")) return fail_cuda();
+  }
   for (int32_t e = 0; e < c.num_experts; ++e) {  // generate into the shape's first slot, stage to the store
     if (rt->store_off[e] < 0) continue;
     const int k = rt->expert_shape[e];
@@ -650,17 +812,24 @@ int coe_runtime_init_experts(coe_runtime *rt) {
       return COE_CUDA_ERR_CONFIG;
     }
     const int64_t half = (int64_t)rt->sd[k] * rt->sh[k];  // elements per matrix
-    __nv_bfloat16 *w = reinterpret_cast<__nv_bfloat16 *>(rt->slabs[k]);
+    __nv_bfloat16 *w = reinterpret_cast<__nv_bfloat16 *>(scratch ? scratch : rt->slabs[k]);
     if (coe_fill_uniform_bf16(w, half, coe_expert_seed(c.weight_seed, e, 0), sqrtf(3.0f / rt->sd[k]), rt->compute) ||
         coe_fill_uniform_bf16(w + half, half, coe_expert_seed(c.weight_seed, e, 1), sqrtf(3.0f / rt->sh[k]),
                               rt->compute))
       return COE_CUDA_ERR_CUDA;
-    if (!ok(cudaMemcpyAsync(rt->host_store + rt->store_off[e], rt->slabs[k], rt->sbytes[k], cudaMemcpyDeviceToHost,
-                            rt->compute),
+    if (!ok(cudaMemcpyAsync(rt->host_store + rt->store_off[e], w, rt->sbytes[k], cudaMemcpyDeviceToHost, rt->compute),
             "expert store D2H"))
       return fail_cuda();
   }
   if (!ok(cudaStreamSynchronize(rt->compute), "init experts")) return fail_cuda();
+  if (scratch) cudaFree(scratch);
+  if (rt->vmm) {  // every slot unmapped, every page free
+    for (int32_t q = 0; q < rt->total_slots; ++q)
+      if (rt->slot_mapped[q] && !vmm_unmap(rt, q)) return fail_cuda();
+    rt->free_pages.clear();
+    for (int64_t p = 0; p < rt->pool_pages; ++p) rt->free_pages.push_back((int32_t)p);
+    std::fill(rt->page_owner.begin(), rt->page_owner.end(), -1);
+  }
   std::fill(rt->slot_expert.begin(), rt->slot_expert.end(), -1);
   std::fill(rt->expert_slot.begin(), rt->expert_slot.end(), -1);
   std::fill(rt->slot_free_valid.begin(), rt->slot_free_valid.end(), 0);
@@ -874,6 +1043,10 @@ int coe_runtime_attach_peers(coe_runtime *rt, int32_t rank, int32_t world, const
 int coe_runtime_bench_mlp(coe_runtime *rt, int32_t groups, int32_t requests_per_group, int32_t iters,
                           float *up_ms, float *down_ms) {
   const auto &c = rt->cfg;
+  if (rt->vmm) {
+    coe_set_error("bench_mlp: expert slots are mapped on demand in pooled (VMM) mode");
+    return COE_CUDA_ERR_CONFIG;
+  }
   const int64_t rows = (int64_t)requests_per_group * c.T;
   const int32_t nreq = groups * requests_per_group;
   if (groups < 1 || requests_per_group < 1 || nreq > c.max_requests || rows * groups > c.max_wave_rows ||
@@ -1039,6 +1212,8 @@ struct CopyInfo {
   bool restore;
   std::vector<int32_t> readers;    // batches reading the slot's previous content this step
   bool first_write;                // slot not written earlier this step
+  std::vector<int32_t> deps;       // slots whose readers must finish first (VMM: the pages' last users)
+  std::vector<int32_t> pages;      // VMM: pool pages this copy maps
   double up_end = 0.0, end = 0.0;  // estimated
   bool issued = false;
   int64_t op_pos = 0;              // op-log position of the LOAD (restores: of the first batch)
@@ -1170,13 +1345,40 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
   std::vector<std::vector<int32_t>> slot_readers(NS);
   std::vector<uint8_t> slot_written(NS, 0);
   for (int32_t i = 0; i < in->num_initial; ++i) plan_res[in->initial[i]] = 1;
+  // VMM: pages behind each slot this step, and per page the readers (batches, this step) of
+  // the residency that freed it
+  std::vector<std::vector<int32_t>> cur_pages;
+  std::vector<std::shared_ptr<const std::vector<int32_t>>> page_rd;
+  if (rt->vmm) {
+    cur_pages.assign(NS, {});
+    page_rd.assign((size_t)rt->pool_pages, nullptr);
+  }
+  auto vmm_free = [&](int32_t q) {  // the expert in slot q left: its pages return to the pool
+    auto snap = std::make_shared<const std::vector<int32_t>>(slot_readers[q]);
+    for (int32_t pg : cur_pages[q]) {
+      rt->free_pages.push_back(pg);
+      page_rd[pg] = snap;
+    }
+    cur_pages[q].clear();
+  };
   for (int32_t s = 0; s < NS; ++s) {  // slots outside the initial placement are free again
     int32_t e = rt->slot_expert[s];
+    if (rt->vmm && e >= 0) cur_pages[s] = rt->slot_pages[s];
     if (e >= 0 && !plan_res[e]) {
       rt->expert_slot[e] = -1;
       rt->slot_expert[s] = -1;
+      if (rt->vmm) vmm_free(s);
     }
   }
+  if (rt->vmm)  // stale mappings whose readers are done can go now (no host wait later)
+    for (int32_t s = 0; s < NS; ++s) {
+      if (!rt->slot_mapped[s] || rt->slot_expert[s] >= 0) continue;
+      bool done = true;
+      for (int k = 0; k < NCLS && done; ++k)
+        if (rt->slot_free_valid[(size_t)s * NCLS + k])
+          done = cudaEventQuery(rt->slot_free_down[(size_t)s * NCLS + k]) == cudaSuccess;
+      if (done && !vmm_unmap(rt, s)) return fail_cuda();
+    }
   for (int32_t i = 0; i < in->num_initial; ++i)
     if (rt->expert_slot[in->initial[i]] < 0) pending_restore[in->initial[i]] = 1;
 
@@ -1199,16 +1401,41 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     }
     const int k = rt->expert_shape[e];
     int32_t best = -1;  // free slot of the expert's shape whose readers were issued earliest
-    for (int32_t s = rt->slot_base[k]; s < rt->slot_base[k] + rt->slot_count[k]; ++s) {
-      if (rt->slot_expert[s] >= 0) continue;
-      auto age = [&](int32_t q) { return slot_readers[q].empty() ? -1 : slot_readers[q].back(); };
-      if (best < 0 || age(s) < age(best)) best = s;
+    if (rt->vmm) {
+      best = rt->expert_vslot[e];  // the expert's own virtual slot
+    } else {
+      for (int32_t s = rt->slot_base[k]; s < rt->slot_base[k] + rt->slot_count[k]; ++s) {
+        if (rt->slot_expert[s] >= 0) continue;
+        auto age = [&](int32_t q) { return slot_readers[q].empty() ? -1 : slot_readers[q].back(); };
+        if (best < 0 || age(s) < age(best)) best = s;
+      }
     }
-    if (best < 0) {
+    if (best < 0 || rt->slot_expert[best] >= 0) {
       coe_set_error("no free HBM expert slot (planner residency exceeds the slot count)");
       return false;
     }
     CopyInfo ci{e, best, restore, slot_readers[best], !slot_written[best]};
+    ci.deps.push_back(best);
+    if (rt->vmm) {  // map free pool pages; wait for the readers of whatever last used them
+      const int64_t n = rt->sstride[k] / rt->page;
+      if ((int64_t)rt->free_pages.size() < n) {
+        coe_set_error("expert pool out of pages (planner residency exceeds the byte budget)");
+        return false;
+      }
+      for (int64_t i = 0; i < n; ++i) {
+        const int32_t pg = rt->free_pages.front();
+        rt->free_pages.pop_front();
+        ci.pages.push_back(pg);
+        const int32_t owner = rt->page_owner[pg];
+        if (owner >= 0 && std::find(ci.deps.begin(), ci.deps.end(), owner) == ci.deps.end()) ci.deps.push_back(owner);
+        if (page_rd[pg])
+          for (int32_t r : *page_rd[pg])
+            if (std::find(ci.readers.begin(), ci.readers.end(), r) == ci.readers.end()) ci.readers.push_back(r);
+        page_rd[pg] = nullptr;
+        rt->page_owner[pg] = best;
+      }
+      cur_pages[best] = ci.pages;
+    }
     ci.op_pos = op_pos;
     copies.push_back(ci);
     slot_readers[best].clear();
@@ -1231,6 +1458,7 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
         if (s >= 0) {
           rt->expert_slot[v] = -1;
           rt->slot_expert[s] = -1;
+          if (rt->vmm) vmm_free(s);
         }
       }
       plan_res[op.expert] = 1;
@@ -1238,6 +1466,7 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
         int32_t s = rt->expert_slot[op.expert];
         rt->slot_expert[s] = -1;
         rt->expert_slot[op.expert] = -1;
+        if (rt->vmm) vmm_free(s);
       }
       if (!issue_copy(op.expert, false, my_ops[k])) return COE_CUDA_ERR_CHECK;
       continue;
@@ -1625,12 +1854,20 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
         ca.expert = ci.expert;
         ca.slot = ci.slot;
         ca.restore = ci.restore;
-        for (int k = 0; k < NCLS; ++k) {
-          const int32_t wv = last_reader_wave[ci.slot * NCLS + k];
-          if (wv >= 0) ca.wait_waves.push_back(wv);
-          else if (!written[ci.slot]) ca.wait_prev[k] = rt->slot_free_valid[(size_t)ci.slot * NCLS + k] != 0;
-          last_reader_wave[ci.slot * NCLS + k] = -1;
-        }
+        ca.pages = ci.pages;
+        for (int32_t q : ci.deps)  // the slot itself, and (VMM) the last users of its pages
+          for (int k = 0; k < NCLS; ++k) {
+            const int32_t wv = last_reader_wave[q * NCLS + k];
+            if (wv >= 0) {
+              if (std::find(ca.wait_waves.begin(), ca.wait_waves.end(), wv) == ca.wait_waves.end())
+                ca.wait_waves.push_back(wv);
+              if (q == ci.slot) ca.own_waves.push_back(wv);
+            } else if (!written[q] && rt->slot_free_valid[(size_t)q * NCLS + k]) {
+              ca.wait_prev.push_back(q * NCLS + k);
+              if (q == ci.slot) ca.own_prev.push_back(q * NCLS + k);
+            }
+          }
+        for (int k = 0; k < NCLS; ++k) last_reader_wave[ci.slot * NCLS + k] = -1;
         written[ci.slot] = 1;
       } else {
         const WaveAct &w = waves[a.index];
@@ -1905,22 +2142,29 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
       char *dst = rt->slot_ptr(cp.slot);
       const char *src = rt->host_store + rt->store_off[cp.expert];
       const int64_t half_bytes = rt->sbytes[rt->slot_shape[cp.slot]] / 2;
+      if (rt->vmm) {  // map the slot's new pages (its stale mapping goes once its readers are done)
+        if (rt->slot_mapped[cp.slot]) {
+          for (int32_t wv : cp.own_waves)
+            if (!ok(cudaEventSynchronize(wave_down_ev[wv]), "unmap waits readers")) return fail_cuda();
+          for (int32_t sk : cp.own_prev)
+            if (!ok(cudaEventSynchronize(rt->slot_free_down[sk]), "unmap waits readers")) return fail_cuda();
+          if (!vmm_unmap(rt, cp.slot)) return fail_cuda();
+        }
+        rt->slot_pages[cp.slot] = cp.pages;
+        if (!vmm_map(rt, cp.slot)) return fail_cuda();
+      }
       for (int32_t wv : cp.wait_waves)
         if (!ok(cudaStreamWaitEvent(ks, wave_up_ev[wv], 0), "copy waits W1 readers")) return fail_cuda();
-      for (int k = 0; k < NCLS; ++k)
-        if (cp.wait_prev[k] &&
-            !ok(cudaStreamWaitEvent(ks, rt->slot_free_up[(size_t)cp.slot * NCLS + k], 0), "copy waits last step"))
-          return fail_cuda();
+      for (int32_t sk : cp.wait_prev)
+        if (!ok(cudaStreamWaitEvent(ks, rt->slot_free_up[sk], 0), "copy waits last step")) return fail_cuda();
       if (c.profile && !ok(cudaEventRecord(rt->t_copy_start[a.index], ks), "record")) return fail_cuda();
       if (!ok(cudaMemcpyAsync(dst, src, half_bytes, cudaMemcpyHostToDevice, ks), "swap-in W1") ||
           !ok(cudaEventRecord(rt->copy_up_ev[a.index], ks), "record"))
         return fail_cuda();
       for (int32_t wv : cp.wait_waves)
         if (!ok(cudaStreamWaitEvent(ks, wave_down_ev[wv], 0), "copy waits W2 readers")) return fail_cuda();
-      for (int k = 0; k < NCLS; ++k)
-        if (cp.wait_prev[k] &&
-            !ok(cudaStreamWaitEvent(ks, rt->slot_free_down[(size_t)cp.slot * NCLS + k], 0), "copy waits last step"))
-          return fail_cuda();
+      for (int32_t sk : cp.wait_prev)
+        if (!ok(cudaStreamWaitEvent(ks, rt->slot_free_down[sk], 0), "copy waits last step")) return fail_cuda();
       if (!ok(cudaMemcpyAsync(dst + half_bytes, src + half_bytes, half_bytes, cudaMemcpyHostToDevice, ks),
               "swap-in W2") ||
           !ok(cudaEventRecord(rt->copy_down_ev[a.index], ks), "record"))

@@ -26,6 +26,7 @@ from ._cuda_sigs import check as _check
 
 DEFAULT_WEIGHT_SEED = 0xC0E5E4E
 DEFAULT_INPUT_SEED = 0x1A7E5
+VMM_PAGE = 8 << 20  # physical page of the pooled expert memory (runtime.cu kVmmPage)
 
 
 class StepInput(ctypes.Structure):
@@ -76,7 +77,7 @@ class RuntimeConfig(ctypes.Structure):
                 ("num_shapes", ctypes.c_int32), ("shape_d", ctypes.c_void_p), ("shape_h", ctypes.c_void_p),
                 ("shape_slots", ctypes.c_void_p), ("expert_shape", ctypes.c_void_p), ("store_mask", ctypes.c_void_p),
                 ("ring_slots", ctypes.c_int32), ("landing_slots", ctypes.c_int32), ("out_slots", ctypes.c_int32),
-                ("device_io", ctypes.c_int32)]
+                ("device_io", ctypes.c_int32), ("expert_pool_bytes", ctypes.c_int64)]
 
 
 _declared = False
@@ -195,7 +196,7 @@ class B200Runtime:
                  store_path: str | None = None, wave_rows_cap: int | None = None,
                  urgent_rows_cap: int | None = 8192, expert_shape=None, store_mask=None,
                  ring_slots: int | None = None, landing_slots: int = 0, out_slots: int = 0,
-                 device_io: bool = True):
+                 device_io: bool = True, expert_pool_bytes: int = 0):
         """``shape``: one ``RuntimeShape`` or a list (heterogeneous experts, ``expert_shape``
         maps each expert to its index); ``num_slots``: HBM slots (per shape for a list).
         ``ring_slots`` / ``landing_slots``: activation rows (``plan_rows``; default: one ring
@@ -235,7 +236,8 @@ class B200Runtime:
                             len(shapes), k["d"].ctypes.data, k["h"].ctypes.data, k["slots"].ctypes.data,
                             k["es"].ctypes.data, None if k["mask"] is None else k["mask"].ctypes.data,
                             int(ring_slots if ring_slots is not None else max_requests), int(landing_slots),
-                            int(out_slots), 1 if device_io else 0)
+                            int(out_slots), 1 if device_io else 0, int(expert_pool_bytes))
+        self.expert_pool_bytes = int(expert_pool_bytes)
         self.ring_slots = cfg.ring_slots
         self.landing_slots = cfg.landing_slots
         self.device_io = device_io
@@ -256,7 +258,8 @@ class B200Runtime:
         act = {"ring": self.ring_slots * row, "landing": self.landing_slots * row,
                "h_scratch": 3 * self.max_wave_rows * max(s.h for s in self.shapes) * 2,
                "out_staging": self.out_slots * row}
-        slots = sum(n * s.expert_bytes for n, s in zip(self._keep["slots"].tolist(), self.shapes))
+        slots = self.expert_pool_bytes or sum(n * s.expert_bytes
+                                              for n, s in zip(self._keep["slots"].tolist(), self.shapes))
         return {"expert_slots": int(slots), "activations": act, "activations_total": int(sum(act.values())),
                 "device_io_xy": (2 * self.max_requests * row) if self.device_io else 0,
                 "ring_slots": self.ring_slots, "landing_rows": self.landing_slots}
@@ -309,23 +312,46 @@ class B200Runtime:
         # slots per shape = that shape's peak concurrent residency in this executor's op log
         # (initial placement, then each LOAD's victims out and its expert in): exactly what the
         # planner's byte-budgeted pool (expert_pool.py:27-59) holds at once, shape by shape
+        # An initially resident expert only takes HBM once materialised: the runtime restores it
+        # at its first batch (an expert this executor never runs needs no slot)
         cur = np.zeros(len(shapes), np.int64)
-        for e in plan.initial_residency()[executor]:
-            cur[expert_shape[int(e)]] += 1
         peak = cur.copy()
+        pending = {int(e) for e in plan.initial_residency()[executor]}
+        live = set()
         args = plan.op_args()
         for op in plan.ops():
-            if op["executor"] != executor or op["kind"] != _native.OP_LOAD:
+            if op["executor"] != executor:
                 continue
-            o = int(op["offset"])
-            for v in args[o:o + int(op["count"])]:
-                cur[expert_shape[int(v)]] -= 1
-            k = expert_shape[int(op["expert"])]
-            cur[k] += 1
-            peak[k] = max(peak[k], cur[k])
-        slots = [max(1, int(p)) for p in peak]
+            e = int(op["expert"])
+            if op["kind"] == _native.OP_LOAD:
+                o = int(op["offset"])
+                for v in args[o:o + int(op["count"])]:
+                    v = int(v)
+                    pending.discard(v)
+                    if v in live:
+                        live.discard(v)
+                        cur[expert_shape[v]] -= 1
+                pending.discard(e)
+            elif e not in pending:
+                continue
+            else:
+                pending.discard(e)
+            if e not in live:
+                live.add(e)
+                k = expert_shape[e]
+                cur[k] += 1
+                peak[k] = max(peak[k], cur[k])
         if not kw.get("store_path"):
             kw.setdefault("store_mask", touched)
+        if kw.pop("pooled", True):
+            # one physical pool for every shape (CUDA VMM): each expert a static virtual slot,
+            # physical bytes = the planner's budget (capped by what this executor can hold at
+            # once) plus < 8 MB page rounding per resident expert
+            counts = [int((expert_shape == i).sum()) for i in range(len(shapes))]
+            held = sum(int(p) * s.expert_bytes for p, s in zip(peak, shapes))
+            kw.setdefault("expert_pool_bytes", int(min(budget, held)) + int(peak.sum()) * VMM_PAGE)
+            return cls(shapes, len(ids), counts, len(resolved.request_ids), adm, expert_shape=expert_shape, **kw)
+        slots = [max(1, int(p)) for p in peak]  # per-shape slabs of each shape's peak residency
         return cls(shapes, len(ids), slots, len(resolved.request_ids), adm, expert_shape=expert_shape, **kw)
 
     def close(self) -> None:

@@ -210,3 +210,41 @@ def test_c1_10k_end_to_end_ring_reuse(out_slots):
         assert sorted(order.tolist()) == list(range(n))
         assert torch.equal(h.view(n, shape.T, shape.d), ref[torch.from_numpy(order).long()])
     rt.close()
+
+
+def test_c5_pooled_budget_swaps_across_shapes():
+    """Heterogeneous experts under ONE byte budget (CUDA VMM pool): config 5's 11 shapes with the
+    reference's alloc_override = the 24 most-used experts' bytes, so loads evict experts of
+    other shapes and reuse their physical pages.  The pool is the planner's budget (+ page
+    rounding), far below the touched experts' bytes; grouping is exact, the step moves exactly
+    the planned loads, two steps give identical outputs and every request matches its fp32
+    chain."""
+    w = _subset(configs.load("c5", 1000), range(24))
+    cfg = configs.run_config(w, trace=False, alloc_override={"gpu": 24}, search_enabled=False)
+    plan = engine.plan(cfg)
+    reg, ids = plan.resolved.config.registry, plan.resolved.expert_ids
+    loads = [o for o in plan.ops() if o["kind"] == 0]
+    assert len(loads) >= 10
+    used = {e for c in plan.resolved.chains for e in c}
+    budget = plan.resolved.executors[0][1]
+    rt = runtime.B200Runtime.for_plan(plan, w.shapes)
+    assert 0 < rt.expert_pool_bytes <= budget + len(used) * runtime.VMM_PAGE
+    assert rt.expert_pool_bytes < sum(reg.experts[ids[e]].param_bytes for e in used)
+    n = len(plan.resolved.request_ids)
+    rt.fill_inputs(n)
+    shape_of = lambda e: tuple(w.shapes[reg.experts[ids[e]].arch][:2])  # noqa: E731
+    T = rt.shapes[0].T
+    outs = []
+    for _ in range(2):
+        stats = rt.step(plan)
+        rt.synchronize()
+        _grouping_equal(plan, rt, stats)
+        assert stats["loads"] == len(loads)
+        outs.append(rt.download_requests(list(range(n)), [len(c) - 1 for c in plan.resolved.chains]))
+    assert np.array_equal(outs[0], outs[1])
+    errs = selfcheck.check_requests(rt, plan, range(n), shape_of, T,
+                                    ref=selfcheck.ChainReference(shape_of, cache_bytes=48 << 30))
+    rt.close()
+    worst = max(errs.values())
+    print(f"C5 pooled: {len(loads)} loads, pool {budget / 1e9:.1f} GB budget, worst rel-L2 {worst:.3e}")
+    assert worst <= CHAIN_TOL, {r: e for r, e in errs.items() if e > CHAIN_TOL}
