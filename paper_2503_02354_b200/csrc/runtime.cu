@@ -280,7 +280,7 @@ struct coe_runtime {
   // readers, and a slot's stale mapping is unmapped only after its own readers have finished.
   bool vmm = false;
   int64_t page = 0, pool_pages = 0;
-  CUmemGenericAllocationHandle pool_handle = 0;
+  std::vector<CUmemGenericAllocationHandle> pool_handles;  // one physical allocation per page
   std::vector<int64_t> va_size;          // per shape: reserved bytes
   std::deque<int32_t> free_pages;        // FIFO, persists across steps
   std::vector<int32_t> page_owner;       // slot that last used the page (-1: never)
@@ -387,7 +387,7 @@ struct coe_runtime {
         if (slot_mapped[q]) vmm_unmap(this, q);
       for (int k = 0; k < S; ++k)
         if (slabs[k]) vmm_api().address_free(reinterpret_cast<CUdeviceptr>(slabs[k]), (size_t)va_size[k]);
-      if (pool_handle) vmm_api().release(pool_handle);
+      for (auto h : pool_handles) vmm_api().release(h);
     } else {
       for (char *sl : slabs) dev.push_back(sl);
     }
@@ -467,8 +467,13 @@ bool vmm_create(coe_runtime *rt, int64_t pool_bytes) {
     return false;
   rt->page = ((kVmmPage + (int64_t)gran - 1) / (int64_t)gran) * (int64_t)gran;
   rt->pool_pages = (pool_bytes + rt->page - 1) / rt->page;
-  if (!cu_ok(api.create(&rt->pool_handle, (size_t)(rt->pool_pages * rt->page), &prop, 0), "cuMemCreate (expert pool)"))
-    return false;
+  // cuMemMap maps whole allocations (offset 0), so every page is its own physical allocation
+  rt->pool_handles.reserve((size_t)rt->pool_pages);
+  for (int64_t p = 0; p < rt->pool_pages; ++p) {
+    CUmemGenericAllocationHandle h = 0;
+    if (!cu_ok(api.create(&h, (size_t)rt->page, &prop, 0), "cuMemCreate (expert pool page)")) return false;
+    rt->pool_handles.push_back(h);
+  }
   rt->va_size.assign(rt->S, 0);
   for (int k = 0; k < rt->S; ++k) {
     rt->sstride[k] = (rt->sbytes[k] + rt->page - 1) / rt->page * rt->page;
@@ -502,15 +507,10 @@ bool vmm_map(coe_runtime *rt, int32_t slot) {
   const VmmApi &api = vmm_api();
   const auto &pages = rt->slot_pages[slot];
   const CUdeviceptr base = reinterpret_cast<CUdeviceptr>(rt->slot_ptr(slot));
-  for (size_t i = 0; i < pages.size();) {
-    size_t j = i + 1;
-    while (j < pages.size() && pages[j] == pages[j - 1] + 1) ++j;
-    if (!cu_ok(api.map(base + (CUdeviceptr)(i * rt->page), (size_t)((j - i) * rt->page), (size_t)pages[i] * rt->page,
-                       rt->pool_handle, 0),
+  for (size_t i = 0; i < pages.size(); ++i)
+    if (!cu_ok(api.map(base + (CUdeviceptr)(i * rt->page), (size_t)rt->page, 0, rt->pool_handles[pages[i]], 0),
                "cuMemMap"))
       return false;
-    i = j;
-  }
   int dev = 0;
   cudaGetDevice(&dev);
   CUmemAccessDesc acc{};
@@ -525,7 +525,8 @@ bool vmm_map(coe_runtime *rt, int32_t slot) {
 }  // namespace
 static bool vmm_unmap(coe_runtime *rt, int32_t slot) {
   const CUdeviceptr base = reinterpret_cast<CUdeviceptr>(rt->slot_ptr(slot));
-  if (!cu_ok(vmm_api().unmap(base, (size_t)(rt->slot_pages[slot].size() * rt->page)), "cuMemUnmap")) return false;
+  for (size_t i = 0; i < rt->slot_pages[slot].size(); ++i)
+    if (!cu_ok(vmm_api().unmap(base + (CUdeviceptr)(i * rt->page), (size_t)rt->page), "cuMemUnmap")) return false;
   rt->slot_mapped[slot] = 0;
   return true;
 }
