@@ -387,7 +387,10 @@ def main() -> None:
     max_batch = max(e.max_batch for e in plan0.resolved.perf.entries.values())
     k3_shape = shape if isinstance(shape, runtime.RuntimeShape) else rt.shapes[0]
     groups = max(1, min(16, (32768 // k3_shape.T) // max_batch, n_req // max_batch))
-    up_ms, down_ms = rt.bench_mlp(groups, max_batch, iters=10)
+    if rt.expert_pool_bytes:  # pooled (VMM) experts: slots are mapped on demand, no isolated wave
+        up_ms = down_ms = None
+    else:
+        up_ms, down_ms = rt.bench_mlp(groups, max_batch, iters=10)
     wave_flops = 4.0 * groups * max_batch * k3_shape.T * k3_shape.d * k3_shape.h
 
     # a serving loop plans the next step's requests on a host thread while the current step
@@ -501,7 +504,7 @@ def main() -> None:
     assert abs(flops - timing["k3_flops"]) <= 1e-6 * max(flops, 1.0), (flops, timing["k3_flops"])
     burst = float(peaks.get("bf16_tflops"))
     sustained = float(peaks.get("bf16_tflops_sustained", burst))
-    isolated = wave_flops / ((up_ms + down_ms) / 1e3) / 1e12
+    isolated = wave_flops / ((up_ms + down_ms) / 1e3) / 1e12 if up_ms else None
     # headline: K3 inside the timed serving step -- the step's algorithmic FLOPs over the union of
     # its K3 launch intervals (CUDA events on the launching streams), against the sustained peak
     achieved = flops / (timing["k3_busy_ms"] / 1e3) / 1e12 if timing["k3_busy_ms"] > 0 else None
@@ -558,7 +561,7 @@ def main() -> None:
                                        "k3_busy_ms_per_step": timing["k3_busy_ms"],
                                        "avg_launch_ms": timing["k3_busy_ms"] / max(1, timing["k3_launches"]),
                                        "wave_busy_ms_incl_w2_waits": timing["compute_busy_ms"]},
-                     "isolated_wave": {"batches": groups, "requests_per_batch": max_batch,
+                     "isolated_wave": None if isolated is None else {"batches": groups, "requests_per_batch": max_batch,
                                        "rows": groups * max_batch * k3_shape.T,
                                        "shape": {"d": k3_shape.d, "h": k3_shape.h, "T": k3_shape.T},
                                        "up_ms": up_ms, "down_ms": down_ms, "flops": wave_flops,

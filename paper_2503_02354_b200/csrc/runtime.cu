@@ -1396,7 +1396,9 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     if (adm[i].request >= 0 && adm[i].request < c.max_requests)
       final_stage[adm[i].request] = std::max(final_stage[adm[i].request], adm[i].stage);
   auto issue_copy = [&](int32_t e, bool restore, int64_t op_pos) -> bool {
-    if (rt->store_off[e] < 0) {
+    // an initially resident expert outside the host store (never loaded, never evicted by the
+    // plan) is materialised on the device the first time it is used instead of restored
+    if (rt->store_off[e] < 0 && !restore) {
       coe_set_error("swap-in of an expert that is not in the host store");
       return false;
     }
@@ -1445,7 +1447,7 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     rt->expert_slot[e] = best;
     slot_copy[best] = (int32_t)copies.size() - 1;
     (restore ? st.restores : st.loads) += 1;
-    (restore ? st.restore_bytes : st.load_bytes) += rt->sbytes[k];
+    if (rt->store_off[e] >= 0) (restore ? st.restore_bytes : st.load_bytes) += rt->sbytes[k];  // else: generated
     return true;
   };
   for (size_t k = 0; k < my_ops.size(); ++k) {
@@ -2141,8 +2143,10 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     if (a.is_copy) {
       const CopyAct &cp = copy_acts[a.index];
       char *dst = rt->slot_ptr(cp.slot);
-      const char *src = rt->host_store + rt->store_off[cp.expert];
+      const bool generate = rt->store_off[cp.expert] < 0;
+      const char *src = generate ? nullptr : rt->host_store + rt->store_off[cp.expert];
       const int64_t half_bytes = rt->sbytes[rt->slot_shape[cp.slot]] / 2;
+      const int ksh = rt->slot_shape[cp.slot];
       if (rt->vmm) {  // map the slot's new pages (its stale mapping goes once its readers are done)
         if (rt->slot_mapped[cp.slot]) {
           for (int32_t wv : cp.own_waves)
@@ -2159,17 +2163,27 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
       for (int32_t sk : cp.wait_prev)
         if (!ok(cudaStreamWaitEvent(ks, rt->slot_free_up[sk], 0), "copy waits last step")) return fail_cuda();
       if (c.profile && !ok(cudaEventRecord(rt->t_copy_start[a.index], ks), "record")) return fail_cuda();
-      if (!ok(cudaMemcpyAsync(dst, src, half_bytes, cudaMemcpyHostToDevice, ks), "swap-in W1") ||
-          !ok(cudaEventRecord(rt->copy_up_ev[a.index], ks), "record"))
+      if (generate) {
+        if (coe_fill_uniform_bf16(dst, half_bytes / 2, coe_expert_seed(c.weight_seed, cp.expert, 0),
+                                  sqrtf(3.0f / rt->sd[ksh]), ks))
+          return COE_CUDA_ERR_CUDA;
+      } else if (!ok(cudaMemcpyAsync(dst, src, half_bytes, cudaMemcpyHostToDevice, ks), "swap-in W1")) {
         return fail_cuda();
+      }
+      if (!ok(cudaEventRecord(rt->copy_up_ev[a.index], ks), "record")) return fail_cuda();
       for (int32_t wv : cp.wait_waves)
         if (!ok(cudaStreamWaitEvent(ks, wave_down_ev[wv], 0), "copy waits W2 readers")) return fail_cuda();
       for (int32_t sk : cp.wait_prev)
         if (!ok(cudaStreamWaitEvent(ks, rt->slot_free_down[sk], 0), "copy waits last step")) return fail_cuda();
-      if (!ok(cudaMemcpyAsync(dst + half_bytes, src + half_bytes, half_bytes, cudaMemcpyHostToDevice, ks),
-              "swap-in W2") ||
-          !ok(cudaEventRecord(rt->copy_down_ev[a.index], ks), "record"))
+      if (generate) {
+        if (coe_fill_uniform_bf16(dst + half_bytes, half_bytes / 2, coe_expert_seed(c.weight_seed, cp.expert, 1),
+                                  sqrtf(3.0f / rt->sh[ksh]), ks))
+          return COE_CUDA_ERR_CUDA;
+      } else if (!ok(cudaMemcpyAsync(dst + half_bytes, src + half_bytes, half_bytes, cudaMemcpyHostToDevice, ks),
+                     "swap-in W2")) {
         return fail_cuda();
+      }
+      if (!ok(cudaEventRecord(rt->copy_down_ev[a.index], ks), "record")) return fail_cuda();
       if (c.profile && !ok(cudaEventRecord(rt->t_copy_end[a.index], ks), "record")) return fail_cuda();
       continue;
     }

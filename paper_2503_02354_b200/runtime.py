@@ -280,9 +280,17 @@ class B200Runtime:
         registry = resolved.config.registry
         ids = resolved.expert_ids
         touched = np.zeros(len(ids), np.uint8)
+        stored = np.zeros(len(ids), np.uint8)  # the host tier: every expert a LOAD moves or evicts
+        op_args = plan.op_args()
         for op in plan.ops():
             if op["executor"] == executor:
                 touched[int(op["expert"])] = 1
+                if op["kind"] == _native.OP_LOAD:
+                    stored[int(op["expert"])] = 1
+                    o = int(op["offset"])
+                    stored[op_args[o:o + int(op["count"])]] = 1
+        # (an initially resident expert the plan never evicts is generated on the device the
+        # first time it runs; it never crosses PCIe, so it needs no host copy)
         adm = sum(len(c) for c in resolved.chains)
         # activation rows: the ring's peak for this executor's op log, e2e included (stage-0
         # inputs occupy slots too); with several executors also the NCCL transport's needs
@@ -295,7 +303,7 @@ class B200Runtime:
             largest = max(spec.param_bytes for spec in registry.experts.values())
             slots = max(1, min(int(budget // largest), int(touched.sum()) or 1))
             if not kw.get("store_path"):  # a shared store must hold every expert at fixed offsets
-                kw.setdefault("store_mask", touched)
+                kw.setdefault("store_mask", stored)
             return cls(shape, len(ids), slots, len(resolved.request_ids), adm, **kw)
         arch_shapes = shape
         width = {e: arch_shapes[registry.experts[eid].arch][0] for e, eid in enumerate(ids)}
@@ -342,7 +350,7 @@ class B200Runtime:
                 cur[k] += 1
                 peak[k] = max(peak[k], cur[k])
         if not kw.get("store_path"):
-            kw.setdefault("store_mask", touched)
+            kw.setdefault("store_mask", stored)
         if kw.pop("pooled", True):
             # one physical pool for every shape (CUDA VMM): each expert a static virtual slot,
             # physical bytes = the planner's budget (capped by what this executor can hold at
