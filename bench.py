@@ -423,10 +423,7 @@ def main() -> None:
         for _ in range(args.steps):
             p = take_plan()
             stats = rt.step(p, rank)
-            # + K1 (counting read + one kernel per 8-bit pass) + K2 (gather, two batch-scan
-            # kernels past 1,024 batches, batch offsets)
-            launches += (stats["launches"] + 1 + (stats["rank_bits"] + 7) // 8
-                         + 2 + (2 if stats["batches"] > 1024 else 0))
+            launches += stats["launches"]  # K1/K2 (one fused launch at serving size) + 2 K3 per wave
             keep.append(p)
         end.record(stream)
         rt.synchronize()

@@ -67,6 +67,21 @@ int coe_run_compact_routes(const int32_t *perm, const int32_t *sorted_keys, cons
                            int32_t *out_member_stage, int32_t *out_member_in, int32_t *out_member_out,
                            int32_t *out_run_count, int32_t *out_violations, void *scratch, cudaStream_t stream);
 
+/* K1 + K2 of ONE executor in one launch (serving size): one 1,024-thread block sorts the
+ * keys (run_rank << idx_bits | admission) in shared memory -- the stable sort by run-rank --
+ * then gathers members (and their row routes, adm_in / adm_out may be NULL), scans the batch
+ * sizes into offsets and checks that no batch straddles two runs: out_flags[0] = runs,
+ * out_flags[1] = violations, like coe_run_compact.  COE_CUDA_ERR_CONFIG (no launch) when
+ * n > COE_FUSED_MAX_ADMISSIONS, num_batches > COE_FUSED_MAX_BATCHES or the key needs more
+ * than 32 bits; callers then use coe_group_sort + coe_run_compact. */
+#define COE_FUSED_MAX_ADMISSIONS 32768
+#define COE_FUSED_MAX_BATCHES 4096
+int coe_group_compact_fused(const int32_t *run_rank, const int32_t *adm_request, const int32_t *adm_stage,
+                            const int32_t *adm_in, const int32_t *adm_out, int64_t n, int rank_bits,
+                            const int32_t *batch_size, int num_batches, int32_t *out_perm, int32_t *out_batch_off,
+                            int32_t *out_member_req, int32_t *out_member_stage, int32_t *out_member_in,
+                            int32_t *out_member_out, int32_t *out_flags, cudaStream_t stream);
+
 /* ---------------- K3: grouped expert MLP (tcgen05) ------------------------ */
 
 typedef struct coe_mlp_config {

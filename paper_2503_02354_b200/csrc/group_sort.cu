@@ -25,6 +25,9 @@
 #include <string>
 
 #include <cuda_bf16.h>
+#include <cub/block/block_radix_sort.cuh>
+#include <cub/block/block_reduce.cuh>
+#include <cub/block/block_scan.cuh>
 
 #include "coe_cuda.h"
 #include "common.cuh"
@@ -348,6 +351,109 @@ __global__ void __launch_bounds__(BATCH_THREADS) compact_batches(const int32_t *
   }
 }
 
+// K1 + K2 fused for one executor's step at serving size (<= 32,768 admissions, <= 4,096
+// batches): ONE block of 1,024 threads sorts (run_rank << idx_bits | admission) -- unique keys,
+// so the order is the stable sort by run-rank -- in shared memory, gathers the members and
+// their row routes, scans the batch sizes into offsets and checks the one-run-per-batch
+// contract.  One launch instead of the counting pass, the radix passes, three memsets and the
+// compaction kernels, which at this size are pure launch latency.
+constexpr int FUSED_THREADS = 1024;
+constexpr int FUSED_BATCH_IPT = 4;
+
+template <int IPT>
+__global__ void __launch_bounds__(FUSED_THREADS, 1)
+    group_compact_block(const int32_t *run_rank, const int32_t *adm_req, const int32_t *adm_stage,
+                        const int32_t *adm_in, const int32_t *adm_out, int n, int rank_bits, int idx_bits,
+                        const int32_t *batch_size, int num_batches, int32_t *out_perm, int32_t *batch_off,
+                        int32_t *member_req, int32_t *member_stage, int32_t *member_in, int32_t *member_out,
+                        int32_t *flags) {
+  using Sort = cub::BlockRadixSort<uint32_t, FUSED_THREADS, IPT>;
+  using Reduce = cub::BlockReduce<int, FUSED_THREADS>;
+  using Scan = cub::BlockScan<int, FUSED_THREADS>;
+  extern __shared__ __align__(16) uint8_t fused_smem[];
+  __shared__ typename Reduce::TempStorage red;
+  __shared__ typename Scan::TempStorage scan;
+  const int t = threadIdx.x;
+  const uint32_t idx_mask = (1u << idx_bits) - 1u;
+  const uint32_t pad = 1u << (rank_bits + idx_bits);  // sorts after every admission
+  uint32_t keys[IPT];
+#pragma unroll
+  for (int k = 0; k < IPT; ++k) {
+    const int i = t * IPT + k;
+    keys[k] = i < n ? ((uint32_t)run_rank[i] << idx_bits) | (uint32_t)i : pad;
+  }
+  Sort(*reinterpret_cast<typename Sort::TempStorage *>(fused_smem)).Sort(keys, 0, rank_bits + idx_bits + 1);
+  __syncthreads();  // the sort's storage now holds the sorted ranks
+  int32_t *s_rank = reinterpret_cast<int32_t *>(fused_smem);
+#pragma unroll
+  for (int k = 0; k < IPT; ++k) {
+    const int pos = t * IPT + k;
+    if (pos < n) {
+      const int32_t i = (int32_t)(keys[k] & idx_mask);
+      s_rank[pos] = (int32_t)(keys[k] >> idx_bits);
+      out_perm[pos] = i;
+      member_req[pos] = adm_req[i];
+      member_stage[pos] = adm_stage[i];
+      if (adm_in) {
+        member_in[pos] = adm_in[i];
+        member_out[pos] = adm_out[i];
+      }
+    }
+  }
+  __syncthreads();
+  int starts = 0;
+#pragma unroll
+  for (int k = 0; k < IPT; ++k) {
+    const int pos = t * IPT + k;
+    if (pos < n && (pos == 0 || s_rank[pos - 1] != s_rank[pos])) ++starts;
+  }
+  const int runs = Reduce(red).Sum(starts);
+  int sizes[FUSED_BATCH_IPT], offs[FUSED_BATCH_IPT];
+#pragma unroll
+  for (int k = 0; k < FUSED_BATCH_IPT; ++k) {
+    const int b = t * FUSED_BATCH_IPT + k;
+    sizes[k] = b < num_batches ? batch_size[b] : 0;
+  }
+  Scan(scan).ExclusiveSum(sizes, offs);
+  int bad = 0;
+#pragma unroll
+  for (int k = 0; k < FUSED_BATCH_IPT; ++k) {
+    const int b = t * FUSED_BATCH_IPT + k;
+    if (b < num_batches) {
+      batch_off[b] = offs[k];
+      const int lo = offs[k], hi = lo + sizes[k] - 1;
+      bad += (sizes[k] <= 0 || hi >= n || s_rank[lo] != s_rank[hi]) ? 1 : 0;
+    }
+  }
+  __syncthreads();
+  const int violations = Reduce(red).Sum(bad);
+  if (t == 0) {
+    flags[0] = runs;
+    flags[1] = violations;
+  }
+}
+
+template <int IPT>
+bool launch_fused(const int32_t *run_rank, const int32_t *adm_req, const int32_t *adm_stage, const int32_t *adm_in,
+                  const int32_t *adm_out, int n, int rank_bits, int idx_bits, const int32_t *batch_size,
+                  int num_batches, int32_t *out_perm, int32_t *out_batch_off, int32_t *member_req,
+                  int32_t *member_stage, int32_t *member_in, int32_t *member_out, int32_t *flags,
+                  cudaStream_t stream) {
+  using Sort = cub::BlockRadixSort<uint32_t, FUSED_THREADS, IPT>;
+  constexpr size_t smem = sizeof(typename Sort::TempStorage) > (size_t)FUSED_THREADS * IPT * 4
+                              ? sizeof(typename Sort::TempStorage)
+                              : (size_t)FUSED_THREADS * IPT * 4;
+  static const bool configured =
+      cudaFuncSetAttribute(group_compact_block<IPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) ==
+      cudaSuccess;
+  if (!configured) return false;
+  group_compact_block<IPT><<<1, FUSED_THREADS, smem, stream>>>(run_rank, adm_req, adm_stage, adm_in, adm_out, n,
+                                                                rank_bits, idx_bits, batch_size, num_batches, out_perm,
+                                                                out_batch_off, member_req, member_stage, member_in,
+                                                                member_out, flags);
+  return coe_cuda_ok(cudaGetLastError(), "group_compact_block");
+}
+
 // counter-based uniform generator (splitmix64), mirrored in oracle/synth.py
 __device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
@@ -505,6 +611,32 @@ int coe_run_compact_routes(const int32_t *perm, const int32_t *sorted_keys, cons
                                                           rank_bits, out_batch_off, out_violations);
   }
   return check(cudaGetLastError(), "coe_run_compact") ? COE_CUDA_OK : COE_CUDA_ERR_CUDA;
+}
+
+int coe_group_compact_fused(const int32_t *run_rank, const int32_t *adm_request, const int32_t *adm_stage,
+                            const int32_t *adm_in, const int32_t *adm_out, int64_t n, int rank_bits,
+                            const int32_t *batch_size, int num_batches, int32_t *out_perm, int32_t *out_batch_off,
+                            int32_t *out_member_req, int32_t *out_member_stage, int32_t *out_member_in,
+                            int32_t *out_member_out, int32_t *out_flags, cudaStream_t stream) {
+  int idx_bits = 1;
+  while ((1ll << idx_bits) < n) ++idx_bits;
+  if (n < 1 || n > COE_FUSED_MAX_ADMISSIONS || num_batches > COE_FUSED_MAX_BATCHES || rank_bits + idx_bits + 1 > 32) {
+    coe_set_error("coe_group_compact_fused: step too large for one block (use coe_group_sort + coe_run_compact)");
+    return COE_CUDA_ERR_CONFIG;
+  }
+  const int ni = (int)n;
+  bool good = ni <= FUSED_THREADS * 8
+                  ? launch_fused<8>(run_rank, adm_request, adm_stage, adm_in, adm_out, ni, rank_bits, idx_bits,
+                                    batch_size, num_batches, out_perm, out_batch_off, out_member_req,
+                                    out_member_stage, out_member_in, out_member_out, out_flags, stream)
+              : ni <= FUSED_THREADS * 16
+                  ? launch_fused<16>(run_rank, adm_request, adm_stage, adm_in, adm_out, ni, rank_bits, idx_bits,
+                                     batch_size, num_batches, out_perm, out_batch_off, out_member_req,
+                                     out_member_stage, out_member_in, out_member_out, out_flags, stream)
+                  : launch_fused<32>(run_rank, adm_request, adm_stage, adm_in, adm_out, ni, rank_bits, idx_bits,
+                                     batch_size, num_batches, out_perm, out_batch_off, out_member_req,
+                                     out_member_stage, out_member_in, out_member_out, out_flags, stream);
+  return good ? COE_CUDA_OK : COE_CUDA_ERR_CUDA;
 }
 
 int coe_fill_uniform_bf16_at(void *dst, int64_t start, int64_t n, uint64_t seed, float scale, cudaStream_t stream) {

@@ -315,6 +315,7 @@ struct coe_runtime {
   std::deque<OutUse> out_hist;         // e2e: staging rows still being downloaded
   std::vector<cudaEvent_t> out_ev_pool;
   int step_parity = 0;                 // wave events alternate by step (the next step refers back)
+  bool last_group_fused = false;       // the last step grouped with coe_group_compact_fused
   __nv_bfloat16 *hbuf[NCLS] = {nullptr, nullptr, nullptr};
   StepBuffers sets[2];
   int cur_set = 0;
@@ -2018,11 +2019,24 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
       !ok(cudaStreamWaitEvent(cs, rt->staged, 0), "compute waits upload"))
     return fail_cuda();
   int32_t *d_exec = sb.adm, *d_rank = sb.adm + n_adm, *d_req = sb.adm + 2 * n_adm, *d_stage = sb.adm + 3 * n_adm;
-  if (n_adm) {
-    int rc = coe_group_sort(d_exec, d_rank, n_adm, rank_bits, passes, rt->d_perm, rt->d_keys, rt->d_sort_scratch, cs);
+  int idx_bits = 1;
+  while ((1ll << idx_bits) < n_adm) ++idx_bits;
+  const bool fused = n_adm >= 1 && n_adm <= COE_FUSED_MAX_ADMISSIONS && n_batches <= COE_FUSED_MAX_BATCHES &&
+                     rank_bits + idx_bits + 1 <= 32 && !getenv("COE_GROUP_MULTI");
+  rt->last_group_fused = fused;
+  if (fused) {  // serving size: K1 + K2 in one block, one launch
+    int rc = coe_group_compact_fused(d_rank, d_req, d_stage, sb.adm + 4 * n_adm, sb.adm + 5 * n_adm, n_adm, rank_bits,
+                                     sb.batch + n_batches, (int)n_batches, rt->d_perm, sb.boff, sb.mreq, sb.mstage,
+                                     sb.min, sb.mout, rt->d_flags, cs);
     if (rc) return rc;
-  }
-  {
+    st.launches += 1;
+  } else {
+    st.launches += (n_adm ? 1 + passes : 0) + (n_adm ? 1 : 0) + (n_batches > 1024 ? 2 : 0) + (n_batches ? 1 : 0);
+    if (n_adm) {
+      int rc = coe_group_sort(d_exec, d_rank, n_adm, rank_bits, passes, rt->d_perm, rt->d_keys, rt->d_sort_scratch,
+                              cs);
+      if (rc) return rc;
+    }
     int rc = coe_run_compact_routes(rt->d_perm, rt->d_keys, d_req, d_stage, sb.adm + 4 * n_adm, sb.adm + 5 * n_adm,
                                     n_adm, rank_bits, sb.batch, sb.batch + n_batches, (int)n_batches, 1, sb.boff,
                                     sb.mreq, sb.mstage, sb.min, sb.mout, rt->d_flags, rt->d_flags + 1,

@@ -330,3 +330,66 @@ def test_hop_all_to_all_entry_point(lib, world):
     for c in comms:
         lib.coe_comm_destroy(c)
     lib.coe_local_hub_destroy(hub)
+
+
+@pytest.mark.parametrize("n", [1, 7, 1000, 8192, 8193, 13642, 16384, 16385, 32768])
+def test_group_compact_fused_matches_stable_sort(lib, n):
+    """coe_group_compact_fused (K1 + K2 of one executor in one block): the permutation is the
+    stable sort by run-rank, members and routes follow it, batch offsets are the scan of the
+    sizes, runs are counted, and a batch shifted across a run boundary is flagged."""
+    import torch
+
+    lib.coe_group_compact_fused.argtypes = [ctypes.c_void_p] * 5 + [ctypes.c_int64, ctypes.c_int, ctypes.c_void_p,
+                                                                     ctypes.c_int] + [ctypes.c_void_p] * 8
+    lib.coe_group_compact_fused.restype = ctypes.c_int
+    rng = np.random.default_rng(n)
+    _, rank = _run_ranks(rng, n, 1)
+    bits = max(1, int(rank.max()).bit_length())
+    order = np.argsort(rank, kind="stable")
+    runs = np.split(order, np.flatnonzero(np.diff(rank[order])) + 1)
+    sizes = []
+    for run in runs:
+        left = len(run)
+        while left:
+            take = int(min(left, rng.integers(1, 7)))
+            sizes.append(take)
+            left -= take
+    dev = torch.device("cuda")
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.int32)).to(dev)  # noqa: E731
+    req = rng.integers(0, 10**6, n).astype(np.int32)
+    stage = rng.integers(0, 5, n).astype(np.int32)
+    rin = rng.integers(0, 2**30, n).astype(np.int32)
+    rout = rng.integers(0, 2**30, n).astype(np.int32)
+    t = {k: T(v) for k, v in dict(rank=rank, req=req, stage=stage, rin=rin, rout=rout).items()}
+    out = {k: torch.empty(max(1, n), dtype=torch.int32, device=dev) for k in ("perm", "mreq", "mst", "min", "mout")}
+    nb = len(sizes)
+    boff = torch.empty(nb, dtype=torch.int32, device=dev)
+    flags = torch.full((2,), -1, dtype=torch.int32, device=dev)
+
+    def run(sz):
+        t_sz = T(sz)
+        _ck(lib, lib.coe_group_compact_fused(t["rank"].data_ptr(), t["req"].data_ptr(), t["stage"].data_ptr(),
+                                             t["rin"].data_ptr(), t["rout"].data_ptr(), n, bits, t_sz.data_ptr(), nb,
+                                             out["perm"].data_ptr(), boff.data_ptr(), out["mreq"].data_ptr(),
+                                             out["mst"].data_ptr(), out["min"].data_ptr(), out["mout"].data_ptr(),
+                                             flags.data_ptr(), _stream()), "fused")
+        torch.cuda.synchronize()
+        return boff.cpu().numpy(), flags.cpu().numpy()
+
+    off, fl = run(sizes)
+    g = lambda k: out[k].cpu().numpy()[:n]  # noqa: E731
+    assert np.array_equal(g("perm"), order)
+    assert np.array_equal(g("mreq"), req[order]) and np.array_equal(g("mst"), stage[order])
+    assert np.array_equal(g("min"), rin[order]) and np.array_equal(g("mout"), rout[order])
+    assert fl[0] == len(runs) and fl[1] == 0
+    assert off.tolist() == np.concatenate([[0], np.cumsum(sizes)[:-1]]).tolist()
+    if len(runs) > 1:  # move one member of the first run into the next batch's run
+        bad = list(sizes)
+        first_end = next(i for i in range(nb) if sum(sizes[:i + 1]) == len(runs[0]))
+        bad[first_end] += 1
+        bad[first_end + 1] -= 1
+        if bad[first_end + 1] == 0:
+            bad[first_end + 1] = 1
+            bad[-1] -= 1
+        _, fl = run(bad)
+        assert fl[1] >= 1
