@@ -389,7 +389,7 @@ def main() -> None:
     max_batch = max(e.max_batch for e in plan0.resolved.perf.entries.values())
     k3_shape = shape if isinstance(shape, runtime.RuntimeShape) else rt.shapes[0]
     groups = max(1, min(16, (32768 // k3_shape.T) // max_batch, n_req // max_batch))
-    if rt.expert_pool_bytes:  # pooled (VMM) experts: slots are mapped on demand, no isolated wave
+    if rt.expert_pool_bytes:  # pooled experts: placed on demand, no fixed slot for an isolated wave
         up_ms = down_ms = None
     else:
         up_ms, down_ms = rt.bench_mlp(groups, max_batch, iters=10)

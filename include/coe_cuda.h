@@ -182,10 +182,10 @@ typedef struct coe_runtime_config {
   int32_t ring_slots, landing_slots, out_slots;
   int32_t device_io;        /* 1: X / Y of max_requests rows for device-resident steps
                                (fill_inputs, value-mode steps, download_*); 0: e2e only */
-  /* > 0: experts of every shape share ONE physical pool of this many bytes (the planner's
-   * byte budget, rounded to 8 MB pages per expert): each expert owns a static virtual slot
-   * (shape_slots[k] = experts of shape k) and a load maps free pool pages into it (CUDA
-   * VMM).  0: fixed per-shape slabs of shape_slots[k] slots. */
+  /* > 0: experts of every shape share ONE slab of this many bytes (the planner's byte budget
+   * + unit rounding + fragmentation slack), addressed in 2 MB units: a load takes a best-fit
+   * run of free units, an eviction returns it; shape_slots[k] = experts of shape k (one
+   * bookkeeping slot each).  0: fixed per-shape slabs of shape_slots[k] slots. */
   int64_t expert_pool_bytes;
 } coe_runtime_config;
 

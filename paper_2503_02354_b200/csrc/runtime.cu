@@ -39,6 +39,7 @@
 #include <cstring>
 #include <climits>
 #include <deque>
+#include <map>
 #include <memory>
 #include <cstdlib>
 #include <string>
@@ -83,8 +84,7 @@ struct CopyAct {
   bool restore;
   std::vector<int32_t> wait_waves;  // last issued reader wave of the bytes overwritten, per stream (this step)
   std::vector<int32_t> wait_prev;   // slot * NCLS + stream: last step's readers (slot_free events)
-  std::vector<int32_t> own_waves, own_prev;  // VMM: readers of this slot's stale mapping (unmap safety)
-  std::vector<int32_t> pages;       // VMM: pool pages mapped behind the slot
+  int32_t unit0 = -1;               // pooled: first unit of the expert's new place
 };
 
 struct WaveAct {
@@ -212,45 +212,7 @@ bool batched_copy(std::vector<void *> &dsts, std::vector<void *> &srcs, std::vec
 
 void coe_set_error(const std::string &msg) { g_last_error = msg; }
 
-// CUDA VMM driver entry points (resolved once through the runtime, no -lcuda)
-struct VmmApi {
-  CUresult (*create)(CUmemGenericAllocationHandle *, size_t, const CUmemAllocationProp *, unsigned long long) = nullptr;
-  CUresult (*release)(CUmemGenericAllocationHandle) = nullptr;
-  CUresult (*address_reserve)(CUdeviceptr *, size_t, size_t, CUdeviceptr, unsigned long long) = nullptr;
-  CUresult (*address_free)(CUdeviceptr, size_t) = nullptr;
-  CUresult (*map)(CUdeviceptr, size_t, size_t, CUmemGenericAllocationHandle, unsigned long long) = nullptr;
-  CUresult (*unmap)(CUdeviceptr, size_t) = nullptr;
-  CUresult (*set_access)(CUdeviceptr, size_t, const CUmemAccessDesc *, size_t) = nullptr;
-  CUresult (*granularity)(size_t *, const CUmemAllocationProp *, CUmemAllocationGranularity_flags) = nullptr;
-  bool ok = false;
-};
-const VmmApi &vmm_api() {
-  static VmmApi a;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
-    auto get = [](const char *name, void **fn) {
-      cudaDriverEntryPointQueryResult q;
-      return cudaGetDriverEntryPoint(name, fn, cudaEnableDefault, &q) == cudaSuccess && q == cudaDriverEntryPointSuccess;
-    };
-    a.ok = get("cuMemCreate", reinterpret_cast<void **>(&a.create)) &&
-           get("cuMemRelease", reinterpret_cast<void **>(&a.release)) &&
-           get("cuMemAddressReserve", reinterpret_cast<void **>(&a.address_reserve)) &&
-           get("cuMemAddressFree", reinterpret_cast<void **>(&a.address_free)) &&
-           get("cuMemMap", reinterpret_cast<void **>(&a.map)) && get("cuMemUnmap", reinterpret_cast<void **>(&a.unmap)) &&
-           get("cuMemSetAccess", reinterpret_cast<void **>(&a.set_access)) &&
-           get("cuMemGetAllocationGranularity", reinterpret_cast<void **>(&a.granularity));
-  }
-  return a;
-}
-bool cu_ok(CUresult r, const char *what) {
-  if (r == CUDA_SUCCESS) return true;
-  coe_set_error(std::string(what) + " failed (CUresult " + std::to_string((int)r) + ")");
-  return false;
-}
-
 struct coe_runtime;
-static bool vmm_unmap(coe_runtime *rt, int32_t slot);
 
 struct StepBuffers {  // device arrays one step uses; two sets alternate
   int32_t *adm = nullptr;   // [6][max_adm]: exec, rank, req, stage, in route, out route
@@ -272,23 +234,24 @@ struct coe_runtime {
   std::vector<char *> slabs;
   int32_t act_ld = 0, h_max = 0, total_slots = 0;
   int64_t row_elems = 0;  // T * act_ld
-  // Expert memory under ONE byte budget for several shapes (cfg.expert_pool_bytes > 0): every
-  // expert owns a static virtual slot in its shape's reserved range, and a load maps pages of
-  // a shared physical pool into it (CUDA VMM) -- the planner's byte-budgeted pool
-  // (expert_pool.py:27-59) then bounds physical HBM exactly, whatever the shape mix.  Freed
-  // pages remember the slot that last used them: a later copy into them waits for that slot's
-  // readers, and a slot's stale mapping is unmapped only after its own readers have finished.
-  bool vmm = false;
-  int64_t page = 0, pool_pages = 0;
-  std::vector<CUmemGenericAllocationHandle> pool_handles;  // one physical allocation per page
-  std::vector<int64_t> va_size;          // per shape: reserved bytes
-  std::deque<int32_t> free_pages;        // FIFO, persists across steps
-  std::vector<int32_t> page_owner;       // slot that last used the page (-1: never)
-  std::vector<std::vector<int32_t>> slot_pages;  // pages mapped (or stale) behind each slot
-  std::vector<uint8_t> slot_mapped;
-  std::vector<int32_t> expert_vslot;     // expert -> its static slot
+  // Expert memory under ONE byte budget for several shapes (cfg.expert_pool_bytes > 0): one
+  // slab addressed in 2 MB units; a load takes a best-fit run of free units, an eviction
+  // returns its run -- so the planner's byte-budgeted pool (expert_pool.py:27-59) bounds
+  // physical HBM whatever the shape mix (the slab is the budget plus one largest expert of
+  // slack against fragmentation).  Every shape's weight tensor maps span the whole slab with
+  // a one-unit "slot" stride, so an expert is addressed by its first unit.  Each expert keeps
+  // a static bookkeeping slot (readers, events); freed units remember the slot that last used
+  // them, and a later copy into them waits for that slot's readers.
+  bool pooled = false;
+  int64_t unit = 0, pool_units = 0;
+  char *pool = nullptr;
+  std::map<int32_t, int32_t> free_runs;  // first unit -> run length
+  std::vector<int32_t> unit_owner;       // slot that last used the unit (-1: never)
+  std::vector<int32_t> slot_unit, slot_units;  // per slot: first unit / units of its residency
+  std::vector<int32_t> expert_vslot;     // expert -> its bookkeeping slot
 
   char *slot_ptr(int32_t s) const {
+    if (pooled) return pool + (int64_t)slot_unit[s] * unit;
     const int k = slot_shape[s];
     return slabs[k] + (int64_t)(s - slot_base[k]) * sstride[k];
   }
@@ -383,12 +346,8 @@ struct coe_runtime {
         if (m) coe_mlp_destroy(m);
     std::vector<void *> dev = {x, y, act, hbuf[0], hbuf[1], hbuf[2], outbuf, d_perm, d_keys, d_flags, d_last,
                                d_sort_scratch, d_compact_scratch};
-    if (vmm) {
-      for (int32_t q = 0; q < (int32_t)slot_mapped.size(); ++q)
-        if (slot_mapped[q]) vmm_unmap(this, q);
-      for (int k = 0; k < S; ++k)
-        if (slabs[k]) vmm_api().address_free(reinterpret_cast<CUdeviceptr>(slabs[k]), (size_t)va_size[k]);
-      for (auto h : pool_handles) vmm_api().release(h);
+    if (pooled) {
+      dev.push_back(pool);
     } else {
       for (char *sl : slabs) dev.push_back(sl);
     }
@@ -447,92 +406,39 @@ bool dmalloc(T **p, size_t bytes, const char *what) {
 
 int fail_cuda() { return COE_CUDA_ERR_CUDA; }
 
-constexpr int64_t kVmmPage = 8ll << 20;  // physical page of the expert pool (a multiple of the 2 MB granularity)
+constexpr int64_t kPoolUnit = 2ll << 20;  // allocation unit of the pooled expert slab
 
-// Reserve one virtual range per shape (a static slot per expert of that shape, stride rounded
-// up to whole pages) and one physical pool of pool_bytes; nothing is mapped yet.
-bool vmm_create(coe_runtime *rt, int64_t pool_bytes) {
-  const VmmApi &api = vmm_api();
-  if (!api.ok) {
-    coe_set_error("CUDA VMM entry points unavailable");
+// One slab of pool_bytes for every shape; each expert gets a bookkeeping slot (its rank among
+// the experts of its shape); every unit free.
+bool pool_create(coe_runtime *rt, int64_t pool_bytes) {
+  rt->unit = kPoolUnit;
+  rt->pool_units = (pool_bytes + rt->unit - 1) / rt->unit;
+  if (rt->pool_units >= (1ll << 27)) {
+    coe_set_error("pooled expert memory: too many units");
     return false;
   }
-  int dev = 0;
-  cudaGetDevice(&dev);
-  CUmemAllocationProp prop{};
-  prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
-  prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
-  prop.location.id = dev;
-  size_t gran = 0;
-  if (!cu_ok(api.granularity(&gran, &prop, CU_MEM_ALLOC_GRANULARITY_MINIMUM), "cuMemGetAllocationGranularity"))
-    return false;
-  rt->page = ((kVmmPage + (int64_t)gran - 1) / (int64_t)gran) * (int64_t)gran;
-  rt->pool_pages = (pool_bytes + rt->page - 1) / rt->page;
-  // cuMemMap maps whole allocations (offset 0), so every page is its own physical allocation
-  rt->pool_handles.reserve((size_t)rt->pool_pages);
-  for (int64_t p = 0; p < rt->pool_pages; ++p) {
-    CUmemGenericAllocationHandle h = 0;
-    if (!cu_ok(api.create(&h, (size_t)rt->page, &prop, 0), "cuMemCreate (expert pool page)")) return false;
-    rt->pool_handles.push_back(h);
-  }
-  rt->va_size.assign(rt->S, 0);
+  if (!ok(cudaMalloc(&rt->pool, (size_t)(rt->pool_units * rt->unit)), "expert pool alloc")) return false;
   for (int k = 0; k < rt->S; ++k) {
-    rt->sstride[k] = (rt->sbytes[k] + rt->page - 1) / rt->page * rt->page;
-    rt->va_size[k] = rt->sstride[k] * std::max(1, rt->slot_count[k]) + rt->page;
-    CUdeviceptr va = 0;
-    if (!cu_ok(api.address_reserve(&va, (size_t)rt->va_size[k], (size_t)rt->page, 0, 0), "cuMemAddressReserve"))
-      return false;
-    rt->slabs[k] = reinterpret_cast<char *>(va);
+    rt->slabs[k] = rt->pool;
+    rt->sstride[k] = rt->unit;
   }
-  rt->vmm = true;
-  rt->page_owner.assign(rt->pool_pages, -1);
-  for (int64_t p = 0; p < rt->pool_pages; ++p) rt->free_pages.push_back((int32_t)p);
-  rt->slot_pages.assign(rt->total_slots, {});
-  rt->slot_mapped.assign(rt->total_slots, 0);
-  // static slot of each expert: its rank among the experts of its shape
+  rt->pooled = true;
+  rt->free_runs = {{0, (int32_t)rt->pool_units}};
+  rt->unit_owner.assign((size_t)rt->pool_units, -1);
+  rt->slot_unit.assign(rt->total_slots, -1);
+  rt->slot_units.assign(rt->total_slots, 0);
   rt->expert_vslot.assign(rt->cfg.num_experts, -1);
   std::vector<int32_t> next(rt->S, 0);
   for (int32_t e = 0; e < rt->cfg.num_experts; ++e) {
     const int k = rt->expert_shape[e];
     if (next[k] >= rt->slot_count[k]) {
-      coe_set_error("VMM expert memory: more experts of a shape than its slots");
+      coe_set_error("pooled expert memory: more experts of a shape than its slots");
       return false;
     }
     rt->expert_vslot[e] = rt->slot_base[k] + next[k]++;
   }
   return true;
 }
-
-// Map the slot's pages (consecutive pages as one mapping) and enable device access.
-bool vmm_map(coe_runtime *rt, int32_t slot) {
-  const VmmApi &api = vmm_api();
-  const auto &pages = rt->slot_pages[slot];
-  const CUdeviceptr base = reinterpret_cast<CUdeviceptr>(rt->slot_ptr(slot));
-  for (size_t i = 0; i < pages.size(); ++i)
-    if (!cu_ok(api.map(base + (CUdeviceptr)(i * rt->page), (size_t)rt->page, 0, rt->pool_handles[pages[i]], 0),
-               "cuMemMap"))
-      return false;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  CUmemAccessDesc acc{};
-  acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
-  acc.location.id = dev;
-  acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
-  if (!cu_ok(api.set_access(base, (size_t)(pages.size() * rt->page), &acc, 1), "cuMemSetAccess")) return false;
-  rt->slot_mapped[slot] = 1;
-  return true;
-}
-
-}  // namespace
-static bool vmm_unmap(coe_runtime *rt, int32_t slot) {
-  const CUdeviceptr base = reinterpret_cast<CUdeviceptr>(rt->slot_ptr(slot));
-  for (size_t i = 0; i < rt->slot_pages[slot].size(); ++i)
-    if (!cu_ok(vmm_api().unmap(base + (CUdeviceptr)(i * rt->page), (size_t)rt->page), "cuMemUnmap")) return false;
-  rt->slot_mapped[slot] = 0;
-  return true;
-}
-namespace {
-
 
 float elapsed(cudaEvent_t a, cudaEvent_t b) {
   float ms = 0.f;
@@ -679,7 +585,7 @@ int coe_runtime_create(const coe_runtime_config *cfg, coe_runtime **out) {
   rt->slabs.assign(rt->S, nullptr);
   rt->sstride = rt->sbytes;
   if (c.expert_pool_bytes > 0) {
-    good = good && vmm_create(rt, c.expert_pool_bytes);
+    good = good && pool_create(rt, c.expert_pool_bytes);
   } else {
     for (int k = 0; k < rt->S; ++k)
       good = good && dmalloc(&rt->slabs[k], (size_t)rt->sbytes[k] * std::max(1, rt->slot_count[k]), "slab alloc");
@@ -728,7 +634,7 @@ int coe_runtime_create(const coe_runtime_config *cfg, coe_runtime **out) {
       mc.act_ld = rt->act_ld;
       mc.h_rows = c.max_wave_rows;
       mc.slab = rt->slabs[sk];
-      mc.num_slots = std::max(1, rt->slot_count[sk]);
+      mc.num_slots = rt->pooled ? (int32_t)rt->pool_units : std::max(1, rt->slot_count[sk]);
       mc.slot_stride_bytes = rt->sstride[sk];
       for (int k = 0; k < coe_runtime::NCLS && good; ++k) {
         mc.h_scratch = rt->hbuf[k];
@@ -801,8 +707,8 @@ int coe_runtime_slot_of(coe_runtime *rt, int32_t expert) {
 int coe_runtime_init_experts(coe_runtime *rt) {
   const auto &c = rt->cfg;
   if (!ok(cudaDeviceSynchronize(), "init experts sync")) return fail_cuda();
-  char *scratch = nullptr;  // VMM: no slot is mapped yet -- generate into a scratch expert
-  if (rt->vmm) {
+  char *scratch = nullptr;  // pooled: no expert has units yet -- generate into a scratch expert
+  if (rt->pooled) {
     const int64_t big = *std::max_element(rt->sbytes.begin(), rt->sbytes.end());
     if (!ok(cudaMalloc(&scratch, (size_t)big), "init scratch")) return fail_cuda();
   }
@@ -825,12 +731,10 @@ int coe_runtime_init_experts(coe_runtime *rt) {
   }
   if (!ok(cudaStreamSynchronize(rt->compute), "init experts")) return fail_cuda();
   if (scratch) cudaFree(scratch);
-  if (rt->vmm) {  // every slot unmapped, every page free
-    for (int32_t q = 0; q < rt->total_slots; ++q)
-      if (rt->slot_mapped[q] && !vmm_unmap(rt, q)) return fail_cuda();
-    rt->free_pages.clear();
-    for (int64_t p = 0; p < rt->pool_pages; ++p) rt->free_pages.push_back((int32_t)p);
-    std::fill(rt->page_owner.begin(), rt->page_owner.end(), -1);
+  if (rt->pooled) {  // every unit free
+    rt->free_runs = {{0, (int32_t)rt->pool_units}};
+    std::fill(rt->unit_owner.begin(), rt->unit_owner.end(), -1);
+    std::fill(rt->slot_units.begin(), rt->slot_units.end(), 0);
   }
   std::fill(rt->slot_expert.begin(), rt->slot_expert.end(), -1);
   std::fill(rt->expert_slot.begin(), rt->expert_slot.end(), -1);
@@ -1045,8 +949,8 @@ int coe_runtime_attach_peers(coe_runtime *rt, int32_t rank, int32_t world, const
 int coe_runtime_bench_mlp(coe_runtime *rt, int32_t groups, int32_t requests_per_group, int32_t iters,
                           float *up_ms, float *down_ms) {
   const auto &c = rt->cfg;
-  if (rt->vmm) {
-    coe_set_error("bench_mlp: expert slots are mapped on demand in pooled (VMM) mode");
+  if (rt->pooled) {
+    coe_set_error("bench_mlp: experts are placed on demand in pooled mode");
     return COE_CUDA_ERR_CONFIG;
   }
   const int64_t rows = (int64_t)requests_per_group * c.T;
@@ -1195,6 +1099,7 @@ namespace {
 struct BatchInfo {
   int32_t op_index;   // index into the op log
   int32_t expert, slot, count, cls;
+  int32_t tma_slot;   // weight-map slot index: slot within its shape's slab, or (pooled) first unit
   int32_t copy;       // copy that wrote this batch's slot this step (-1: resident since step start)
   bool release;       // last reader of a slot a later LOAD overwrites
   int64_t rows;
@@ -1214,8 +1119,8 @@ struct CopyInfo {
   bool restore;
   std::vector<int32_t> readers;    // batches reading the slot's previous content this step
   bool first_write;                // slot not written earlier this step
-  std::vector<int32_t> deps;       // slots whose readers must finish first (VMM: the pages' last users)
-  std::vector<int32_t> pages;      // VMM: pool pages this copy maps
+  std::vector<int32_t> deps;       // slots whose readers must finish first (pooled: the units' last users)
+  int32_t unit0 = -1;              // pooled: first unit of the expert's new place
   double up_end = 0.0, end = 0.0;  // estimated
   bool issued = false;
   int64_t op_pos = 0;              // op-log position of the LOAD (restores: of the first batch)
@@ -1347,40 +1252,37 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
   std::vector<std::vector<int32_t>> slot_readers(NS);
   std::vector<uint8_t> slot_written(NS, 0);
   for (int32_t i = 0; i < in->num_initial; ++i) plan_res[in->initial[i]] = 1;
-  // VMM: pages behind each slot this step, and per page the readers (batches, this step) of
-  // the residency that freed it
-  std::vector<std::vector<int32_t>> cur_pages;
-  std::vector<std::shared_ptr<const std::vector<int32_t>>> page_rd;
-  if (rt->vmm) {
-    cur_pages.assign(NS, {});
-    page_rd.assign((size_t)rt->pool_pages, nullptr);
-  }
-  auto vmm_free = [&](int32_t q) {  // the expert in slot q left: its pages return to the pool
+  // pooled: per unit, the readers (batches, this step) of the residency that freed it
+  std::vector<std::shared_ptr<const std::vector<int32_t>>> unit_rd;
+  if (rt->pooled) unit_rd.assign((size_t)rt->pool_units, nullptr);
+  auto pool_free = [&](int32_t q) {  // the expert in slot q left: its units return to the pool
     auto snap = std::make_shared<const std::vector<int32_t>>(slot_readers[q]);
-    for (int32_t pg : cur_pages[q]) {
-      rt->free_pages.push_back(pg);
-      page_rd[pg] = snap;
+    const int32_t u0 = rt->slot_unit[q], n = rt->slot_units[q];
+    for (int32_t u = u0; u < u0 + n; ++u) unit_rd[u] = snap;
+    auto it = rt->free_runs.emplace(u0, n).first;  // coalesce with the neighbours
+    if (it != rt->free_runs.begin()) {
+      auto prev = std::prev(it);
+      if (prev->first + prev->second == it->first) {
+        prev->second += it->second;
+        rt->free_runs.erase(it);
+        it = prev;
+      }
     }
-    cur_pages[q].clear();
+    auto next = std::next(it);
+    if (next != rt->free_runs.end() && it->first + it->second == next->first) {
+      it->second += next->second;
+      rt->free_runs.erase(next);
+    }
+    rt->slot_units[q] = 0;
   };
   for (int32_t s = 0; s < NS; ++s) {  // slots outside the initial placement are free again
     int32_t e = rt->slot_expert[s];
-    if (rt->vmm && e >= 0) cur_pages[s] = rt->slot_pages[s];
     if (e >= 0 && !plan_res[e]) {
       rt->expert_slot[e] = -1;
       rt->slot_expert[s] = -1;
-      if (rt->vmm) vmm_free(s);
+      if (rt->pooled) pool_free(s);
     }
   }
-  if (rt->vmm)  // stale mappings whose readers are done can go now (no host wait later)
-    for (int32_t s = 0; s < NS; ++s) {
-      if (!rt->slot_mapped[s] || rt->slot_expert[s] >= 0) continue;
-      bool done = true;
-      for (int k = 0; k < NCLS && done; ++k)
-        if (rt->slot_free_valid[(size_t)s * NCLS + k])
-          done = cudaEventQuery(rt->slot_free_down[(size_t)s * NCLS + k]) == cudaSuccess;
-      if (done && !vmm_unmap(rt, s)) return fail_cuda();
-    }
   for (int32_t i = 0; i < in->num_initial; ++i)
     if (rt->expert_slot[in->initial[i]] < 0) pending_restore[in->initial[i]] = 1;
 
@@ -1405,8 +1307,8 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     }
     const int k = rt->expert_shape[e];
     int32_t best = -1;  // free slot of the expert's shape whose readers were issued earliest
-    if (rt->vmm) {
-      best = rt->expert_vslot[e];  // the expert's own virtual slot
+    if (rt->pooled) {
+      best = rt->expert_vslot[e];  // the expert's own bookkeeping slot
     } else {
       for (int32_t s = rt->slot_base[k]; s < rt->slot_base[k] + rt->slot_count[k]; ++s) {
         if (rt->slot_expert[s] >= 0) continue;
@@ -1420,25 +1322,33 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     }
     CopyInfo ci{e, best, restore, slot_readers[best], !slot_written[best]};
     ci.deps.push_back(best);
-    if (rt->vmm) {  // map free pool pages; wait for the readers of whatever last used them
-      const int64_t n = rt->sstride[k] / rt->page;
-      if ((int64_t)rt->free_pages.size() < n) {
-        coe_set_error("expert pool out of pages (planner residency exceeds the byte budget)");
+    if (rt->pooled) {  // best-fit run of free units; wait for the readers of whatever used them last
+      const int32_t n = (int32_t)((rt->sbytes[k] + rt->unit - 1) / rt->unit);
+      auto pick = rt->free_runs.end();
+      for (auto it = rt->free_runs.begin(); it != rt->free_runs.end(); ++it)
+        if (it->second >= n && (pick == rt->free_runs.end() || it->second < pick->second)) pick = it;
+      if (pick == rt->free_runs.end()) {
+        coe_set_error("pooled expert memory: no free run for a load (byte budget exceeded or fragmented)");
         return false;
       }
-      for (int64_t i = 0; i < n; ++i) {
-        const int32_t pg = rt->free_pages.front();
-        rt->free_pages.pop_front();
-        ci.pages.push_back(pg);
-        const int32_t owner = rt->page_owner[pg];
+      const int32_t u0 = pick->first, len = pick->second;
+      rt->free_runs.erase(pick);
+      if (len > n) rt->free_runs.emplace(u0 + n, len - n);
+      const std::vector<int32_t> *last_rd = nullptr;
+      for (int32_t u = u0; u < u0 + n; ++u) {
+        const int32_t owner = rt->unit_owner[u];
         if (owner >= 0 && std::find(ci.deps.begin(), ci.deps.end(), owner) == ci.deps.end()) ci.deps.push_back(owner);
-        if (page_rd[pg])
-          for (int32_t r : *page_rd[pg])
+        if (unit_rd[u] && unit_rd[u].get() != last_rd) {
+          last_rd = unit_rd[u].get();
+          for (int32_t r : *unit_rd[u])
             if (std::find(ci.readers.begin(), ci.readers.end(), r) == ci.readers.end()) ci.readers.push_back(r);
-        page_rd[pg] = nullptr;
-        rt->page_owner[pg] = best;
+        }
+        unit_rd[u] = nullptr;
+        rt->unit_owner[u] = best;
       }
-      cur_pages[best] = ci.pages;
+      rt->slot_unit[best] = u0;
+      rt->slot_units[best] = n;
+      ci.unit0 = u0;
     }
     ci.op_pos = op_pos;
     copies.push_back(ci);
@@ -1462,7 +1372,7 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
         if (s >= 0) {
           rt->expert_slot[v] = -1;
           rt->slot_expert[s] = -1;
-          if (rt->vmm) vmm_free(s);
+          if (rt->pooled) pool_free(s);
         }
       }
       plan_res[op.expert] = 1;
@@ -1470,7 +1380,7 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
         int32_t s = rt->expert_slot[op.expert];
         rt->slot_expert[s] = -1;
         rt->expert_slot[op.expert] = -1;
-        if (rt->vmm) vmm_free(s);
+        if (rt->pooled) pool_free(s);
       }
       if (!issue_copy(op.expert, false, my_ops[k])) return COE_CUDA_ERR_CHECK;
       continue;
@@ -1488,6 +1398,7 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     b.op_index = (int32_t)my_ops[k];
     b.expert = e;
     b.slot = rt->expert_slot[e];
+    b.tma_slot = rt->pooled ? rt->slot_unit[b.slot] : b.slot - rt->slot_base[rt->slot_shape[b.slot]];
     b.count = op.count;
     b.rows = (int64_t)op.count * c.T;
     b.copy = slot_copy[b.slot];
@@ -1666,7 +1577,7 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
       const int32_t m_tiles = (int32_t)((b.rows + BM - 1) / BM);
       coe_mlp_group gu{};
       gu.rows = (int32_t)b.rows;
-      gu.slot = b.slot - rt->slot_base[w.shape];  // local index in the shape's slab
+      gu.slot = b.tma_slot;
       gu.batch = bi;
       gu.h_row = (int32_t)w.rows;
       gu.tile_start = w.tiles_up;
@@ -1858,17 +1769,15 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
         ca.expert = ci.expert;
         ca.slot = ci.slot;
         ca.restore = ci.restore;
-        ca.pages = ci.pages;
+        ca.unit0 = ci.unit0;
         for (int32_t q : ci.deps)  // the slot itself, and (VMM) the last users of its pages
           for (int k = 0; k < NCLS; ++k) {
             const int32_t wv = last_reader_wave[q * NCLS + k];
             if (wv >= 0) {
               if (std::find(ca.wait_waves.begin(), ca.wait_waves.end(), wv) == ca.wait_waves.end())
                 ca.wait_waves.push_back(wv);
-              if (q == ci.slot) ca.own_waves.push_back(wv);
             } else if (!written[q] && rt->slot_free_valid[(size_t)q * NCLS + k]) {
               ca.wait_prev.push_back(q * NCLS + k);
-              if (q == ci.slot) ca.own_prev.push_back(q * NCLS + k);
             }
           }
         for (int k = 0; k < NCLS; ++k) last_reader_wave[ci.slot * NCLS + k] = -1;
@@ -2156,22 +2065,11 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     }
     if (a.is_copy) {
       const CopyAct &cp = copy_acts[a.index];
-      char *dst = rt->slot_ptr(cp.slot);
+      char *dst = rt->pooled ? rt->pool + (int64_t)cp.unit0 * rt->unit : rt->slot_ptr(cp.slot);
       const bool generate = rt->store_off[cp.expert] < 0;
       const char *src = generate ? nullptr : rt->host_store + rt->store_off[cp.expert];
       const int64_t half_bytes = rt->sbytes[rt->slot_shape[cp.slot]] / 2;
       const int ksh = rt->slot_shape[cp.slot];
-      if (rt->vmm) {  // map the slot's new pages (its stale mapping goes once its readers are done)
-        if (rt->slot_mapped[cp.slot]) {
-          for (int32_t wv : cp.own_waves)
-            if (!ok(cudaEventSynchronize(wave_down_ev[wv]), "unmap waits readers")) return fail_cuda();
-          for (int32_t sk : cp.own_prev)
-            if (!ok(cudaEventSynchronize(rt->slot_free_down[sk]), "unmap waits readers")) return fail_cuda();
-          if (!vmm_unmap(rt, cp.slot)) return fail_cuda();
-        }
-        rt->slot_pages[cp.slot] = cp.pages;
-        if (!vmm_map(rt, cp.slot)) return fail_cuda();
-      }
       for (int32_t wv : cp.wait_waves)
         if (!ok(cudaStreamWaitEvent(ks, wave_up_ev[wv], 0), "copy waits W1 readers")) return fail_cuda();
       for (int32_t sk : cp.wait_prev)

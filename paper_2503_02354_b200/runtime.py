@@ -26,7 +26,7 @@ from ._cuda_sigs import check as _check
 
 DEFAULT_WEIGHT_SEED = 0xC0E5E4E
 DEFAULT_INPUT_SEED = 0x1A7E5
-VMM_PAGE = 8 << 20  # physical page of the pooled expert memory (runtime.cu kVmmPage)
+POOL_UNIT = 2 << 20  # allocation unit of the pooled expert slab (runtime.cu kPoolUnit)
 
 
 class StepInput(ctypes.Structure):
@@ -352,12 +352,14 @@ class B200Runtime:
         if not kw.get("store_path"):
             kw.setdefault("store_mask", stored)
         if kw.pop("pooled", True):
-            # one physical pool for every shape (CUDA VMM): each expert a static virtual slot,
-            # physical bytes = the planner's budget (capped by what this executor can hold at
-            # once) plus < 8 MB page rounding per resident expert
+            # one slab for every shape, addressed in 2 MB units: the planner's byte budget
+            # (capped by what this executor ever holds at once), unit rounding per resident
+            # expert, and one largest expert of slack against fragmentation (best-fit)
             counts = [int((expert_shape == i).sum()) for i in range(len(shapes))]
             held = sum(int(p) * s.expert_bytes for p, s in zip(peak, shapes))
-            kw.setdefault("expert_pool_bytes", int(min(budget, held)) + int(peak.sum()) * VMM_PAGE)
+            largest = max(s.expert_bytes for s, p in zip(shapes, peak) if p > 0)
+            kw.setdefault("expert_pool_bytes",
+                          int(min(budget, held)) + largest + int(peak.sum()) * POOL_UNIT)
             return cls(shapes, len(ids), counts, len(resolved.request_ids), adm, expert_shape=expert_shape, **kw)
         slots = [max(1, int(p)) for p in peak]  # per-shape slabs of each shape's peak residency
         return cls(shapes, len(ids), slots, len(resolved.request_ids), adm, expert_shape=expert_shape, **kw)
