@@ -189,20 +189,10 @@ int release_grid(int reserved, int /*sms*/) {
   return reserved;
 }
 
-// Many row copies as one cudaMemcpyBatchAsync (CUDA 12.8+): the e2e path moves one
-// T x d row block per request, and per-call launch cost would dominate small rows.
-bool batched_copy(std::vector<void *> &dsts, std::vector<void *> &srcs, std::vector<size_t> &sizes,
-                  cudaStream_t stream, const char *what) {
-  if (dsts.empty()) return true;
-  if (dsts.size() > 1) {
-    cudaMemcpyAttributes attr{};
-    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-    size_t attr_idx = 0, fail = 0;
-    cudaError_t e = cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), dsts.size(), &attr, &attr_idx, 1,
-                                         &fail, stream);
-    if (e == cudaSuccess) return true;
-    cudaGetLastError();  // unsupported driver: fall back to one call per copy
-  }
+// Row-run copies, one cudaMemcpyAsync each: the e2e path merges each chunk's requests into
+// runs that are contiguous on both sides (usually the whole chunk), so the count stays small.
+bool run_copies(const std::vector<void *> &dsts, const std::vector<void *> &srcs, const std::vector<size_t> &sizes,
+                cudaStream_t stream, const char *what) {
   for (size_t i = 0; i < dsts.size(); ++i)
     if (!ok(cudaMemcpyAsync(dsts[i], srcs[i], sizes[i], cudaMemcpyDefault, stream), what)) return false;
   return true;
@@ -2002,7 +1992,7 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
       st.h2d_input_bytes += (int64_t)((j - i) * rb);
       i = j;
     }
-    return batched_copy(dsts, srcs, sizes, ks, "input H2D") && io_mark(ks) &&
+    return run_copies(dsts, srcs, sizes, ks, "input H2D") && io_mark(ks) &&
            ok(cudaEventRecord(rt->in_ev[k], ks), "record");
   };
   size_t hop_cursor = 0;
