@@ -53,8 +53,9 @@ enum {
 /* Op kinds of the physical op log */
 enum { COE_OP_LOAD = 0, COE_OP_BATCH = 1 };
 
-/* Tier ids (types.py:17) */
-enum { COE_TIER_DEVICE = 0, COE_TIER_HOST = 1, COE_TIER_SSD = 2 };
+/* Tier ids (types.py:17); COE_TIER_PEER is the (f3) extension: an NVLink copy
+ * from another GPU executor's HBM (RunConfig.peer_tier) */
+enum { COE_TIER_DEVICE = 0, COE_TIER_HOST = 1, COE_TIER_SSD = 2, COE_TIER_PEER = 3 };
 
 typedef struct coe_plan_config {
   /* experts, indexed densely in lexicographic order of their string ids so
@@ -109,6 +110,13 @@ typedef struct coe_plan_config {
 
   int32_t record_trace;             /* RunConfig.trace                        */
   int32_t record_ops;               /* emit op log + admission records        */
+
+  /* (f3) peer-GPU swap-in tier (RunConfig.peer_tier): a load of an expert that
+   * another GPU executor holds (and is not loading) copies it from that
+   * executor at peer_bw / peer_overhead; the scheduler's switch-cost
+   * predictions keep the reference's host/ssd tier (engine.py:583-586) */
+  int32_t peer_enabled;
+  double peer_bw, peer_overhead;
 } coe_plan_config;
 
 typedef struct coe_plan coe_plan;
@@ -132,7 +140,8 @@ typedef struct coe_op {
   int64_t offset;      /* into coe_plan_op_args (victims or member pairs)    */
   double time_s;       /* virtual start time                                  */
   int32_t tier;        /* LOAD: source tier                                   */
-  int32_t seq;         /* BATCH: index of the batch within its executor      */
+  int32_t seq;         /* BATCH: index of the batch within its executor;
+                          LOAD: source executor for COE_TIER_PEER, else -1   */
 } coe_op;
 
 /* One admission (a request entering an executor queue for one stage). */

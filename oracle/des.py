@@ -178,6 +178,9 @@ class _Run:
         for r in requests:
             self.requests[r["request_id"]] = dict(r)
         self.rr = 0
+        peer = opts.get("peer_tier")
+        self.peer = None if peer is None else (float(peer["read_bandwidth_bytes_per_s"]),
+                                               float(peer["fixed_load_overhead_s"]))
 
     # -- allocation (engine.py:412-495) --------------------------------------
     def _desc(self):
@@ -333,10 +336,19 @@ class _Run:
         hc["stamp"][eid] = hc["clock"]
         hc["clock"] += 1
 
-    def _tier(self, eid):
+    def _tier(self, eid):  # engine.py:579-582
         return "host" if self.hc is not None and eid in self.hc["res"] else "ssd"
 
-    def _load_s(self, eid):
+    def _peer_src(self, eid):
+        """(f3) lowest-id GPU executor holding eid and not loading it right now, else None."""
+        if self.peer is None:
+            return None
+        for x in self.ex:
+            if x["proc"] == "gpu" and eid in x["resident"] and x.get("loading") != eid:
+                return x["id"]
+        return None
+
+    def _load_s(self, eid):  # engine.py:583-586 (predictions keep the host/ssd tier)
         return self.device.load_latency(self._tier(eid), self.experts[eid]["param_bytes"])
 
     # -- event loop ----------------------------------------------------------
@@ -463,8 +475,14 @@ class _Run:
                                 e[5] = True
                                 x["total"] += lat
                             break
-            tier = self._tier(eid)
-            lat = self.device.load_latency(tier, spec["param_bytes"])
+            src = self._peer_src(eid)
+            if src is not None:  # (f3) NVLink copy from another GPU's pool
+                tier = "peer"
+                lat = spec["param_bytes"] / self.peer[0] + self.peer[1]
+            else:
+                tier = self._tier(eid)
+                lat = self.device.load_latency(tier, spec["param_bytes"])
+            x["loading"] = eid
             x["resident"][eid] = spec["param_bytes"]
             x["used"] += spec["param_bytes"]
             if self.evict in ("lru", "fifo"):
@@ -481,6 +499,7 @@ class _Run:
             x["busy"] = True
             x["busy_s"] += lat
             self.loads.append((x["id"], eid, victims, tier))
+            self.load_src.append(src)
             self.ops.append(("load", x["id"], eid, list(victims)))
             self._rec(t, x["id"], "load", eid, None)
             self._push(t + lat, "load_done", x["id"])
@@ -554,7 +573,7 @@ class _Run:
     def run(self):
         self._initial()
         self.heap, self.seq, self.trace = [], 0, []
-        self.batches, self.loads, self.ops = [], [], []
+        self.batches, self.loads, self.ops, self.load_src = [], [], [], []
         self.completed = self.fu_made = self.fu_done = self.evictions = self.stale = 0
         self.last = 0.0
         for rid in self.requests:
@@ -575,6 +594,7 @@ class _Run:
                 self._step(t, self.ex[data])
             elif kind == "load_done":
                 self.ex[data]["busy"] = False
+                self.ex[data]["loading"] = None
                 self._rec(t, data, "load_done", None, None)
                 self._step(t, self.ex[data])
             else:
@@ -594,7 +614,7 @@ class _Run:
             "per_executor": per, "alloc": {p: self.alloc[p] for p in sorted(self.alloc)},
         }
         return {"metrics": metrics, "trace": self.trace, "batches": self.batches, "loads": self.loads,
-                "ops": self.ops, "initial": self.initial}
+                "ops": self.ops, "initial": self.initial, "load_src": self.load_src}
 
 
 DEFAULTS = {
@@ -602,7 +622,7 @@ DEFAULTS = {
     "cpu_mem_fraction": 0.4, "alloc_override": None, "alloc_threshold": 0.15, "plateau_threshold": 0.02,
     "initial_window": 15, "error_margin": 0.05, "fit_points": 3, "search_enabled": True,
     "search_sample_requests": 400, "window_choose": "random", "samba_gpu_only": True, "trace": True,
-    "routes": None,
+    "routes": None, "peer_tier": None,
 }
 
 

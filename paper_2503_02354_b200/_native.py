@@ -27,7 +27,8 @@ COE_ERR_CUDA = 6
 EVENT_NAMES = ("arrival", "assign", "evict", "load", "load_done", "batch_start", "batch_done",
                "follow_up", "complete")
 OP_LOAD, OP_BATCH = 0, 1
-TIER_NAMES = ("device", "host", "ssd")
+TIER_NAMES = ("device", "host", "ssd", "peer")  # "peer": the (f3) NVLink tier extension
+TIER_HOST, TIER_SSD, TIER_PEER = 1, 2, 3
 
 
 class PlanConfig(ctypes.Structure):
@@ -73,6 +74,9 @@ class PlanConfig(ctypes.Structure):
         ("chain_experts", POINTER(c_int32)),
         ("record_trace", c_int32),
         ("record_ops", c_int32),
+        ("peer_enabled", c_int32),
+        ("peer_bw", c_double),
+        ("peer_overhead", c_double),
     ]
 
 

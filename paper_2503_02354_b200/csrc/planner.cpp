@@ -113,6 +113,7 @@ struct Executor {
   double busy_s = 0.0;
   int64_t switches = 0;
   int32_t batches = 0;
+  int32_t loading = -1;            // expert of the load in flight (f3 peer tier), else -1
 
   double free_bytes() const { return expert_budget - (double)used_bytes; }
 };
@@ -146,6 +147,8 @@ struct coe_plan {
   std::vector<int64_t> cost_nsat, cost_base, cost_item;
   int32_t numa = 1;
   double host_bw = 1, host_ovh = 0, ssd_bw = 1, ssd_ovh = 0;
+  int32_t peer_enabled = 0;
+  double peer_bw = 1, peer_ovh = 0;
   int32_t host_mode = -1;
   double host_budget = 0;
   int32_t assign_makespan = 1, arrange = 1, evict = 0;
@@ -197,12 +200,21 @@ struct coe_plan {
   // costmodel.py:69-73
   double load_latency_from(int tier, int64_t nbytes) const {
     if (tier == COE_TIER_HOST) return (double)nbytes / host_bw + host_ovh;
+    if (tier == COE_TIER_PEER) return (double)nbytes / peer_bw + peer_ovh;
     return (double)nbytes / ssd_bw + ssd_ovh;
   }
   int source_tier(int32_t e) const {  // engine.py:579-582
     return (hc.enabled && hc.resident[e]) ? COE_TIER_HOST : COE_TIER_SSD;
   }
+  // switch-cost predictions (engine.py:583-586): the reference's tier, also with a peer tier
   double load_latency(int32_t e) const { return load_latency_from(source_tier(e), bytes[e]); }
+  // (f3) lowest-id GPU executor holding e that is not loading it right now, else -1
+  int32_t peer_source(int32_t e) const {
+    if (!peer_enabled) return -1;
+    for (const Executor &y : ex)
+      if (y.proc == 0 && y.resident[e] && y.loading != e) return y.id;
+    return -1;
+  }
 
   // costmodel.py:55-64
   double exec_latency(int32_t a, int32_t proc, int64_t n, double k_scale) const {
@@ -484,9 +496,11 @@ struct coe_plan {
       if (hc.enabled && x.proc == 0) hc_insert(v, nb);
       invalidate_prediction(x, v);
     }
-    int tier = source_tier(e);
+    const int32_t peer_src = peer_source(e);
+    int tier = peer_src >= 0 ? COE_TIER_PEER : source_tier(e);
     double latency = load_latency_from(tier, bytes[e]);
     pool_add(x, e);
+    x.loading = e;
     if (evict == 1 || evict == 2) x.stamp[e] = x.clock++;  // LRU touch / FIFO on_resident
     if (tier == COE_TIER_HOST) hc_note_read(e);
     x.switches += 1;
@@ -506,7 +520,7 @@ struct coe_plan {
       op.offset = (int64_t)op_args.size();
       op.time_s = t;
       op.tier = tier;
-      op.seq = -1;
+      op.seq = peer_src;
       for (int32_t v : victims) op_args.push_back(v);
       ops.push_back(op);
     }
@@ -679,6 +693,7 @@ struct coe_plan {
           break;
         case K_LOAD_DONE:
           ex[ev.a].busy = false;
+          ex[ev.a].loading = -1;
           record(ev.t, ev.a, COE_EV_LOAD_DONE, -1, -1);
           step(ev.t, ex[ev.a]);
           break;
@@ -743,6 +758,10 @@ int coe_plan_create(const coe_plan_config *c, coe_plan **out) {
     p->host_ovh = c->host_overhead;
     p->ssd_bw = c->ssd_bw;
     p->ssd_ovh = c->ssd_overhead;
+    p->peer_enabled = c->peer_enabled;
+    p->peer_bw = c->peer_bw;
+    p->peer_ovh = c->peer_overhead;
+    if (p->peer_enabled && !(p->peer_bw > 0)) fail(COE_ERR_CONFIG, "peer tier bandwidth must be positive");
     p->host_mode = c->host_mode;
     p->host_budget = c->host_cache_budget;
     p->assign_makespan = c->assign_makespan;

@@ -88,6 +88,9 @@ class RunConfig:
     perf: PerfProfile | None = None
     trace: bool = False
     routes: dict | None = None  # component -> RoutePlan (N-stage extension)
+    # (f3) peer-GPU swap-in tier: {"read_bandwidth_bytes_per_s", "fixed_load_overhead_s"}; a LOAD
+    # of an expert another GPU executor holds copies it over NVLink (planner.cpp peer_source)
+    peer_tier: dict | None = None
 
 
 @dataclass
@@ -418,6 +421,12 @@ class Plan:
         c.chain_experts = _ptr(keep["ch_exp"], ctypes.c_int32)
         c.record_trace = 1 if record_trace else 0
         c.record_ops = 1 if record_ops else 0
+        peer = cfg.peer_tier
+        if peer is not None:
+            bw, ovh = float(peer["read_bandwidth_bytes_per_s"]), float(peer["fixed_load_overhead_s"])
+            if not bw > 0 or ovh < 0:
+                raise ConfigurationError("peer_tier needs a positive bandwidth and a non-negative overhead")
+            c.peer_enabled, c.peer_bw, c.peer_overhead = 1, bw, ovh
 
         self.lib = _native.planner_lib()
         self.handle = ctypes.c_void_p()

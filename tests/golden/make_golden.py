@@ -26,11 +26,13 @@ ROOT = os.path.dirname(os.path.dirname(HERE))
 sys.path.insert(0, "/root/reference/pkg/src")
 
 from coesim import engine, workload  # noqa: E402
-from coesim.costmodel import load_device_preset  # noqa: E402
+from coesim.costmodel import CostModel, load_device_preset  # noqa: E402
 from coesim.types import DeviceProfile, ModelRegistry  # noqa: E402
 
 CONFIGS = os.path.join(ROOT, "paper_2503_02354_b200", "data", "configs")
 FULL_TRACE_LIMIT = 12000
+# nominal NVLink 5 peer copy: 900 GB/s per direction, ~80 % as copy-engine payload, 10 us setup
+PEER_TIER = {"read_bandwidth_bytes_per_s": 720e9, "fixed_load_overhead_s": 1e-5}
 
 
 def read(path):
@@ -54,14 +56,73 @@ class NStage(engine.Simulation):
         self._admit(t, req, follow_up=False)
 
 
+class PeerCost(CostModel):
+    """The reference cost model plus a 'peer' tier (an NVLink copy from another GPU's HBM)."""
+
+    peer = (1.0, 0.0)  # (read_bandwidth_bytes_per_s, fixed_load_overhead_s)
+
+    def load_latency_from(self, tier_name, nbytes):
+        if tier_name == "peer":
+            if nbytes <= 0:
+                raise ValueError(f"load size must be positive, got {nbytes}")
+            return nbytes / self.peer[0] + self.peer[1]
+        return super().load_latency_from(tier_name, nbytes)
+
+
+class PeerTier(NStage):
+    """Reference engine with a peer-GPU swap-in tier.
+
+    Extension semantics (the repo's RunConfig.peer_tier): a LOAD of an expert that some GPU
+    executor holds in its pool -- and is not loading right now -- copies it over NVLink from the
+    lowest-id such executor instead of from the host/ssd tier (engine.py:643-677 picks the source
+    at load start, :579-586).  The scheduler's switch-cost predictions (_load_latency, used by
+    _admit and _invalidate_prediction, engine.py:583-586) keep the reference's host/ssd tier: a
+    peer copy is an opportunistic fast path.  (Quoting the peer latency to assign() as well makes
+    the makespan rule replicate experts across GPUs and evict others: -6 % to -59 % throughput
+    on these cases -- DESIGN.md §6b.)  Everything else is the unmodified reference.
+    """
+
+    def __init__(self, config):
+        super().__init__(config)
+        self.cost = PeerCost(config.device)
+        self._loading = {}
+
+    def _peer_source(self, expert_id):
+        for ex in self.executors:
+            if ex.proc == "gpu" and ex.pool.has(expert_id) and self._loading.get(ex.id) != expert_id:
+                return ex.id
+        return None
+
+    def _source_tier(self, expert_id):
+        if self._peer_source(expert_id) is not None:
+            return "peer"
+        return super()._source_tier(expert_id)
+
+    def _load_latency(self, expert_id):
+        spec = self.registry.experts[expert_id]
+        return self.cost.load_latency_from(super()._source_tier(expert_id), spec.param_bytes)
+
+    def _start_load(self, t, ex, run_entries, spec):
+        super()._start_load(t, ex, run_entries, spec)
+        self._loading[ex.id] = spec.expert_id
+
+    def _on_load_done(self, t, ex):
+        self._loading.pop(ex.id, None)
+        super()._on_load_done(t, ex)
+
+
 def run_case(registry_doc, device_doc, stream_doc, routes_doc, run):
     registry = ModelRegistry.from_doc(registry_doc)
     device = DeviceProfile.from_doc(device_doc)
     stream = workload.stream_from_doc(stream_doc)
+    run = dict(run)
+    peer = run.pop("peer_tier", None)
     cfg = engine.RunConfig(registry=registry, device=device, stream=stream, trace=True, **run)
     sim_cls = NStage if routes_doc else engine.Simulation
-    if routes_doc:
-        NStage.routes_doc = routes_doc
+    if peer is not None:
+        sim_cls = PeerTier
+        PeerCost.peer = (float(peer["read_bandwidth_bytes_per_s"]), float(peer["fixed_load_overhead_s"]))
+    NStage.routes_doc = routes_doc or {}
     metrics, trace = sim_cls(cfg).run()
     return engine.metrics_json(metrics), engine.trace_jsonl(trace)
 
@@ -110,6 +171,14 @@ def cases():
         out[f"c4_10k_g{n}_pergpu"] = config_case("c4", 10000, gpu_executors=n, alloc_override={"gpu": 59 * n})
         out[f"c3_10k_g{n}_pergpu"] = config_case("c3", 10000, gpu_executors=n, alloc_override={"gpu": 59 * n})
     out["c5_10k_g8"] = config_case("c5", 10000, gpu_executors=8)
+    # (f3) peer-GPU swap-in tier: NVLink 5 copies from another GPU's HBM (PEER_TIER, nominal)
+    for n in (2, 4):
+        out[f"c3_10k_g{n}_pergpu_peer"] = config_case("c3", 10000, gpu_executors=n, alloc_override={"gpu": 59 * n},
+                                                       peer_tier=PEER_TIER)
+        out[f"c4_10k_g{n}_pergpu_peer"] = config_case("c4", 10000, gpu_executors=n, alloc_override={"gpu": 59 * n},
+                                                       peer_tier=PEER_TIER)
+    out["c4_1k_g2_peer"] = config_case("c4", 1000, gpu_executors=2, peer_tier=PEER_TIER)
+    out["c5_1k_g8_peer"] = config_case("c5", 1000, gpu_executors=8, peer_tier=PEER_TIER)
     for policy in ("coserve", "coserve_em_ra", "coserve_em", "coserve_none", "samba_lru", "samba_fifo",
                    "samba_parallel"):
         out[f"numa_a80_{policy}"] = inline_case("numa-3080ti", 80, 300, 0.004, 3, policy=policy, seed=3,

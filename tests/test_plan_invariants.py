@@ -108,3 +108,36 @@ def test_multi_gpu_configs_give_each_gpu_its_own_budget():
     r8 = engine.resolve(configs.run_config(configs.load("c3", 1000, gpu_executors=8)))
     total = sum(s.param_bytes for s in r8.config.registry.experts.values())
     assert r8.alloc["gpu"]["expert_budget_bytes"] == total / 8  # all 300 experts fit: full residency
+
+
+PEER_CASES = [n for n in golden_cases.names() if n.endswith("_peer")]
+
+
+@pytest.mark.parametrize("name", PEER_CASES)
+def test_peer_tier_loads_match_oracle(name):
+    """(f3) every LOAD's source tier and source executor equal the oracle's (reference + peer tier)."""
+    from oracle import des
+
+    case = golden_cases.load(name)
+    reg, dev, stream, routes, run = golden_cases.docs(case)
+    ref = des.simulate(reg, dev, stream, routes=routes, trace=False, **run)
+    p = engine.plan(golden_cases.run_config(case))
+    ids = p.resolved.expert_ids
+    tiers = {_native.TIER_HOST: "host", _native.TIER_SSD: "ssd", _native.TIER_PEER: "peer"}
+    ours = [(int(o["executor"]), ids[int(o["expert"])], tiers[int(o["tier"])],
+             int(o["seq"]) if int(o["tier"]) == _native.TIER_PEER else None)
+            for o in p.ops() if o["kind"] == _native.OP_LOAD]
+    theirs = [(x, e, tier, src) for (x, e, _v, tier), src in zip(ref["loads"], ref["load_src"])]
+    assert ours == theirs
+    peer = [o for o in ours if o[2] == "peer"]
+    assert peer, "the case exercises no peer load"
+    for x, _e, _t, src in peer:
+        assert src != x and 0 <= src < len(p.resolved.executors)
+
+
+def test_peer_tier_rejects_bad_bandwidth():
+    case = golden_cases.load("c4_1k_g2_peer")
+    cfg = golden_cases.run_config(case)
+    cfg.peer_tier = {"read_bandwidth_bytes_per_s": 0.0, "fixed_load_overhead_s": 0.0}
+    with pytest.raises(ConfigurationError):
+        engine.plan(cfg)
