@@ -343,17 +343,28 @@ def test_group_compact_fused_matches_stable_sort(lib, n):
                                                                      ctypes.c_int] + [ctypes.c_void_p] * 8
     lib.coe_group_compact_fused.restype = ctypes.c_int
     rng = np.random.default_rng(n)
-    _, rank = _run_ranks(rng, n, 1)
+    # serving-shaped steps: at most ~2,000 runs, batches of up to 6 (or more when runs are long)
+    # so the step stays inside COE_FUSED_MAX_BATCHES (the runtime falls back to K1 + K2 beyond)
+    rank = np.zeros(n, np.int32)
+    nxt, p_new = 0, min(0.3, 2000.0 / n)
+    for i in range(n):
+        if nxt == 0 or rng.random() < p_new:
+            rank[i] = nxt
+            nxt += 1
+        else:
+            rank[i] = rng.integers(max(0, nxt - 6), nxt)
     bits = max(1, int(rank.max()).bit_length())
     order = np.argsort(rank, kind="stable")
     runs = np.split(order, np.flatnonzero(np.diff(rank[order])) + 1)
+    hi = max(7, 2 * n // 3000 + 2)
     sizes = []
     for run in runs:
         left = len(run)
         while left:
-            take = int(min(left, rng.integers(1, 7)))
+            take = int(min(left, rng.integers(1, hi)))
             sizes.append(take)
             left -= take
+    assert len(sizes) <= 4096
     dev = torch.device("cuda")
     T = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.int32)).to(dev)  # noqa: E731
     req = rng.integers(0, 10**6, n).astype(np.int32)

@@ -10,6 +10,9 @@ nreq = int(sys.argv[2]) if len(sys.argv) > 2 else 10000
 e2e = len(sys.argv) > 3 and sys.argv[3] == "1"
 w = configs.load(name, nreq)
 cfg = configs.run_config(w, trace=False)
+if os.environ.get("ALLOC_COUNT"):  # expert budget as alloc_override={'gpu': N} (bench --alloc-count)
+    cfg = configs.run_config(w, trace=False, alloc_override={"gpu": int(os.environ["ALLOC_COUNT"])},
+                             search_enabled=False)
 plan = engine.plan(cfg)
 rt = runtime.B200Runtime.for_plan(plan, runtime.shape_of(w))
 n = len(plan.resolved.request_ids)

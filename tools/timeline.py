@@ -39,6 +39,9 @@ def main():
     w = configs.load(name, nreq)
     shape = runtime.shape_of(w)
     cfg = configs.run_config(w, trace=False)
+    if os.environ.get("ALLOC_COUNT"):  # expert budget as alloc_override={'gpu': N} (bench --alloc-count)
+        cfg = configs.run_config(w, trace=False, alloc_override={"gpu": int(os.environ["ALLOC_COUNT"])},
+                                 search_enabled=False)
     plan = engine.plan(cfg)
     rt = runtime.B200Runtime.for_plan(plan, shape, profile=True)
     rt.fill_inputs(len(plan.resolved.request_ids))
