@@ -78,6 +78,37 @@ __global__ void gather_rows(const __nv_bfloat16 *p0, const __nv_bfloat16 *p1, co
   for (int64_t i = threadIdx.x; i < row_elems / 8; i += blockDim.x) dv[i] = sv[i];
 }
 
+// e2e inputs: a chunk's request rows read straight from pinned host memory over PCIe (the host
+// rows are in request order, the chunk is in the order batches need it, so a DMA per request
+// would be one small copy each).  A few CTAs keep ~100 KB of 16-byte loads in flight -- enough
+// to fill PCIe Gen5 -- and fit next to a resident K3 CTA (94 registers x 384 threads, ~197 KB
+// shared): the copy stream runs this kernel in H2D-queue order with the swap-in DMAs.
+__global__ void __launch_bounds__(256) gather_inputs(const uint4 *__restrict__ host, const int64_t *__restrict__ map,
+                                                     int32_t first, int32_t n, int64_t row_vec,
+                                                     uint4 *__restrict__ dst) {
+  const int64_t total = (int64_t)n * row_vec;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < total; i += 4 * stride) {
+    uint4 v[4];
+    int64_t d[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t e = i + u * stride, r = e / row_vec, c = e - r * row_vec;
+      v[u] = host[map[2 * (first + r)] * row_vec + c];
+      d[u] = map[2 * (first + r) + 1] * row_vec + c;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) dst[d[u]] = v[u];
+  }
+  for (; i < total; i += stride) {
+    const int64_t r = i / row_vec, c = i - r * row_vec;
+    dst[map[2 * (first + r) + 1] * row_vec + c] = host[map[2 * (first + r)] * row_vec + c];
+  }
+}
+
+const int kInputGatherCtas = getenv("COE_INPUT_CTAS") ? atoi(getenv("COE_INPUT_CTAS")) : 32;
+
 struct CopyAct {
   int32_t expert;
   int32_t slot;
@@ -210,6 +241,7 @@ struct StepBuffers {  // device arrays one step uses; two sets alternate
   int32_t *boff = nullptr;
   int32_t *mreq = nullptr, *mstage = nullptr, *min = nullptr, *mout = nullptr;
   coe_mlp_group *groups = nullptr;  // [2][max_batches]
+  int64_t *in_map = nullptr;        // e2e inputs, need order: [max_requests][host row, A row]
   cudaEvent_t free_ev = nullptr;    // recorded on compute when the step using this set ends
   bool used = false;
 };
@@ -342,7 +374,7 @@ struct coe_runtime {
       for (char *sl : slabs) dev.push_back(sl);
     }
     for (auto &s : sets) {
-      for (void *p : {(void *)s.adm, (void *)s.batch, (void *)s.boff, (void *)s.mreq, (void *)s.mstage,
+      for (void *p : {(void *)s.adm, (void *)s.batch, (void *)s.boff, (void *)s.mreq, (void *)s.mstage, (void *)s.in_map,
                       (void *)s.min, (void *)s.mout, (void *)s.groups})
         dev.push_back(p);
       if (s.free_ev) cudaEventDestroy(s.free_ev);
@@ -585,10 +617,11 @@ int coe_runtime_create(const coe_runtime_config *cfg, coe_runtime **out) {
            dmalloc(&s.boff, 4 * B, "boff alloc") && dmalloc(&s.mreq, 4 * A, "member alloc") &&
            dmalloc(&s.mstage, 4 * A, "member alloc") && dmalloc(&s.min, 4 * A, "member alloc") &&
            dmalloc(&s.mout, 4 * A, "member alloc") && dmalloc(&s.groups, 2 * sizeof(coe_mlp_group) * B, "groups") &&
+           dmalloc(&s.in_map, 16 * (size_t)c.max_requests, "input map") &&
            ok(cudaEventCreateWithFlags(&s.free_ev, cudaEventDisableTiming), "event");
   rt->compute = rt->cls_stream[0];
   if (good) {
-    rt->staging_bytes = 24 * A + 8 * B + 2 * sizeof(coe_mlp_group) * B + 512;
+    rt->staging_bytes = 24 * A + 8 * B + 2 * sizeof(coe_mlp_group) * B + 16 * (int64_t)c.max_requests + 1024;
     good = ok(cudaHostAlloc(reinterpret_cast<void **>(&rt->staging[0]), rt->staging_bytes, cudaHostAllocDefault), "staging") &&
            ok(cudaHostAlloc(reinterpret_cast<void **>(&rt->staging[1]), rt->staging_bytes, cudaHostAllocDefault), "staging") &&
            ok(cudaHostAlloc(reinterpret_cast<void **>(&rt->h_last), 4 * (size_t)c.max_requests, cudaHostAllocDefault), "last") &&
@@ -1354,6 +1387,10 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
   for (size_t k = 0; k < my_ops.size(); ++k) {
     const coe_op &op = ops[my_ops[k]];
     if (op.kind == COE_OP_LOAD) {
+      if (op.tier == COE_TIER_PEER) {
+        coe_set_error("plan has a peer-tier LOAD (RunConfig.peer_tier): peer swap-ins are not executed by this runtime");
+        return COE_CUDA_ERR_CONFIG;
+      }
       for (int32_t j = 0; j < op.count; ++j) {
         int32_t v = in->op_args[op.offset + j];
         plan_res[v] = 0;
@@ -1897,6 +1934,22 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     std::memcpy(s_groups, g_up.data(), sizeof(coe_mlp_group) * n_batches);
     std::memcpy(s_groups + n_batches, g_down.data(), sizeof(coe_mlp_group) * n_batches);
   }
+  // e2e inputs read by gather_inputs: per request in need order, its host row and A row
+  const uint4 *host_in_dev = nullptr;
+  if (e2e_in && !getenv("COE_INPUT_DMA")) {
+    void *dp = nullptr;
+    if (cudaHostGetDevicePointer(&dp, const_cast<void *>(in->host_inputs), 0) == cudaSuccess)
+      host_in_dev = static_cast<const uint4 *>(dp);
+    else
+      cudaGetLastError();  // not page-locked: one DMA per row run instead
+  }
+  int64_t *s_in = reinterpret_cast<int64_t *>(
+      (reinterpret_cast<uintptr_t>(s_groups + 2 * n_batches) + 15) & ~uintptr_t(15));
+  if (host_in_dev)
+    for (size_t i = 0; i < in_reqs.size(); ++i) {
+      s_in[2 * i] = host_row[in_reqs[i]];
+      s_in[2 * i + 1] = rows.in_slot[in_reqs[i]];
+    }
 
   cudaStream_t cs = rt->compute, ks = rt->copy;
   if (c.profile && !ok(cudaEventRecord(rt->t_step_start, cs), "record")) return fail_cuda();
@@ -1908,6 +1961,9 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
        !ok(cudaMemcpyAsync(sb.groups, s_groups, 2 * sizeof(coe_mlp_group) * (size_t)n_batches,
                            cudaMemcpyHostToDevice, ks),
            "group H2D")))
+    return fail_cuda();
+  if (host_in_dev && !in_reqs.empty() &&
+      !ok(cudaMemcpyAsync(sb.in_map, s_in, 16 * in_reqs.size(), cudaMemcpyHostToDevice, ks), "input map H2D"))
     return fail_cuda();
   // step fence: every peer has finished the previous step (its landing rows are free).
   // Same-process peers (hub) are stepped and synchronised together (runtime.step_executors).
@@ -1978,6 +2034,14 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
       if (!ok(cudaStreamWaitEvent(ks, ev, 0), "inputs wait slot readers")) return false;
     if (c.profile) rt->io_kind.push_back(0);
     if (!io_mark(ks)) return false;
+    if (host_in_dev) {  // one gather kernel per chunk (host rows scattered in need order)
+      const int32_t n = chunk_start[k + 1] - chunk_start[k];
+      gather_inputs<<<kInputGatherCtas, 256, 0, ks>>>(host_in_dev, sb.in_map, chunk_start[k], n, (int64_t)(rb / 16),
+                                                       reinterpret_cast<uint4 *>(rt->act));
+      st.h2d_input_bytes += (int64_t)n * (int64_t)rb;
+      st.launches += 1;
+      return ok(cudaGetLastError(), "gather_inputs") && io_mark(ks) && ok(cudaEventRecord(rt->in_ev[k], ks), "record");
+    }
     const char *hin = static_cast<const char *>(in->host_inputs);
     std::vector<void *> dsts, srcs;
     std::vector<size_t> sizes;
