@@ -207,8 +207,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
   if (warp == 2) sm100::tmem_alloc<TMEM_COLS, CG>(tmem_slot);
   sm100::tc_fence_before();
-  if constexpr (CG == 2) sm100::cluster_sync();  // peer barriers initialised, TMEM allocated in both
-  else __syncthreads();
+  if constexpr (CG == 2) {
+    sm100::cluster_sync();  // peer barriers initialised, TMEM allocated in both
+    __syncthreads();        // (also a CTA barrier: compute-sanitizer racecheck does not model cluster barriers)
+  } else {
+    __syncthreads();
+  }
   sm100::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int total_tiles = CG == 1 ? args.total_tiles : *total_slot;
