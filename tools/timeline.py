@@ -87,6 +87,7 @@ def main():
                        "busy_union_ms": union([(a, b) for a, b in phases[m][:, 0:2]] +
                                               [(a, b) for a, b in phases[m][:, 2:4]]),
                        "tflops_serial": float(flops[m].sum() / (t / 1e3) / 1e12) if t > 0 else None}
+    st = {k: v for k, v in st.items() if not isinstance(v, np.ndarray)}
     summary = {
         "config": name, "requests": nreq, "timing": timing, "stats": st,
         "k3": {"busy_ms": busy, "flops": float(flops.sum()), "tflops_busy": float(flops.sum() / (busy / 1e3) / 1e12),
