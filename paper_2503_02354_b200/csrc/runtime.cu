@@ -335,6 +335,7 @@ struct coe_runtime {
   int64_t last_adm = 0, last_batches = 0;
   int last_set = 0;
   cudaStream_t out_stream = nullptr;  // e2e output downloads (inputs ride the copy engine)
+  cudaStream_t copy_in = nullptr;     // e2e inputs, second H2D queue (COE_INPUT_DMA=2 experiment)
   std::vector<cudaEvent_t> in_ev;
   cudaEvent_t out_drained = nullptr;
   bool have_out = false;
@@ -404,6 +405,7 @@ struct coe_runtime {
     for (auto st : cls_stream)
       if (st) cudaStreamDestroy(st);
     if (copy) cudaStreamDestroy(copy);
+    if (copy_in) cudaStreamDestroy(copy_in);
     if (hop) cudaStreamDestroy(hop);
     if (out_stream) cudaStreamDestroy(out_stream);
   }
@@ -590,6 +592,7 @@ int coe_runtime_create(const coe_runtime_config *cfg, coe_runtime **out) {
               ok(cudaStreamCreateWithFlags(&rt->copy, cudaStreamNonBlocking), "stream") &&
               ok(cudaStreamCreateWithFlags(&rt->hop, cudaStreamNonBlocking), "stream") &&
               ok(cudaStreamCreateWithFlags(&rt->out_stream, cudaStreamNonBlocking), "stream") &&
+              ok(cudaStreamCreateWithFlags(&rt->copy_in, cudaStreamNonBlocking), "stream") &&
               (!c.device_io || (dmalloc(&rt->x, io_bytes, "X alloc") && dmalloc(&rt->y, io_bytes, "Y alloc"))) &&
               dmalloc(&rt->act, a_rows * rt->row_elems * 2, "activation ring alloc") &&
               dmalloc(&rt->outbuf, (int64_t)rt->out_slots * rt->row_elems * 2, "output staging alloc") &&
@@ -2016,7 +2019,9 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     return ok(cudaEventRecord(rt->t_io[io_n++], s_), "record");
   };
   const size_t rb = (size_t)rt->row_elems * 2;
+  const bool two_queues = getenv("COE_INPUT_DMA") && atoi(getenv("COE_INPUT_DMA")) == 2;
   auto upload_inputs = [&](int32_t k) -> bool {
+    const cudaStream_t ks = (two_queues && (k & 1)) ? rt->copy_in : rt->copy;  // odd chunks: second queue
     if (!in_prev_waited && rt->prev_nccl_hold && rt->have_step_end) {  // slots held for NCCL sends
       in_prev_waited = true;
       if (!ok(cudaStreamWaitEvent(ks, rt->step_end, 0), "inputs wait last step")) return false;
