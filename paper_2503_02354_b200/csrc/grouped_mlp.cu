@@ -54,6 +54,20 @@ constexpr int NUM_THREADS = 384;
 constexpr int EPI_WARP0 = 4;
 constexpr int EPI_WARPS = 8;  // two warps per TMEM lane quarter, each drains half the columns
 constexpr int MAX_GROUPS = 1024;
+constexpr int CRD_STAGES = 6;  // tile-coordinate ring (warp 3 -> TMA producer + epilogue warps)
+
+// Per-tile coordinates resolved ahead by the coordinate warp (warp 3): the dependent global
+// loads (group -> batch offset -> member routes) leave the TMA producer's and the epilogue's
+// critical path.  One entry per tile of this CTA.
+struct TileCrd {
+  int32_t box_row[4];        // A: first row of each TMA box (per-request boxes in the up pass)
+  int32_t box_par[4];        // A: which activation map (0 = X / H, 1, 2)
+  int32_t nboxes, slot, b_row;
+  uint32_t a_bytes;
+  __nv_bfloat16 *qbase[4];   // epilogue: output row of the first row of each 32-row lane quarter
+  int32_t qvalid[4];         // rows of the quarter inside the group
+};
+static_assert(sizeof(TileCrd) <= 128, "TileCrd exceeds its slot");
 
 // CG = CTAs per MMA: 1 -- one CTA computes a 128 x 256 tile and loads A (128 x 64) and B
 // (256 x 64) per stage; 2 -- a CTA pair (cluster of 2 on one TPC) computes a 256 x 256 tile
@@ -67,7 +81,8 @@ struct Tiling {
   static constexpr int B_BYTES = B_ROWS * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = CG == 1 ? 4 : 6;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + MAX_GROUPS * 4;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + MAX_GROUPS * 4 +
+                              CRD_STAGES * 128;
 };
 
 struct GemmArgs {
@@ -161,6 +176,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty_bar + 2);
   int32_t *total_slot = reinterpret_cast<int32_t *>(tmem_slot + 1);
   int32_t *tile_start = reinterpret_cast<int32_t *>(smem + TL::STAGES * TL::STAGE_BYTES + 256);
+  TileCrd *crd = reinterpret_cast<TileCrd *>(smem + TL::STAGES * TL::STAGE_BYTES + 256 + MAX_GROUPS * 4);
+  uint64_t *crd_full = reinterpret_cast<uint64_t *>(tmem_slot + 2);  // after tmem_slot / total_slot, 8-aligned
+  uint64_t *crd_empty = crd_full + CRD_STAGES;
 
   const uint32_t warp = sm100::warp_id();
   const uint32_t lane = sm100::lane_id();
@@ -198,6 +216,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       sm100::mbar_init(&full_bar[s], 1);
       sm100::mbar_init(&empty_bar[s], 1);
     }
+    for (int s = 0; s < CRD_STAGES; ++s) {
+      sm100::mbar_init(&crd_full[s], 1);
+      sm100::mbar_init(&crd_empty[s], 1 + EPI_WARPS);  // the TMA producer + one lane per epilogue warp
+    }
     for (int s = 0; s < 2; ++s) {
       sm100::mbar_init(&tfull_bar[s], 1);
       // CG 1: every epilogue thread arrives; CG 2: one lane per epilogue warp of both CTAs
@@ -223,45 +245,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       // ===== TMA producer (both CTAs of a pair: own A rows, own half of B) =====
       int stage = 0;
       uint32_t phase = 0;
+      int cs = 0;
+      uint32_t cph = 0;
       for (int t = tile0; t < total_tiles; t += tile_step) {
-        TileCoord c = decode_tile<CG>(t, tile_start, args.num_groups, args.groups);
-        const coe_mlp_group grp = args.groups[c.g];
-        const int m0 = c.m_blk * TL::TILE_M + (int)cta_rank * BM;  // first row of this CTA's half
+        sm100::mbar_wait(&crd_full[cs], cph);
+        const TileCrd &e = crd[cs];
         int box_row[BM / 32];
         int box_par[BM / 32];
-        int nboxes;
-        uint32_t a_bytes;
-        if (args.mode == 0) {
-          const int boff = args.batch_off[grp.batch];
-          const int members = grp.rows / args.T;
-          if constexpr (CG == 1) {
-            const int rows_here = min(grp.rows - m0, BM);
-            nboxes = (rows_here + args.a_box_rows - 1) / args.a_box_rows;
-          } else {
-            nboxes = BM / args.a_box_rows;  // full boxes: the leader expects a fixed byte count
-          }
-          for (int b = 0; b < nboxes; ++b) {
-            const int r = m0 + b * args.a_box_rows;
-            int j = r / args.T;
-            const int within = r - j * args.T;
-            j = min(j, members - 1);  // rows past the group (pair tail): any valid member, discarded
-            if (args.member_in) {
-              const int code = args.member_in[boff + j];
-              box_row[b] = (code >> 1) * args.T + within;
-              box_par[b] = (code & 1) ? 0 : 1;
-            } else {
-              box_row[b] = args.member_req[boff + j] * args.T + within;
-              box_par[b] = a_source(args.member_stage[boff + j]);
-            }
-          }
-          a_bytes = (uint32_t)(nboxes * args.a_box_rows * BK * 2);
-        } else {
-          nboxes = 1;
-          box_row[0] = grp.h_row + m0;  // past the H scratch end TMA fills zeros (bytes still counted)
-          box_par[0] = 0;
-          a_bytes = TL::A_BYTES;
+        const int nboxes = e.nboxes;
+        for (int b = 0; b < nboxes; ++b) {
+          box_row[b] = e.box_row[b];
+          box_par[b] = e.box_par[b];
         }
-        const int b_row = c.n_blk * BN + (int)cta_rank * TL::B_ROWS;
+        const uint32_t a_bytes = e.a_bytes;
+        const int b_row = e.b_row, slot = e.slot;
+        sm100::mbar_arrive(&crd_empty[cs]);
+        if (++cs == CRD_STAGES) {
+          cs = 0;
+          cph ^= 1;
+        }
         for (int kb = 0; kb < k_blocks; ++kb) {
           sm100::mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t *sa = stage_base + stage * TL::STAGE_BYTES;
@@ -272,7 +274,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               sm100::tma_load_2d(sa + b * args.a_box_rows * 128,
                                  box_par[b] == 0 ? &tm_a0 : (box_par[b] == 1 ? &tm_a1 : &tm_a2), &full_bar[stage],
                                  kb * BK, box_row[b]);
-            sm100::tma_load_3d(sb, &tm_b, &full_bar[stage], kb * BK, b_row, grp.slot);
+            sm100::tma_load_3d(sb, &tm_b, &full_bar[stage], kb * BK, b_row, slot);
           } else {
             const uint32_t bar = sm100::mapa_shared(sm100::smem_u32(&full_bar[stage]), 0);
             if (cta_rank == 0) sm100::mbar_arrive_expect_tx(&full_bar[stage], 2 * TL::STAGE_BYTES);
@@ -280,13 +282,103 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               sm100::tma_load_2d_pair(sa + b * args.a_box_rows * 128,
                                       box_par[b] == 0 ? &tm_a0 : (box_par[b] == 1 ? &tm_a1 : &tm_a2), bar, kb * BK,
                                       box_row[b]);
-            sm100::tma_load_3d_pair(sb, &tm_b, bar, kb * BK, b_row, grp.slot);
+            sm100::tma_load_3d_pair(sb, &tm_b, bar, kb * BK, b_row, slot);
           }
           if (++stage == TL::STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
+      }
+    }
+  } else if (warp == 3) {
+    // ===== coordinate warp: resolves each tile's A boxes, weight slot and output rows ahead
+    // of the producer and the epilogue (lanes 0-3: one A box / one lane quarter each) =====
+    int cs = 0;
+    uint32_t cph = 0;
+    for (int t = tile0; t < total_tiles; t += tile_step) {
+      const TileCoord c = decode_tile<CG>(t, tile_start, args.num_groups, args.groups);
+      const coe_mlp_group grp = args.groups[c.g];
+      const int m0 = c.m_blk * TL::TILE_M + (int)cta_rank * BM;  // first row of this CTA's half
+      const int boff = args.batch_off[grp.batch];
+      int nboxes;
+      if (args.mode == 0) {
+        if constexpr (CG == 1) nboxes = (min(grp.rows - m0, BM) + args.a_box_rows - 1) / args.a_box_rows;
+        else nboxes = BM / args.a_box_rows;  // full boxes: the leader expects a fixed byte count
+      } else {
+        nboxes = 1;
+      }
+      int brow = 0, bpar = 0;
+      __nv_bfloat16 *qbase = nullptr;
+      int qvalid = 0;
+      if (lane < 4) {
+        if (lane < nboxes) {
+          if (args.mode == 0) {
+            const int members = grp.rows / args.T;
+            const int r = m0 + (int)lane * args.a_box_rows;
+            int j = r / args.T;
+            const int within = r - j * args.T;
+            j = min(j, members - 1);  // rows past the group (pair tail): any valid member, discarded
+            if (args.member_in) {
+              const int code = args.member_in[boff + j];
+              brow = (code >> 1) * args.T + within;
+              bpar = (code & 1) ? 0 : 1;
+            } else {
+              brow = args.member_req[boff + j] * args.T + within;
+              bpar = a_source(args.member_stage[boff + j]);
+            }
+          } else {
+            brow = grp.h_row + m0;  // past the H scratch end TMA fills zeros (bytes still counted)
+          }
+        }
+        const int row = m0 + (int)lane * 32;  // a 32-row quarter never straddles members (T % 32 == 0)
+        qvalid = max(0, min(32, grp.rows - row));
+        if (qvalid > 0) {
+          if (args.mode == 0) {
+            qbase = args.out_h + (size_t)(grp.h_row + row) * args.N;
+          } else {
+            const int j = row / args.T;
+            if (args.member_out) {
+              const int code = args.member_out[boff + j];
+              const int kind = code & 15;
+              __nv_bfloat16 *dst = kind == 0   ? args.out_act0
+                                   : kind == 1 ? args.out_y
+                                   : kind == 2 ? args.out_stage
+                                               : args.peer_act[kind - 3][0];
+              qbase = dst + ((size_t)(code >> 4) * args.T + (row - j * args.T)) * args.ld;
+            } else {
+              const int req = args.member_req[boff + j];
+              const int st = args.member_stage[boff + j];
+              __nv_bfloat16 *dst = (st & 1) ? args.out_act1 : args.out_act0;
+              if (args.hop_dst) {
+                const int hd = args.hop_dst[(size_t)req * args.hop_stride + st];
+                if (hd >= 0) dst = args.peer_act[hd][st & 1];
+              }
+              qbase = dst + ((size_t)req * args.T + (row - j * args.T)) * args.ld;
+            }
+          }
+          qbase += c.n_blk * BN;
+        }
+      }
+      sm100::mbar_wait(&crd_empty[cs], cph ^ 1);
+      TileCrd &e = crd[cs];
+      if (lane < 4) {
+        e.box_row[lane] = brow;
+        e.box_par[lane] = bpar;
+        e.qbase[lane] = qbase;
+        e.qvalid[lane] = qvalid;
+      }
+      if (lane == 0) {
+        e.nboxes = nboxes;
+        e.slot = grp.slot;
+        e.b_row = c.n_blk * BN + (int)cta_rank * TL::B_ROWS;
+        e.a_bytes = args.mode == 0 ? (uint32_t)(nboxes * args.a_box_rows * BK * 2) : (uint32_t)TL::A_BYTES;
+      }
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(&crd_full[cs]);
+      if (++cs == CRD_STAGES) {
+        cs = 0;
+        cph ^= 1;
       }
     }
   } else if (warp == 1) {
@@ -335,40 +427,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int chunk0 = (int)((warp - EPI_WARP0) >> 2) * (BN / 32 / 2);
     constexpr int CHUNKS = BN / 32 / 2;
     const uint32_t tempty_leader = CG == 2 ? sm100::mapa_shared(sm100::smem_u32(&tempty_bar[0]), 0) : 0;
+    const size_t out_stride = args.mode == 0 ? (size_t)args.N : (size_t)args.ld;
     int acc = 0;
     uint32_t acc_phase = 0;
+    int cs = 0;
+    uint32_t cph = 0;
     for (int t = tile0; t < total_tiles; t += tile_step) {
-      TileCoord c = decode_tile<CG>(t, tile_start, args.num_groups, args.groups);
-      const coe_mlp_group grp = args.groups[c.g];
-      const int row = c.m_blk * TL::TILE_M + (int)cta_rank * BM + quarter * 32 + lane;
-      const bool valid = row < grp.rows;
-      __nv_bfloat16 *out_row = nullptr;
-      if (valid) {
-        if (args.mode == 0) {
-          out_row = args.out_h + (size_t)(grp.h_row + row) * args.N;
-        } else {
-          const int boff = args.batch_off[grp.batch];
-          const int j = row / args.T;
-          if (args.member_out) {
-            const int code = args.member_out[boff + j];
-            const int kind = code & 15;
-            __nv_bfloat16 *dst = kind == 0   ? args.out_act0
-                                 : kind == 1 ? args.out_y
-                                 : kind == 2 ? args.out_stage
-                                             : args.peer_act[kind - 3][0];
-            out_row = dst + ((size_t)(code >> 4) * args.T + (row - j * args.T)) * args.ld;
-          } else {
-            const int req = args.member_req[boff + j];
-            const int st = args.member_stage[boff + j];
-            __nv_bfloat16 *dst = (st & 1) ? args.out_act1 : args.out_act0;
-            if (args.hop_dst) {
-              const int hd = args.hop_dst[(size_t)req * args.hop_stride + st];
-              if (hd >= 0) dst = args.peer_act[hd][st & 1];
-            }
-            out_row = dst + ((size_t)req * args.T + (row - j * args.T)) * args.ld;
-          }
-        }
-        out_row += c.n_blk * BN;
+      sm100::mbar_wait(&crd_full[cs], cph);
+      const bool valid = (int)lane < crd[cs].qvalid[quarter];
+      __nv_bfloat16 *out_row = valid ? crd[cs].qbase[quarter] + lane * out_stride : nullptr;
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(&crd_empty[cs]);
+      if (++cs == CRD_STAGES) {
+        cs = 0;
+        cph ^= 1;
       }
       sm100::mbar_wait(&tfull_bar[acc], acc_phase);
       sm100::tc_fence_after();

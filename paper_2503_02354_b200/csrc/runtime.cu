@@ -84,30 +84,29 @@ __global__ void gather_rows(const __nv_bfloat16 *p0, const __nv_bfloat16 *p1, co
 // to fill PCIe Gen5 -- and fit next to a resident K3 CTA (94 registers x 384 threads, ~197 KB
 // shared): the copy stream runs this kernel in H2D-queue order with the swap-in DMAs.
 __global__ void __launch_bounds__(256) gather_inputs(const uint4 *__restrict__ host, const int64_t *__restrict__ map,
-                                                     int32_t first, int32_t n, int64_t row_vec,
+                                                     int32_t first, int32_t n, int64_t row_vec, int32_t segs_per_row,
                                                      uint4 *__restrict__ dst) {
-  const int64_t total = (int64_t)n * row_vec;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  for (; i + 3 * stride < total; i += 4 * stride) {
-    uint4 v[4];
-    int64_t d[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int64_t e = i + u * stride, r = e / row_vec, c = e - r * row_vec;
-      v[u] = host[map[2 * (first + r)] * row_vec + c];
-      d[u] = map[2 * (first + r) + 1] * row_vec + c;
+  constexpr int SEG = 2048;  // 32 KB of a row per work item; 4 loads in flight per thread
+  const int32_t items = n * segs_per_row;
+  for (int32_t item = blockIdx.x; item < items; item += gridDim.x) {
+    const int32_t r = item / segs_per_row, sg = item - r * segs_per_row;
+    const int64_t off = (int64_t)sg * SEG;
+    const int32_t len = (int32_t)(row_vec - off < SEG ? row_vec - off : SEG);
+    const uint4 *src = host + map[2 * (first + r)] * row_vec + off;
+    uint4 *out = dst + map[2 * (first + r) + 1] * row_vec + off;
+    int32_t i = threadIdx.x;
+    for (; i + 768 < len; i += 1024) {
+      const uint4 v0 = src[i], v1 = src[i + 256], v2 = src[i + 512], v3 = src[i + 768];
+      out[i] = v0;
+      out[i + 256] = v1;
+      out[i + 512] = v2;
+      out[i + 768] = v3;
     }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) dst[d[u]] = v[u];
-  }
-  for (; i < total; i += stride) {
-    const int64_t r = i / row_vec, c = i - r * row_vec;
-    dst[map[2 * (first + r) + 1] * row_vec + c] = host[map[2 * (first + r)] * row_vec + c];
+    for (; i < len; i += 256) out[i] = src[i];
   }
 }
 
-const int kInputGatherCtas = getenv("COE_INPUT_CTAS") ? atoi(getenv("COE_INPUT_CTAS")) : 32;
+const int kInputGatherCtas = getenv("COE_INPUT_CTAS") ? atoi(getenv("COE_INPUT_CTAS")) : 64;
 
 struct CopyAct {
   int32_t expert;
@@ -2041,7 +2040,9 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     if (!io_mark(ks)) return false;
     if (host_in_dev) {  // one gather kernel per chunk (host rows scattered in need order)
       const int32_t n = chunk_start[k + 1] - chunk_start[k];
-      gather_inputs<<<kInputGatherCtas, 256, 0, ks>>>(host_in_dev, sb.in_map, chunk_start[k], n, (int64_t)(rb / 16),
+      const int64_t row_vec = (int64_t)(rb / 16);
+      gather_inputs<<<kInputGatherCtas, 256, 0, ks>>>(host_in_dev, sb.in_map, chunk_start[k], n, row_vec,
+                                                       (int32_t)((row_vec + 2047) / 2048),
                                                        reinterpret_cast<uint4 *>(rt->act));
       st.h2d_input_bytes += (int64_t)n * (int64_t)rb;
       st.launches += 1;
