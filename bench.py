@@ -420,7 +420,12 @@ def main() -> None:
     end = torch.cuda.Event(enable_timing=True)
     launches = 0
     stats = None
+    # COE_PROFILE_RANGE=1: only the timed steps are profiled (ncu --profile-from-start off), so
+    # the launch list is that of warm steady-state steps, not of the cold first step
+    profile_range = os.environ.get("COE_PROFILE_RANGE") == "1"
     with ClockSampler(not args.no_clocks, local) as clocks, PcieSampler(not args.no_clocks, local) as pcie:
+        if profile_range:
+            torch.cuda.profiler.start()
         start.record(stream)
         for _ in range(args.steps):
             p = take_plan()
@@ -429,6 +434,8 @@ def main() -> None:
             keep.append(p)
         end.record(stream)
         rt.synchronize()
+        if profile_range:
+            torch.cuda.profiler.stop()
     barrier()
     elapsed_ms = start.elapsed_time(end)
     timing = rt.timing()

@@ -160,7 +160,7 @@ __device__ __forceinline__ TileCoord decode_tile(int t, const int32_t *tile_star
   return c;
 }
 
-template <int CG>
+template <int CG, bool CW>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tm_a0, const __grid_constant__ CUtensorMap tm_a1,
                         const __grid_constant__ CUtensorMap tm_a2, const __grid_constant__ CUtensorMap tm_b,
@@ -242,6 +242,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   if (warp == 0) {
     if (lane == 0) {
+      if constexpr (CW) {
       // ===== TMA producer (both CTAs of a pair: own A rows, own half of B) =====
       int stage = 0;
       uint32_t phase = 0;
@@ -253,7 +254,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         int box_row[BM / 32];
         int box_par[BM / 32];
         const int nboxes = e.nboxes;
-        for (int b = 0; b < nboxes; ++b) {
+#pragma unroll
+        for (int b = 0; b < BM / 32; ++b) {
           box_row[b] = e.box_row[b];
           box_par[b] = e.box_par[b];
         }
@@ -270,16 +272,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           uint8_t *sb = sa + TL::A_BYTES;
           if constexpr (CG == 1) {
             sm100::mbar_arrive_expect_tx(&full_bar[stage], a_bytes + TL::B_BYTES);
-            for (int b = 0; b < nboxes; ++b)
-              sm100::tma_load_2d(sa + b * args.a_box_rows * 128,
+#pragma unroll
+            for (int b = 0; b < BM / 32; ++b)
+              if (b < nboxes)
+                sm100::tma_load_2d(sa + b * args.a_box_rows * 128,
                                  box_par[b] == 0 ? &tm_a0 : (box_par[b] == 1 ? &tm_a1 : &tm_a2), &full_bar[stage],
                                  kb * BK, box_row[b]);
             sm100::tma_load_3d(sb, &tm_b, &full_bar[stage], kb * BK, b_row, slot);
           } else {
             const uint32_t bar = sm100::mapa_shared(sm100::smem_u32(&full_bar[stage]), 0);
             if (cta_rank == 0) sm100::mbar_arrive_expect_tx(&full_bar[stage], 2 * TL::STAGE_BYTES);
-            for (int b = 0; b < nboxes; ++b)
-              sm100::tma_load_2d_pair(sa + b * args.a_box_rows * 128,
+#pragma unroll
+            for (int b = 0; b < BM / 32; ++b)
+              if (b < nboxes)
+                sm100::tma_load_2d_pair(sa + b * args.a_box_rows * 128,
                                       box_par[b] == 0 ? &tm_a0 : (box_par[b] == 1 ? &tm_a1 : &tm_a2), bar, kb * BK,
                                       box_row[b]);
             sm100::tma_load_3d_pair(sb, &tm_b, bar, kb * BK, b_row, slot);
@@ -290,8 +296,84 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         }
       }
+      } else {
+      // ===== TMA producer (both CTAs of a pair: own A rows, own half of B) =====
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = tile0; t < total_tiles; t += tile_step) {
+        TileCoord c = decode_tile<CG>(t, tile_start, args.num_groups, args.groups);
+        const coe_mlp_group grp = args.groups[c.g];
+        const int m0 = c.m_blk * TL::TILE_M + (int)cta_rank * BM;  // first row of this CTA's half
+        int box_row[BM / 32];
+        int box_par[BM / 32];
+        int nboxes;
+        uint32_t a_bytes;
+        if (args.mode == 0) {
+          const int boff = args.batch_off[grp.batch];
+          const int members = grp.rows / args.T;
+          if constexpr (CG == 1) {
+            const int rows_here = min(grp.rows - m0, BM);
+            nboxes = (rows_here + args.a_box_rows - 1) / args.a_box_rows;
+          } else {
+            nboxes = BM / args.a_box_rows;  // full boxes: the leader expects a fixed byte count
+          }
+#pragma unroll
+          for (int b = 0; b < BM / 32; ++b) {
+            if (b >= nboxes) break;
+            const int r = m0 + b * args.a_box_rows;
+            int j = r / args.T;
+            const int within = r - j * args.T;
+            j = min(j, members - 1);  // rows past the group (pair tail): any valid member, discarded
+            if (args.member_in) {
+              const int code = args.member_in[boff + j];
+              box_row[b] = (code >> 1) * args.T + within;
+              box_par[b] = (code & 1) ? 0 : 1;
+            } else {
+              box_row[b] = args.member_req[boff + j] * args.T + within;
+              box_par[b] = a_source(args.member_stage[boff + j]);
+            }
+          }
+          a_bytes = (uint32_t)(nboxes * args.a_box_rows * BK * 2);
+        } else {
+          nboxes = 1;
+          box_row[0] = grp.h_row + m0;  // past the H scratch end TMA fills zeros (bytes still counted)
+          box_par[0] = 0;
+          a_bytes = TL::A_BYTES;
+        }
+        const int b_row = c.n_blk * BN + (int)cta_rank * TL::B_ROWS;
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          sm100::mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t *sa = stage_base + stage * TL::STAGE_BYTES;
+          uint8_t *sb = sa + TL::A_BYTES;
+          if constexpr (CG == 1) {
+            sm100::mbar_arrive_expect_tx(&full_bar[stage], a_bytes + TL::B_BYTES);
+#pragma unroll
+            for (int b = 0; b < BM / 32; ++b)
+              if (b < nboxes)
+                sm100::tma_load_2d(sa + b * args.a_box_rows * 128,
+                                 box_par[b] == 0 ? &tm_a0 : (box_par[b] == 1 ? &tm_a1 : &tm_a2), &full_bar[stage],
+                                 kb * BK, box_row[b]);
+            sm100::tma_load_3d(sb, &tm_b, &full_bar[stage], kb * BK, b_row, grp.slot);
+          } else {
+            const uint32_t bar = sm100::mapa_shared(sm100::smem_u32(&full_bar[stage]), 0);
+            if (cta_rank == 0) sm100::mbar_arrive_expect_tx(&full_bar[stage], 2 * TL::STAGE_BYTES);
+#pragma unroll
+            for (int b = 0; b < BM / 32; ++b)
+              if (b < nboxes)
+                sm100::tma_load_2d_pair(sa + b * args.a_box_rows * 128,
+                                      box_par[b] == 0 ? &tm_a0 : (box_par[b] == 1 ? &tm_a1 : &tm_a2), bar, kb * BK,
+                                      box_row[b]);
+            sm100::tma_load_3d_pair(sb, &tm_b, bar, kb * BK, b_row, grp.slot);
+          }
+          if (++stage == TL::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
     }
-  } else if (warp == 3) {
+    }
+  } else if (CW && warp == 3) {
     // ===== coordinate warp: resolves each tile's A boxes, weight slot and output rows ahead
     // of the producer and the epilogue (lanes 0-3: one A box / one lane quarter each) =====
     int cs = 0;
@@ -433,14 +515,50 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     int cs = 0;
     uint32_t cph = 0;
     for (int t = tile0; t < total_tiles; t += tile_step) {
-      sm100::mbar_wait(&crd_full[cs], cph);
-      const bool valid = (int)lane < crd[cs].qvalid[quarter];
-      __nv_bfloat16 *out_row = valid ? crd[cs].qbase[quarter] + lane * out_stride : nullptr;
-      __syncwarp();
-      if (lane == 0) sm100::mbar_arrive(&crd_empty[cs]);
-      if (++cs == CRD_STAGES) {
-        cs = 0;
-        cph ^= 1;
+      bool valid;
+      __nv_bfloat16 *out_row = nullptr;
+      if constexpr (CW) {
+        sm100::mbar_wait(&crd_full[cs], cph);
+        valid = (int)lane < crd[cs].qvalid[quarter];
+        if (valid) out_row = crd[cs].qbase[quarter] + lane * out_stride;
+        __syncwarp();
+        if (lane == 0) sm100::mbar_arrive(&crd_empty[cs]);
+        if (++cs == CRD_STAGES) {
+          cs = 0;
+          cph ^= 1;
+        }
+      } else {
+      TileCoord c = decode_tile<CG>(t, tile_start, args.num_groups, args.groups);
+      const coe_mlp_group grp = args.groups[c.g];
+      const int row = c.m_blk * TL::TILE_M + (int)cta_rank * BM + quarter * 32 + lane;
+      valid = row < grp.rows;
+      if (valid) {
+        if (args.mode == 0) {
+          out_row = args.out_h + (size_t)(grp.h_row + row) * args.N;
+        } else {
+          const int boff = args.batch_off[grp.batch];
+          const int j = row / args.T;
+          if (args.member_out) {
+            const int code = args.member_out[boff + j];
+            const int kind = code & 15;
+            __nv_bfloat16 *dst = kind == 0   ? args.out_act0
+                                 : kind == 1 ? args.out_y
+                                 : kind == 2 ? args.out_stage
+                                             : args.peer_act[kind - 3][0];
+            out_row = dst + ((size_t)(code >> 4) * args.T + (row - j * args.T)) * args.ld;
+          } else {
+            const int req = args.member_req[boff + j];
+            const int st = args.member_stage[boff + j];
+            __nv_bfloat16 *dst = (st & 1) ? args.out_act1 : args.out_act0;
+            if (args.hop_dst) {
+              const int hd = args.hop_dst[(size_t)req * args.hop_stride + st];
+              if (hd >= 0) dst = args.peer_act[hd][st & 1];
+            }
+            out_row = dst + ((size_t)req * args.T + (row - j * args.T)) * args.ld;
+          }
+        }
+        out_row += c.n_blk * BN;
+      }
       }
       sm100::mbar_wait(&tfull_bar[acc], acc_phase);
       sm100::tc_fence_after();
@@ -548,6 +666,7 @@ struct coe_mlp {
   int num_sms;
   int a_box_rows;
   int cg = 2;                        // CTAs per MMA (COE_K3_CG=1 selects the single-CTA kernel)
+  bool cw = true;                    // coordinate warp (COE_K3_COORD=0: producer / epilogue resolve tiles inline)
   CUtensorMap xmap_alt;              // stage-0 inputs from a second X buffer (coe_mlp_set_input)
   const void *x_alt = nullptr;
   bool use_alt = false;
@@ -575,6 +694,7 @@ int coe_mlp_create(const coe_mlp_config *cfg, coe_mlp **out) {
   auto *m = new coe_mlp();
   m->cfg = *cfg;
   if (const char *v = getenv("COE_K3_CG")) m->cg = atoi(v) == 1 ? 1 : 2;
+  if (const char *v = getenv("COE_K3_COORD")) m->cw = atoi(v) != 0;
   m->a_box_rows = cfg->T < BM ? cfg->T : BM;
   bool ok = true;
   const uint64_t ld = cfg->act_ld > 0 ? (uint64_t)cfg->act_ld : (uint64_t)cfg->d;
@@ -597,10 +717,16 @@ int coe_mlp_create(const coe_mlp_config *cfg, coe_mlp **out) {
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&m->num_sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaError_t e = m->cg == 1 ? cudaFuncSetAttribute(grouped_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                     Tiling<1>::SMEM)
-                              : cudaFuncSetAttribute(grouped_gemm_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                     Tiling<2>::SMEM);
+  cudaError_t e = cudaSuccess;
+  for (cudaError_t r : {cudaFuncSetAttribute(grouped_gemm_kernel<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             Tiling<1>::SMEM),
+                        cudaFuncSetAttribute(grouped_gemm_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             Tiling<1>::SMEM),
+                        cudaFuncSetAttribute(grouped_gemm_kernel<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             Tiling<2>::SMEM),
+                        cudaFuncSetAttribute(grouped_gemm_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             Tiling<2>::SMEM)})
+    if (r != cudaSuccess) e = r;
   if (e != cudaSuccess) {
     delete m;
     coe_set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
@@ -718,7 +844,8 @@ static int launch_grouped(coe_mlp *m, const coe_mlp_group *groups_up, const coe_
     cudaError_t e;
     if (m->cg == 1) {
       const int grid = a.total_tiles < cap ? a.total_tiles : cap;
-      grouped_gemm_kernel<1><<<grid, NUM_THREADS, Tiling<1>::SMEM, stream>>>(ta0, ta1, ta2, tb, a);
+      if (m->cw) grouped_gemm_kernel<1, true><<<grid, NUM_THREADS, Tiling<1>::SMEM, stream>>>(ta0, ta1, ta2, tb, a);
+      else grouped_gemm_kernel<1, false><<<grid, NUM_THREADS, Tiling<1>::SMEM, stream>>>(ta0, ta1, ta2, tb, a);
       e = cudaGetLastError();
     } else {
       // pairs: at most one per 128-row tile (the kernel recounts 256-row pair tiles itself)
@@ -735,7 +862,8 @@ static int launch_grouped(coe_mlp *m, const coe_mlp_group *groups_up, const coe_
       attr[0].val.clusterDim.z = 1;
       lc.attrs = attr;
       lc.numAttrs = 1;
-      e = cudaLaunchKernelEx(&lc, grouped_gemm_kernel<2>, ta0, ta1, ta2, tb, a);
+      e = m->cw ? cudaLaunchKernelEx(&lc, grouped_gemm_kernel<2, true>, ta0, ta1, ta2, tb, a)
+                : cudaLaunchKernelEx(&lc, grouped_gemm_kernel<2, false>, ta0, ta1, ta2, tb, a);
     }
     if (e != cudaSuccess) {
       coe_set_error(std::string("grouped_gemm_kernel launch: ") + cudaGetErrorString(e));
