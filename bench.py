@@ -482,8 +482,10 @@ def main() -> None:
         e2e = {"value": n_req * args.e2e_steps / (e2e_ms / 1e3), "unit": "requests/s",
                "h2d_bytes_per_step": io["h2d_input_bytes"], "d2h_bytes_per_step": io["d2h_output_bytes"],
                "ms_per_step": e2e_ms / args.e2e_steps,
-               "note": "planner (each step's plan made on a host thread one step ahead) + stage-0 inputs streamed H2D just in time (32 MB chunks on the swap-in copy "
-                       "engine) + final outputs gathered per wave and streamed D2H in completion order, all "
+               "note": "planner (each step's plan made on a host thread one step ahead) + stage-0 inputs streamed H2D just in time "
+                       "(32 MB chunks in need order, each read from the pinned host rows by one gather kernel on the "
+                       "swap-in copy stream) + final outputs stored per wave into the staging ring and streamed D2H "
+                       "in completion order, all "
                        "inside the timed region; swap-ins and inputs share the PCIe H2D link"}
 
     planner.shutdown(wait=True)

@@ -116,6 +116,7 @@ struct GemmArgs {
   const int32_t *member_out;
   __nv_bfloat16 *out_y;
   __nv_bfloat16 *out_stage;
+  int debug;  // experiments only (COE_K3_DEBUG): bit 0 skips the epilogue stores, bit 1 the gelu
 };
 
 // A-operand source of a member at chain stage s: 0 = X, 1 = P0, 2 = P1.
@@ -570,13 +571,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int k = 0; k < CHUNKS; ++k) {
         uint32_t(&cur)[32] = v[k & 1];
         if (k + 1 < CHUNKS) sm100::tmem_ld_32x32b_x32(taddr + (chunk0 + k + 1) * 32, v[(k + 1) & 1]);
-        if (valid) {
+        if (valid && !(args.debug & 1)) {
           uint32_t packed[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             float lo = __uint_as_float(cur[2 * i]);
             float hi = __uint_as_float(cur[2 * i + 1]);
-            if (args.mode == 0) {
+            if (args.mode == 0 && !(args.debug & 2)) {
               lo = gelu_tanh(lo);
               hi = gelu_tanh(hi);
             }
@@ -666,7 +667,8 @@ struct coe_mlp {
   int num_sms;
   int a_box_rows;
   int cg = 2;                        // CTAs per MMA (COE_K3_CG=1 selects the single-CTA kernel)
-  bool cw = true;                    // coordinate warp (COE_K3_COORD=0: producer / epilogue resolve tiles inline)
+  int cw = -1;  // coordinate warp: -1 auto (up passes with K <= 2048: +6-10 %; elsewhere -1-3 %,
+                // profiles/r2o_k3_coord_ab.json), 0 / 1 forced by COE_K3_COORD
   CUtensorMap xmap_alt;              // stage-0 inputs from a second X buffer (coe_mlp_set_input)
   const void *x_alt = nullptr;
   bool use_alt = false;
@@ -694,7 +696,7 @@ int coe_mlp_create(const coe_mlp_config *cfg, coe_mlp **out) {
   auto *m = new coe_mlp();
   m->cfg = *cfg;
   if (const char *v = getenv("COE_K3_CG")) m->cg = atoi(v) == 1 ? 1 : 2;
-  if (const char *v = getenv("COE_K3_COORD")) m->cw = atoi(v) != 0;
+  if (const char *v = getenv("COE_K3_COORD")) m->cw = atoi(v) != 0 ? 1 : 0;
   m->a_box_rows = cfg->T < BM ? cfg->T : BM;
   bool ok = true;
   const uint64_t ld = cfg->act_ld > 0 ? (uint64_t)cfg->act_ld : (uint64_t)cfg->d;
@@ -837,14 +839,16 @@ static int launch_grouped(coe_mlp *m, const coe_mlp_group *groups_up, const coe_
     a.member_out = member_out;
     a.out_y = m->out_y;
     a.out_stage = m->out_stage;
+    a.debug = getenv("COE_K3_DEBUG") ? atoi(getenv("COE_K3_DEBUG")) : 0;
     if (a.total_tiles <= 0) continue;
     int cap = (max_ctas > 0 && max_ctas < m->num_sms) ? max_ctas : m->num_sms;
     const CUtensorMap &ta0 = pass == 0 ? (m->use_alt ? m->xmap_alt : m->xmap) : m->hmap, &ta1 = pass == 0 ? m->act0 : m->hmap,
                       &ta2 = pass == 0 ? (member_in ? m->act0 : m->act1) : m->hmap, &tb = pass == 0 ? m->w1 : m->w2;
     cudaError_t e;
+    const bool cw = m->cw >= 0 ? m->cw == 1 : (pass == 0 && a.K <= 2048);
     if (m->cg == 1) {
       const int grid = a.total_tiles < cap ? a.total_tiles : cap;
-      if (m->cw) grouped_gemm_kernel<1, true><<<grid, NUM_THREADS, Tiling<1>::SMEM, stream>>>(ta0, ta1, ta2, tb, a);
+      if (cw) grouped_gemm_kernel<1, true><<<grid, NUM_THREADS, Tiling<1>::SMEM, stream>>>(ta0, ta1, ta2, tb, a);
       else grouped_gemm_kernel<1, false><<<grid, NUM_THREADS, Tiling<1>::SMEM, stream>>>(ta0, ta1, ta2, tb, a);
       e = cudaGetLastError();
     } else {
@@ -862,7 +866,7 @@ static int launch_grouped(coe_mlp *m, const coe_mlp_group *groups_up, const coe_
       attr[0].val.clusterDim.z = 1;
       lc.attrs = attr;
       lc.numAttrs = 1;
-      e = m->cw ? cudaLaunchKernelEx(&lc, grouped_gemm_kernel<2, true>, ta0, ta1, ta2, tb, a)
+      e = cw ? cudaLaunchKernelEx(&lc, grouped_gemm_kernel<2, true>, ta0, ta1, ta2, tb, a)
                 : cudaLaunchKernelEx(&lc, grouped_gemm_kernel<2, false>, ta0, ta1, ta2, tb, a);
     }
     if (e != cudaSuccess) {
