@@ -54,7 +54,8 @@ constexpr int NUM_THREADS = 384;
 constexpr int EPI_WARP0 = 4;
 constexpr int EPI_WARPS = 8;  // two warps per TMEM lane quarter, each drains half the columns
 constexpr int MAX_GROUPS = 1024;
-constexpr int CRD_STAGES = 6;  // tile-coordinate ring (warp 3 -> TMA producer + epilogue warps)
+constexpr int CRD_STAGES = 6;
+constexpr int EPI_SCRATCH = 2048;  // per epilogue warp: one 32-row x 32-column bf16 chunk, staged for coalesced stores  // tile-coordinate ring (warp 3 -> TMA producer + epilogue warps)
 
 // Per-tile coordinates resolved ahead by the coordinate warp (warp 3): the dependent global
 // loads (group -> batch offset -> member routes) leave the TMA producer's and the epilogue's
@@ -82,7 +83,7 @@ struct Tiling {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = CG == 1 ? 4 : 6;
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + MAX_GROUPS * 4 +
-                              CRD_STAGES * 128;
+                              CRD_STAGES * 128 + EPI_WARPS * EPI_SCRATCH;
 };
 
 struct GemmArgs {
@@ -178,6 +179,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   int32_t *total_slot = reinterpret_cast<int32_t *>(tmem_slot + 1);
   int32_t *tile_start = reinterpret_cast<int32_t *>(smem + TL::STAGES * TL::STAGE_BYTES + 256);
   TileCrd *crd = reinterpret_cast<TileCrd *>(smem + TL::STAGES * TL::STAGE_BYTES + 256 + MAX_GROUPS * 4);
+  uint8_t *epi_scratch = smem + TL::STAGES * TL::STAGE_BYTES + 256 + MAX_GROUPS * 4 + CRD_STAGES * 128;
   uint64_t *crd_full = reinterpret_cast<uint64_t *>(tmem_slot + 2);  // after tmem_slot / total_slot, 8-aligned
   uint64_t *crd_empty = crd_full + CRD_STAGES;
 
@@ -508,6 +510,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // quarter and split its 256 columns; TMEM loads run one 32-column chunk ahead) =====
     const uint32_t quarter = warp & 3;
     const int chunk0 = (int)((warp - EPI_WARP0) >> 2) * (BN / 32 / 2);
+    uint8_t *my_scratch = epi_scratch + (warp - EPI_WARP0) * EPI_SCRATCH;
     constexpr int CHUNKS = BN / 32 / 2;
     const uint32_t tempty_leader = CG == 2 ? sm100::mapa_shared(sm100::smem_u32(&tempty_bar[0]), 0) : 0;
     const size_t out_stride = args.mode == 0 ? (size_t)args.N : (size_t)args.ld;
@@ -563,6 +566,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       sm100::mbar_wait(&tfull_bar[acc], acc_phase);
       sm100::tc_fence_after();
+      // coalesced stores: each lane holds one row's 32 columns (64 B); the chunk is staged in the
+      // warp's scratch (16 B units XOR-swizzled by row: conflict-free both ways) and written back
+      // as 8 rows x 64 B per store instruction -- full 32 B sectors instead of 32 rows x 16 B
+      if (!valid) out_row = nullptr;
+      uint64_t row_ptr[4];  // rows it * 8 + lane / 4 of this quarter (null: outside the group)
+#pragma unroll
+      for (int it = 0; it < 4; ++it)
+        row_ptr[it] = __shfl_sync(0xffffffffu, reinterpret_cast<uint64_t>(out_row), it * 8 + (int)(lane >> 2));
+      const uint32_t piece = lane & 3;
       const uint32_t taddr = tmem_base + ((quarter * 32) << 16) + acc * BN;
       uint32_t v[2][32];
       sm100::tmem_ld_32x32b_x32(taddr + chunk0 * 32, v[0]);
@@ -571,7 +583,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int k = 0; k < CHUNKS; ++k) {
         uint32_t(&cur)[32] = v[k & 1];
         if (k + 1 < CHUNKS) sm100::tmem_ld_32x32b_x32(taddr + (chunk0 + k + 1) * 32, v[(k + 1) & 1]);
-        if (valid && !(args.debug & 1)) {
+        if (!(args.debug & 1)) {
           uint32_t packed[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
@@ -583,10 +595,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
             packed[i] = pack_bf16(lo, hi);
           }
-          uint4 *dst = reinterpret_cast<uint4 *>(out_row + (chunk0 + k) * 32);
+          const uint32_t sw = (lane >> 1) & 3;
 #pragma unroll
           for (int i = 0; i < 4; ++i)
-            dst[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
+            *reinterpret_cast<uint4 *>(my_scratch + lane * 64 + ((i ^ sw) << 4)) =
+                make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
+          __syncwarp();
+#pragma unroll
+          for (int it = 0; it < 4; ++it) {
+            const uint32_t rr = it * 8 + (lane >> 2);
+            if (row_ptr[it]) {
+              const uint4 val = *reinterpret_cast<const uint4 *>(my_scratch + rr * 64 + ((piece ^ ((rr >> 1) & 3)) << 4));
+              reinterpret_cast<uint4 *>(reinterpret_cast<__nv_bfloat16 *>(row_ptr[it]) + (chunk0 + k) * 32)[piece] = val;
+            }
+          }
+          __syncwarp();
         }
         if (k + 1 < CHUNKS) sm100::tmem_ld_wait_regs(v[(k + 1) & 1]);
       }
