@@ -33,6 +33,9 @@ def main() -> None:
         stream = [dataclasses.replace(r, arrival_time_s=i * gap) for i, r in enumerate(base.stream)]
         w = dataclasses.replace(base, stream=stream)
         cfg = configs.run_config(w, trace=False)
+        if os.environ.get("ALLOC_COUNT"):  # expert budget as alloc_override={'gpu': N} (bench --alloc-count)
+            cfg = configs.run_config(w, trace=False, alloc_override={"gpu": int(os.environ["ALLOC_COUNT"])},
+                                     search_enabled=False)
         plan = engine.plan(cfg)
         metrics = engine.metrics_from_plan(plan)
         counts = [int(o["count"]) for o in plan.ops() if o["kind"] == 1]
@@ -61,7 +64,7 @@ def main() -> None:
                "gb_swapped": st["load_bytes"] / 1e9, "waves": st["waves"]}
         rows.append(row)
         print(json.dumps(row), flush=True)
-    json.dump({"config": name, "requests": nreq, "rows": rows,
+    json.dump({"config": name, "requests": nreq, "alloc_count": os.environ.get("ALLOC_COUNT"), "rows": rows,
                "note": "stream re-timed to arrival i*gap; measured = GPU capacity executing the planner's schedule "
                        "for that rate (device-resident inputs, CUDA events); virtual = the reference's simulated "
                        "throughput (bounded by the offered load)"}, open(out, "w"), indent=1)

@@ -131,9 +131,22 @@ if summary["shapes"]:
 
 kg = grouping()
 if kg:
-    summ = {"launches": kg, "note": "ncu --set full, one bench step of C3 (13,642 admissions): K1 counting read + "
-                                    "one-kernel 8-bit LSD passes (decoupled look-back), K2 compaction. Latency-bound: "
-                                    "~218 KB of algorithmic traffic per step (16 B per admission)",
+    summ = {"launches": kg, "note": "ncu --set full --profile-from-start off, one WARM bench step of C3 (13,642 "
+                                    "admissions, 2,400 batches): at serving size K1 + K2 run as ONE 1,024-thread block "
+                                    "(coe_group_compact_fused: stable sort by run-rank in shared memory, member / route "
+                                    "gather, batch scan, run check). Latency-bound: ~218 KB of algorithmic traffic per "
+                                    "step (16 B per admission)",
             "total_us": sum(k["duration_us"] for k in kg), "total_dram_bytes": sum(k["dram_bytes"] for k in kg)}
     json.dump(summ, open(os.path.join(PROF, f"{tag}_k12_ncu_summary.json"), "w"), indent=1)
     print(json.dumps(summ, indent=1))
+
+# bench lines and sweeps of this round: last JSON line of each gpurun_out/<tag>_bench_*.log
+for fn in sorted(os.listdir(OUT)) if os.path.isdir(OUT) else []:
+    m = re.fullmatch(re.escape(tag) + r"_(bench_[a-z0-9_]+)\.log", fn)
+    if m:
+        lines = [l for l in open(os.path.join(OUT, fn)) if l.startswith("{")]
+        if lines:
+            open(os.path.join(PROF, f"{tag}_{m.group(1)}.json"), "w").write(lines[-1])
+            print("bench line ->", f"profiles/{tag}_{m.group(1)}.json")
+    if fn == f"{tag}_rate_sweep_c5_10000.json":
+        open(os.path.join(PROF, fn), "w").write(open(os.path.join(OUT, fn)).read())
