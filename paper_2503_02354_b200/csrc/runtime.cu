@@ -53,6 +53,7 @@
 #include "common.cuh"
 #include "act_rows.h"
 #include "hops.h"
+#include "sm100.cuh"
 
 namespace {
 
@@ -106,7 +107,55 @@ __global__ void __launch_bounds__(256) gather_inputs(const uint4 *__restrict__ h
   }
 }
 
+// Bulk-copy (TMA) variant: one thread per CTA moves 4 KB pieces host -> shared -> HBM with
+// cp.async.bulk (large PCIe reads issued by the TMA unit instead of 16-byte loads), two pieces
+// in flight per CTA; 8 KB of shared memory fits next to a resident K3 CTA.
+constexpr int kBulkPiece = 4096, kBulkStages = 2;
+__global__ void __launch_bounds__(32) gather_inputs_bulk(const char *__restrict__ host, const int64_t *__restrict__ map,
+                                                         int32_t first, int32_t n, int64_t row_bytes,
+                                                         char *__restrict__ dst) {
+  __shared__ alignas(128) uint8_t buf[kBulkStages][kBulkPiece];
+  __shared__ alignas(8) uint64_t bar[kBulkStages];
+  if (threadIdx.x != 0) return;
+  const int64_t per_row = row_bytes / kBulkPiece;
+  const int64_t total = (int64_t)n * per_row;
+  for (int s = 0; s < kBulkStages; ++s) sm100::mbar_init(&bar[s], 1);
+  sm100::fence_mbar_init();
+  auto src_of = [&](int64_t p) {
+    const int64_t r = p / per_row, off = (p - r * per_row) * kBulkPiece;
+    return host + map[2 * (first + r)] * row_bytes + off;
+  };
+  auto dst_of = [&](int64_t p) {
+    const int64_t r = p / per_row, off = (p - r * per_row) * kBulkPiece;
+    return dst + map[2 * (first + r) + 1] * row_bytes + off;
+  };
+  auto load = [&](int64_t p, int s) {
+    sm100::mbar_arrive_expect_tx(&bar[s], kBulkPiece);
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     sm100::smem_u32(buf[s])),
+                 "l"(src_of(p)), "r"(kBulkPiece), "r"(sm100::smem_u32(&bar[s]))
+                 : "memory");
+  };
+  int64_t p = blockIdx.x;
+  for (int s = 0; s < kBulkStages && p + (int64_t)s * gridDim.x < total; ++s) load(p + (int64_t)s * gridDim.x, s);
+  for (int64_t it = 0; p < total; ++it, p += gridDim.x) {
+    const int s = (int)(it % kBulkStages);
+    sm100::mbar_wait(&bar[s], (uint32_t)((it / kBulkStages) & 1));
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst_of(p)),
+                 "r"(sm100::smem_u32(buf[s])), "r"(kBulkPiece)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    const int64_t nxt = p + (int64_t)kBulkStages * gridDim.x;
+    if (nxt < total) {
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // buf[s] read by the store
+      load(nxt, s);
+    }
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 const int kInputGatherCtas = getenv("COE_INPUT_CTAS") ? atoi(getenv("COE_INPUT_CTAS")) : 64;
+const bool kInputBulk = getenv("COE_INPUT_BULK") && atoi(getenv("COE_INPUT_BULK")) != 0;  // experiment
 
 struct CopyAct {
   int32_t expert;
@@ -2018,9 +2067,11 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     return ok(cudaEventRecord(rt->t_io[io_n++], s_), "record");
   };
   const size_t rb = (size_t)rt->row_elems * 2;
-  const bool two_queues = getenv("COE_INPUT_DMA") && atoi(getenv("COE_INPUT_DMA")) == 2;
+  // experiment COE_INPUT_QUEUE: 0 = the swap-in copy stream (one H2D queue), 1 = a second
+  // queue for every input chunk (inputs and swap-ins share the link concurrently), 2 = odd chunks
+  const int input_queue = getenv("COE_INPUT_QUEUE") ? atoi(getenv("COE_INPUT_QUEUE")) : 0;
   auto upload_inputs = [&](int32_t k) -> bool {
-    const cudaStream_t ks = (two_queues && (k & 1)) ? rt->copy_in : rt->copy;  // odd chunks: second queue
+    const cudaStream_t ks = (input_queue == 1 || (input_queue == 2 && (k & 1))) ? rt->copy_in : rt->copy;
     if (!in_prev_waited && rt->prev_nccl_hold && rt->have_step_end) {  // slots held for NCCL sends
       in_prev_waited = true;
       if (!ok(cudaStreamWaitEvent(ks, rt->step_end, 0), "inputs wait last step")) return false;
@@ -2040,6 +2091,15 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     if (!io_mark(ks)) return false;
     if (host_in_dev) {  // one gather kernel per chunk (host rows scattered in need order)
       const int32_t n = chunk_start[k + 1] - chunk_start[k];
+      if (kInputBulk && rb % kBulkPiece == 0) {
+        gather_inputs_bulk<<<kInputGatherCtas, 32, 0, ks>>>(reinterpret_cast<const char *>(host_in_dev), sb.in_map,
+                                                             chunk_start[k], n, (int64_t)rb,
+                                                             reinterpret_cast<char *>(rt->act));
+        st.h2d_input_bytes += (int64_t)n * (int64_t)rb;
+        st.launches += 1;
+        return ok(cudaGetLastError(), "gather_inputs_bulk") && io_mark(ks) &&
+               ok(cudaEventRecord(rt->in_ev[k], ks), "record");
+      }
       const int64_t row_vec = (int64_t)(rb / 16);
       gather_inputs<<<kInputGatherCtas, 256, 0, ks>>>(host_in_dev, sb.in_map, chunk_start[k], n, row_vec,
                                                        (int32_t)((row_vec + 2047) / 2048),
