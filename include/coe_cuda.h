@@ -207,6 +207,11 @@ typedef struct coe_step_input {
    * one D2H copy -- and coe_runtime_output_order names the request of every output row */
   const void *host_inputs;
   void *host_outputs;
+  /* (f3) initial residency of EVERY executor, CSR over executors (optional: null disables
+   * physical peer copies -- peer-tier LOADs are then served from the host tier) */
+  int32_t num_executors;
+  const int32_t *initial_offsets;           /* [num_executors + 1]                          */
+  const int32_t *initial_all;
 } coe_step_input;
 
 /* Activation rows one step of `in` needs on executor in->executor (host only, no GPU):
@@ -224,6 +229,9 @@ typedef struct coe_step_stats {
   int32_t rank_bits;
   int32_t ring_peak;        /* activation ring slots occupied at most during the step  */
   int32_t landing_rows;     /* landing rows the step's hop-ins used                     */
+  int64_t peer_loads;       /* (f3) peer-tier LOADs copied from another executor's HBM  */
+  int64_t peer_bytes;
+  int64_t peer_tier_loads;  /* peer-tier LOADs in the plan (the rest came from the host) */
 } coe_step_stats;
 
 typedef struct coe_step_timing {
@@ -349,6 +357,14 @@ int coe_hop(coe_comm *comm, const void *sendbuf, const int64_t *send_counts, voi
 /* Attach to a runtime (rank == the executor it serves); steps then exchange
  * hopped activations on a dedicated hop stream. */
 int coe_runtime_attach_comm(coe_runtime *rt, coe_comm *comm);
+/* (f3) Peer-GPU swap-in tier for executors of ONE process (one runtime each, stepped in
+ * lockstep and synchronised between steps: runtime.step_executors).  A peer-tier LOAD of
+ * expert e from executor j is copied from j's HBM (cudaMemcpyPeerAsync) when e was resident
+ * on j when the previous step ended, is in j's initial placement and is not a victim of any
+ * of j's LOADs in this plan -- so j never rewrites those bytes during the step; otherwise it
+ * is served from the host tier (identical bytes, decisions unchanged).  peers[r] = the
+ * runtime of executor r (world entries; peers[rank] is rt itself). */
+int coe_runtime_attach_local_experts(coe_runtime *rt, coe_runtime *const *peers, int32_t world);
 /* scheduling knobs (see coe_runtime_config); reserve_sms < 0 keeps the current split */
 int coe_runtime_set_knobs(coe_runtime *rt, int64_t wave_rows_cap, int64_t urgent_rows_cap, int32_t reserve_sms);
 

@@ -164,6 +164,9 @@ struct CopyAct {
   std::vector<int32_t> wait_waves;  // last issued reader wave of the bytes overwritten, per stream (this step)
   std::vector<int32_t> wait_prev;   // slot * NCLS + stream: last step's readers (slot_free events)
   int32_t unit0 = -1;               // pooled: first unit of the expert's new place
+  const char *peer_src = nullptr;   // (f3) peer executor's bytes (else host store / generate)
+  coe_runtime *peer_rt = nullptr;
+  int32_t peer_par = 0;
 };
 
 struct WaveAct {
@@ -391,6 +394,14 @@ struct coe_runtime {
   cudaStream_t hop = nullptr;
   std::vector<cudaEvent_t> recv_ev;
   cudaEvent_t hop_drained = nullptr, step_end = nullptr;
+  // (f3) peer-GPU swap-in tier between runtimes of one process: at the end of every step the
+  // runtime records where each resident expert's bytes live (double-buffered by step parity,
+  // so a peer in the next step reads a stable copy) and an event after the step's work
+  int device = 0;
+  int64_t step_count = 0;
+  std::vector<const char *> res_snap[2];
+  cudaEvent_t res_ready[2] = {nullptr, nullptr};
+  std::vector<coe_runtime *> local_peers;
   bool have_step_end = false;
   // fused hops over peer memory (coe_runtime_attach_peers): K3's down pass stores a hopping
   // request's rows into the destination executor's P buffer; flags are published with stream
@@ -448,7 +459,7 @@ struct coe_runtime {
     }
     for (auto &u : out_hist) cudaEventDestroy(u.ev);
     for (cudaEvent_t e : {out_drained, hop_drained, step_end, staged, copy_drained, grouped, cls_drained[0], cls_drained[1], cls_drained[2], t_step_start, t_group_end, t_step_end, staging_done[0],
-                          staging_done[1]})
+                          staging_done[1], res_ready[0], res_ready[1]})
       if (e) cudaEventDestroy(e);
     for (auto st : cls_stream)
       if (st) cudaStreamDestroy(st);
@@ -641,6 +652,9 @@ int coe_runtime_create(const coe_runtime_config *cfg, coe_runtime **out) {
               ok(cudaStreamCreateWithFlags(&rt->hop, cudaStreamNonBlocking), "stream") &&
               ok(cudaStreamCreateWithFlags(&rt->out_stream, cudaStreamNonBlocking), "stream") &&
               ok(cudaStreamCreateWithFlags(&rt->copy_in, cudaStreamNonBlocking), "stream") &&
+              ok(cudaGetDevice(&rt->device), "device") &&
+              ok(cudaEventCreateWithFlags(&rt->res_ready[0], cudaEventDisableTiming), "event") &&
+              ok(cudaEventCreateWithFlags(&rt->res_ready[1], cudaEventDisableTiming), "event") &&
               (!c.device_io || (dmalloc(&rt->x, io_bytes, "X alloc") && dmalloc(&rt->y, io_bytes, "Y alloc"))) &&
               dmalloc(&rt->act, a_rows * rt->row_elems * 2, "activation ring alloc") &&
               dmalloc(&rt->outbuf, (int64_t)rt->out_slots * rt->row_elems * 2, "output staging alloc") &&
@@ -970,6 +984,15 @@ int coe_runtime_set_knobs(coe_runtime *rt, int64_t wave_rows_cap, int64_t urgent
   return COE_CUDA_OK;
 }
 
+int coe_runtime_attach_local_experts(coe_runtime *rt, coe_runtime *const *peers, int32_t world) {
+  if (world < 1 || !peers) {
+    coe_set_error("attach_local_experts: bad peer list");
+    return COE_CUDA_ERR_CONFIG;
+  }
+  rt->local_peers.assign(peers, peers + world);
+  return COE_CUDA_OK;
+}
+
 int coe_runtime_attach_comm(coe_runtime *rt, coe_comm *comm) {
   rt->comm = comm;
   return COE_CUDA_OK;
@@ -1195,6 +1218,9 @@ struct CopyInfo {
   bool first_write;                // slot not written earlier this step
   std::vector<int32_t> deps;       // slots whose readers must finish first (pooled: the units' last users)
   int32_t unit0 = -1;              // pooled: first unit of the expert's new place
+  const char *peer_src = nullptr;  // (f3) copy from this peer executor's HBM instead of the host store
+  coe_runtime *peer_rt = nullptr;
+  int32_t peer_par = 0;            // parity of the peer's snapshot / ready event
   double up_end = 0.0, end = 0.0;  // estimated
   bool issued = false;
   int64_t op_pos = 0;              // op-log position of the LOAD (restores: of the first batch)
@@ -1435,13 +1461,29 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     if (rt->store_off[e] >= 0) (restore ? st.restore_bytes : st.load_bytes) += rt->sbytes[k];  // else: generated
     return true;
   };
+  // (f3) physical source of a peer-tier LOAD: executor j's bytes, when they were resident on j
+  // at the end of the previous step, e is in j's initial placement (so j's step start keeps
+  // it) and no LOAD of j in this plan evicts it -- j never rewrites them during this step
+  std::vector<std::vector<uint8_t>> peer_keep(rt->local_peers.size());
+  auto peer_source = [&](int32_t j, int32_t e) -> const char * {
+    if (j < 0 || j >= (int32_t)rt->local_peers.size() || !rt->local_peers[j] || j == x || rt->step_count == 0 ||
+        !in->initial_offsets || j >= in->num_executors)
+      return nullptr;
+    coe_runtime *pr = rt->local_peers[j];
+    const auto &snap = pr->res_snap[(rt->step_count - 1) & 1];
+    if (e >= (int32_t)snap.size() || !snap[e]) return nullptr;
+    if (peer_keep[j].empty()) {
+      peer_keep[j].assign(c.num_experts, 0);
+      for (int32_t i = in->initial_offsets[j]; i < in->initial_offsets[j + 1]; ++i) peer_keep[j][in->initial_all[i]] = 1;
+      for (int64_t i = 0; i < in->num_ops; ++i)
+        if (ops[i].executor == j && ops[i].kind == COE_OP_LOAD)
+          for (int32_t v = 0; v < ops[i].count; ++v) peer_keep[j][in->op_args[ops[i].offset + v]] = 0;
+    }
+    return peer_keep[j][e] ? snap[e] : nullptr;
+  };
   for (size_t k = 0; k < my_ops.size(); ++k) {
     const coe_op &op = ops[my_ops[k]];
     if (op.kind == COE_OP_LOAD) {
-      if (op.tier == COE_TIER_PEER) {
-        coe_set_error("plan has a peer-tier LOAD (RunConfig.peer_tier): peer swap-ins are not executed by this runtime");
-        return COE_CUDA_ERR_CONFIG;
-      }
       for (int32_t j = 0; j < op.count; ++j) {
         int32_t v = in->op_args[op.offset + j];
         plan_res[v] = 0;
@@ -1461,6 +1503,15 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
         if (rt->pooled) pool_free(s);
       }
       if (!issue_copy(op.expert, false, my_ops[k])) return COE_CUDA_ERR_CHECK;
+      if (op.tier == COE_TIER_PEER) {
+        st.peer_tier_loads += 1;
+        if (const char *src = peer_source(op.seq, op.expert)) {
+          CopyInfo &ci = copies.back();
+          ci.peer_src = src;
+          ci.peer_rt = rt->local_peers[op.seq];
+          ci.peer_par = (int32_t)((rt->step_count - 1) & 1);
+        }
+      }
       continue;
     }
     const int32_t e = op.expert;
@@ -1848,6 +1899,9 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
         ca.slot = ci.slot;
         ca.restore = ci.restore;
         ca.unit0 = ci.unit0;
+        ca.peer_src = ci.peer_src;
+        ca.peer_rt = ci.peer_rt;
+        ca.peer_par = ci.peer_par;
         for (int32_t q : ci.deps)  // the slot itself, and (VMM) the last users of its pages
           for (int k = 0; k < NCLS; ++k) {
             const int32_t wv = last_reader_wave[q * NCLS + k];
@@ -2195,7 +2249,11 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
       for (int32_t sk : cp.wait_prev)
         if (!ok(cudaStreamWaitEvent(ks, rt->slot_free_up[sk], 0), "copy waits last step")) return fail_cuda();
       if (c.profile && !ok(cudaEventRecord(rt->t_copy_start[a.index], ks), "record")) return fail_cuda();
-      if (generate) {
+      if (cp.peer_src) {  // (f3) NVLink / same-device copy from the peer executor's HBM
+        if (!ok(cudaStreamWaitEvent(ks, cp.peer_rt->res_ready[cp.peer_par], 0), "peer copy waits peer") ||
+            !ok(cudaMemcpyPeerAsync(dst, rt->device, cp.peer_src, cp.peer_rt->device, half_bytes, ks), "peer W1"))
+          return fail_cuda();
+      } else if (generate) {
         if (coe_fill_uniform_bf16(dst, half_bytes / 2, coe_expert_seed(c.weight_seed, cp.expert, 0),
                                   sqrtf(3.0f / rt->sd[ksh]), ks))
           return COE_CUDA_ERR_CUDA;
@@ -2207,7 +2265,14 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
         if (!ok(cudaStreamWaitEvent(ks, wave_down_ev[wv], 0), "copy waits W2 readers")) return fail_cuda();
       for (int32_t sk : cp.wait_prev)
         if (!ok(cudaStreamWaitEvent(ks, rt->slot_free_down[sk], 0), "copy waits last step")) return fail_cuda();
-      if (generate) {
+      if (cp.peer_src) {
+        if (!ok(cudaMemcpyPeerAsync(dst + half_bytes, rt->device, cp.peer_src + half_bytes, cp.peer_rt->device,
+                                    half_bytes, ks),
+                "peer W2"))
+          return fail_cuda();
+        st.peer_loads += 1;
+        st.peer_bytes += 2 * half_bytes;
+      } else if (generate) {
         if (coe_fill_uniform_bf16(dst + half_bytes, half_bytes / 2, coe_expert_seed(c.weight_seed, cp.expert, 1),
                                   sqrtf(3.0f / rt->sh[ksh]), ks))
           return COE_CUDA_ERR_CUDA;
@@ -2335,6 +2400,17 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
   if (!ok(cudaEventRecord(sb.free_ev, cs), "record") || !ok(cudaEventRecord(rt->step_end, cs), "record"))
     return fail_cuda();
   rt->have_step_end = true;
+  {  // (f3) where each resident expert's bytes live once this step's work is done
+    const int par = (int)(rt->step_count & 1);
+    auto &snap = rt->res_snap[par];
+    snap.assign(c.num_experts, nullptr);
+    for (int32_t e = 0; e < c.num_experts; ++e) {
+      const int32_t sl = rt->expert_slot[e];
+      if (sl >= 0) snap[e] = rt->pooled ? rt->pool + (int64_t)rt->slot_unit[sl] * rt->unit : rt->slot_ptr(sl);
+    }
+    if (!ok(cudaEventRecord(rt->res_ready[par], cs), "record")) return fail_cuda();
+    rt->step_count += 1;
+  }
   // the ring carries over: the free list in release order, and for the next step's input
   // uploads the wave (this parity) whose up pass last read each slot freed in this step
   std::fill(rt->act_prev_wave.begin(), rt->act_prev_wave.end(), -1);

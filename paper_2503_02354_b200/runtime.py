@@ -37,6 +37,7 @@ class StepInput(ctypes.Structure):
         ("num_op_args", ctypes.c_int64), ("op_args", ctypes.c_void_p),
         ("num_initial", ctypes.c_int32), ("initial", ctypes.c_void_p),
         ("host_inputs", ctypes.c_void_p), ("host_outputs", ctypes.c_void_p),
+        ("num_executors", ctypes.c_int32), ("initial_offsets", ctypes.c_void_p), ("initial_all", ctypes.c_void_p),
     ]
 
 
@@ -45,7 +46,8 @@ class StepStats(ctypes.Structure):
                                                "d2h_output_bytes", "loads", "load_bytes",
                                                "restores", "restore_bytes", "max_wave_rows")] + \
                [("max_wave_groups", ctypes.c_int32), ("rank_bits", ctypes.c_int32), ("ring_peak", ctypes.c_int32),
-                ("landing_rows", ctypes.c_int32)]
+                ("landing_rows", ctypes.c_int32), ("peer_loads", ctypes.c_int64), ("peer_bytes", ctypes.c_int64),
+                ("peer_tier_loads", ctypes.c_int64)]
 
     def as_dict(self) -> dict:
         return {name: getattr(self, name) for name, _ in self._fields_}
@@ -148,6 +150,8 @@ def _lib():
         lib.coe_runtime_ipc_open.restype = ctypes.c_int
         lib.coe_runtime_attach_peers.argtypes = [V, I32, I32, V, V]
         lib.coe_runtime_attach_peers.restype = ctypes.c_int
+        lib.coe_runtime_attach_local_experts.argtypes = [V, V, I32]
+        lib.coe_runtime_attach_local_experts.restype = ctypes.c_int
         lib.coe_runtime_plan_rows.argtypes = [P(StepInput), I32, ctypes.c_int, ctypes.c_int, P(I32), P(I32)]
         lib.coe_runtime_plan_rows.restype = ctypes.c_int
         lib.coe_expert_seed.argtypes = [ctypes.c_uint64, I32, I32]
@@ -473,14 +477,18 @@ class B200Runtime:
         out per wave in completion order (``output_order()`` names each row's request)."""
         lib = plan.lib
         h = plan.handle
-        init = np.ascontiguousarray(plan.initial_residency()[executor], dtype=np.int32)
-        self._init_keep = init
+        residency = plan.initial_residency()
+        init = np.ascontiguousarray(residency[executor], dtype=np.int32)
+        off = np.cumsum([0] + [len(r) for r in residency]).astype(np.int32)
+        flat = np.ascontiguousarray(np.concatenate([np.asarray(r, np.int32) for r in residency] + [np.zeros(1, np.int32)]))
+        self._init_keep = (init, off, flat)
         inp = StepInput(
             executor,
             lib.coe_plan_num_admissions(h), ctypes.cast(lib.coe_plan_admissions(h), ctypes.c_void_p),
             lib.coe_plan_num_ops(h), ctypes.cast(lib.coe_plan_ops(h), ctypes.c_void_p),
             lib.coe_plan_num_op_args(h), ctypes.cast(lib.coe_plan_op_args(h), ctypes.c_void_p),
             len(init), init.ctypes.data if len(init) else None, host_inputs, host_outputs,
+            len(residency), off.ctypes.data, flat.ctypes.data,
         )
         stats = StepStats()
         _check(self.lib, self.lib.coe_runtime_step(self.handle, ctypes.byref(inp), ctypes.byref(stats)), "step")
@@ -604,11 +612,14 @@ class LocalHub:
 def attach_peers_local(runtimes: list) -> "LocalHub":
     """Fused hops between runtimes of ONE process (several executors on one GPU): each stores
     straight into the others' buffers; readiness is handed over through a LocalHub (pass it
-    to step_executors, which resets it between steps)."""
+    to step_executors, which resets it between steps).  Also enables the (f3) peer-GPU
+    swap-in tier between them (coe_runtime_attach_local_experts)."""
     hub = LocalHub(len(runtimes))
     peers = [rt.peer_buffers() for rt in runtimes]
+    handles = (ctypes.c_void_p * len(runtimes))(*[rt.handle.value for rt in runtimes])
     for x, rt in enumerate(runtimes):
         rt._attach_peers(x, peers, hub)
+        _check(rt.lib, rt.lib.coe_runtime_attach_local_experts(rt.handle, handles, len(runtimes)), "attach experts")
     return hub
 
 
@@ -658,7 +669,7 @@ def _step_input(plan, executor: int) -> StepInput:
                      lib.coe_plan_num_admissions(h), ctypes.cast(lib.coe_plan_admissions(h), ctypes.c_void_p),
                      lib.coe_plan_num_ops(h), ctypes.cast(lib.coe_plan_ops(h), ctypes.c_void_p),
                      lib.coe_plan_num_op_args(h), ctypes.cast(lib.coe_plan_op_args(h), ctypes.c_void_p),
-                     0, None, None, None)
+                     0, None, None, None, 0, None, None)
 
 
 def plan_rows(plan, executor: int = 0, e2e: bool = True, nccl: bool = False) -> tuple:

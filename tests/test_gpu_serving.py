@@ -559,3 +559,58 @@ def test_c4_full_shape_two_executors_fused_hops():
     for rt in rts:
         rt.close()
     assert worst <= TOL, worst
+
+
+def test_peer_tier_swap_ins_between_executors():
+    """(f3) Peer-GPU swap-in tier, executed: config 5 on three in-process executors (a small
+    physical expert shape) with RunConfig.peer_tier -- every LOAD is a peer-tier load.  The
+    first step has no peer snapshot yet, so its peer-tier loads come from the host tier; from
+    the second step on they are copied from the source executor's HBM (cudaMemcpyPeerAsync)
+    when the planner's choice is physically safe (resident there since the previous step,
+    never evicted there in this step).  Grouping and outputs are identical either way and
+    match the numpy fp32 chain."""
+    import torch
+
+    peer = {"read_bandwidth_bytes_per_s": 720e9, "fixed_load_overhead_s": 1e-5}
+    w = _trim(configs.load("c5", 1000, gpu_executors=3), 300)
+    plan = engine.plan(configs.run_config(w, trace=False, peer_tier=peer))
+    docs = w.docs
+    ref = des.simulate(docs["registry"], docs["device"], docs["stream"], routes=docs["routes"], trace=False,
+                       peer_tier=peer, **w.run)
+    ids, rid = plan.resolved.expert_ids, plan.resolved.request_ids
+    for x in range(3):
+        ours = [(ids[e], [(rid[r], s) for r, s in m]) for e, m in runtime.batches_from_plan(plan, executor=x)]
+        assert ours == [(e, list(m)) for xx, e, m in ref["batches"] if xx == x]
+    n_peer = sum(1 for t, src in zip(ref["loads"], ref["load_src"]) if t[3] == "peer")
+    assert n_peer > 0
+    shape = runtime.RuntimeShape(1024, 2048, 64)
+    rts = []
+    for x in range(3):
+        rt = runtime.B200Runtime.for_plan(plan, shape, executor=x)
+        rt.fill_inputs(len(rid))
+        rts.append(rt)
+    hub = runtime.attach_peers_local(rts)
+    n = len(rid)
+    chains = plan.resolved.chains
+    final_exec = {}
+    for x in range(3):
+        for _e, members in runtime.batches_from_plan(plan, executor=x):
+            for r, s in members:
+                if s == len(chains[r]) - 1:
+                    final_exec[r] = x
+    outs, peer_counts = [], []
+    for _step in range(3):
+        stats = runtime.step_executors(plan, rts, hub)
+        assert sum(s["peer_tier_loads"] for s in stats) == n_peer
+        peer_counts.append(sum(s["peer_loads"] for s in stats))
+        per_exec = []
+        for x, rt in enumerate(rts):
+            assert rt.check()[1] == 0
+            host = torch.empty(n * shape.T * shape.d, dtype=torch.bfloat16).pin_memory()
+            rt.download_outputs(runtime.last_stages(plan), host.data_ptr())
+            rt.synchronize()
+            per_exec.append(host.view(n, shape.T, shape.d).float().numpy().copy())
+        outs.append(np.stack([per_exec[final_exec[r]][r] for r in range(n)]))
+    assert peer_counts[0] == 0 and peer_counts[1] > 0 and peer_counts[2] == peer_counts[1], peer_counts
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[1], outs[2])
+    _check_outputs(plan, outs[1:2], shape, sample=12)
