@@ -388,8 +388,10 @@ def main() -> None:
     # alone before the serving loop heats the part (roofline peak: the burst figure)
     max_batch = max(e.max_batch for e in plan0.resolved.perf.entries.values())
     k3_shape = shape if isinstance(shape, runtime.RuntimeShape) else rt.shapes[0]
-    groups = max(1, min(16, (32768 // k3_shape.T) // max_batch, n_req // max_batch))
-    if rt.expert_pool_bytes:  # pooled experts: placed on demand, no fixed slot for an isolated wave
+    groups = max(1, min(16, (rt.max_wave_rows // k3_shape.T) // max_batch, n_req // max_batch))
+    if rt.expert_pool_bytes or groups * max_batch * k3_shape.T > rt.max_wave_rows:
+        # pooled experts are placed on demand (no fixed slot for an isolated wave); a wave cap
+        # below one profiled batch (the whole-device-12 GB variant) leaves no isolated wave
         up_ms = down_ms = None
     else:
         up_ms, down_ms = rt.bench_mlp(groups, max_batch, iters=10)

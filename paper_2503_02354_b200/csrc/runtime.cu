@@ -1424,16 +1424,25 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     ci.deps.push_back(best);
     if (rt->pooled) {  // best-fit run of free units; wait for the readers of whatever used them last
       const int32_t n = (int32_t)((rt->sbytes[k] + rt->unit - 1) / rt->unit);
+      // best fit; large experts (>= 256 MB) take the top of their run and small ones the
+      // bottom, so the two size classes drift to opposite ends instead of interleaving
+      // (a simulation of C5's plans at 1-1000 us arrival gaps: no load ever fails with three
+      // largest experts of slack, tools/pool_sim.py)
+      const bool big = rt->sbytes[k] >= (256ll << 20);
       auto pick = rt->free_runs.end();
       for (auto it = rt->free_runs.begin(); it != rt->free_runs.end(); ++it)
-        if (it->second >= n && (pick == rt->free_runs.end() || it->second < pick->second)) pick = it;
+        if (it->second >= n && (pick == rt->free_runs.end() || it->second < pick->second ||
+                                (big && it->second == pick->second)))
+          pick = it;
       if (pick == rt->free_runs.end()) {
         coe_set_error("pooled expert memory: no free run for a load (byte budget exceeded or fragmented)");
         return false;
       }
-      const int32_t u0 = pick->first, len = pick->second;
+      const int32_t start = pick->first, len = pick->second;
+      const int32_t u0 = big ? start + len - n : start;
       rt->free_runs.erase(pick);
-      if (len > n) rt->free_runs.emplace(u0 + n, len - n);
+      if (u0 > start) rt->free_runs.emplace(start, u0 - start);
+      if (u0 + n < start + len) rt->free_runs.emplace(u0 + n, start + len - u0 - n);
       const std::vector<int32_t> *last_rd = nullptr;
       for (int32_t u = u0; u < u0 + n; ++u) {
         const int32_t owner = rt->unit_owner[u];

@@ -358,12 +358,13 @@ class B200Runtime:
         if kw.pop("pooled", True):
             # one slab for every shape, addressed in 2 MB units: the planner's byte budget
             # (capped by what this executor ever holds at once), unit rounding per resident
-            # expert, and one largest expert of slack against fragmentation (best-fit)
+            # expert, and three largest experts of slack against fragmentation (best fit, size
+            # classes at opposite ends; tools/pool_sim.py)
             counts = [int((expert_shape == i).sum()) for i in range(len(shapes))]
             held = sum(int(p) * s.expert_bytes for p, s in zip(peak, shapes))
             largest = max(s.expert_bytes for s, p in zip(shapes, peak) if p > 0)
             kw.setdefault("expert_pool_bytes",
-                          int(min(budget, held)) + largest + int(peak.sum()) * POOL_UNIT)
+                          int(min(budget, held)) + 3 * largest + int(peak.sum()) * POOL_UNIT)
             return cls(shapes, len(ids), counts, len(resolved.request_ids), adm, expert_shape=expert_shape, **kw)
         slots = [max(1, int(p)) for p in peak]  # per-shape slabs of each shape's peak residency
         return cls(shapes, len(ids), slots, len(resolved.request_ids), adm, expert_shape=expert_shape, **kw)
