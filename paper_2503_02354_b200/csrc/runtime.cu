@@ -2090,8 +2090,12 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
   int32_t *d_exec = sb.adm, *d_rank = sb.adm + n_adm, *d_req = sb.adm + 2 * n_adm, *d_stage = sb.adm + 3 * n_adm;
   int idx_bits = 1;
   while ((1ll << idx_bits) < n_adm) ++idx_bits;
-  const bool fused = n_adm >= 1 && n_adm <= COE_FUSED_MAX_ADMISSIONS && n_batches <= COE_FUSED_MAX_BATCHES &&
-                     rank_bits + idx_bits + 1 <= 32 && !getenv("COE_GROUP_MULTI");
+  // one-block K1+K2 only for small steps: at C3's 13,642 admissions the single block takes
+  // ~100 us (ncu, profiles/r2r_k12_ncu_summary.json) against ~39 us for the multi-block
+  // kernels (profiles/r1m_k12_ncu_summary.json), so launch count is not worth it there
+  static const int64_t fused_max = getenv("COE_FUSED_MAX") ? atoll(getenv("COE_FUSED_MAX")) : 4096;
+  const bool fused = n_adm >= 1 && n_adm <= std::min<int64_t>(fused_max, COE_FUSED_MAX_ADMISSIONS) &&
+                     n_batches <= COE_FUSED_MAX_BATCHES && rank_bits + idx_bits + 1 <= 32 && !getenv("COE_GROUP_MULTI");
   rt->last_group_fused = fused;
   if (fused) {  // serving size: K1 + K2 in one block, one launch
     int rc = coe_group_compact_fused(d_rank, d_req, d_stage, sb.adm + 4 * n_adm, sb.adm + 5 * n_adm, n_adm, rank_bits,

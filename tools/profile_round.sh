@@ -27,7 +27,7 @@ for w in "16 6 4096 12288 256" "11 22 2048 8192 128" "11 44 1024 4096 64"; do
     -o gpurun_out/k3_full_$1_$2_$3x$4x$5 python tools/k3_profile.py $1 $2 1 $3 $4 $5 \
     > gpurun_out/${TAG}_ncu_k3_$3.log 2>&1
 done
-COE_PROFILE_RANGE=1 timeout 900 ncu --profile-from-start off --set full --clock-control none -k regex:"group|radix|onesweep|compact|batch" -c 4 -f \
+COE_PROFILE_RANGE=1 timeout 900 ncu --profile-from-start off --set full --clock-control none -k regex:"group_compact|radix|onesweep|compact_batches|batch_block|scan_block" -c 4 -f \
   -o gpurun_out/k12_full python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-clocks \
   > gpurun_out/${TAG}_ncu_k12.log 2>&1
 ALLOC_COUNT=201 timeout 1800 python tools/rate_sweep.py c5 10000 gpurun_out/${TAG}_rate_sweep_c5_10000.json > gpurun_out/${TAG}_rate_sweep_c5.log 2>&1
