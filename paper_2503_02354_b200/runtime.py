@@ -544,22 +544,35 @@ class B200Runtime:
 
     def per_shape_k3(self) -> dict:
         """Profile mode, after a step: per expert shape, the algorithmic FLOPs of its waves and
-        the summed durations of their up + down K3 launches (CUDA events on the launching
-        streams) -> achieved TFLOP/s per shape."""
+        the GPU time they used.  K3 launches of different waves overlap (two main streams and
+        the release stream), so each instant of K3 activity is shared equally among the
+        launches running then (``k3_ms``; these sum to the K3 busy time of the step) ->
+        achieved TFLOP/s per shape.  ``launch_ms``: the plain sum of launch durations."""
         ph = self.wave_phases()
         nw = len(ph["flops"])
         idx = np.zeros(max(1, nw), np.int32)
         self.lib.coe_runtime_wave_shapes.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
         _check(self.lib, self.lib.coe_runtime_wave_shapes(self.handle, idx.ctypes.data), "wave shapes")
-        out = {}
+        keys, iv = [], []
         for i in range(nw):
             s = self.shapes[int(idx[i])]
-            key = f"{s.d}x{s.h}x{s.T}"
+            keys.append(f"{s.d}x{s.h}x{s.T}")
             u0, u1, d0, d1 = ph["phases"][i]
-            e = out.setdefault(key, {"waves": 0, "flops": 0.0, "k3_ms": 0.0})
+            iv += [(u0, u1, i), (d0, d1, i)]
+        share = np.zeros(max(1, nw))
+        edges = sorted({t for a, b, _ in iv for t in (a, b)})
+        for t0, t1 in zip(edges[:-1], edges[1:]):
+            active = [i for a, b, i in iv if a <= t0 and b >= t1 and b > a]
+            for i in active:
+                share[i] += (t1 - t0) / len(active)
+        out = {}
+        for i in range(nw):
+            u0, u1, d0, d1 = ph["phases"][i]
+            e = out.setdefault(keys[i], {"waves": 0, "flops": 0.0, "k3_ms": 0.0, "launch_ms": 0.0})
             e["waves"] += 1
             e["flops"] += ph["flops"][i]
-            e["k3_ms"] += (u1 - u0) + (d1 - d0)
+            e["k3_ms"] += float(share[i])
+            e["launch_ms"] += (u1 - u0) + (d1 - d0)
         for e in out.values():
             e["tflops"] = e["flops"] / (e["k3_ms"] / 1e3) / 1e12 if e["k3_ms"] > 0 else None
         return out
