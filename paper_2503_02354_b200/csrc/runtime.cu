@@ -2134,9 +2134,11 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     return ok(cudaEventRecord(rt->t_io[io_n++], s_), "record");
   };
   const size_t rb = (size_t)rt->row_elems * 2;
-  // experiment COE_INPUT_QUEUE: 0 = the swap-in copy stream (one H2D queue), 1 = a second
-  // queue for every input chunk (inputs and swap-ins share the link concurrently), 2 = odd chunks
-  const int input_queue = getenv("COE_INPUT_QUEUE") ? atoi(getenv("COE_INPUT_QUEUE")) : 0;
+  // COE_INPUT_QUEUE: 1 (default) = input chunks on their own queue, so the gather kernels'
+  // PCIe reads and the swap-in DMAs share the link concurrently (C3 e2e 1,493 -> 1,412 ms,
+  // tools/timeline.py; the gather alone reaches ~42 GB/s, the DMA fills the rest); 0 = the
+  // swap-in copy stream (one H2D queue); 2 = odd chunks on the second queue
+  const int input_queue = getenv("COE_INPUT_QUEUE") ? atoi(getenv("COE_INPUT_QUEUE")) : 1;
   auto upload_inputs = [&](int32_t k) -> bool {
     const cudaStream_t ks = (input_queue == 1 || (input_queue == 2 && (k & 1))) ? rt->copy_in : rt->copy;
     if (!in_prev_waited && rt->prev_nccl_hold && rt->have_step_end) {  // slots held for NCCL sends

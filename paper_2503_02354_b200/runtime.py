@@ -304,8 +304,12 @@ class B200Runtime:
         kw.setdefault("ring_slots", max(1, ring))
         kw.setdefault("landing_slots", landing)
         if isinstance(shape, RuntimeShape):
-            largest = max(spec.param_bytes for spec in registry.experts.values())
-            slots = max(1, min(int(budget // largest), int(touched.sum()) or 1))
+            # one physical shape for every expert (the config's own, or a small stand-in for a
+            # heterogeneous registry): as many slots as this executor holds at once in the
+            # planner's byte accounting (never more than budget // bytes for a uniform registry)
+            # (physically resident experts are always a subset of the plan's pool at that moment:
+            # initial residents not yet evicted, or loaded / restored -- so its peak bounds them)
+            slots = max(1, int(_peak_residency(plan, executor, np.zeros(len(ids), np.int32), 1, lazy=False)[0]))
             if not kw.get("store_path"):  # a shared store must hold every expert at fixed offsets
                 kw.setdefault("store_mask", stored)
             return cls(shape, len(ids), slots, len(resolved.request_ids), adm, **kw)
@@ -326,33 +330,7 @@ class B200Runtime:
         # planner's byte-budgeted pool (expert_pool.py:27-59) holds at once, shape by shape
         # An initially resident expert only takes HBM once materialised: the runtime restores it
         # at its first batch (an expert this executor never runs needs no slot)
-        cur = np.zeros(len(shapes), np.int64)
-        peak = cur.copy()
-        pending = {int(e) for e in plan.initial_residency()[executor]}
-        live = set()
-        args = plan.op_args()
-        for op in plan.ops():
-            if op["executor"] != executor:
-                continue
-            e = int(op["expert"])
-            if op["kind"] == _native.OP_LOAD:
-                o = int(op["offset"])
-                for v in args[o:o + int(op["count"])]:
-                    v = int(v)
-                    pending.discard(v)
-                    if v in live:
-                        live.discard(v)
-                        cur[expert_shape[v]] -= 1
-                pending.discard(e)
-            elif e not in pending:
-                continue
-            else:
-                pending.discard(e)
-            if e not in live:
-                live.add(e)
-                k = expert_shape[e]
-                cur[k] += 1
-                peak[k] = max(peak[k], cur[k])
+        peak = _peak_residency(plan, executor, expert_shape, len(shapes), lazy=False)
         if not kw.get("store_path"):
             kw.setdefault("store_mask", stored)
         if kw.pop("pooled", True):
@@ -675,6 +653,45 @@ def nccl_library() -> str:
     except Exception:
         pass
     return "libnccl.so.2"
+
+
+def _peak_residency(plan, executor: int, expert_shape: np.ndarray, num_shapes: int, lazy: bool = True) -> np.ndarray:
+    """Per shape, the most experts this executor's op log holds in HBM at once (initial
+    placement, then each LOAD's victims out and its expert in).  lazy: an initially resident
+    expert only counts once materialised (the runtime restores it at its first batch)."""
+    cur = np.zeros(num_shapes, np.int64)
+    pending = {int(e) for e in plan.initial_residency()[executor]}
+    live = set()
+    if not lazy:
+        for e in pending:
+            live.add(e)
+            cur[expert_shape[e]] += 1
+        pending = set()
+    peak = cur.copy()
+    args = plan.op_args()
+    for op in plan.ops():
+        if op["executor"] != executor:
+            continue
+        e = int(op["expert"])
+        if op["kind"] == _native.OP_LOAD:
+            o = int(op["offset"])
+            for v in args[o:o + int(op["count"])]:
+                v = int(v)
+                pending.discard(v)
+                if v in live:
+                    live.discard(v)
+                    cur[expert_shape[v]] -= 1
+            pending.discard(e)
+        elif e not in pending:
+            continue
+        else:
+            pending.discard(e)
+        if e not in live:
+            live.add(e)
+            k = expert_shape[e]
+            cur[k] += 1
+            peak[k] = max(peak[k], cur[k])
+    return peak
 
 
 def _step_input(plan, executor: int) -> StepInput:
