@@ -1497,9 +1497,16 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     }
     rt->slot_units[q] = 0;
   };
-  for (int32_t s = 0; s < NS; ++s) {  // slots outside the initial placement are free again
+  // experts this executor's op log touches (loads or batches) in this step
+  std::vector<uint8_t> touched(c.num_experts, 0);
+  for (int64_t i = 0; i < in->num_ops; ++i)
+    if (ops[i].executor == x && ops[i].expert >= 0 && ops[i].expert < c.num_experts) touched[ops[i].expert] = 1;
+  // slots outside the initial placement are free again, and so are residents this step never
+  // uses: what is physically resident is then always part of the planner's pool at that
+  // moment, restricted to the experts this step touches (the runtime's slot sizing)
+  for (int32_t s = 0; s < NS; ++s) {
     int32_t e = rt->slot_expert[s];
-    if (e >= 0 && !plan_res[e]) {
+    if (e >= 0 && (!plan_res[e] || !touched[e])) {
       rt->expert_slot[e] = -1;
       rt->slot_expert[s] = -1;
       if (rt->pooled) pool_free(s);

@@ -658,12 +658,16 @@ def nccl_library() -> str:
 def _peak_residency(plan, executor: int, expert_shape: np.ndarray, num_shapes: int, lazy: bool = True) -> np.ndarray:
     """Per shape, the most experts this executor's op log holds in HBM at once (initial
     placement, then each LOAD's victims out and its expert in).  lazy: an initially resident
-    expert only counts once materialised (the runtime restores it at its first batch)."""
+    expert only counts once materialised (the runtime restores it at its first batch); else
+    from the start, if this executor ever touches it -- a bound on what is physically
+    resident whatever earlier steps left behind (the runtime frees untouched residents at
+    step start)."""
     cur = np.zeros(num_shapes, np.int64)
     pending = {int(e) for e in plan.initial_residency()[executor]}
     live = set()
-    if not lazy:
-        for e in pending:
+    if not lazy:  # initial residents count from the start -- those this executor ever touches
+        touched = {int(op["expert"]) for op in plan.ops() if op["executor"] == executor}
+        for e in pending & touched:
             live.add(e)
             cur[expert_shape[e]] += 1
         pending = set()
