@@ -195,6 +195,7 @@ struct CopyAct {
   int32_t unit0 = -1;               // pooled: first unit of the expert's new place
   const char *peer_src = nullptr;   // (f3) peer executor's bytes (else host store / generate)
   coe_runtime *peer_rt = nullptr;
+  int32_t peer_exec = -1;
   int32_t peer_par = 0;
 };
 
@@ -431,6 +432,12 @@ struct coe_runtime {
   std::vector<const char *> res_snap[2];
   cudaEvent_t res_ready[2] = {nullptr, nullptr};
   std::vector<coe_runtime *> local_peers;
+  // ... and between processes (CUDA IPC): each peer's expert allocations mapped here, the
+  // peer's end-of-step residency (exchanged on the host after every step, as slab<<40|offset
+  // codes), and whether a peer read our experts last step (our copies then wait for its end)
+  std::vector<std::vector<char *>> peer_exp_base;      // [rank][slab]
+  std::vector<std::vector<const char *>> ipc_snap;     // [rank][expert] (previous step)
+  bool peer_read_prev = false;
   bool have_step_end = false;
   // fused hops over peer memory (coe_runtime_attach_peers): K3's down pass stores a hopping
   // request's rows into the destination executor's P buffer; flags are published with stream
@@ -1086,6 +1093,64 @@ int coe_runtime_attach_local_experts(coe_runtime *rt, coe_runtime *const *peers,
   return COE_CUDA_OK;
 }
 
+int coe_runtime_ipc_export_experts(coe_runtime *rt, void *handles, int32_t *count) {
+  auto *h = static_cast<cudaIpcMemHandle_t *>(handles);
+  const int n = rt->pooled ? 1 : rt->S;
+  for (int k = 0; k < n; ++k)
+    if (!ok(cudaIpcGetMemHandle(&h[k], rt->pooled ? rt->pool : rt->slabs[k]), "ipc export experts")) return fail_cuda();
+  *count = n;
+  return COE_CUDA_OK;
+}
+
+int coe_runtime_ipc_open_experts(coe_runtime *rt, int32_t rank, const void *handles, int32_t count) {
+  const auto *h = static_cast<const cudaIpcMemHandle_t *>(handles);
+  if (rank < 0 || count < 1) {
+    coe_set_error("ipc_open_experts: bad rank / count");
+    return COE_CUDA_ERR_CONFIG;
+  }
+  if ((int)rt->peer_exp_base.size() <= rank) rt->peer_exp_base.resize(rank + 1);
+  rt->peer_exp_base[rank].clear();
+  for (int k = 0; k < count; ++k) {
+    void *p = nullptr;
+    if (!ok(cudaIpcOpenMemHandle(&p, h[k], cudaIpcMemLazyEnablePeerAccess), "ipc open experts")) return fail_cuda();
+    rt->ipc_opened.push_back(p);
+    rt->peer_exp_base[rank].push_back(static_cast<char *>(p));
+  }
+  return COE_CUDA_OK;
+}
+
+int coe_runtime_residency_codes(coe_runtime *rt, int64_t *codes) {
+  if (rt->step_count == 0) {
+    for (int32_t e = 0; e < rt->cfg.num_experts; ++e) codes[e] = -1;
+    return COE_CUDA_OK;
+  }
+  const auto &snap = rt->res_snap[(rt->step_count - 1) & 1];
+  for (int32_t e = 0; e < rt->cfg.num_experts; ++e) {
+    codes[e] = -1;
+    if (e >= (int32_t)snap.size() || !snap[e]) continue;
+    const int k = rt->pooled ? 0 : rt->expert_shape[e];
+    const char *base = rt->pooled ? rt->pool : rt->slabs[k];
+    codes[e] = ((int64_t)k << 40) | (int64_t)(snap[e] - base);
+  }
+  return COE_CUDA_OK;
+}
+
+int coe_runtime_set_peer_residency(coe_runtime *rt, int32_t rank, const int64_t *codes) {
+  if (rank < 0 || rank >= (int32_t)rt->peer_exp_base.size() || rt->peer_exp_base[rank].empty()) {
+    coe_set_error("set_peer_residency: the peer's experts are not mapped (coe_runtime_ipc_open_experts)");
+    return COE_CUDA_ERR_CONFIG;
+  }
+  if ((int)rt->ipc_snap.size() <= rank) rt->ipc_snap.resize(rank + 1);
+  auto &snap = rt->ipc_snap[rank];
+  snap.assign(rt->cfg.num_experts, nullptr);
+  for (int32_t e = 0; e < rt->cfg.num_experts; ++e) {
+    if (codes[e] < 0) continue;
+    const int64_t k = codes[e] >> 40, off = codes[e] & ((1ll << 40) - 1);
+    if (k < (int64_t)rt->peer_exp_base[rank].size()) snap[e] = rt->peer_exp_base[rank][k] + off;
+  }
+  return COE_CUDA_OK;
+}
+
 int coe_runtime_attach_comm(coe_runtime *rt, coe_comm *comm) {
   rt->comm = comm;
   return COE_CUDA_OK;
@@ -1312,7 +1377,8 @@ struct CopyInfo {
   std::vector<int32_t> deps;       // slots whose readers must finish first (pooled: the units' last users)
   int32_t unit0 = -1;              // pooled: first unit of the expert's new place
   const char *peer_src = nullptr;  // (f3) copy from this peer executor's HBM instead of the host store
-  coe_runtime *peer_rt = nullptr;
+  coe_runtime *peer_rt = nullptr;  // in-process peer (else another process: peer_exec's IPC mapping)
+  int32_t peer_exec = -1;
   int32_t peer_par = 0;            // parity of the peer's snapshot / ready event
   double up_end = 0.0, end = 0.0;  // estimated
   bool issued = false;
@@ -1602,14 +1668,9 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
   // (f3) physical source of a peer-tier LOAD: executor j's bytes, when they were resident on j
   // at the end of the previous step, e is in j's initial placement (so j's step start keeps
   // it) and no LOAD of j in this plan evicts it -- j never rewrites them during this step
-  std::vector<std::vector<uint8_t>> peer_keep(rt->local_peers.size());
-  auto peer_source = [&](int32_t j, int32_t e) -> const char * {
-    if (j < 0 || j >= (int32_t)rt->local_peers.size() || !rt->local_peers[j] || j == x || rt->step_count == 0 ||
-        !in->initial_offsets || j >= in->num_executors)
-      return nullptr;
-    coe_runtime *pr = rt->local_peers[j];
-    const auto &snap = pr->res_snap[(rt->step_count - 1) & 1];
-    if (e >= (int32_t)snap.size() || !snap[e]) return nullptr;
+  std::vector<std::vector<uint8_t>> peer_keep(std::max<size_t>(rt->local_peers.size(), rt->ipc_snap.size()));
+  auto keep_of = [&](int32_t j) -> std::vector<uint8_t> & {
+    if ((int32_t)peer_keep.size() <= j) peer_keep.resize(j + 1);
     if (peer_keep[j].empty()) {
       peer_keep[j].assign(c.num_experts, 0);
       for (int32_t i = in->initial_offsets[j]; i < in->initial_offsets[j + 1]; ++i) peer_keep[j][in->initial_all[i]] = 1;
@@ -1617,7 +1678,17 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
         if (ops[i].executor == j && ops[i].kind == COE_OP_LOAD)
           for (int32_t v = 0; v < ops[i].count; ++v) peer_keep[j][in->op_args[ops[i].offset + v]] = 0;
     }
-    return peer_keep[j][e] ? snap[e] : nullptr;
+    return peer_keep[j];
+  };
+  auto peer_source = [&](int32_t j, int32_t e) -> const char * {
+    if (j < 0 || j == x || rt->step_count == 0 || !in->initial_offsets || j >= in->num_executors) return nullptr;
+    const std::vector<const char *> *snap = nullptr;
+    if (j < (int32_t)rt->local_peers.size() && rt->local_peers[j])  // in-process peer
+      snap = &rt->local_peers[j]->res_snap[(rt->step_count - 1) & 1];
+    else if (j < (int32_t)rt->ipc_snap.size())  // another process: its residency, exchanged after the last step
+      snap = &rt->ipc_snap[j];
+    if (!snap || e >= (int32_t)snap->size() || !(*snap)[e]) return nullptr;
+    return keep_of(j)[e] ? (*snap)[e] : nullptr;
   };
   for (size_t k = 0; k < my_ops.size(); ++k) {
     const coe_op &op = ops[my_ops[k]];
@@ -1646,7 +1717,8 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
         if (const char *src = peer_source(op.seq, op.expert)) {
           CopyInfo &ci = copies.back();
           ci.peer_src = src;
-          ci.peer_rt = rt->local_peers[op.seq];
+          ci.peer_rt = op.seq < (int32_t)rt->local_peers.size() ? rt->local_peers[op.seq] : nullptr;
+          ci.peer_exec = op.seq;
           ci.peer_par = (int32_t)((rt->step_count - 1) & 1);
         }
       }
@@ -1697,6 +1769,18 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     }
     slot_readers[b.slot].push_back(bi);
     batches.push_back(std::move(b));
+  }
+  // (f3, between processes) do other executors copy experts out of this one's HBM this step?
+  // Then next step's copies into this HBM must wait for their end (see phase C)
+  bool read_by_peers = false;
+  if (peer_mode && !rt->peer_hub && in->initial_offsets && rt->step_count > 0 && x < in->num_executors) {
+    const auto &mine = rt->res_snap[(rt->step_count - 1) & 1];
+    for (int64_t i = 0; i < in->num_ops && !read_by_peers; ++i) {
+      const coe_op &o = ops[i];
+      if (o.executor != x && o.kind == COE_OP_LOAD && o.tier == COE_TIER_PEER && o.seq == x &&
+          o.expert < (int32_t)mine.size() && mine[o.expert] && keep_of(x)[o.expert])
+        read_by_peers = true;
+    }
   }
   const int64_t n_batches = (int64_t)batches.size();
   if (n_batches > c.max_batches) {
@@ -2039,6 +2123,7 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
         ca.unit0 = ci.unit0;
         ca.peer_src = ci.peer_src;
         ca.peer_rt = ci.peer_rt;
+        ca.peer_exec = ci.peer_exec;
         ca.peer_par = ci.peer_par;
         for (int32_t q : ci.deps)  // the slot itself, and (VMM) the last users of its pages
           for (int k = 0; k < NCLS; ++k) {
@@ -2420,6 +2505,10 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
   };
   // issue() for sends must only see producers already issued in phase C
   std::fill(issued.begin(), issued.end(), 0);
+  if (peer_mode && !rt->peer_hub && rt->peer_read_prev)  // peers read our experts last step
+    for (int r = 0; r < rt->peer_world; ++r)
+      if (r != x && !wait_flag(ks, rt->d_hflags + rt->hflag_step_base + r, seq - 1)) return COE_CUDA_ERR_CUDA;
+  rt->peer_read_prev = read_by_peers;
 
   const coe_mlp_group *dg_up = sb.groups, *dg_down = sb.groups + n_batches;
   for (const Action &a : actions) {
@@ -2440,9 +2529,15 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
         if (!ok(cudaStreamWaitEvent(ks, rt->slot_free_up[sk], 0), "copy waits last step")) return fail_cuda();
       if (c.profile && !ok(cudaEventRecord(rt->t_copy_start[a.index], ks), "record")) return fail_cuda();
       if (cp.peer_src) {  // (f3) NVLink / same-device copy from the peer executor's HBM
-        if (!ok(cudaStreamWaitEvent(ks, cp.peer_rt->res_ready[cp.peer_par], 0), "peer copy waits peer") ||
-            !ok(cudaMemcpyPeerAsync(dst, rt->device, cp.peer_src, cp.peer_rt->device, half_bytes, ks), "peer W1"))
-          return fail_cuda();
+        if (cp.peer_rt) {  // in-process: its ready event of the previous step
+          if (!ok(cudaStreamWaitEvent(ks, cp.peer_rt->res_ready[cp.peer_par], 0), "peer copy waits peer") ||
+              !ok(cudaMemcpyPeerAsync(dst, rt->device, cp.peer_src, cp.peer_rt->device, half_bytes, ks), "peer W1"))
+            return fail_cuda();
+        } else {  // another process: its end of the previous step (step fence flag), then a UVA copy
+          if (!wait_flag(ks, rt->d_hflags + rt->hflag_step_base + cp.peer_exec, seq - 1) ||
+              !ok(cudaMemcpyAsync(dst, cp.peer_src, half_bytes, cudaMemcpyDefault, ks), "peer W1"))
+            return fail_cuda();
+        }
       } else if (generate) {
         if (coe_fill_uniform_bf16(dst, half_bytes / 2, coe_expert_seed(c.weight_seed, cp.expert, 0),
                                   sqrtf(3.0f / rt->sd[ksh]), ks))
@@ -2456,9 +2551,12 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
       for (int32_t sk : cp.wait_prev)
         if (!ok(cudaStreamWaitEvent(ks, rt->slot_free_down[sk], 0), "copy waits last step")) return fail_cuda();
       if (cp.peer_src) {
-        if (!ok(cudaMemcpyPeerAsync(dst + half_bytes, rt->device, cp.peer_src + half_bytes, cp.peer_rt->device,
-                                    half_bytes, ks),
-                "peer W2"))
+        if (!(cp.peer_rt ? ok(cudaMemcpyPeerAsync(dst + half_bytes, rt->device, cp.peer_src + half_bytes,
+                                                   cp.peer_rt->device, half_bytes, ks),
+                              "peer W2")
+                         : ok(cudaMemcpyAsync(dst + half_bytes, cp.peer_src + half_bytes, half_bytes, cudaMemcpyDefault,
+                                              ks),
+                              "peer W2")))
           return fail_cuda();
         st.peer_loads += 1;
         st.peer_bytes += 2 * half_bytes;

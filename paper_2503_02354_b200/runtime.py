@@ -152,6 +152,14 @@ def _lib():
         lib.coe_runtime_attach_peers.restype = ctypes.c_int
         lib.coe_runtime_attach_local_experts.argtypes = [V, V, I32]
         lib.coe_runtime_attach_local_experts.restype = ctypes.c_int
+        lib.coe_runtime_ipc_export_experts.argtypes = [V, V, P(I32)]
+        lib.coe_runtime_ipc_export_experts.restype = ctypes.c_int
+        lib.coe_runtime_ipc_open_experts.argtypes = [V, I32, V, I32]
+        lib.coe_runtime_ipc_open_experts.restype = ctypes.c_int
+        lib.coe_runtime_residency_codes.argtypes = [V, V]
+        lib.coe_runtime_residency_codes.restype = ctypes.c_int
+        lib.coe_runtime_set_peer_residency.argtypes = [V, I32, V]
+        lib.coe_runtime_set_peer_residency.restype = ctypes.c_int
         lib.coe_runtime_plan_rows.argtypes = [P(StepInput), I32, ctypes.c_int, ctypes.c_int, P(I32), P(I32)]
         lib.coe_runtime_plan_rows.restype = ctypes.c_int
         lib.coe_expert_seed.argtypes = [ctypes.c_uint64, I32, I32]
@@ -409,6 +417,19 @@ class B200Runtime:
             _check(self.lib, self.lib.coe_runtime_ipc_open(self.handle, h, ctypes.byref(pb)), "ipc open")
             peers.append(pb)
         self._attach_peers(rank, peers)
+        # (f3) expert memory too: peer-tier loads copy straight from the source rank's HBM
+        exp = (ctypes.c_char * (64 * 16))()
+        count = ctypes.c_int32()
+        _check(self.lib, self.lib.coe_runtime_ipc_export_experts(self.handle, exp, ctypes.byref(count)), "ipc experts")
+        gathered = [None] * world
+        dist.all_gather_object(gathered, bytes(exp)[:64 * count.value])
+        for r in range(world):
+            if r != rank:
+                blob = gathered[r]
+                buf = (ctypes.c_char * len(blob)).from_buffer_copy(blob)
+                _check(self.lib, self.lib.coe_runtime_ipc_open_experts(self.handle, r, buf, len(blob) // 64),
+                       "ipc open experts")
+        self._ipc = (rank, world)
 
     def __del__(self):
         try:
@@ -471,10 +492,29 @@ class B200Runtime:
         )
         stats = StepStats()
         _check(self.lib, self.lib.coe_runtime_step(self.handle, ctypes.byref(inp), ctypes.byref(stats)), "step")
+        if getattr(self, "_ipc", None) and _has_peer_loads(plan):
+            self._exchange_residency()
         out = stats.as_dict()
         if host_outputs is not None:  # the completion order is fixed at issue time
             out["output_order"] = self.output_order()
         return out
+
+    def _exchange_residency(self) -> None:
+        """(f3, one executor per process) after every step of a plan with peer-tier loads: each
+        rank's end-of-step residency (slab / offset codes) goes to every other rank, which
+        copies peer-tier loads of the next step straight from that HBM (CUDA IPC mapping)."""
+        import torch.distributed as dist
+
+        rank, world = self._ipc
+        n = self.num_experts
+        codes = np.zeros(n, np.int64)
+        _check(self.lib, self.lib.coe_runtime_residency_codes(self.handle, codes.ctypes.data), "residency")
+        gathered = [None] * world
+        dist.all_gather_object(gathered, codes)
+        for r in range(world):
+            if r != rank:
+                c = np.ascontiguousarray(gathered[r], np.int64)
+                _check(self.lib, self.lib.coe_runtime_set_peer_residency(self.handle, r, c.ctypes.data), "peer residency")
 
     def join(self) -> None:
         """Order the compute stream after the last e2e step's output downloads."""
@@ -653,6 +693,11 @@ def nccl_library() -> str:
     except Exception:
         pass
     return "libnccl.so.2"
+
+
+def _has_peer_loads(plan) -> bool:
+    ops = plan.ops()
+    return bool(len(ops)) and bool(((ops["kind"] == _native.OP_LOAD) & (ops["tier"] == _native.TIER_PEER)).any())
 
 
 def _peak_residency(plan, executor: int, expert_shape: np.ndarray, num_shapes: int, lazy: bool = True) -> np.ndarray:

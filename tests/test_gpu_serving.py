@@ -385,6 +385,61 @@ def test_fused_hops_across_processes_ipc():
     assert worst <= TOL, worst
 
 
+def test_peer_tier_across_processes_ipc():
+    """(f3) Peer-GPU tier between two processes (the multi-GPU layout, sharing the one GPU):
+    config 5 with RunConfig.peer_tier, expert memory mapped across processes, each rank's
+    end-of-step residency exchanged after every step.  From the second step on, peer-tier
+    loads are copied from the other rank's HBM (after its step-end flag); outputs are
+    identical on every step and match the numpy fp32 chain."""
+    import os
+    import socket
+    import subprocess
+    import sys
+    import tempfile
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    with tempfile.TemporaryDirectory() as tmp:
+        procs = []
+        for rank in range(2):
+            env = dict(os.environ, RANK=str(rank), WORLD_SIZE="2", MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port),
+                       PYTHONPATH=root)
+            procs.append(subprocess.Popen([sys.executable, os.path.join(root, "tests", "ipc_hop_worker.py"), tmp, "peer"],
+                                          env=env, stdout=subprocess.PIPE, stderr=subprocess.STDOUT))
+        logs = []
+        for p in procs:
+            out, _ = p.communicate(timeout=600)
+            logs.append(out.decode(errors="replace"))
+        assert all(p.returncode == 0 for p in procs), "\n".join(l[-3000:] for l in logs)
+        parts = [np.load(os.path.join(tmp, f"rank{r}.npz")) for r in range(2)]
+    peer = np.stack([part["peer"] for part in parts])  # [rank][step][peer_loads, peer_tier_loads]
+    assert peer[:, 0, 0].sum() == 0 and peer[:, 1:, 0].sum() > 0, peer.tolist()
+    assert (peer[:, :, 0] <= peer[:, :, 1]).all()
+    w = _trim(configs.load("c5", 1000, gpu_executors=2), 300)
+    plan = engine.plan(configs.run_config(w, trace=False, peer_tier={"read_bandwidth_bytes_per_s": 720e9,
+                                                                     "fixed_load_overhead_s": 1e-5}))
+    shape = runtime.RuntimeShape(1024, 2048, 64)
+    chains = plan.resolved.chains
+    cache = {}
+
+    def weights(e):
+        if e not in cache:
+            cache[e] = synth.expert_weights(runtime.DEFAULT_WEIGHT_SEED, e, shape.d, shape.h)
+        return cache[e]
+
+    worst, seen = 0.0, 0
+    for part in parts:
+        reqs, outs = part["requests"], part["outputs"]
+        assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[1], outs[2])
+        for i, r in enumerate(reqs.tolist()[:12]):
+            x = synth.request_inputs(runtime.DEFAULT_INPUT_SEED, r, shape.T, shape.d)
+            worst = max(worst, mlp.rel_l2(outs[2][i], mlp.chain_forward(x, chains[r], weights)))
+            seen += 1
+    assert seen >= 12 and worst <= TOL, worst
+
+
 def test_c3_full_shape_swapped_experts():
     """Config 3 at its real expert shape (d=4096, h=12288, T=256; 201 MB experts, 59 HBM
     slots = the 12 GB budget), first 200 requests: 108 planned swap-ins.  The GPU grouping
