@@ -2265,8 +2265,10 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
   // e2e inputs: staged by host threads (default), else read by gather_inputs; either way the
   // device needs, per request in need order, its host row and A row
   const int64_t in_chunk_bytes = in_chunk * (int64_t)rt->row_elems * 2;
-  const bool staged = e2e_in && !getenv("COE_INPUT_DMA") && !getenv("COE_INPUT_GATHER") && stream_memops() &&
-                      input_staging_init(rt, in_chunk_bytes);
+  // staged by host threads only on request (COE_INPUT_STAGE=1): slower than the gather kernel on
+  // the B200 box (C1 e2e step 46.9 vs 40.1 ms, C3 1,528 vs 1,405 ms; profiles/r2u_*)
+  const bool staged = e2e_in && getenv("COE_INPUT_STAGE") && atoi(getenv("COE_INPUT_STAGE")) != 0 &&
+                      !getenv("COE_INPUT_DMA") && stream_memops() && input_staging_init(rt, in_chunk_bytes);
   if (e2e_in && !staged) cudaGetLastError();
   const uint4 *host_in_dev = nullptr;
   if (e2e_in && !staged && !getenv("COE_INPUT_DMA")) {

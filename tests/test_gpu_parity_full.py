@@ -229,7 +229,8 @@ def test_c5_pooled_budget_swaps_across_shapes():
     budget = plan.resolved.executors[0][1]
     rt = runtime.B200Runtime.for_plan(plan, w.shapes)
     largest = max(reg.experts[ids[e]].param_bytes for e in used)
-    assert 0 < rt.expert_pool_bytes <= budget + largest + len(used) * runtime.POOL_UNIT
+    # the byte budget, three largest experts of slack against fragmentation, unit rounding
+    assert 0 < rt.expert_pool_bytes <= budget + 3 * largest + len(used) * runtime.POOL_UNIT
     assert rt.expert_pool_bytes < sum(reg.experts[ids[e]].param_bytes for e in used)
     n = len(plan.resolved.request_ids)
     rt.fill_inputs(n)
