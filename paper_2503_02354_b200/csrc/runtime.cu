@@ -197,6 +197,9 @@ struct CopyAct {
   coe_runtime *peer_rt = nullptr;
   int32_t peer_exec = -1;
   int32_t peer_par = 0;
+  // pooled memory: the W1 half may land on bytes another expert (of another shape, or placed
+  // elsewhere) used as ITS W2, so it must wait for the down passes too, not just the up passes
+  bool w1_waits_down = false;
 };
 
 struct WaveAct {
@@ -1567,6 +1570,24 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
   std::vector<uint8_t> touched(c.num_experts, 0);
   for (int64_t i = 0; i < in->num_ops; ++i)
     if (ops[i].executor == x && ops[i].expert >= 0 && ops[i].expert < c.num_experts) touched[ops[i].expert] = 1;
+  // (f3) experts other executors copy from this one this step: kept (initial placement, never
+  // evicted here) and materialised at step start, so that this step's end snapshot has them
+  std::vector<uint8_t> exported(c.num_experts, 0);
+  bool any_export = false;
+  if (in->initial_offsets && x < in->num_executors && (!rt->local_peers.empty() || !rt->peer_exp_base.empty())) {
+    std::vector<uint8_t> mine(c.num_experts, 0);
+    for (int32_t i = in->initial_offsets[x]; i < in->initial_offsets[x + 1]; ++i) mine[in->initial_all[i]] = 1;
+    for (int64_t i = 0; i < in->num_ops; ++i)
+      if (ops[i].executor == x && ops[i].kind == COE_OP_LOAD)
+        for (int32_t v = 0; v < ops[i].count; ++v) mine[in->op_args[ops[i].offset + v]] = 0;
+    for (int64_t i = 0; i < in->num_ops; ++i) {
+      const coe_op &o = ops[i];
+      if (o.executor != x && o.kind == COE_OP_LOAD && o.tier == COE_TIER_PEER && o.seq == x && mine[o.expert]) {
+        exported[o.expert] = touched[o.expert] = 1;
+        any_export = true;
+      }
+    }
+  }
   // slots outside the initial placement are free again, and so are residents this step never
   // uses: what is physically resident is then always part of the planner's pool at that
   // moment, restricted to the experts this step touches (the runtime's slot sizing)
@@ -1692,6 +1713,12 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     if (!snap || e >= (int32_t)snap->size() || !(*snap)[e]) return nullptr;
     return keep_of(j)[e] ? (*snap)[e] : nullptr;
   };
+  if (any_export)
+    for (int32_t e = 0; e < c.num_experts; ++e)
+      if (exported[e] && rt->expert_slot[e] < 0 && pending_restore[e]) {
+        pending_restore[e] = 0;
+        if (!issue_copy(e, true, my_ops.empty() ? 0 : my_ops[0])) return COE_CUDA_ERR_CHECK;
+      }
   for (size_t k = 0; k < my_ops.size(); ++k) {
     const coe_op &op = ops[my_ops[k]];
     if (op.kind == COE_OP_LOAD) {
@@ -2127,6 +2154,8 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
         ca.peer_rt = ci.peer_rt;
         ca.peer_exec = ci.peer_exec;
         ca.peer_par = ci.peer_par;
+        if (rt->pooled)
+          for (int32_t q : ci.deps) ca.w1_waits_down |= q != ci.slot;
         for (int32_t q : ci.deps)  // the slot itself, and (VMM) the last users of its pages
           for (int k = 0; k < NCLS; ++k) {
             const int32_t wv = last_reader_wave[q * NCLS + k];
@@ -2528,9 +2557,12 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
       const int64_t half_bytes = rt->sbytes[rt->slot_shape[cp.slot]] / 2;
       const int ksh = rt->slot_shape[cp.slot];
       for (int32_t wv : cp.wait_waves)
-        if (!ok(cudaStreamWaitEvent(ks, wave_up_ev[wv], 0), "copy waits W1 readers")) return fail_cuda();
+        if (!ok(cudaStreamWaitEvent(ks, cp.w1_waits_down ? wave_down_ev[wv] : wave_up_ev[wv], 0), "copy waits W1 readers"))
+          return fail_cuda();
       for (int32_t sk : cp.wait_prev)
-        if (!ok(cudaStreamWaitEvent(ks, rt->slot_free_up[sk], 0), "copy waits last step")) return fail_cuda();
+        if (!ok(cudaStreamWaitEvent(ks, cp.w1_waits_down ? rt->slot_free_down[sk] : rt->slot_free_up[sk], 0),
+                "copy waits last step"))
+          return fail_cuda();
       if (c.profile && !ok(cudaEventRecord(rt->t_copy_start[a.index], ks), "record")) return fail_cuda();
       if (cp.peer_src) {  // (f3) NVLink / same-device copy from the peer executor's HBM
         if (cp.peer_rt) {  // in-process: its ready event of the previous step

@@ -711,7 +711,15 @@ def _peak_residency(plan, executor: int, expert_shape: np.ndarray, num_shapes: i
     pending = {int(e) for e in plan.initial_residency()[executor]}
     live = set()
     if not lazy:  # initial residents count from the start -- those this executor ever touches
-        touched = {int(op["expert"]) for op in plan.ops() if op["executor"] == executor}
+        ops = plan.ops()
+        touched = {int(op["expert"]) for op in ops if op["executor"] == executor}
+        # (f3) and those other executors copy from it (kept all step, materialised at step start)
+        args = plan.op_args()
+        victims = {int(v) for op in ops if op["executor"] == executor and op["kind"] == _native.OP_LOAD
+                   for v in args[int(op["offset"]):int(op["offset"]) + int(op["count"])]}
+        touched |= {int(op["expert"]) for op in ops
+                    if op["executor"] != executor and op["kind"] == _native.OP_LOAD
+                    and op["tier"] == _native.TIER_PEER and int(op["seq"]) == executor} - victims
         for e in pending & touched:
             live.add(e)
             cur[expert_shape[e]] += 1
