@@ -185,6 +185,7 @@ __global__ void __launch_bounds__(256) scatter_inputs(const uint4 *__restrict__ 
 
 const int kInputGatherCtas = getenv("COE_INPUT_CTAS") ? atoi(getenv("COE_INPUT_CTAS")) : 64;
 const bool kInputBulk = getenv("COE_INPUT_BULK") && atoi(getenv("COE_INPUT_BULK")) != 0;  // experiment
+const int kInputSplitPct = getenv("COE_INPUT_SPLIT") ? std::max(0, std::min(100, atoi(getenv("COE_INPUT_SPLIT")))) : 0;
 
 struct CopyAct {
   int32_t expert;
@@ -419,7 +420,9 @@ struct coe_runtime {
   int64_t last_adm = 0, last_batches = 0;
   int last_set = 0;
   cudaStream_t out_stream = nullptr;  // e2e output downloads (inputs ride the copy engine)
-  cudaStream_t copy_in = nullptr;     // e2e inputs, second H2D queue (COE_INPUT_DMA=2 experiment)
+  cudaStream_t copy_in = nullptr;     // e2e inputs: the gather kernels' queue
+  cudaStream_t copy_in2 = nullptr;    // e2e inputs: the DMA share of a split chunk (COE_INPUT_SPLIT)
+  std::vector<cudaEvent_t> in_part_ev;
   std::vector<cudaEvent_t> in_ev;
   cudaEvent_t out_drained = nullptr;
   bool have_out = false;
@@ -509,6 +512,7 @@ struct coe_runtime {
       if (st) cudaStreamSynchronize(st);
     if (copy) cudaStreamSynchronize(copy);
     if (copy_in) cudaStreamSynchronize(copy_in);  // its waits are on chunks the workers fill
+    if (copy_in2) cudaStreamSynchronize(copy_in2);
     if (in_scatter) cudaStreamSynchronize(in_scatter);
     if (!in_workers.empty()) {
       {
@@ -568,6 +572,8 @@ struct coe_runtime {
       if (st) cudaStreamDestroy(st);
     if (copy) cudaStreamDestroy(copy);
     if (copy_in) cudaStreamDestroy(copy_in);
+    if (copy_in2) cudaStreamDestroy(copy_in2);
+    for (auto e : in_part_ev) cudaEventDestroy(e);
     if (hop) cudaStreamDestroy(hop);
     if (out_stream) cudaStreamDestroy(out_stream);
   }
@@ -755,6 +761,7 @@ int coe_runtime_create(const coe_runtime_config *cfg, coe_runtime **out) {
               ok(cudaStreamCreateWithFlags(&rt->hop, cudaStreamNonBlocking), "stream") &&
               ok(cudaStreamCreateWithFlags(&rt->out_stream, cudaStreamNonBlocking), "stream") &&
               ok(cudaStreamCreateWithFlags(&rt->copy_in, cudaStreamNonBlocking), "stream") &&
+              ok(cudaStreamCreateWithFlags(&rt->copy_in2, cudaStreamNonBlocking), "stream") &&
               ok(cudaGetDevice(&rt->device), "device") &&
               ok(cudaEventCreateWithFlags(&rt->res_ready[0], cudaEventDisableTiming), "event") &&
               ok(cudaEventCreateWithFlags(&rt->res_ready[1], cudaEventDisableTiming), "event") &&
@@ -2376,6 +2383,7 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
   if (!my_hops.empty() && rt->have_step_end && !ok(cudaStreamWaitEvent(rt->hop, rt->step_end, 0), "hop waits step"))
     return fail_cuda();
   if (e2e_in && (!rt->ensure_events(rt->in_ev, (size_t)n_chunks, false) ||
+                 (kInputSplitPct > 0 && !rt->ensure_events(rt->in_part_ev, 2 * (size_t)n_chunks, false)) ||
                  (staged && !rt->ensure_events(rt->in_dma_ev, (size_t)n_chunks, false))))
     return fail_cuda();
   bool in_prev_waited = false;
@@ -2463,11 +2471,31 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
                ok(cudaEventRecord(rt->in_ev[k], ks), "record");
       }
       const int64_t row_vec = (int64_t)(rb / 16);
-      gather_inputs<<<kInputGatherCtas, 256, 0, ks>>>(host_in_dev, sb.in_map, chunk_start[k], n, row_vec,
-                                                       (int32_t)((row_vec + 2047) / 2048),
-                                                       reinterpret_cast<uint4 *>(rt->act));
+      // optional split (COE_INPUT_SPLIT = percent of a chunk's rows): that share moves as one
+      // DMA per row on a third queue, concurrently with the gather kernel's PCIe reads
+      const int32_t n_dma = std::min<int32_t>(n, (int32_t)((int64_t)n * kInputSplitPct / 100));
+      if (n_dma > 0) {
+        // the slot readers' waits were queued on ks (before this point); the DMA queue follows ks
+        if (!ok(cudaEventRecord(rt->in_part_ev[2 * k], ks), "record") ||
+            !ok(cudaStreamWaitEvent(rt->copy_in2, rt->in_part_ev[2 * k], 0), "split waits readers"))
+          return false;
+        const char *hin = static_cast<const char *>(in->host_inputs);
+        for (int32_t i = chunk_start[k] + (n - n_dma); i < chunk_start[k + 1]; ++i)
+          if (!ok(cudaMemcpyAsync(reinterpret_cast<char *>(rt->act) + (size_t)rows.in_slot[in_reqs[i]] * rb,
+                                  hin + (size_t)host_row[in_reqs[i]] * rb, rb, cudaMemcpyHostToDevice, rt->copy_in2),
+                  "input H2D share"))
+            return false;
+      }
+      if (n - n_dma > 0) {
+        gather_inputs<<<kInputGatherCtas, 256, 0, ks>>>(host_in_dev, sb.in_map, chunk_start[k], n - n_dma, row_vec,
+                                                         (int32_t)((row_vec + 2047) / 2048),
+                                                         reinterpret_cast<uint4 *>(rt->act));
+        st.launches += 1;
+      }
+      if (n_dma > 0 && (!ok(cudaEventRecord(rt->in_part_ev[2 * k + 1], rt->copy_in2), "record") ||
+                        !ok(cudaStreamWaitEvent(ks, rt->in_part_ev[2 * k + 1], 0), "chunk joins its DMA share")))
+        return false;
       st.h2d_input_bytes += (int64_t)n * (int64_t)rb;
-      st.launches += 1;
       return ok(cudaGetLastError(), "gather_inputs") && io_mark(ks) && ok(cudaEventRecord(rt->in_ev[k], ks), "record");
     }
     const char *hin = static_cast<const char *>(in->host_inputs);
