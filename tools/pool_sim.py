@@ -63,26 +63,27 @@ def sim(plan, pool_bytes, policy="bestfit", steps=3):
                     pending.discard(e)
                     if not alloc(e): return f"fail step {st} restore {e}"
     return "ok"
-for gap in ():  # (single-slack table: see the sweep below)
-    base = configs.load("c5", 10000)
-    stream = [dataclasses.replace(r, arrival_time_s=i * gap) for i, r in enumerate(base.stream)]
-    w = dataclasses.replace(base, stream=stream)
-    cfg = configs.run_config(w, trace=False, alloc_override={"gpu": 201}, search_enabled=False)
-    p = engine.plan(cfg)
-    budget = p.resolved.executors[0][1]
-    # the runtime's pool: min(budget, held) + largest + peak * unit  (approximate with budget + largest + 300 units)
-    largest = max(e.param_bytes for e in p.resolved.config.registry.experts.values())
-    pool = int(budget) + largest + 300 * UNIT
-    print(gap, "bestfit", sim(p, pool), "| split", sim(p, pool, "split"))
-print("--- slack sweep")
-for gap in (1e-4, 3e-4, 1e-3):
-    base = configs.load("c5", 10000)
-    stream = [dataclasses.replace(r, arrival_time_s=i * gap) for i, r in enumerate(base.stream)]
-    w = dataclasses.replace(base, stream=stream)
-    cfg = configs.run_config(w, trace=False, alloc_override={"gpu": 201}, search_enabled=False)
-    p = engine.plan(cfg)
-    budget = p.resolved.executors[0][1]
-    largest = max(e.param_bytes for e in p.resolved.config.registry.experts.values())
-    for k in (2, 3, 4, 6):
-        pool = int(budget) + k * largest + 300 * UNIT
-        print(gap, k, sim(p, pool), sim(p, pool, "split"))
+if __name__ == "__main__":
+    for gap in ():  # (single-slack table: see the sweep below)
+        base = configs.load("c5", 10000)
+        stream = [dataclasses.replace(r, arrival_time_s=i * gap) for i, r in enumerate(base.stream)]
+        w = dataclasses.replace(base, stream=stream)
+        cfg = configs.run_config(w, trace=False, alloc_override={"gpu": 201}, search_enabled=False)
+        p = engine.plan(cfg)
+        budget = p.resolved.executors[0][1]
+        # the runtime's pool: min(budget, held) + largest + peak * unit  (approximate with budget + largest + 300 units)
+        largest = max(e.param_bytes for e in p.resolved.config.registry.experts.values())
+        pool = int(budget) + largest + 300 * UNIT
+        print(gap, "bestfit", sim(p, pool), "| split", sim(p, pool, "split"))
+    print("--- slack sweep")
+    for gap in (1e-4, 3e-4, 1e-3):
+        base = configs.load("c5", 10000)
+        stream = [dataclasses.replace(r, arrival_time_s=i * gap) for i, r in enumerate(base.stream)]
+        w = dataclasses.replace(base, stream=stream)
+        cfg = configs.run_config(w, trace=False, alloc_override={"gpu": 201}, search_enabled=False)
+        p = engine.plan(cfg)
+        budget = p.resolved.executors[0][1]
+        largest = max(e.param_bytes for e in p.resolved.config.registry.experts.values())
+        for k in (2, 3, 4, 6):
+            pool = int(budget) + k * largest + 300 * UNIT
+            print(gap, k, sim(p, pool), sim(p, pool, "split"))
