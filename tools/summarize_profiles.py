@@ -132,10 +132,10 @@ if summary["shapes"]:
 kg = grouping()
 if kg:
     summ = {"launches": kg, "note": "ncu --set full --profile-from-start off, one WARM bench step of C3 (13,642 "
-                                    "admissions, 2,400 batches): at serving size K1 + K2 run as ONE 1,024-thread block "
-                                    "(coe_group_compact_fused: stable sort by run-rank in shared memory, member / route "
-                                    "gather, batch scan, run check). Latency-bound: ~218 KB of algorithmic traffic per "
-                                    "step (16 B per admission)",
+                                    "admissions, 2,400 batches): K1 (counting read + one-kernel 8-bit LSD passes) and "
+                                    "K2 (member gather, batch scans, compaction); the one-block fused K1+K2 is used up "
+                                    "to 4,096 admissions only. Latency-bound: ~218 KB of algorithmic traffic per step "
+                                    "(16 B per admission)",
             "total_us": sum(k["duration_us"] for k in kg), "total_dram_bytes": sum(k["dram_bytes"] for k in kg)}
     json.dump(summ, open(os.path.join(PROF, f"{tag}_k12_ncu_summary.json"), "w"), indent=1)
     print(json.dumps(summ, indent=1))
