@@ -64,31 +64,66 @@ def load_peaks() -> tuple:
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks / throttle reasons / power sampled during the timed region: NVML on a thread
+    every 5 ms (a 16 ms C1 step still gets samples), nvidia-smi -lms 200 as the fallback."""
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    # nvmlClocksEventReason* bits
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
 
     def __init__(self, enabled: bool, gpu_index: int):
         self.enabled = enabled
         self.gpu = gpu_index
         self.proc = None
         self.path = None
+        self.rows = []  # (sm_mhz, max_mhz, power_w, reasons bitmask) from NVML
+        self._stop = None
+        self._thread = None
+
+    def _nvml_loop(self):
+        import pynvml
+
+        h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+        get_reasons = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+        mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        while True:
+            self.rows.append((pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM), mx,
+                              pynvml.nvmlDeviceGetPowerUsage(h) / 1e3, get_reasons(h)))
+            if self._stop.wait(0.005):
+                break
 
     def __enter__(self):
-        if self.enabled:
-            fd, self.path = tempfile.mkstemp(suffix=".csv")
-            os.close(fd)
-            try:
-                self.proc = subprocess.Popen(
-                    ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                     "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
-            except OSError:
-                self.proc = None
+        if not self.enabled:
+            return self
+        try:
+            import threading
+
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._stop = threading.Event()
+            self._thread = threading.Thread(target=self._nvml_loop, daemon=True)
+            self._thread.start()
+            return self
+        except Exception:
+            self._thread = None
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
         return self
 
     def __exit__(self, *exc):
+        if self._thread is not None:
+            self._stop.set()
+            self._thread.join(timeout=5)
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -97,6 +132,13 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self) -> dict:
+        if self.rows:
+            sm = [r[0] for r in self.rows]
+            pw = [r[2] for r in self.rows]
+            reasons = sorted({n for r in self.rows for n, bit in self.REASONS.items() if r[3] & bit})
+            return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(self.rows[0][1]), "reasons": reasons,
+                    "samples": len(self.rows), "source": "NVML every 5 ms", "power_w_median": statistics.median(pw),
+                    "power_w_max": max(pw)}
         if not self.path or not os.path.exists(self.path):
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
         rows = []
@@ -113,7 +155,7 @@ class ClockSampler:
         pw = [float(r[3]) for r in rows if r[3].replace(".", "").isdigit()]
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": float(rows[0][2]) if rows[0][2].replace(".", "").isdigit() else None,
-                "reasons": reasons, "samples": len(rows),
+                "reasons": reasons, "samples": len(rows), "source": "nvidia-smi -lms 200",
                 "power_w_median": statistics.median(pw) if pw else None, "power_w_max": max(pw) if pw else None}
 
 
