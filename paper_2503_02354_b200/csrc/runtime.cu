@@ -1022,7 +1022,9 @@ int coe_runtime_download_requests(coe_runtime *rt, const int32_t *requests, cons
 
 int coe_runtime_synchronize(coe_runtime *rt) {
   bool good = ok(cudaStreamSynchronize(rt->copy), "sync copy") && ok(cudaStreamSynchronize(rt->hop), "sync hop") &&
-              ok(cudaStreamSynchronize(rt->out_stream), "sync out");
+              ok(cudaStreamSynchronize(rt->out_stream), "sync out") && ok(cudaStreamSynchronize(rt->copy_in), "sync in") &&
+              ok(cudaStreamSynchronize(rt->copy_in2), "sync in") &&
+              (!rt->in_scatter || ok(cudaStreamSynchronize(rt->in_scatter), "sync in"));
   for (int k = coe_runtime::NCLS - 1; k >= 0; --k) good = ok(cudaStreamSynchronize(rt->cls_stream[k]), "sync") && good;
   return good ? COE_CUDA_OK : fail_cuda();
 }
