@@ -36,10 +36,6 @@
 
 #include <algorithm>
 #include <array>
-#include <chrono>
-#include <condition_variable>
-#include <mutex>
-#include <thread>
 #include <cstring>
 #include <climits>
 #include <deque>
@@ -57,7 +53,6 @@
 #include "common.cuh"
 #include "act_rows.h"
 #include "hops.h"
-#include "sm100.cuh"
 
 namespace {
 
@@ -111,81 +106,7 @@ __global__ void __launch_bounds__(256) gather_inputs(const uint4 *__restrict__ h
   }
 }
 
-// Bulk-copy (TMA) variant: one thread per CTA moves 4 KB pieces host -> shared -> HBM with
-// cp.async.bulk (large PCIe reads issued by the TMA unit instead of 16-byte loads), two pieces
-// in flight per CTA; 8 KB of shared memory fits next to a resident K3 CTA.
-constexpr int kBulkPiece = 4096, kBulkStages = 2;
-__global__ void __launch_bounds__(32) gather_inputs_bulk(const char *__restrict__ host, const int64_t *__restrict__ map,
-                                                         int32_t first, int32_t n, int64_t row_bytes,
-                                                         char *__restrict__ dst) {
-  __shared__ alignas(128) uint8_t buf[kBulkStages][kBulkPiece];
-  __shared__ alignas(8) uint64_t bar[kBulkStages];
-  if (threadIdx.x != 0) return;
-  const int64_t per_row = row_bytes / kBulkPiece;
-  const int64_t total = (int64_t)n * per_row;
-  for (int s = 0; s < kBulkStages; ++s) sm100::mbar_init(&bar[s], 1);
-  sm100::fence_mbar_init();
-  auto src_of = [&](int64_t p) {
-    const int64_t r = p / per_row, off = (p - r * per_row) * kBulkPiece;
-    return host + map[2 * (first + r)] * row_bytes + off;
-  };
-  auto dst_of = [&](int64_t p) {
-    const int64_t r = p / per_row, off = (p - r * per_row) * kBulkPiece;
-    return dst + map[2 * (first + r) + 1] * row_bytes + off;
-  };
-  auto load = [&](int64_t p, int s) {
-    sm100::mbar_arrive_expect_tx(&bar[s], kBulkPiece);
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     sm100::smem_u32(buf[s])),
-                 "l"(src_of(p)), "r"(kBulkPiece), "r"(sm100::smem_u32(&bar[s]))
-                 : "memory");
-  };
-  int64_t p = blockIdx.x;
-  for (int s = 0; s < kBulkStages && p + (int64_t)s * gridDim.x < total; ++s) load(p + (int64_t)s * gridDim.x, s);
-  for (int64_t it = 0; p < total; ++it, p += gridDim.x) {
-    const int s = (int)(it % kBulkStages);
-    sm100::mbar_wait(&bar[s], (uint32_t)((it / kBulkStages) & 1));
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst_of(p)),
-                 "r"(sm100::smem_u32(buf[s])), "r"(kBulkPiece)
-                 : "memory");
-    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-    const int64_t nxt = p + (int64_t)kBulkStages * gridDim.x;
-    if (nxt < total) {
-      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // buf[s] read by the store
-      load(nxt, s);
-    }
-  }
-  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-}
-
-// staged inputs: a chunk's rows, contiguous in the device staging buffer in need order, into
-// their activation slots (map[2 * (first + i) + 1] = A row of the chunk's i-th request)
-__global__ void __launch_bounds__(256) scatter_inputs(const uint4 *__restrict__ stage, const int64_t *__restrict__ map,
-                                                      int32_t first, int32_t n, int64_t row_vec, int32_t segs_per_row,
-                                                      uint4 *__restrict__ dst) {
-  constexpr int SEG = 2048;
-  const int32_t items = n * segs_per_row;
-  for (int32_t item = blockIdx.x; item < items; item += gridDim.x) {
-    const int32_t r = item / segs_per_row, sg = item - r * segs_per_row;
-    const int64_t off = (int64_t)sg * SEG;
-    const int32_t len = (int32_t)(row_vec - off < SEG ? row_vec - off : SEG);
-    const uint4 *src = stage + (int64_t)r * row_vec + off;
-    uint4 *out = dst + map[2 * (first + r) + 1] * row_vec + off;
-    int32_t i = threadIdx.x;
-    for (; i + 768 < len; i += 1024) {
-      const uint4 v0 = src[i], v1 = src[i + 256], v2 = src[i + 512], v3 = src[i + 768];
-      out[i] = v0;
-      out[i + 256] = v1;
-      out[i + 512] = v2;
-      out[i + 768] = v3;
-    }
-    for (; i < len; i += 256) out[i] = src[i];
-  }
-}
-
 const int kInputGatherCtas = getenv("COE_INPUT_CTAS") ? atoi(getenv("COE_INPUT_CTAS")) : 64;
-const bool kInputBulk = getenv("COE_INPUT_BULK") && atoi(getenv("COE_INPUT_BULK")) != 0;  // experiment
-const int kInputSplitPct = getenv("COE_INPUT_SPLIT") ? std::max(0, std::min(100, atoi(getenv("COE_INPUT_SPLIT")))) : 0;
 
 struct CopyAct {
   int32_t expert;
@@ -421,8 +342,6 @@ struct coe_runtime {
   int last_set = 0;
   cudaStream_t out_stream = nullptr;  // e2e output downloads (inputs ride the copy engine)
   cudaStream_t copy_in = nullptr;     // e2e inputs: the gather kernels' queue
-  cudaStream_t copy_in2 = nullptr;    // e2e inputs: the DMA share of a split chunk (COE_INPUT_SPLIT)
-  std::vector<cudaEvent_t> in_part_ev;
   std::vector<cudaEvent_t> in_ev;
   cudaEvent_t out_drained = nullptr;
   bool have_out = false;
@@ -459,69 +378,11 @@ struct coe_runtime {
   int m_ctas = 148, r_ctas = 16;  // SM split: main waves vs the swap-in-gating waves
   int rel_launch_ctas = 148;      // grid of a release wave (all SMs; see phase C)
 
-  // e2e inputs staged by host threads (default when stream memory operations exist): worker
-  // threads copy each chunk's scattered host rows, in need order, into a pinned ring of chunk
-  // buffers; one DMA per chunk moves it into a device ring at full PCIe rate and a scatter
-  // kernel puts the rows into their activation slots.  The input stream waits on a host
-  // flag the worker writes after filling (cuStreamWaitValue32 on mapped pinned memory); a
-  // worker refills a buffer only after the flag the GPU writes when that buffer's DMA is done.
-  struct InJob {
-    uint32_t q;
-    int slot;
-    const char *host;
-    int64_t rb;
-    std::vector<int64_t> rows;
-  };
-  int in_slots = 0;
-  int64_t in_slot_bytes = 0;
-  char *in_stage_h = nullptr, *in_stage_d = nullptr;
-  uint32_t *in_fill = nullptr, *in_drain = nullptr;  // pinned, mapped: [in_slots] each
-  uint32_t *in_fill_dev = nullptr, *in_drain_dev = nullptr;
-  uint32_t in_seq = 0;
-  cudaStream_t in_scatter = nullptr;      // scatters wait for slot readers; the DMA stream does not
-  std::vector<cudaEvent_t> in_dma_ev;     // per chunk of the step: its DMA is done
-  std::vector<cudaEvent_t> in_slot_ev;    // per staging slot: its last scatter is done (DMA reuse)
-  std::vector<uint8_t> in_slot_used;
-  std::vector<std::thread> in_workers;
-  std::mutex in_mu;
-  std::condition_variable in_cv;
-  std::deque<InJob> in_jobs;
-  bool in_stop = false;
-
-  void in_worker() {
-    for (;;) {
-      InJob j;
-      {
-        std::unique_lock<std::mutex> lk(in_mu);
-        in_cv.wait(lk, [&] { return in_stop || !in_jobs.empty(); });
-        if (in_jobs.empty()) return;
-        j = std::move(in_jobs.front());
-        in_jobs.pop_front();
-      }
-      if (j.q > (uint32_t)in_slots)  // the buffer's previous chunk has left on the GPU's DMA
-        while ((int32_t)(__atomic_load_n(&in_drain[j.slot], __ATOMIC_ACQUIRE) - (j.q - in_slots)) < 0)
-          std::this_thread::sleep_for(std::chrono::microseconds(20));
-      char *dst = in_stage_h + (int64_t)j.slot * in_slot_bytes;
-      for (size_t i = 0; i < j.rows.size(); ++i) std::memcpy(dst + (int64_t)i * j.rb, j.host + j.rows[i] * j.rb, j.rb);
-      __atomic_store_n(&in_fill[j.slot], j.q, __ATOMIC_RELEASE);
-    }
-  }
-
   ~coe_runtime() {
     for (auto st : cls_stream)
       if (st) cudaStreamSynchronize(st);
     if (copy) cudaStreamSynchronize(copy);
-    if (copy_in) cudaStreamSynchronize(copy_in);  // its waits are on chunks the workers fill
-    if (copy_in2) cudaStreamSynchronize(copy_in2);
-    if (in_scatter) cudaStreamSynchronize(in_scatter);
-    if (!in_workers.empty()) {
-      {
-        std::lock_guard<std::mutex> lk(in_mu);
-        in_stop = true;
-      }
-      in_cv.notify_all();
-      for (auto &t : in_workers) t.join();
-    }
+    if (copy_in) cudaStreamSynchronize(copy_in);
     if (hop) cudaStreamSynchronize(hop);
     if (out_stream) cudaStreamSynchronize(out_stream);
     for (auto &per : mlps)
@@ -544,12 +405,6 @@ struct coe_runtime {
       if (p) cudaFree(p);
     for (void *p : ipc_opened) cudaIpcCloseMemHandle(p);
     if (d_hflags) cudaFree(d_hflags);
-    if (in_stage_d) cudaFree(in_stage_d);
-    for (auto e : in_dma_ev) cudaEventDestroy(e);
-    for (auto e : in_slot_ev) cudaEventDestroy(e);
-    if (in_scatter) cudaStreamDestroy(in_scatter);
-    for (void *p : {(void *)in_stage_h, (void *)in_fill, (void *)in_drain})
-      if (p) cudaFreeHost(p);
     for (void *p : {(void *)staging[0], (void *)staging[1], (void *)h_last})
       if (p) cudaFreeHost(p);
     if (host_store && store_mapped) {
@@ -572,8 +427,6 @@ struct coe_runtime {
       if (st) cudaStreamDestroy(st);
     if (copy) cudaStreamDestroy(copy);
     if (copy_in) cudaStreamDestroy(copy_in);
-    if (copy_in2) cudaStreamDestroy(copy_in2);
-    for (auto e : in_part_ev) cudaEventDestroy(e);
     if (hop) cudaStreamDestroy(hop);
     if (out_stream) cudaStreamDestroy(out_stream);
   }
@@ -761,7 +614,6 @@ int coe_runtime_create(const coe_runtime_config *cfg, coe_runtime **out) {
               ok(cudaStreamCreateWithFlags(&rt->hop, cudaStreamNonBlocking), "stream") &&
               ok(cudaStreamCreateWithFlags(&rt->out_stream, cudaStreamNonBlocking), "stream") &&
               ok(cudaStreamCreateWithFlags(&rt->copy_in, cudaStreamNonBlocking), "stream") &&
-              ok(cudaStreamCreateWithFlags(&rt->copy_in2, cudaStreamNonBlocking), "stream") &&
               ok(cudaGetDevice(&rt->device), "device") &&
               ok(cudaEventCreateWithFlags(&rt->res_ready[0], cudaEventDisableTiming), "event") &&
               ok(cudaEventCreateWithFlags(&rt->res_ready[1], cudaEventDisableTiming), "event") &&
@@ -1022,9 +874,7 @@ int coe_runtime_download_requests(coe_runtime *rt, const int32_t *requests, cons
 
 int coe_runtime_synchronize(coe_runtime *rt) {
   bool good = ok(cudaStreamSynchronize(rt->copy), "sync copy") && ok(cudaStreamSynchronize(rt->hop), "sync hop") &&
-              ok(cudaStreamSynchronize(rt->out_stream), "sync out") && ok(cudaStreamSynchronize(rt->copy_in), "sync in") &&
-              ok(cudaStreamSynchronize(rt->copy_in2), "sync in") &&
-              (!rt->in_scatter || ok(cudaStreamSynchronize(rt->in_scatter), "sync in"));
+              ok(cudaStreamSynchronize(rt->out_stream), "sync out") && ok(cudaStreamSynchronize(rt->copy_in), "sync in");
   for (int k = coe_runtime::NCLS - 1; k >= 0; --k) good = ok(cudaStreamSynchronize(rt->cls_stream[k]), "sync") && good;
   return good ? COE_CUDA_OK : fail_cuda();
 }
@@ -1433,35 +1283,6 @@ extern "C" int coe_runtime_plan_rows(const coe_step_input *in, int32_t max_reque
   *ring_slots = rows.peak_ring;
   *landing_slots = rows.landing;
   return COE_CUDA_OK;
-}
-
-// e2e input staging (see coe_runtime::InJob): allocated on the first staged step.
-static bool input_staging_init(coe_runtime *rt, int64_t chunk_bytes) {
-  if (rt->in_slots) return chunk_bytes <= rt->in_slot_bytes;
-  const int slots = getenv("COE_INPUT_SLOTS") ? std::max(2, atoi(getenv("COE_INPUT_SLOTS"))) : 8;
-  const int workers = getenv("COE_INPUT_WORKERS") ? std::max(1, atoi(getenv("COE_INPUT_WORKERS"))) : 8;
-  void *fill_d = nullptr, *drain_d = nullptr;
-  if (!ok(cudaHostAlloc(reinterpret_cast<void **>(&rt->in_stage_h), (size_t)slots * chunk_bytes, cudaHostAllocDefault),
-          "input staging (host)") ||
-      !ok(cudaMalloc(reinterpret_cast<void **>(&rt->in_stage_d), (size_t)slots * chunk_bytes), "input staging") ||
-      !ok(cudaHostAlloc(reinterpret_cast<void **>(&rt->in_fill), 4 * (size_t)slots, cudaHostAllocMapped), "fill flags") ||
-      !ok(cudaHostAlloc(reinterpret_cast<void **>(&rt->in_drain), 4 * (size_t)slots, cudaHostAllocMapped), "drain flags") ||
-      !ok(cudaHostGetDevicePointer(&fill_d, rt->in_fill, 0), "fill flags") ||
-      !ok(cudaHostGetDevicePointer(&drain_d, rt->in_drain, 0), "drain flags"))
-    return false;
-  if (!ok(cudaStreamCreateWithFlags(&rt->in_scatter, cudaStreamNonBlocking), "stream")) return false;
-  rt->in_slot_ev.resize(slots, nullptr);
-  rt->in_slot_used.assign(slots, 0);
-  for (auto &e : rt->in_slot_ev)
-    if (!ok(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event")) return false;
-  std::memset(rt->in_fill, 0, 4 * (size_t)slots);
-  std::memset(rt->in_drain, 0, 4 * (size_t)slots);
-  rt->in_fill_dev = static_cast<uint32_t *>(fill_d);
-  rt->in_drain_dev = static_cast<uint32_t *>(drain_d);
-  rt->in_slot_bytes = chunk_bytes;
-  rt->in_slots = slots;
-  for (int i = 0; i < workers; ++i) rt->in_workers.emplace_back([rt] { rt->in_worker(); });
-  return true;
 }
 
 extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_step_stats *stats) {
@@ -2302,16 +2123,10 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     std::memcpy(s_groups, g_up.data(), sizeof(coe_mlp_group) * n_batches);
     std::memcpy(s_groups + n_batches, g_down.data(), sizeof(coe_mlp_group) * n_batches);
   }
-  // e2e inputs: staged by host threads (default), else read by gather_inputs; either way the
-  // device needs, per request in need order, its host row and A row
-  const int64_t in_chunk_bytes = in_chunk * (int64_t)rt->row_elems * 2;
-  // staged by host threads only on request (COE_INPUT_STAGE=1): slower than the gather kernel on
-  // the B200 box (C1 e2e step 46.9 vs 40.1 ms, C3 1,528 vs 1,405 ms; profiles/r2u_*)
-  const bool staged = e2e_in && getenv("COE_INPUT_STAGE") && atoi(getenv("COE_INPUT_STAGE")) != 0 &&
-                      !getenv("COE_INPUT_DMA") && stream_memops() && input_staging_init(rt, in_chunk_bytes);
-  if (e2e_in && !staged) cudaGetLastError();
+  // e2e inputs: read by gather_inputs straight from the pinned host rows; the device needs,
+  // per request in need order, its host row and A row (COE_INPUT_DMA: one DMA per row run)
   const uint4 *host_in_dev = nullptr;
-  if (e2e_in && !staged && !getenv("COE_INPUT_DMA")) {
+  if (e2e_in && !getenv("COE_INPUT_DMA")) {
     void *dp = nullptr;
     if (cudaHostGetDevicePointer(&dp, const_cast<void *>(in->host_inputs), 0) == cudaSuccess)
       host_in_dev = static_cast<const uint4 *>(dp);
@@ -2320,7 +2135,7 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
   }
   int64_t *s_in = reinterpret_cast<int64_t *>(
       (reinterpret_cast<uintptr_t>(s_groups + 2 * n_batches) + 15) & ~uintptr_t(15));
-  if (host_in_dev || staged)
+  if (host_in_dev)
     for (size_t i = 0; i < in_reqs.size(); ++i) {
       s_in[2 * i] = host_row[in_reqs[i]];
       s_in[2 * i + 1] = rows.in_slot[in_reqs[i]];
@@ -2337,7 +2152,7 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
                            cudaMemcpyHostToDevice, ks),
            "group H2D")))
     return fail_cuda();
-  if ((host_in_dev || staged) && !in_reqs.empty() &&
+  if (host_in_dev && !in_reqs.empty() &&
       !ok(cudaMemcpyAsync(sb.in_map, s_in, 16 * in_reqs.size(), cudaMemcpyHostToDevice, ks), "input map H2D"))
     return fail_cuda();
   // step fence: every peer has finished the previous step (its landing rows are free).
@@ -2384,10 +2199,7 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
 
   if (!my_hops.empty() && rt->have_step_end && !ok(cudaStreamWaitEvent(rt->hop, rt->step_end, 0), "hop waits step"))
     return fail_cuda();
-  if (e2e_in && (!rt->ensure_events(rt->in_ev, (size_t)n_chunks, false) ||
-                 (kInputSplitPct > 0 && !rt->ensure_events(rt->in_part_ev, 2 * (size_t)n_chunks, false)) ||
-                 (staged && !rt->ensure_events(rt->in_dma_ev, (size_t)n_chunks, false))))
-    return fail_cuda();
+  if (e2e_in && !rt->ensure_events(rt->in_ev, (size_t)n_chunks, false)) return fail_cuda();
   bool in_prev_waited = false;
   // stage-0 rows of a chunk, pinned host -> their ring slots, coalescing consecutive rows
   int32_t io_n = 0;  // profile events recorded this step
@@ -2405,38 +2217,9 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
   const int input_queue = getenv("COE_INPUT_QUEUE") ? atoi(getenv("COE_INPUT_QUEUE")) : 1;
   auto upload_inputs = [&](int32_t k) -> bool {
     const cudaStream_t ks = (input_queue == 1 || (input_queue == 2 && (k & 1))) ? rt->copy_in : rt->copy;
-    const int32_t n_in = chunk_start[k + 1] - chunk_start[k];
-    int in_slot = -1;
-    if (staged) {  // host threads gather the rows into staging slot q % slots; one DMA moves them
-      const uint32_t q = ++rt->in_seq;
-      in_slot = (int)(q % (uint32_t)rt->in_slots);
-      coe_runtime::InJob job{q, in_slot, static_cast<const char *>(in->host_inputs), (int64_t)rb, {}};
-      job.rows.reserve(n_in);
-      for (int32_t i = chunk_start[k]; i < chunk_start[k + 1]; ++i) job.rows.push_back(host_row[in_reqs[i]]);
-      {
-        std::lock_guard<std::mutex> lk(rt->in_mu);
-        rt->in_jobs.push_back(std::move(job));
-      }
-      rt->in_cv.notify_one();
-      if (c.profile) rt->io_kind.push_back(0);
-      if (rt->in_slot_used[in_slot] &&  // the device buffer's previous chunk has been scattered
-          !ok(cudaStreamWaitEvent(ks, rt->in_slot_ev[in_slot], 0), "staging slot reuse"))
-        return false;
-      if (!io_mark(ks) || !wait_flag(ks, reinterpret_cast<const int32_t *>(rt->in_fill_dev + in_slot), q, false) ||
-          !ok(cudaMemcpyAsync(rt->in_stage_d + (int64_t)in_slot * rt->in_slot_bytes,
-                              rt->in_stage_h + (int64_t)in_slot * rt->in_slot_bytes, (size_t)n_in * rb,
-                              cudaMemcpyHostToDevice, ks),
-              "staged input H2D") ||
-          !write_flag(ks, reinterpret_cast<int32_t *>(rt->in_drain_dev + in_slot), q) ||
-          !ok(cudaEventRecord(rt->in_dma_ev[k], ks), "record") ||
-          !ok(cudaStreamWaitEvent(rt->in_scatter, rt->in_dma_ev[k], 0), "scatter waits DMA"))
-        return false;
-      st.h2d_input_bytes += (int64_t)n_in * (int64_t)rb;
-    }
-    const cudaStream_t ws_in = staged ? rt->in_scatter : ks;  // where the slot-reader waits go
     if (!in_prev_waited && rt->prev_nccl_hold && rt->have_step_end) {  // slots held for NCCL sends
       in_prev_waited = true;
-      if (!ok(cudaStreamWaitEvent(ws_in, rt->step_end, 0), "inputs wait last step")) return false;
+      if (!ok(cudaStreamWaitEvent(ks, rt->step_end, 0), "inputs wait last step")) return false;
     }
     // write-after-read: the batches that last read these slots (this step, or the previous one)
     std::vector<cudaEvent_t> waits;
@@ -2448,55 +2231,16 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
       if (ev && std::find(waits.begin(), waits.end(), ev) == waits.end()) waits.push_back(ev);
     }
     for (cudaEvent_t ev : waits)
-      if (!ok(cudaStreamWaitEvent(ws_in, ev, 0), "inputs wait slot readers")) return false;
-    if (staged) {  // staging -> the requests' activation slots (after their last readers)
-      const int64_t row_vec = (int64_t)(rb / 16);
-      scatter_inputs<<<kInputGatherCtas, 256, 0, ws_in>>>(
-          reinterpret_cast<const uint4 *>(rt->in_stage_d + (int64_t)in_slot * rt->in_slot_bytes), sb.in_map,
-          chunk_start[k], n_in, row_vec, (int32_t)((row_vec + 2047) / 2048), reinterpret_cast<uint4 *>(rt->act));
-      st.launches += 1;
-      rt->in_slot_used[in_slot] = 1;
-      return ok(cudaGetLastError(), "scatter_inputs") && ok(cudaEventRecord(rt->in_slot_ev[in_slot], ws_in), "record") &&
-             io_mark(ws_in) && ok(cudaEventRecord(rt->in_ev[k], ws_in), "record");
-    }
+      if (!ok(cudaStreamWaitEvent(ks, ev, 0), "inputs wait slot readers")) return false;
     if (c.profile) rt->io_kind.push_back(0);
     if (!io_mark(ks)) return false;
     if (host_in_dev) {  // one gather kernel per chunk (host rows scattered in need order)
       const int32_t n = chunk_start[k + 1] - chunk_start[k];
-      if (kInputBulk && rb % kBulkPiece == 0) {
-        gather_inputs_bulk<<<kInputGatherCtas, 32, 0, ks>>>(reinterpret_cast<const char *>(host_in_dev), sb.in_map,
-                                                             chunk_start[k], n, (int64_t)rb,
-                                                             reinterpret_cast<char *>(rt->act));
-        st.h2d_input_bytes += (int64_t)n * (int64_t)rb;
-        st.launches += 1;
-        return ok(cudaGetLastError(), "gather_inputs_bulk") && io_mark(ks) &&
-               ok(cudaEventRecord(rt->in_ev[k], ks), "record");
-      }
       const int64_t row_vec = (int64_t)(rb / 16);
-      // optional split (COE_INPUT_SPLIT = percent of a chunk's rows): that share moves as one
-      // DMA per row on a third queue, concurrently with the gather kernel's PCIe reads
-      const int32_t n_dma = std::min<int32_t>(n, (int32_t)((int64_t)n * kInputSplitPct / 100));
-      if (n_dma > 0) {
-        // the slot readers' waits were queued on ks (before this point); the DMA queue follows ks
-        if (!ok(cudaEventRecord(rt->in_part_ev[2 * k], ks), "record") ||
-            !ok(cudaStreamWaitEvent(rt->copy_in2, rt->in_part_ev[2 * k], 0), "split waits readers"))
-          return false;
-        const char *hin = static_cast<const char *>(in->host_inputs);
-        for (int32_t i = chunk_start[k] + (n - n_dma); i < chunk_start[k + 1]; ++i)
-          if (!ok(cudaMemcpyAsync(reinterpret_cast<char *>(rt->act) + (size_t)rows.in_slot[in_reqs[i]] * rb,
-                                  hin + (size_t)host_row[in_reqs[i]] * rb, rb, cudaMemcpyHostToDevice, rt->copy_in2),
-                  "input H2D share"))
-            return false;
-      }
-      if (n - n_dma > 0) {
-        gather_inputs<<<kInputGatherCtas, 256, 0, ks>>>(host_in_dev, sb.in_map, chunk_start[k], n - n_dma, row_vec,
-                                                         (int32_t)((row_vec + 2047) / 2048),
-                                                         reinterpret_cast<uint4 *>(rt->act));
-        st.launches += 1;
-      }
-      if (n_dma > 0 && (!ok(cudaEventRecord(rt->in_part_ev[2 * k + 1], rt->copy_in2), "record") ||
-                        !ok(cudaStreamWaitEvent(ks, rt->in_part_ev[2 * k + 1], 0), "chunk joins its DMA share")))
-        return false;
+      gather_inputs<<<kInputGatherCtas, 256, 0, ks>>>(host_in_dev, sb.in_map, chunk_start[k], n, row_vec,
+                                                       (int32_t)((row_vec + 2047) / 2048),
+                                                       reinterpret_cast<uint4 *>(rt->act));
+      st.launches += 1;
       st.h2d_input_bytes += (int64_t)n * (int64_t)rb;
       return ok(cudaGetLastError(), "gather_inputs") && io_mark(ks) && ok(cudaEventRecord(rt->in_ev[k], ks), "record");
     }
