@@ -1423,8 +1423,7 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
   // moment, restricted to the experts this step touches (the runtime's slot sizing)
   for (int32_t s = 0; s < NS; ++s) {
     int32_t e = rt->slot_expert[s];
-    static const bool keep_untouched = getenv("COE_KEEP_UNTOUCHED") != nullptr;  // debug
-    if (e >= 0 && (!plan_res[e] || (!touched[e] && !keep_untouched))) {
+    if (e >= 0 && (!plan_res[e] || !touched[e])) {
       rt->expert_slot[e] = -1;
       rt->slot_expert[s] = -1;
       if (rt->pooled) pool_free(s);
@@ -1475,8 +1474,7 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
       // bottom, so the two size classes drift to opposite ends instead of interleaving
       // (a simulation of C5's plans at 1-1000 us arrival gaps: no load ever fails with three
       // largest experts of slack, tools/pool_sim.py)
-      static const bool plain_fit = getenv("COE_POOL_PLAIN_FIT") != nullptr;  // debug: lowest-address best fit
-      const bool big = !plain_fit && rt->sbytes[k] >= (256ll << 20);
+      const bool big = rt->sbytes[k] >= (256ll << 20);
       auto pick = rt->free_runs.end();
       for (auto it = rt->free_runs.begin(); it != rt->free_runs.end(); ++it)
         if (it->second >= n && (pick == rt->free_runs.end() || it->second < pick->second ||
