@@ -118,7 +118,6 @@ struct GemmArgs {
   __nv_bfloat16 *out_y;
   __nv_bfloat16 *out_stage;
   int debug;  // experiments only (COE_K3_DEBUG): bit 0 skips the epilogue stores, bit 1 the gelu
-  int tma_store;  // up pass: each 32 x 32 chunk of H leaves by one TMA bulk tensor store (tm_hs)
 };
 
 // A-operand source of a member at chain stage s: 0 = X, 1 = P0, 2 = P1.
@@ -163,11 +162,11 @@ __device__ __forceinline__ TileCoord decode_tile(int t, const int32_t *tile_star
   return c;
 }
 
-template <int CG, bool CW, bool TS = false>
+template <int CG, bool CW>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tm_a0, const __grid_constant__ CUtensorMap tm_a1,
                         const __grid_constant__ CUtensorMap tm_a2, const __grid_constant__ CUtensorMap tm_b,
-                        const __grid_constant__ CUtensorMap tm_hs, GemmArgs args) {
+                        GemmArgs args) {
   using TL = Tiling<CG>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -596,35 +595,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
             packed[i] = pack_bf16(lo, hi);
           }
-          if (TS && args.mode == 0) {
-            // the chunk as a dense 32 x 64 B box in the scratch (pieces rotated by lane to spread
-            // banks), then one bulk tensor store by lane 0; the next chunk reuses the scratch
-            // once the store has read it
-            const uint4 q0 = make_uint4(packed[0], packed[1], packed[2], packed[3]);
-            const uint4 q1 = make_uint4(packed[4], packed[5], packed[6], packed[7]);
-            const uint4 q2 = make_uint4(packed[8], packed[9], packed[10], packed[11]);
-            const uint4 q3 = make_uint4(packed[12], packed[13], packed[14], packed[15]);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const int i = (j + (int)lane) & 3;
-              const uint4 v = i == 0 ? q0 : i == 1 ? q1 : i == 2 ? q2 : q3;
-              *reinterpret_cast<uint4 *>(my_scratch + lane * 64 + (i << 4)) = v;
-            }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            __syncwarp();
-            if (lane == 0 && row_ptr[0]) {
-              const int64_t off = reinterpret_cast<__nv_bfloat16 *>(row_ptr[0]) - args.out_h;
-              const int32_t hrow = (int32_t)(off / args.N), hcol = (int32_t)(off - (int64_t)hrow * args.N) + (chunk0 + k) * 32;
-              asm volatile(
-                  "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
-                      reinterpret_cast<uint64_t>(&tm_hs)),
-                  "r"(sm100::smem_u32(my_scratch)), "r"(hcol), "r"(hrow)
-                  : "memory");
-              asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-              asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-            }
-            __syncwarp();
-          } else {
           const uint32_t sw = (lane >> 1) & 3;
 #pragma unroll
           for (int i = 0; i < 4; ++i)
@@ -640,7 +610,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
           }
           __syncwarp();
-          }
         }
         if (k + 1 < CHUNKS) sm100::tmem_ld_wait_regs(v[(k + 1) & 1]);
       }
@@ -658,7 +627,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   }
 
-  if (TS && warp >= EPI_WARP0 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   sm100::tc_fence_before();
   if constexpr (CG == 2) sm100::cluster_sync();  // no CTA leaves while its peer may still signal it
   else __syncthreads();
@@ -718,8 +686,7 @@ bool make_map_3d(CUtensorMap *map, void *base, uint64_t slots, uint64_t rows, ui
 
 struct coe_mlp {
   coe_mlp_config cfg;
-  CUtensorMap xmap, act0, act1, hmap, w1, w2, hstore;
-  bool tma_store = false;  // COE_K3_TMA_STORE: H leaves the up pass by TMA bulk tensor stores
+  CUtensorMap xmap, act0, act1, hmap, w1, w2;
   int num_sms;
   int a_box_rows;
   int cg = 2;                        // CTAs per MMA (COE_K3_CG=1 selects the single-CTA kernel)
@@ -761,17 +728,6 @@ int coe_mlp_create(const coe_mlp_config *cfg, coe_mlp **out) {
   ok &= make_map_2d(&m->act0, cfg->act0, (uint64_t)cfg->act_rows, cfg->d, m->a_box_rows, ld);
   ok &= make_map_2d(&m->act1, cfg->act1, (uint64_t)cfg->act_rows, cfg->d, m->a_box_rows, ld);
   ok &= make_map_2d(&m->hmap, cfg->h_scratch, (uint64_t)cfg->h_rows, cfg->h, BM);
-  {  // H as the up pass's store target: 32 x 32 boxes, no swizzle (the epilogue's dense chunk)
-    EncodeTiledFn fn = encode_fn();
-    cuuint64_t dims[2] = {(cuuint64_t)cfg->h, (cuuint64_t)cfg->h_rows};
-    cuuint64_t strides[1] = {(cuuint64_t)cfg->h * 2};
-    cuuint32_t box[2] = {32, 32};
-    cuuint32_t estr[2] = {1, 1};
-    ok &= fn && fn(&m->hstore, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, cfg->h_scratch, dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-  }
-  m->tma_store = getenv("COE_K3_TMA_STORE") && atoi(getenv("COE_K3_TMA_STORE")) != 0;
   // slot layout: [W1: h x d][W2: d x h]
   // B box: the whole 256-column n-block (1 CTA) or each pair CTA's half of it
   const uint32_t b_rows = (uint32_t)(BN / m->cg);
@@ -794,11 +750,7 @@ int coe_mlp_create(const coe_mlp_config *cfg, coe_mlp **out) {
                         cudaFuncSetAttribute(grouped_gemm_kernel<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              Tiling<2>::SMEM),
                         cudaFuncSetAttribute(grouped_gemm_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             Tiling<2>::SMEM),
-                        cudaFuncSetAttribute(grouped_gemm_kernel<2, false, true>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, Tiling<2>::SMEM),
-                        cudaFuncSetAttribute(grouped_gemm_kernel<2, true, true>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, Tiling<2>::SMEM)})
+                                             Tiling<2>::SMEM)})
     if (r != cudaSuccess) e = r;
   if (e != cudaSuccess) {
     delete m;
@@ -911,7 +863,6 @@ static int launch_grouped(coe_mlp *m, const coe_mlp_group *groups_up, const coe_
     a.out_y = m->out_y;
     a.out_stage = m->out_stage;
     a.debug = getenv("COE_K3_DEBUG") ? atoi(getenv("COE_K3_DEBUG")) : 0;
-    a.tma_store = (m->tma_store && pass == 0) ? 1 : 0;
     if (a.total_tiles <= 0) continue;
     int cap = (max_ctas > 0 && max_ctas < m->num_sms) ? max_ctas : m->num_sms;
     const CUtensorMap &ta0 = pass == 0 ? (m->use_alt ? m->xmap_alt : m->xmap) : m->hmap, &ta1 = pass == 0 ? m->act0 : m->hmap,
@@ -920,8 +871,8 @@ static int launch_grouped(coe_mlp *m, const coe_mlp_group *groups_up, const coe_
     const bool cw = m->cw >= 0 ? m->cw == 1 : (pass == 0 && a.K <= 2048);
     if (m->cg == 1) {
       const int grid = a.total_tiles < cap ? a.total_tiles : cap;
-      if (cw) grouped_gemm_kernel<1, true><<<grid, NUM_THREADS, Tiling<1>::SMEM, stream>>>(ta0, ta1, ta2, tb, m->hstore, a);
-      else grouped_gemm_kernel<1, false><<<grid, NUM_THREADS, Tiling<1>::SMEM, stream>>>(ta0, ta1, ta2, tb, m->hstore, a);
+      if (cw) grouped_gemm_kernel<1, true><<<grid, NUM_THREADS, Tiling<1>::SMEM, stream>>>(ta0, ta1, ta2, tb, a);
+      else grouped_gemm_kernel<1, false><<<grid, NUM_THREADS, Tiling<1>::SMEM, stream>>>(ta0, ta1, ta2, tb, a);
       e = cudaGetLastError();
     } else {
       // pairs: at most one per 128-row tile (the kernel recounts 256-row pair tiles itself)
@@ -938,12 +889,8 @@ static int launch_grouped(coe_mlp *m, const coe_mlp_group *groups_up, const coe_
       attr[0].val.clusterDim.z = 1;
       lc.attrs = attr;
       lc.numAttrs = 1;
-      if (m->tma_store && pass == 0)
-        e = cw ? cudaLaunchKernelEx(&lc, grouped_gemm_kernel<2, true, true>, ta0, ta1, ta2, tb, m->hstore, a)
-               : cudaLaunchKernelEx(&lc, grouped_gemm_kernel<2, false, true>, ta0, ta1, ta2, tb, m->hstore, a);
-      else
-        e = cw ? cudaLaunchKernelEx(&lc, grouped_gemm_kernel<2, true>, ta0, ta1, ta2, tb, m->hstore, a)
-               : cudaLaunchKernelEx(&lc, grouped_gemm_kernel<2, false>, ta0, ta1, ta2, tb, m->hstore, a);
+      e = cw ? cudaLaunchKernelEx(&lc, grouped_gemm_kernel<2, true>, ta0, ta1, ta2, tb, a)
+                : cudaLaunchKernelEx(&lc, grouped_gemm_kernel<2, false>, ta0, ta1, ta2, tb, a);
     }
     if (e != cudaSuccess) {
       coe_set_error(std::string("grouped_gemm_kernel launch: ") + cudaGetErrorString(e));
