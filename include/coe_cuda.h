@@ -365,6 +365,16 @@ int coe_runtime_attach_comm(coe_runtime *rt, coe_comm *comm);
  * is served from the host tier (identical bytes, decisions unchanged).  peers[r] = the
  * runtime of executor r (world entries; peers[rank] is rt itself). */
 int coe_runtime_attach_local_experts(coe_runtime *rt, coe_runtime *const *peers, int32_t world);
+/* The same tier between PROCESSES (one executor per rank, CUDA IPC): export this runtime's
+ * expert allocations (pooled slab, or one slab per shape; *count handles of 64 bytes), map a
+ * peer rank's, and after every step hand each rank's end-of-step residency to the others
+ * (per expert: slab << 40 | byte offset, -1 when not resident).  A qualifying peer-tier copy
+ * waits for the source rank's step-end flag; a rank whose experts were read makes its next
+ * step's copies wait for the readers' step end. */
+int coe_runtime_ipc_export_experts(coe_runtime *rt, void *handles, int32_t *count);
+int coe_runtime_ipc_open_experts(coe_runtime *rt, int32_t rank, const void *handles, int32_t count);
+int coe_runtime_residency_codes(coe_runtime *rt, int64_t *codes /* [num_experts] */);
+int coe_runtime_set_peer_residency(coe_runtime *rt, int32_t rank, const int64_t *codes);
 /* scheduling knobs (see coe_runtime_config); reserve_sms < 0 keeps the current split */
 int coe_runtime_set_knobs(coe_runtime *rt, int64_t wave_rows_cap, int64_t urgent_rows_cap, int32_t reserve_sms);
 
