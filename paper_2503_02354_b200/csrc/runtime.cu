@@ -2159,7 +2159,9 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     for (int r = 0; r < rt->peer_world; ++r)
       if (r != x && !wait_flag(cs, rt->d_hflags + rt->hflag_step_base + r, seq - 1)) return COE_CUDA_ERR_CUDA;
   if (!ok(cudaEventRecord(rt->staging_done[set_idx], ks), "record") || !ok(cudaEventRecord(rt->staged, ks), "record") ||
-      !ok(cudaStreamWaitEvent(cs, rt->staged, 0), "compute waits upload"))
+      !ok(cudaStreamWaitEvent(cs, rt->staged, 0), "compute waits upload") ||
+      // the input gathers read this step's input map (uploaded above on the copy stream)
+      (e2e_in && !ok(cudaStreamWaitEvent(rt->copy_in, rt->staged, 0), "inputs wait upload")))
     return fail_cuda();
   int32_t *d_exec = sb.adm, *d_rank = sb.adm + n_adm, *d_req = sb.adm + 2 * n_adm, *d_stage = sb.adm + 3 * n_adm;
   int idx_bits = 1;
