@@ -119,7 +119,7 @@ struct CopyAct {
   coe_runtime *peer_rt = nullptr;
   int32_t peer_exec = -1;
   int32_t peer_par = 0;
-  // pooled memory: the W1 half may land on bytes another expert (of another shape, or placed
+  // pooled memory: the W1 half lands on bytes an earlier expert (another shape, or placed
   // elsewhere) used as ITS W2, so it must wait for the down passes too, not just the up passes
   bool w1_waits_down = false;
 };
@@ -275,6 +275,7 @@ struct coe_runtime {
   char *pool = nullptr;
   std::map<int32_t, int32_t> free_runs;  // first unit -> run length
   std::vector<int32_t> unit_owner;       // slot that last used the unit (-1: never)
+  std::vector<uint8_t> unit_w2;          // the unit held the W2 half of its last expert
   std::vector<int32_t> slot_unit, slot_units;  // per slot: first unit / units of its residency
   std::vector<int32_t> expert_vslot;     // expert -> its bookkeeping slot
 
@@ -470,6 +471,7 @@ bool pool_create(coe_runtime *rt, int64_t pool_bytes) {
   rt->pooled = true;
   rt->free_runs = {{0, (int32_t)rt->pool_units}};
   rt->unit_owner.assign((size_t)rt->pool_units, -1);
+  rt->unit_w2.assign((size_t)rt->pool_units, 0);
   rt->slot_unit.assign(rt->total_slots, -1);
   rt->slot_units.assign(rt->total_slots, 0);
   rt->expert_vslot.assign(rt->cfg.num_experts, -1);
@@ -784,6 +786,7 @@ int coe_runtime_init_experts(coe_runtime *rt) {
   if (rt->pooled) {  // every unit free
     rt->free_runs = {{0, (int32_t)rt->pool_units}};
     std::fill(rt->unit_owner.begin(), rt->unit_owner.end(), -1);
+    std::fill(rt->unit_w2.begin(), rt->unit_w2.end(), 0);
     std::fill(rt->slot_units.begin(), rt->slot_units.end(), 0);
   }
   std::fill(rt->slot_expert.begin(), rt->slot_expert.end(), -1);
@@ -1238,6 +1241,7 @@ struct CopyInfo {
   bool first_write;                // slot not written earlier this step
   std::vector<int32_t> deps;       // slots whose readers must finish first (pooled: the units' last users)
   int32_t unit0 = -1;              // pooled: first unit of the expert's new place
+  bool w1_over_w2 = false;         // pooled: its W1 lands on units an earlier expert used for W2
   const char *peer_src = nullptr;  // (f3) copy from this peer executor's HBM instead of the host store
   coe_runtime *peer_rt = nullptr;  // in-process peer (else another process: peer_exec's IPC mapping)
   int32_t peer_exec = -1;
@@ -1490,7 +1494,13 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
       if (u0 > start) rt->free_runs.emplace(start, u0 - start);
       if (u0 + n < start + len) rt->free_runs.emplace(u0 + n, start + len - u0 - n);
       const std::vector<int32_t> *last_rd = nullptr;
+      // the W1 half lands on units that held an earlier expert's W2 (any byte of it) -> it
+      // must wait for their down passes; a unit holding any W2 byte counts as W2
+      const int64_t half = rt->sbytes[k] / 2;
+      const int32_t w1_units = (int32_t)((half + rt->unit - 1) / rt->unit);  // units with W1 bytes
+      for (int32_t u = u0; u < u0 + w1_units; ++u) ci.w1_over_w2 |= rt->unit_w2[u] != 0;
       for (int32_t u = u0; u < u0 + n; ++u) {
+        rt->unit_w2[u] = (int64_t)(u - u0 + 1) * rt->unit > half;
         const int32_t owner = rt->unit_owner[u];
         if (owner >= 0 && std::find(ci.deps.begin(), ci.deps.end(), owner) == ci.deps.end()) ci.deps.push_back(owner);
         if (unit_rd[u] && unit_rd[u].get() != last_rd) {
@@ -1982,8 +1992,7 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
         ca.peer_rt = ci.peer_rt;
         ca.peer_exec = ci.peer_exec;
         ca.peer_par = ci.peer_par;
-        if (rt->pooled)
-          for (int32_t q : ci.deps) ca.w1_waits_down |= q != ci.slot;
+        ca.w1_waits_down = ci.w1_over_w2;
         for (int32_t q : ci.deps)  // the slot itself, and (VMM) the last users of its pages
           for (int k = 0; k < NCLS; ++k) {
             const int32_t wv = last_reader_wave[q * NCLS + k];
