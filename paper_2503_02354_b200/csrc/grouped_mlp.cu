@@ -74,20 +74,14 @@ static_assert(sizeof(TileCrd) <= 128, "TileCrd exceeds its slot");
 // (256 x 64) per stage; 2 -- a CTA pair (cluster of 2 on one TPC) computes a 256 x 256 tile
 // with tcgen05.mma.cta_group::2: each CTA loads its own 128 A rows and HALF of B (128 x 64),
 // so per-CTA operand traffic per stage drops from 48 KB to 32 KB for the same MMA work.
-// W (CG = 2 only): 256 x 512 pair tiles -- each A stage feeds TWO 256-column MMAs (two B boxes
-// per CTA per stage, 48 KB stages, 4 deep), a single 512-column TMEM accumulator: 25 % fewer
-// operand bytes per FLOP for the latency-bound small-K up passes, at the cost of an epilogue
-// the next tile's MMAs cannot overlap.
-template <int CG, bool W = false>
+template <int CG>
 struct Tiling {
   static constexpr int TILE_M = BM * CG;
-  static constexpr int TILE_N = W ? 2 * BN : BN;
-  static constexpr int B_ROWS = BN / CG;  // rows of one B box (one 256-column MMA's half)
+  static constexpr int B_ROWS = BN / CG;
   static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = (W ? 2 : 1) * B_ROWS * BK * 2;
+  static constexpr int B_BYTES = B_ROWS * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = W ? 4 : (CG == 1 ? 4 : 6);
-  static constexpr int ACC = W ? 1 : 2;  // TMEM accumulators (512 columns either way)
+  static constexpr int STAGES = CG == 1 ? 4 : 6;
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + MAX_GROUPS * 4 +
                               CRD_STAGES * 128 + EPI_WARPS * EPI_SCRATCH;
 };
@@ -168,12 +162,12 @@ __device__ __forceinline__ TileCoord decode_tile(int t, const int32_t *tile_star
   return c;
 }
 
-template <int CG, bool CW, bool W = false>
+template <int CG, bool CW>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tm_a0, const __grid_constant__ CUtensorMap tm_a1,
                         const __grid_constant__ CUtensorMap tm_a2, const __grid_constant__ CUtensorMap tm_b,
                         GemmArgs args) {
-  using TL = Tiling<CG, W>;
+  using TL = Tiling<CG>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *stage_base = smem;
@@ -298,7 +292,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                                       box_par[b] == 0 ? &tm_a0 : (box_par[b] == 1 ? &tm_a1 : &tm_a2), bar, kb * BK,
                                       box_row[b]);
             sm100::tma_load_3d_pair(sb, &tm_b, bar, kb * BK, b_row, slot);
-            if constexpr (W) sm100::tma_load_3d_pair(sb + TL::B_ROWS * BK * 2, &tm_b, bar, kb * BK, b_row + BN, slot);
           }
           if (++stage == TL::STAGES) {
             stage = 0;
@@ -350,7 +343,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           box_par[0] = 0;
           a_bytes = TL::A_BYTES;
         }
-        const int b_row = c.n_blk * TL::TILE_N + (int)cta_rank * TL::B_ROWS;
+        const int b_row = c.n_blk * BN + (int)cta_rank * TL::B_ROWS;
         for (int kb = 0; kb < k_blocks; ++kb) {
           sm100::mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t *sa = stage_base + stage * TL::STAGE_BYTES;
@@ -374,8 +367,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                                       box_par[b] == 0 ? &tm_a0 : (box_par[b] == 1 ? &tm_a1 : &tm_a2), bar, kb * BK,
                                       box_row[b]);
             sm100::tma_load_3d_pair(sb, &tm_b, bar, kb * BK, b_row, grp.slot);
-            if constexpr (W)
-              sm100::tma_load_3d_pair(sb + TL::B_ROWS * BK * 2, &tm_b, bar, kb * BK, b_row + BN, grp.slot);
           }
           if (++stage == TL::STAGES) {
             stage = 0;
@@ -451,7 +442,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               qbase = dst + ((size_t)req * args.T + (row - j * args.T)) * args.ld;
             }
           }
-          qbase += c.n_blk * TL::TILE_N;
+          qbase += c.n_blk * BN;
         }
       }
       sm100::mbar_wait(&crd_empty[cs], cph ^ 1);
@@ -465,7 +456,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if (lane == 0) {
         e.nboxes = nboxes;
         e.slot = grp.slot;
-        e.b_row = c.n_blk * TL::TILE_N + (int)cta_rank * TL::B_ROWS;
+        e.b_row = c.n_blk * BN + (int)cta_rank * TL::B_ROWS;
         e.a_bytes = args.mode == 0 ? (uint32_t)(nboxes * args.a_box_rows * BK * 2) : (uint32_t)TL::A_BYTES;
       }
       __syncwarp();
@@ -498,10 +489,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             uint64_t bdesc = sm100::make_desc_k_sw128(sb + k * 32);
             if constexpr (CG == 1) sm100::mma_bf16_ss(d_tmem, adesc, bdesc, idesc, (kb | k) != 0);
             else sm100::mma_bf16_ss_pair(d_tmem, adesc, bdesc, idesc, (kb | k) != 0);
-            if constexpr (W) {  // the second 256 columns, same A
-              uint64_t bdesc1 = sm100::make_desc_k_sw128(sb + TL::B_ROWS * BK * 2 + k * 32);
-              sm100::mma_bf16_ss_pair(d_tmem + BN, adesc, bdesc1, idesc, (kb | k) != 0);
-            }
           }
           if constexpr (CG == 1) sm100::mma_commit(&empty_bar[stage]);
           else sm100::mma_commit_pair(&empty_bar[stage], 0x3);  // frees the stage in both CTAs
@@ -512,7 +499,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         if constexpr (CG == 1) sm100::mma_commit(&tfull_bar[acc]);
         else sm100::mma_commit_pair(&tfull_bar[acc], 0x3);
-        if (++acc == TL::ACC) {
+        if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
         }
@@ -522,9 +509,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // ===== epilogue (each CTA drains its own 128 TMEM lanes; warps w and w+4 share a lane
     // quarter and split its 256 columns; TMEM loads run one 32-column chunk ahead) =====
     const uint32_t quarter = warp & 3;
-    constexpr int CHUNKS = TL::TILE_N / 32 / 2;
-    const int chunk0 = (int)((warp - EPI_WARP0) >> 2) * CHUNKS;
+    const int chunk0 = (int)((warp - EPI_WARP0) >> 2) * (BN / 32 / 2);
     uint8_t *my_scratch = epi_scratch + (warp - EPI_WARP0) * EPI_SCRATCH;
+    constexpr int CHUNKS = BN / 32 / 2;
     const uint32_t tempty_leader = CG == 2 ? sm100::mapa_shared(sm100::smem_u32(&tempty_bar[0]), 0) : 0;
     const size_t out_stride = args.mode == 0 ? (size_t)args.N : (size_t)args.ld;
     int acc = 0;
@@ -574,7 +561,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             out_row = dst + ((size_t)req * args.T + (row - j * args.T)) * args.ld;
           }
         }
-        out_row += c.n_blk * TL::TILE_N;
+        out_row += c.n_blk * BN;
       }
       }
       sm100::mbar_wait(&tfull_bar[acc], acc_phase);
@@ -633,7 +620,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         __syncwarp();
         if (lane == 0) sm100::mbar_arrive_cluster(tempty_leader + acc * 8);  // the leader's tempty[acc]
       }
-      if (++acc == TL::ACC) {
+      if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
       }
@@ -703,7 +690,6 @@ struct coe_mlp {
   int num_sms;
   int a_box_rows;
   int cg = 2;                        // CTAs per MMA (COE_K3_CG=1 selects the single-CTA kernel)
-  bool wide = false;  // COE_K3_WIDE: 256 x 512 pair tiles for up passes (experiment)
   int cw = -1;  // coordinate warp: -1 auto (up passes with K <= 2048: +6-10 %; elsewhere -1-3 %,
                 // profiles/r2o_k3_coord_ab.json), 0 / 1 forced by COE_K3_COORD
   CUtensorMap xmap_alt;              // stage-0 inputs from a second X buffer (coe_mlp_set_input)
@@ -734,7 +720,6 @@ int coe_mlp_create(const coe_mlp_config *cfg, coe_mlp **out) {
   m->cfg = *cfg;
   if (const char *v = getenv("COE_K3_CG")) m->cg = atoi(v) == 1 ? 1 : 2;
   if (const char *v = getenv("COE_K3_COORD")) m->cw = atoi(v) != 0 ? 1 : 0;
-  m->wide = getenv("COE_K3_WIDE") && atoi(getenv("COE_K3_WIDE")) != 0 && m->cg == 2 && cfg->h % 512 == 0;
   m->a_box_rows = cfg->T < BM ? cfg->T : BM;
   bool ok = true;
   const uint64_t ld = cfg->act_ld > 0 ? (uint64_t)cfg->act_ld : (uint64_t)cfg->d;
@@ -764,10 +749,6 @@ int coe_mlp_create(const coe_mlp_config *cfg, coe_mlp **out) {
                                              Tiling<1>::SMEM),
                         cudaFuncSetAttribute(grouped_gemm_kernel<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              Tiling<2>::SMEM),
-                        cudaFuncSetAttribute(grouped_gemm_kernel<2, false, true>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, Tiling<2, true>::SMEM),
-                        cudaFuncSetAttribute(grouped_gemm_kernel<2, true, true>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, Tiling<2, true>::SMEM),
                         cudaFuncSetAttribute(grouped_gemm_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              Tiling<2>::SMEM)})
     if (r != cudaSuccess) e = r;
@@ -868,8 +849,7 @@ static int launch_grouped(coe_mlp *m, const coe_mlp_group *groups_up, const coe_
     a.K = pass == 0 ? c.d : c.h;
     a.N = pass == 0 ? c.h : c.d;
     a.ld = c.act_ld > 0 ? c.act_ld : c.d;
-    const bool wide = m->wide && pass == 0;
-    a.n_blocks = a.N / (wide ? 2 * BN : BN);
+    a.n_blocks = a.N / BN;
     a.mode = pass;
     a.a_box_rows = m->a_box_rows;
     a.out_h = reinterpret_cast<__nv_bfloat16 *>(c.h_scratch);
@@ -900,7 +880,7 @@ static int launch_grouped(coe_mlp *m, const coe_mlp_group *groups_up, const coe_
       cudaLaunchConfig_t lc{};
       lc.gridDim = dim3(2 * pairs);
       lc.blockDim = dim3(NUM_THREADS);
-      lc.dynamicSmemBytes = wide ? Tiling<2, true>::SMEM : Tiling<2>::SMEM;
+      lc.dynamicSmemBytes = Tiling<2>::SMEM;
       lc.stream = stream;
       cudaLaunchAttribute attr[1];
       attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -909,12 +889,8 @@ static int launch_grouped(coe_mlp *m, const coe_mlp_group *groups_up, const coe_
       attr[0].val.clusterDim.z = 1;
       lc.attrs = attr;
       lc.numAttrs = 1;
-      if (wide)
-        e = cw ? cudaLaunchKernelEx(&lc, grouped_gemm_kernel<2, true, true>, ta0, ta1, ta2, tb, a)
-               : cudaLaunchKernelEx(&lc, grouped_gemm_kernel<2, false, true>, ta0, ta1, ta2, tb, a);
-      else
-        e = cw ? cudaLaunchKernelEx(&lc, grouped_gemm_kernel<2, true>, ta0, ta1, ta2, tb, a)
-               : cudaLaunchKernelEx(&lc, grouped_gemm_kernel<2, false>, ta0, ta1, ta2, tb, a);
+      e = cw ? cudaLaunchKernelEx(&lc, grouped_gemm_kernel<2, true>, ta0, ta1, ta2, tb, a)
+                : cudaLaunchKernelEx(&lc, grouped_gemm_kernel<2, false>, ta0, ta1, ta2, tb, a);
     }
     if (e != cudaSuccess) {
       coe_set_error(std::string("grouped_gemm_kernel launch: ") + cudaGetErrorString(e));
