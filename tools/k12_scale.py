@@ -27,6 +27,17 @@ def main() -> None:
     stream = torch.cuda.current_stream().cuda_stream
     peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                                        "MEASURED_PEAKS.json"))).get("hbm_gbs", 6539.2)
+    cub = None
+    cub_path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "cub_ab", "libcub_sort.so")
+    if os.path.exists(cub_path):
+        import ctypes
+
+        cub = ctypes.CDLL(cub_path)
+        cub.cub_sort_pairs_scratch_bytes.restype = ctypes.c_size_t
+        cub.cub_sort_pairs_scratch_bytes.argtypes = [ctypes.c_int64]
+        cub.cub_sort_pairs.restype = ctypes.c_int
+        cub.cub_sort_pairs.argtypes = [ctypes.c_void_p] * 4 + [ctypes.c_int64, ctypes.c_int, ctypes.c_void_p,
+                                                                ctypes.c_size_t, ctypes.c_void_p]
     rows = []
     for n in (13642, 262144, 1 << 20, 1 << 22, 1 << 24):
         rng = np.random.default_rng(n)
@@ -66,6 +77,18 @@ def main() -> None:
 
         res = {"admissions": n, "batches": nb, "rank_bits": bits, "passes": passes}
         cases = [("k1", k1, 16 * n), ("k2", k2, 24 * n + 12 * nb)]
+        if cub is not None:  # library baseline: CUB SortPairs on the same keys, values and bit range
+            ck_in = t_rk.clone()  # executor 0: the key is the run-rank
+            cv_in = torch.arange(n, dtype=torch.int32, device=dev)
+            ck_out, cv_out = torch.empty_like(ck_in), torch.empty_like(cv_in)
+            cbytes = cub.cub_sort_pairs_scratch_bytes(n)
+            cscratch = torch.empty(max(1, cbytes), dtype=torch.uint8, device=dev)
+
+            def cub_sort():
+                assert cub.cub_sort_pairs(ck_in.data_ptr(), ck_out.data_ptr(), cv_in.data_ptr(), cv_out.data_ptr(),
+                                          n, bits, cscratch.data_ptr(), cbytes, stream) == 0
+
+            cases.append(("cub_sort_pairs", cub_sort, 16 * n))
         for name, fn, byts in cases:
             for _ in range(3):
                 fn()
@@ -83,6 +106,9 @@ def main() -> None:
         assert int(flags[1].item()) == 0, "batch straddles a run"
         ref = np.lexsort((np.arange(n), rank, ex))
         assert np.array_equal(perm.cpu().numpy(), ref)
+        if cub is not None:
+            assert np.array_equal(cv_out.cpu().numpy(), ref), "CUB baseline order differs"
+            res["k1_speedup_vs_cub"] = res["cub_sort_pairs"]["us"] / res["k1"]["us"]
         rows.append(res)
         print(json.dumps(res), flush=True)
     json.dump({"rows": rows, "hbm_peak_gbs": peak}, open(out, "w"), indent=1)
