@@ -1,9 +1,9 @@
 """K1 (coe_group_sort) and K2 (coe_run_compact) from serving size up to HBM-bound sizes.
 
-    python tools/k12_scale.py [out.json]
+    python tools/k12_scale.py [out.json] [serving|random]
 
 Admissions of one executor with run-ranks like a serving queue (a new run every ~5
-admissions), sorted by (executor, run_rank) and compacted into batches of <= 8.  Times are
+admissions; or uniform 22-bit run-ranks with "random"), sorted by (executor, run_rank) and compacted into batches of <= 8.  Times are
 CUDA events over 20 launches after warm-up; algorithmic bytes: K1 16 B per admission (read
 executor + run_rank, write permutation + key), K2 24 B per admission (read permutation, key,
 request, stage; write member request + stage) plus 12 B per batch.
@@ -22,6 +22,7 @@ from paper_2503_02354_b200._cuda_sigs import check  # noqa: E402
 
 def main() -> None:
     out = sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/k12_scale.json"
+    dist = sys.argv[2] if len(sys.argv) > 2 else "serving"
     lib = _native.cuda_lib()
     dev = torch.device("cuda")
     stream = torch.cuda.current_stream().cuda_stream
@@ -41,8 +42,11 @@ def main() -> None:
     rows = []
     for n in (13642, 262144, 1 << 20, 1 << 22, 1 << 24):
         rng = np.random.default_rng(n)
-        rank = np.cumsum(rng.random(n) < 0.2).astype(np.int32)
-        rank = np.minimum(rank, (1 << 23) - 1)
+        if dist == "random":  # uniform 22-bit run-ranks: every tile touches every digit
+            rank = rng.integers(0, 1 << 22, n).astype(np.int32)
+        else:
+            rank = np.cumsum(rng.random(n) < 0.2).astype(np.int32)
+            rank = np.minimum(rank, (1 << 23) - 1)
         ex = np.zeros(n, np.int32)
         bits = max(1, int(rank.max()).bit_length())
         passes = (bits + 7) // 8
@@ -51,7 +55,7 @@ def main() -> None:
         keys = torch.empty(n, dtype=torch.int32, device=dev)
         scratch = torch.empty(lib.coe_group_sort_scratch_bytes(n), dtype=torch.uint8, device=dev)
         # batches: each run split into slices of <= 8, in run order
-        starts = np.flatnonzero(np.r_[True, np.diff(rank) != 0])
+        starts = np.flatnonzero(np.r_[True, np.diff(np.sort(rank)) != 0])
         lens = np.diff(np.r_[starts, n])
         sizes = np.concatenate([np.r_[np.full(l // 8, 8), [l % 8] if l % 8 else []] for l in lens]).astype(np.int32)
         nb = len(sizes)
@@ -75,7 +79,7 @@ def main() -> None:
                                            mreq.data_ptr(), mst.data_ptr(), flags.data_ptr(), flags[1:].data_ptr(),
                                            cscr.data_ptr(), stream), "compact")
 
-        res = {"admissions": n, "batches": nb, "rank_bits": bits, "passes": passes}
+        res = {"admissions": n, "batches": nb, "rank_bits": bits, "passes": passes, "keys": dist}
         cases = [("k1", k1, 16 * n), ("k2", k2, 24 * n + 12 * nb)]
         if cub is not None:  # library baseline: CUB SortPairs on the same keys, values and bit range
             ck_in = t_rk.clone()  # executor 0: the key is the run-rank
@@ -111,7 +115,7 @@ def main() -> None:
             res["k1_speedup_vs_cub"] = res["cub_sort_pairs"]["us"] / res["k1"]["us"]
         rows.append(res)
         print(json.dumps(res), flush=True)
-    json.dump({"rows": rows, "hbm_peak_gbs": peak}, open(out, "w"), indent=1)
+    json.dump({"rows": rows, "hbm_peak_gbs": peak, "keys": dist}, open(out, "w"), indent=1)
 
 
 if __name__ == "__main__":
