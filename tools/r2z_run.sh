@@ -1,9 +1,8 @@
+# Final round-2 evidence on the final code: GPU suite, smoke, then tools/profile_round.sh r2z
 set -u
 mkdir -p gpurun_out
-for v in 0 20 35 50; do
-  COE_INPUT_SPLIT=$v timeout 600 python tools/timeline.py c1 10000 gpurun_out/r2z_tl_c1_split$v.json e2e > gpurun_out/r2z_tl_c1_split$v.log 2>&1
-  COE_INPUT_SPLIT=$v timeout 600 python tools/timeline.py c3 10000 gpurun_out/r2z_tl_c3_split$v.json e2e > gpurun_out/r2z_tl_c3_split$v.log 2>&1
-  echo "split $v done" >> gpurun_out/r2z_rc.txt
-done
-COE_INPUT_SPLIT=35 timeout 600 python -m pytest tests/test_gpu_serving.py -m gpu -q -x -k "end_to_end or e2e or streamed" > gpurun_out/r2z_e2e_split.log 2>&1; echo "e2e tests split rc=$?" >> gpurun_out/r2z_rc.txt
+timeout 1800 python -m pytest tests -m gpu -q --timeout 400 > gpurun_out/r2z_gputest.log 2>&1; echo "gpu tests rc=$?" >> gpurun_out/r2z_rc.txt
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/r2z_smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/r2z_rc.txt
+bash tools/profile_round.sh r2z > gpurun_out/r2z_profile_round.log 2>&1; echo "profile round rc=$?" >> gpurun_out/r2z_rc.txt
+for f in gpurun_out/r2z_bench_*.log; do echo "$f rc-tail: $(tail -c 200 $f | tr '\n' ' ')" >> gpurun_out/r2z_rc.txt; done
 cat gpurun_out/r2z_rc.txt
