@@ -1,4 +1,7 @@
-"""One coe_group_sort call at n admissions (the command ncu profiles).  python tools/k1_once.py [n]"""
+"""One coe_group_sort call at n admissions (the command ncu profiles).
+
+    python tools/k1_once.py [n] [serving|random]
+serving: run-ranks like a serving queue (a new run every ~5 admissions); random: uniform 22-bit."""
 import os, sys
 import numpy as np
 import torch
@@ -9,7 +12,10 @@ from paper_2503_02354_b200._cuda_sigs import check  # noqa: E402
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 24
 lib = _native.cuda_lib()
 rng = np.random.default_rng(n)
-rank = np.cumsum(rng.random(n) < 0.2).astype(np.int32)
+if len(sys.argv) > 2 and sys.argv[2] == "random":
+    rank = rng.integers(0, 1 << 22, n).astype(np.int32)
+else:
+    rank = np.cumsum(rng.random(n) < 0.2).astype(np.int32)
 bits = max(1, int(rank.max()).bit_length())
 dev = torch.device("cuda")
 t_ex = torch.zeros(n, dtype=torch.int32, device=dev)
