@@ -252,25 +252,42 @@ __global__ void __launch_bounds__(SORT_THREADS, ITEMS >= 16 ? 3 : 6)
   }
 }
 
-// K2 part 1: gather members, mark run starts / executor segment starts.
-__global__ void compact_gather(const int32_t *perm, const uint32_t *keys, const int32_t *adm_req,
+// K2 part 1: gather members, mark run starts / executor segment starts.  Each thread handles
+// GATHER_ITEMS admissions (block-strided, so every load instruction stays coalesced) and issues
+// all their perm / key loads before the dependent member gathers: several independent chains in
+// flight per thread (one per thread left it latency-bound at ~2.6 TB/s, profiles/r2n9_*).
+constexpr int GATHER_ITEMS = 4;
+
+__global__ void __launch_bounds__(256) compact_gather(const int32_t *perm, const uint32_t *keys, const int32_t *adm_req,
                                const int32_t *adm_stage, const int32_t *adm_in, const int32_t *adm_out, int64_t n,
                                int rank_bits, int32_t *member_req, int32_t *member_stage, int32_t *member_in,
                                int32_t *member_out, int32_t *seg_start, int32_t *run_count) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  int starts = 0;
-  if (i < n) {
-    int32_t p = perm[i];
-    member_req[i] = adm_req[p];
-    member_stage[i] = adm_stage[p];
-    if (adm_in) {  // activation-row routes (coe_run_compact_routes)
-      member_in[i] = adm_in[p];
-      member_out[i] = adm_out[p];
+  const int64_t base = (int64_t)blockIdx.x * (blockDim.x * GATHER_ITEMS) + threadIdx.x;
+  int32_t p[GATHER_ITEMS];
+  uint32_t k[GATHER_ITEMS], kp[GATHER_ITEMS];
+#pragma unroll
+  for (int j = 0; j < GATHER_ITEMS; ++j) {
+    const int64_t i = base + (int64_t)j * blockDim.x;
+    if (i < n) {
+      p[j] = perm[i];
+      k[j] = keys[i];
+      kp[j] = i > 0 ? keys[i - 1] : ~k[j];
     }
-    uint32_t k = keys[i];
-    bool new_run = i == 0 || keys[i - 1] != k;
-    starts = new_run ? 1 : 0;
-    if (i == 0 || (keys[i - 1] >> rank_bits) != (k >> rank_bits)) seg_start[k >> rank_bits] = (int32_t)i;
+  }
+  int starts = 0;
+#pragma unroll
+  for (int j = 0; j < GATHER_ITEMS; ++j) {
+    const int64_t i = base + (int64_t)j * blockDim.x;
+    if (i < n) {
+      member_req[i] = adm_req[p[j]];
+      member_stage[i] = adm_stage[p[j]];
+      if (adm_in) {  // activation-row routes (coe_run_compact_routes)
+        member_in[i] = adm_in[p[j]];
+        member_out[i] = adm_out[p[j]];
+      }
+      if (i == 0 || kp[j] != k[j]) ++starts;
+      if (i == 0 || (kp[j] >> rank_bits) != (k[j] >> rank_bits)) seg_start[k[j] >> rank_bits] = (int32_t)i;
+    }
   }
   // block-reduce the run starts into one atomic
   for (int off = 16; off; off >>= 1) starts += __shfl_down_sync(0xffffffffu, starts, off);
@@ -278,9 +295,9 @@ __global__ void compact_gather(const int32_t *perm, const uint32_t *keys, const 
   if ((threadIdx.x & 31) == 0) warp_sum[threadIdx.x >> 5] = starts;
   __syncthreads();
   if (threadIdx.x == 0) {
-    int s = 0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += warp_sum[w];
-    if (s) atomicAdd(run_count, s);
+    int sum = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) sum += warp_sum[w];
+    if (sum) atomicAdd(run_count, sum);
   }
 }
 
@@ -611,7 +628,7 @@ int coe_run_compact_routes(const int32_t *perm, const int32_t *sorted_keys, cons
       !check(cudaMemsetAsync(out_violations, 0, 4, stream), "compact memset"))
     return COE_CUDA_ERR_CUDA;
   if (n > 0) {
-    const int blocks = (int)((n + 255) / 256);
+    const int blocks = (int)((n + 256 * GATHER_ITEMS - 1) / (256 * GATHER_ITEMS));
     compact_gather<<<blocks, 256, 0, stream>>>(perm, reinterpret_cast<const uint32_t *>(sorted_keys), adm_request,
                                                adm_stage, adm_in, adm_out, n, rank_bits, out_member_req,
                                                out_member_stage, out_member_in, out_member_out, seg_start,
