@@ -332,16 +332,27 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int *warp_sums, int &
   return incl - v;
 }
 
+// Each thread owns BATCH_ITEMS consecutive batches (loads of several batches in flight per
+// thread; the block's scan runs over the per-thread sums).
+constexpr int BATCH_ITEMS = 4;
+constexpr int BATCH_PER_BLOCK = BATCH_THREADS * BATCH_ITEMS;
+
 __global__ void __launch_bounds__(BATCH_THREADS) batch_block_sums(const int32_t *batch_exec, const int32_t *batch_size,
                                                                   int num_batches, int num_executors,
                                                                   int32_t *block_sums) {
   __shared__ int warp_sums[32];
-  const int b = blockIdx.x * BATCH_THREADS + threadIdx.x;
-  const int x = b < num_batches ? batch_exec[b] : -1;
-  const int v = b < num_batches ? batch_size[b] : 0;
+  const int b0 = blockIdx.x * BATCH_PER_BLOCK + threadIdx.x * BATCH_ITEMS;
+  int x[BATCH_ITEMS], v[BATCH_ITEMS];
+#pragma unroll
+  for (int j = 0; j < BATCH_ITEMS; ++j) {
+    x[j] = b0 + j < num_batches ? batch_exec[b0 + j] : -1;
+    v[j] = b0 + j < num_batches ? batch_size[b0 + j] : 0;
+  }
   for (int e = 0; e < num_executors; ++e) {
-    int total;
-    block_exclusive_scan(x == e ? v : 0, warp_sums, total);
+    int sum = 0, total;
+#pragma unroll
+    for (int j = 0; j < BATCH_ITEMS; ++j) sum += x[j] == e ? v[j] : 0;
+    block_exclusive_scan(sum, warp_sums, total);
     if (threadIdx.x == 0) block_sums[(int64_t)blockIdx.x * num_executors + e] = total;
   }
 }
@@ -372,21 +383,38 @@ __global__ void __launch_bounds__(BATCH_THREADS) compact_batches(const int32_t *
                                                                  const uint32_t *keys, int64_t n, int rank_bits,
                                                                  int32_t *batch_off, int32_t *violations) {
   __shared__ int warp_sums[32];
-  const int b = blockIdx.x * BATCH_THREADS + threadIdx.x;
-  const int x = b < num_batches ? batch_exec[b] : -1;
-  const int v = b < num_batches ? batch_size[b] : 0;
-  int mine = 0;
+  const int b0 = blockIdx.x * BATCH_PER_BLOCK + threadIdx.x * BATCH_ITEMS;
+  int x[BATCH_ITEMS], v[BATCH_ITEMS], mine[BATCH_ITEMS];
+#pragma unroll
+  for (int j = 0; j < BATCH_ITEMS; ++j) {
+    x[j] = b0 + j < num_batches ? batch_exec[b0 + j] : -1;
+    v[j] = b0 + j < num_batches ? batch_size[b0 + j] : 0;
+    mine[j] = 0;
+  }
   for (int e = 0; e < num_executors; ++e) {
-    int total;
-    const int ex = block_exclusive_scan(x == e ? v : 0, warp_sums, total);
-    if (x == e) mine = seg_start[e] + block_sums[(int64_t)blockIdx.x * num_executors + e] + ex;
+    int sum = 0, total;
+#pragma unroll
+    for (int j = 0; j < BATCH_ITEMS; ++j) sum += x[j] == e ? v[j] : 0;
+    int run = block_exclusive_scan(sum, warp_sums, total);
+    const int base = seg_start[e] + block_sums[(int64_t)blockIdx.x * num_executors + e];
+#pragma unroll
+    for (int j = 0; j < BATCH_ITEMS; ++j)
+      if (x[j] == e) {
+        mine[j] = base + run;
+        run += v[j];
+      }
   }
-  if (b < num_batches) {
-    batch_off[b] = mine;
-    const int64_t lo = mine, hi = lo + v - 1;
-    const bool bad = v <= 0 || lo < 0 || hi >= n || keys[lo] != keys[hi] || (int)(keys[lo] >> rank_bits) != x;
-    if (bad) atomicAdd(violations, 1);
+  int bad_count = 0;
+#pragma unroll
+  for (int j = 0; j < BATCH_ITEMS; ++j) {
+    if (b0 + j < num_batches) {
+      batch_off[b0 + j] = mine[j];
+      const int64_t lo = mine[j], hi = lo + v[j] - 1;
+      const bool bad = v[j] <= 0 || lo < 0 || hi >= n || keys[lo] != keys[hi] || (int)(keys[lo] >> rank_bits) != x[j];
+      bad_count += bad ? 1 : 0;
+    }
   }
+  if (bad_count) atomicAdd(violations, bad_count);
 }
 
 // K1 + K2 fused for one executor's step at serving size (<= 32,768 admissions, <= 4,096
@@ -597,7 +625,7 @@ int coe_group_sort(const int32_t *executor, const int32_t *run_rank, int64_t n, 
 
 int64_t coe_run_compact_scratch_bytes(int64_t n, int num_batches, int num_executors) {
   (void)n;
-  const int64_t blocks = (num_batches + BATCH_THREADS - 1) / BATCH_THREADS;
+  const int64_t blocks = (num_batches + BATCH_PER_BLOCK - 1) / BATCH_PER_BLOCK;
   return 4 * ((int64_t)num_executors + 16) + 4 * (blocks + 1) * num_executors;
 }
 
@@ -635,7 +663,7 @@ int coe_run_compact_routes(const int32_t *perm, const int32_t *sorted_keys, cons
                                                out_run_count);
   }
   if (num_batches > 0) {
-    const int blocks = (num_batches + BATCH_THREADS - 1) / BATCH_THREADS;
+    const int blocks = (num_batches + BATCH_PER_BLOCK - 1) / BATCH_PER_BLOCK;
     if (blocks > 1) {
       batch_block_sums<<<blocks, BATCH_THREADS, 0, stream>>>(batch_exec, batch_size, num_batches, num_executors,
                                                              block_sums);

@@ -2189,7 +2189,7 @@ extern "C" int coe_runtime_step(coe_runtime *rt, const coe_step_input *in, coe_s
     if (rc) return rc;
     st.launches += 1;
   } else {
-    st.launches += (n_adm ? 1 + passes : 0) + (n_adm ? 1 : 0) + (n_batches > 1024 ? 2 : 0) + (n_batches ? 1 : 0);
+    st.launches += (n_adm ? 1 + passes : 0) + (n_adm ? 1 : 0) + (n_batches > 4096 ? 2 : 0) + (n_batches ? 1 : 0);
     if (n_adm) {
       int rc = coe_group_sort(d_exec, d_rank, n_adm, rank_bits, passes, rt->d_perm, rt->d_keys, rt->d_sort_scratch,
                               cs);
